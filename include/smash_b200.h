@@ -1,0 +1,152 @@
+/*
+ * smash_b200.h -- C ABI of the B200-native SMASH hot path (arXiv 1705.05443).
+ *
+ * Drop-in boundary for the reference Python package's tree / construct / matvec
+ * path (/root/reference/pkg/src/smash, "smash/" below).  The reference has no
+ * FFI layer of its own; each entry point replaces the Python function cited next
+ * to it, and the Python package paper_1705_05443_b200 binds these symbols with
+ * ctypes exactly as INTEGRATION.md shows for the reference side.
+ *
+ * Conventions
+ *  - Every pointer argument named X, Y, q, z, out, or an export destination is a
+ *    DEVICE pointer (CUDA global memory) unless documented as host.  Point arrays
+ *    are row-major (n, dim) float64, like smash.PointSet.coords.
+ *  - `stream` is a cudaStream_t passed as void*; all work is stream ordered.  Calls
+ *    that must return sizes synchronise that stream before returning.
+ *  - Node indices in exports are the reference's postorder TreeNode.index (root last).
+ *  - Status codes mirror the reference CLI's exit codes (smash/cli.py:266-278):
+ *      0 ok, 2 invalid argument (Python ValueError), 3 numerical failure
+ *      (Python RuntimeError: sRRQR swap cap smash/lowrank.py:196-197, unsplittable
+ *      cluster smash/cluster.py:340-341, degenerate interpolation box
+ *      smash/lowrank.py:131-134), 4 CUDA / internal error.
+ *    smash_last_error() returns the message of the last failure on this thread.
+ *  - The library never frees caller memory.  Opaque handles own device memory
+ *    (stream-ordered allocations) and are released by their *_free function.
+ */
+#ifndef SMASH_B200_H
+#define SMASH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMASH_OK 0
+#define SMASH_ERR_INVALID 2
+#define SMASH_ERR_NUMERICAL 3
+#define SMASH_ERR_CUDA 4
+
+/* tree modes (smash/cluster.py:263 `mode`) */
+#define SMASH_MODE_BINARY 0
+#define SMASH_MODE_2D 1 /* "2d" / "2^d" */
+
+/* block structures (smash/cluster.py:402 `structure`) */
+#define SMASH_STRUCT_H2 0
+#define SMASH_STRUCT_HSS 1
+
+/* kernels: BASELINE kernels (log, 1/r, exp(-r)) extend smash/kernel.py:200-233;
+ * cauchy is the reference's real 1-D Cauchy 1/(x-y) (smash/kernel.py:286-298). */
+#define SMASH_KERNEL_LOG 0    /* log|x-y|, coincident -> dx (0)       */
+#define SMASH_KERNEL_INV_R 1  /* 1/|x-y|, coincident -> dx (0)        */
+#define SMASH_KERNEL_EXP 2    /* exp(-|x-y|), coincident -> 1         */
+#define SMASH_KERNEL_CAUCHY 3 /* 1/(x-y), d = 1, coincident -> dx     */
+
+typedef struct smash_tree_s* smash_tree_t;
+typedef struct smash_matrix_s* smash_matrix_t;
+
+int smash_abi_version(void);
+const char* smash_last_error(void);
+
+/* ---- cluster tree: replaces smash.cluster.build_tree (smash/cluster.py:263-353) ----
+ * X: (nx, dim) device, Y: (ny, dim) device or NULL (= X, shared points as in the
+ * reference's points_col=None).  mode: SMASH_MODE_*.  */
+int smash_tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, int32_t dim,
+                     int32_t nu0, int32_t mode, void* stream, smash_tree_t* out);
+/* sizes of the finished tree (host outputs) */
+int smash_tree_sizes(smash_tree_t t, int64_t* n_nodes, int32_t* n_levels, int64_t* n_row,
+                     int64_t* n_col, int32_t* dim, int32_t* shared_points);
+/* Copy the tree into caller device buffers, postorder node indexing:
+ *   level/parent/row_start/row_stop/col_start/col_stop: int64[n_nodes]
+ *   child_ptr: int64[n_nodes+1], child_idx: int64[n_nodes-1] (children in order)
+ *   lo/hi: float64[n_nodes, dim]; perm_row: int64[n_row]; perm_col: int64[n_col]
+ *   points_row: float64[n_row, dim]; points_col: float64[n_col, dim]
+ * Any destination may be NULL (skipped).  Mirrors ClusterTree (cluster.py:118-135). */
+int smash_tree_export(smash_tree_t t, int64_t* level, int64_t* parent, int64_t* child_ptr,
+                      int64_t* child_idx, double* lo, double* hi, int64_t* row_start,
+                      int64_t* row_stop, int64_t* col_start, int64_t* col_stop,
+                      int64_t* perm_row, int64_t* perm_col, double* points_row,
+                      double* points_col, void* stream);
+int smash_tree_free(smash_tree_t t);
+
+/* ---- block partition: replaces smash.cluster.leaf_sets (smash/cluster.py:402-447) ----
+ * Computes (and caches on the tree) L and Lm; returns their sizes (host). */
+int smash_leaf_sets(smash_tree_t t, double tau, int32_t structure, void* stream, int64_t* n_L,
+                    int64_t* n_Lm);
+/* L: int64[n_L, 2], Lm: int64[n_Lm, 2] device, lexicographically sorted (i, j). */
+int smash_leaf_sets_export(smash_tree_t t, double tau, int32_t structure, int64_t* L, int64_t* Lm,
+                           void* stream);
+
+/* ---- nearfield sets: replaces smash.cluster.nearfield_set (smash/cluster.py:374-399) ----
+ * N_i for every node, in the reference's candidate order; total entries (host). */
+int smash_nearfield(smash_tree_t t, double tau, void* stream, int64_t* total);
+/* ptr: int64[n_nodes+1], idx: int64[total] device (postorder indexing) */
+int smash_nearfield_export(smash_tree_t t, double tau, int64_t* ptr, int64_t* idx, void* stream);
+
+/* ---- construction: replaces smash.h2.build_h2 (smash/h2.py:25-54) and
+ *      smash.hss.build_hss (smash/hss.py:247-303) with BuildParams (hss.py:23-32)
+ *      plus the sRRQR rank tolerance rtol (smash/lowrank.py:19,163-167). ---- */
+typedef struct {
+  int32_t structure; /* SMASH_STRUCT_* */
+  int32_t kernel;    /* SMASH_KERNEL_* */
+  double dx;         /* value at coincident points (KernelSpec.dx) */
+  int32_t r;         /* interpolation nodes (BuildParams.r) */
+  double tau;        /* admissibility (BuildParams.tau) */
+  double s;          /* swap bound (BuildParams.s) */
+  double rtol;       /* sRRQR rank tolerance */
+  double eps_svd;    /* HSS nearfield SVD cutoff (BuildParams.eps_svd) */
+} smash_build_params;
+
+int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream,
+                       smash_matrix_t* out);
+/* side: 0 = row factors (rowfac), 1 = column factors (colfac).  Host outputs:
+ * n_factors (nodes with a factor = non-root), total |ibar|, total skeleton, total G entries. */
+int smash_matrix_sizes(smash_matrix_t m, int32_t side, int64_t* has_total, int64_t* ibar_total,
+                       int64_t* skel_total, int64_t* g_total);
+/* Per-node interpolative factors (InterpolativeFactor, smash/lowrank.py:206-229), postorder:
+ *   has: int64[n_nodes] (1 if the node has a factor), rank: int64[n_nodes]
+ *   perm_ptr: int64[n_nodes+1], perm: int64[ibar_total]      (local row permutation)
+ *   skel_ptr: int64[n_nodes+1], skel: int64[skel_total]      (tree-order labels, ordered)
+ *   g_ptr: int64[n_nodes+1], G: float64[g_total]             ((|ibar|-k) x k row-major) */
+int smash_matrix_export(smash_matrix_t m, int32_t side, int64_t* has, int64_t* rank,
+                        int64_t* perm_ptr, int64_t* perm, int64_t* skel_ptr, int64_t* skel,
+                        int64_t* g_ptr, double* G, void* stream);
+/* number of sRRQR swap-loop iterations per side (host output) */
+int smash_matrix_stats(smash_matrix_t m, int64_t* swaps_row, int64_t* swaps_col);
+
+/* ---- matvec: replaces smash.apply.matvec_nodewise (smash/apply.py:34-80) ----
+ * q: (n_col, nrhs) row-major device, z: (n_row, nrhs) row-major device; caller order. */
+int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
+int smash_matrix_free(smash_matrix_t m);
+
+/* ---- exact kernel entries: replaces smash.kernel.kernel_block (smash/kernel.py:278-310)
+ *      and the block accessors B / NF (smash/hss.py:138-162) ----
+ * X: (nx, dim), Y: (ny, dim) device; out: (nx, ny) row-major device. */
+int smash_kernel_block(int32_t kernel, double dx, int32_t dim, const double* X, int64_t nx,
+                       const double* Y, int64_t ny, double* out, void* stream);
+
+/* ---- single-call primitives (smash/lowrank.py) ----
+ * interp_basis (lowrank.py:123-144): lo/hi HOST float64[dim]; pts (n, dim) device;
+ * out (n, r) row-major device.  dim 3 is this library's tensor extension. */
+int smash_interp_basis(int32_t dim, const double* lo, const double* hi, const double* pts,
+                       int64_t n, int32_t r, double* out, void* stream);
+/* compr (lowrank.py:232-255) on C (nrows, ncols) row-major device:
+ * perm int64[nrows] device, G float64[nrows*min(nrows,ncols)] device (first (nrows-k)*k
+ * entries valid, row-major), rank/swaps host. */
+int smash_compr(const double* C, int64_t nrows, int64_t ncols, double s, double rtol, int64_t* perm,
+                double* G, int64_t* rank, int64_t* swaps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMASH_B200_H */

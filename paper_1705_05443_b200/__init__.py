@@ -1,0 +1,26 @@
+"""paper_1705_05443_b200 -- B200-native SMASH hot path (arXiv 1705.05443).
+
+Drop-in for the reference package's tree / construct / matvec path
+(``smash.build_tree``, ``leaf_sets``, ``nearfield_set``, ``build_h2``,
+``build_hss``, ``matvec_nodewise`` and the objects they return).  All compute
+runs in hand-written sm_100a CUDA kernels behind the C ABI in
+include/smash_b200.h (libsmash_b200.so, loaded with ctypes); there is no CPU
+fallback.
+"""
+
+from .cluster import (Box, ClusterTree, PointSet, TreeNode, build_tree, leaf_sets, nearfield_set,
+                      well_separated)
+from .kernel import KernelSpec, kernel_block
+from .lowrank import InterpolativeFactor, compr, interp_basis
+from .hss import BuildParams, HssMatrix, build_hss
+from .h2 import H2Matrix, build_h2
+from .apply import matvec_device, matvec_nodewise
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Box", "BuildParams", "ClusterTree", "H2Matrix", "HssMatrix", "InterpolativeFactor",
+    "KernelSpec", "PointSet", "TreeNode", "build_h2", "build_hss", "build_tree", "compr",
+    "interp_basis", "kernel_block", "leaf_sets", "matvec_device", "matvec_nodewise",
+    "nearfield_set", "well_separated",
+]

@@ -1,0 +1,43 @@
+"""Fast matvec -- GPU drop-in for smash.apply.matvec_nodewise
+(/root/reference/pkg/src/smash/apply.py:26-80)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["matvec_nodewise", "matvec_device"]
+
+
+def matvec_device(M, Q, out=None):
+    """A @ Q for a CUDA float64 tensor Q of shape (n_col, nrhs); returns (n_row, nrhs)."""
+    torch = _lib.torch_cuda()
+    if Q.dim() != 2 or Q.shape[0] != M.n_col:
+        raise ValueError("vector length %d does not match matrix (%d)" % (Q.shape[0], M.n_col))
+    Q = Q.contiguous()
+    if out is None:
+        out = torch.empty((M.n_row, Q.shape[1]), dtype=torch.float64, device=Q.device)
+    _lib.check(_lib.load().smash_matvec(M._h, _lib.ptr(Q), _lib.ptr(out), Q.shape[1], _lib.stream_ptr()))
+    return out
+
+
+def matvec_nodewise(M, q):
+    """A @ q through the compressed representation, caller ordering (apply.py:34-80).
+    q: (n,) or (n, nrhs), numpy or torch; the result has q's rank and container."""
+    torch = _lib.torch_cuda()
+    is_torch = isinstance(q, torch.Tensor)
+    if not is_torch:
+        q = np.asarray(q)
+    if q.shape[0] != M.n_col:
+        raise ValueError("vector length %d does not match matrix (%d)" % (q.shape[0], M.n_col))
+    single = q.ndim == 1
+    Q = _lib.to_device(q)
+    if single:
+        Q = Q.reshape(-1, 1)
+    Z = matvec_device(M, Q)
+    if single:
+        Z = Z[:, 0]
+    if is_torch:
+        return Z.to(q.device)
+    return Z.cpu().numpy()

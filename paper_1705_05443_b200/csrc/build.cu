@@ -1,0 +1,558 @@
+// Construction driver: replaces smash.h2.build_h2 (smash/h2.py:25-54) and
+// smash.hss.build_hss (smash/hss.py:247-303).
+//
+// Host orchestration of the level-synchronous bottom-up sweep: for each level
+// L..2 and each side, (1) |ibar| per node, (2) capacity offsets, (3) [HSS] the
+// nearfield SVD, (4) the batched basis + sRRQR kernel, (5) compaction of the
+// level's ordered skeletons (labels + coordinates) so the next level's ibar
+// sets are contiguous slices.  When row and column points are shared the
+// column factors alias the row factors (bitwise identical in the reference,
+// SURVEY.md 7 / probe p12).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "compress.cuh"
+#include "svd.cuh"
+
+namespace smash {
+
+namespace {
+
+template <typename F>
+void cub_call(F f, DBuf<char>& tmp, cudaStream_t s) {
+  size_t bytes = 0;
+  SMASH_CUDA(f((void*)nullptr, bytes));
+  if (bytes > tmp.n) tmp.alloc(bytes, s);
+  SMASH_CUDA(f((void*)tmp.p, bytes));
+}
+
+template <typename T>
+void grow(DBuf<T>& b, size_t used, size_t need, cudaStream_t s) {
+  if (need <= b.n) return;
+  size_t nc = std::max(need, b.n * 2 + 1024);
+  DBuf<T> nb;
+  nb.alloc(nc, s);
+  d2d(nb.p, b.p, used, s);
+  b = std::move(nb);
+}
+
+__global__ void k_level_sizes(int lb, int le, const int* nchild, const int* child_first,
+                              const int* pt_a, const int* pt_b, const int* rank, int* nib,
+                              int64_t* ibcnt, int64_t* gcnt, int mrows_bound) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= le) return;
+  int n;
+  if (nchild[v] == 0) {
+    n = pt_b[v] - pt_a[v];
+  } else {
+    n = 0;
+    for (int c = 0; c < nchild[v]; ++c) n += rank[child_first[v] + c];
+  }
+  nib[v] = n;
+  ibcnt[v - lb] = n;
+  gcnt[v - lb] = (int64_t)n * min(n, mrows_bound);
+}
+
+__global__ void k_add_base(int lb, int le, const int64_t* loc, int64_t base, int64_t* glob) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < le) glob[v] = base + loc[v - lb];
+}
+
+__global__ void k_rank_cnt(int lb, int le, const int* rank, int* cnt) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < le) cnt[v - lb] = rank[v];
+}
+
+__global__ void k_skel_compact(int lb, int le, const int* rank, const int* loc_off, int base,
+                               const int64_t* ib_off, int64_t ib_level_base, const int* tmp_lab,
+                               const double* tmp_pts, int64_t tmp_stride, int dim, int* skel_off,
+                               int* skel, double* skel_pts, int64_t skel_stride) {
+  int v = lb + blockIdx.x;
+  if (v >= le) return;
+  int o = base + loc_off[v - lb];
+  if (threadIdx.x == 0) skel_off[v] = o;
+  int k = rank[v];
+  int64_t src = ib_off[v] - ib_level_base;
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    skel[o + a] = tmp_lab[src + a];
+    for (int d = 0; d < dim; ++d)
+      skel_pts[(size_t)d * skel_stride + o + a] = tmp_pts[(size_t)d * tmp_stride + src + a];
+  }
+}
+
+__global__ void k_skel_bound(int n, int root, const int* pt_a, const int* pt_b, int kb,
+                             int64_t* out) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  out[v] = v == root ? 0 : (int64_t)min(pt_b[v] - pt_a[v], kb);
+}
+
+__global__ void k_max_int(const int* x, int n, int* out) {
+  int m = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = max(m, x[i]);
+  for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// host tables: cos/sin exactly as numpy evaluates them (lowrank.py:103-111)
+struct HostTables {
+  std::vector<double> cosv, wv;
+  std::vector<int> order;
+  int m = 0;
+};
+
+HostTables make_tables(int r, int dim) {
+  HostTables H;
+  int m;
+  if (dim == 1) {
+    m = r;
+  } else if (dim == 2) {
+    m = (int)std::ceil(std::sqrt((double)r));
+  } else {
+    m = 1;
+    while (m * m * m < r) ++m;
+  }
+  H.m = m;
+  for (int k = 0; k < m; ++k) {
+    double arg = ((double)(2 * k + 1) * M_PI) / (double)(2 * m);
+    H.cosv.push_back(std::cos(arg));
+    H.wv.push_back(((k & 1) ? -1.0 : 1.0) * std::sin(arg));
+  }
+  // tensor order: sorted by (degree, i, j[, k]), first r (lowrank.py:143; 3-D extension)
+  std::vector<std::array<int, 4>> idx;
+  if (dim == 1) {
+    for (int i = 0; i < r; ++i) idx.push_back({i, i, 0, 0});
+  } else if (dim == 2) {
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) idx.push_back({i + j, i, j, 0});
+  } else {
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j)
+        for (int k = 0; k < m; ++k) idx.push_back({i + j + k, i, j, k});
+  }
+  std::sort(idx.begin(), idx.end());
+  for (int q = 0; q < r; ++q) {
+    H.order.push_back(idx[q][1]);
+    H.order.push_back(idx[q][2]);
+    H.order.push_back(idx[q][3]);
+  }
+  return H;
+}
+
+struct DevTables {
+  DBuf<double> cosv, wv;
+  DBuf<int> order;
+  BasisTables view;
+  void upload(const HostTables& H, cudaStream_t s) {
+    cosv.alloc(H.cosv.size(), s); wv.alloc(H.wv.size(), s); order.alloc(H.order.size(), s);
+    h2d(cosv.p, H.cosv.data(), H.cosv.size(), s);
+    h2d(wv.p, H.wv.data(), H.wv.size(), s);
+    h2d(order.p, H.order.data(), H.order.size(), s);
+    view.cosv = cosv.p; view.wv = wv.p; view.order = order.p; view.m = H.m;
+  }
+};
+
+void check_basis_params(int r, int dim) {
+  SMASH_CHECK(r >= 1, SMASH_ERR_INVALID, "r must be positive");
+  if (dim == 1)
+    SMASH_CHECK(r <= MAX_M_AXIS_1D, SMASH_ERR_INVALID, "1-D interpolation supports r <= 128");
+  HostTables H = make_tables(r, dim);
+  if (dim > 1)
+    SMASH_CHECK(H.m <= MAX_M_AXIS_ND, SMASH_ERR_INVALID, "interpolation grid too large (m > 16 per axis)");
+  SMASH_CHECK((int)H.order.size() == 3 * r, SMASH_ERR_INVALID, "r exceeds the tensor grid");
+}
+
+double host_norm_fma(const double* v, int d) {
+  double s = v[0] * v[0];
+  for (int k = 1; k < d; ++k) s = std::fma(v[k], v[k], s);
+  return std::sqrt(s);
+}
+
+void raise_dev_err(int e) {
+  if (e & DEV_SWAP_CAP)
+    throw Error(SMASH_ERR_NUMERICAL, "srrqr swap loop exceeded 200 iterations");
+  if (e & DEV_DEGENERATE_BOX)
+    throw Error(SMASH_ERR_NUMERICAL,
+                "degenerate box dimension; interpolation nodes would coincide");
+  if (e & DEV_CAPACITY) throw Error(SMASH_ERR_CUDA, "internal capacity exceeded");
+  if (e) throw Error(SMASH_ERR_NUMERICAL, "numerical failure in construction");
+}
+
+int max_sm_smem() {
+  int dev = 0, v = 0;
+  SMASH_CUDA(cudaGetDevice(&dev));
+  SMASH_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return v;
+}
+
+int num_sms() {
+  int dev = 0, v = 0;
+  SMASH_CUDA(cudaGetDevice(&dev));
+  SMASH_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  return v;
+}
+
+}  // namespace
+
+// Compress one side of the matrix, all levels.
+static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pad,
+                       cudaStream_t s) {
+  TreeImpl* t = M->tree;
+  SideFactors& F = side == 0 ? M->rowf : M->colf_own;
+  const int n = t->n_nodes, dim = t->dim, r = M->p.r;
+  const bool hss = M->p.structure == SMASH_STRUCT_HSS;
+  const int* pt_a = side == 0 ? t->row_a.p : t->col_a.p;
+  const int* pt_b = side == 0 ? t->row_b.p : t->col_b.p;
+  const double* P = side == 0 || t->shared ? t->pts_row.p : t->pts_col.p;
+  const int64_t Pn = side == 0 || t->shared ? t->nx : t->ny;
+
+  F.nib.alloc(n, s); F.rank.alloc(n, s); F.ib_off.alloc(n, s); F.g_off.alloc(n, s);
+  F.skel_off.alloc(n, s);
+  F.rank.zero(s); F.nib.zero(s); F.ib_off.zero(s); F.g_off.zero(s); F.skel_off.zero(s);
+  DBuf<char> tmp;
+  DBuf<int64_t> kb;
+  kb.alloc(n + 1, s);
+  kb.zero(s);
+  const int root = 0;
+  // skeleton capacity: k_v <= min(rows, |points below v|); HSS rows are r + keep <= |ibar|
+  k_skel_bound<<<cdiv(n, 128), 128, 0, s>>>(n, root, pt_a, pt_b, hss ? (1 << 30) : r, kb.p);
+  DBuf<int64_t> kbs;
+  kbs.alloc(1, s);
+  cub_call([&](void* tp, size_t& b) { return cub::DeviceReduce::Sum(tp, b, kb.p, kbs.p, n, s); },
+           tmp, s);
+  int64_t skel_cap = 0;
+  d2h(&skel_cap, kbs.p, 1, s);
+  sync(s);
+  skel_cap = std::max<int64_t>(skel_cap, 1);
+  F.skel.alloc(skel_cap, s);
+  F.skel_pts.alloc((size_t)skel_cap * dim, s);
+  F.perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
+  F.G.alloc(std::max<int64_t>(Pn * 8, 1024), s);
+  F.level_skel_begin.assign(t->n_levels + 2, 0);
+
+  DBuf<int> err;
+  err.alloc(1, s);
+  err.zero(s);
+  DBuf<unsigned long long> swaps;
+  swaps.alloc(1, s);
+  swaps.zero(s);
+  DBuf<int> dmax;
+  dmax.alloc(1, s);
+
+  const int smem_limit = max_sm_smem();
+  const int nsm = num_sms();
+  int64_t skel_used = 0;
+  DBuf<double> gws;
+  NearSets* near = hss ? get_near(t, M->p.tau, s) : nullptr;
+  SvdWorkspace svdws;
+
+  for (int l = t->n_levels; l >= 2; --l) {
+    const int lb = t->level_begin(l), le = t->level_end(l), cnt = le - lb;
+    DBuf<int64_t> ibc, gc, ibo, go;
+    ibc.alloc(cnt + 1, s); gc.alloc(cnt + 1, s); ibo.alloc(cnt + 1, s); go.alloc(cnt + 1, s);
+    SMASH_CUDA(cudaMemsetAsync(ibc.p + cnt, 0, 8, s));
+    SMASH_CUDA(cudaMemsetAsync(gc.p + cnt, 0, 8, s));
+    // HSS: G capacity bound uses |ibar| (rows r + keep may exceed r)
+    k_level_sizes<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a,
+                                                 pt_b, F.rank.p, F.nib.p, ibc.p, gc.p,
+                                                 hss ? (1 << 30) : r);
+    cub_call([&](void* tp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tp, b, ibc.p, ibo.p, cnt + 1, s);
+    }, tmp, s);
+    cub_call([&](void* tp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tp, b, gc.p, go.p, cnt + 1, s);
+    }, tmp, s);
+    dmax.zero(s);
+    k_max_int<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(F.nib.p + lb, cnt, dmax.p);
+    int64_t tot[2];
+    int nmax = 0;
+    d2h(&tot[0], ibo.p + cnt, 1, s);
+    d2h(&tot[1], go.p + cnt, 1, s);
+    d2h(&nmax, dmax.p, 1, s);
+    sync(s);
+    const int64_t lvl_ib = tot[0], lvl_g = tot[1];
+    grow(F.perm, F.ib_total, F.ib_total + lvl_ib, s);
+    grow(F.G, F.g_total, F.g_total + lvl_g, s);
+    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, ibo.p, F.ib_total, F.ib_off.p);
+    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, go.p, F.g_total, F.g_off.p);
+
+    // ---- HSS nearfield SVD (hss.py:279-299)
+    int max_keep = 0;
+    if (hss) {
+      max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s);
+    }
+
+    DBuf<int> tmp_lab;
+    DBuf<double> tmp_pts;
+    tmp_lab.alloc(std::max<int64_t>(lvl_ib, 1), s);
+    tmp_pts.alloc((size_t)std::max<int64_t>(lvl_ib, 1) * dim, s);
+
+    CompressArgs A;
+    A.lb = lb; A.le = le; A.dim = dim; A.r = r; A.side = side;
+    A.nchild = t->nchild.p; A.child_first = t->child_first.p; A.pt_a = pt_a;
+    A.lo = t->lo.p; A.hi = t->hi.p; A.pad = pad; A.half_pad = pad / 2;
+    A.P = P; A.P_stride = Pn;
+    A.Sk = F.skel_pts.p; A.S_stride = skel_cap; A.Slab = F.skel.p; A.skel_off = F.skel_off.p;
+    A.nib = F.nib.p; A.ib_off = F.ib_off.p; A.g_off = F.g_off.p; A.ib_level_base = F.ib_total;
+    if (hss) { A.keep = svdws.keep.p; A.sv_off = svdws.sv_off.p; A.sv = svdws.sv.p; }
+    A.tab = tabs.view;
+    A.s_bound = M->p.s; A.rtol = M->p.rtol;
+    A.rank = F.rank.p; A.perm = F.perm.p; A.G = F.G.p;
+    A.tmp_lab = tmp_lab.p; A.tmp_pts = tmp_pts.p; A.tmp_stride = std::max<int64_t>(lvl_ib, 1);
+    A.err = err.p; A.swaps = swaps.p;
+    A.nmax = std::max(nmax, 1);
+    A.mmax = r + max_keep;
+    size_t smem_full = compress_smem_bytes(A.nmax, A.mmax, true);
+    size_t smem;
+    int grid;
+    if ((int)smem_full <= smem_limit) {
+      A.smem_panel = 1;
+      smem = smem_full;
+      int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, (228 * 1024) / (smem + 1024)));
+      grid = std::min(cnt, nsm * per_sm);
+    } else {
+      A.smem_panel = 0;
+      smem = compress_smem_bytes(A.nmax, A.mmax, false);
+      grid = std::min(cnt, nsm * 2);
+      size_t need = (size_t)grid * A.mmax * A.nmax;
+      if (gws.n < need) gws.alloc(need, s);
+      A.gws = gws.p;
+    }
+    launch_compress(A, grid, smem, s);
+
+    // ---- compact this level's skeletons
+    DBuf<int> rc, ro;
+    rc.alloc(cnt + 1, s); ro.alloc(cnt + 1, s);
+    SMASH_CUDA(cudaMemsetAsync(rc.p + cnt, 0, 4, s));
+    k_rank_cnt<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, F.rank.p, rc.p);
+    cub_call([&](void* tp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tp, b, rc.p, ro.p, cnt + 1, s);
+    }, tmp, s);
+    int lvl_k = 0, herr = 0;
+    d2h(&lvl_k, ro.p + cnt, 1, s);
+    d2h(&herr, err.p, 1, s);
+    sync(s);
+    raise_dev_err(herr);
+    SMASH_CHECK(skel_used + lvl_k <= skel_cap, SMASH_ERR_CUDA, "skeleton capacity exceeded");
+    F.level_skel_begin[l] = skel_used;
+    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F.rank.p, ro.p, (int)skel_used, F.ib_off.p,
+                                       F.ib_total, tmp_lab.p, tmp_pts.p, A.tmp_stride, dim,
+                                       F.skel_off.p, F.skel.p, F.skel_pts.p, skel_cap);
+    skel_used += lvl_k;
+    F.ib_total += lvl_ib;
+    F.g_total += lvl_g;
+  }
+  F.level_skel_begin[1] = skel_used;
+  F.skel_total = skel_used;
+  // keep the SoA stride == capacity (skel_pts rows are skel_cap apart)
+  F.skel_stride = skel_cap;
+  unsigned long long hs = 0;
+  d2h(&hs, swaps.p, 1, s);
+  sync(s);
+  F.swaps = (int64_t)hs;
+  SMASH_CUDA(cudaGetLastError());
+}
+
+MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s) {
+  SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
+              "unknown kernel kind");
+  SMASH_CHECK(p.structure == SMASH_STRUCT_H2 || p.structure == SMASH_STRUCT_HSS,
+              SMASH_ERR_INVALID, "structure must be 'hss' or 'h2'");
+  if (p.kernel == SMASH_KERNEL_CAUCHY)
+    SMASH_CHECK(t->dim == 1, SMASH_ERR_INVALID, "the real Cauchy kernel needs 1-D points");
+  if (p.structure == SMASH_STRUCT_H2)
+    SMASH_CHECK(t->mode == SMASH_MODE_2D || t->dim == 1, SMASH_ERR_INVALID,
+                "H2 construction expects a 2^d-mode tree");
+  check_basis_params(p.r, t->dim);
+  std::unique_ptr<MatrixImpl> M(new MatrixImpl());
+  M->tree = t;
+  M->p = p;
+  M->pl = get_pairs(t, p.tau, p.structure, s);
+  HostTables H = make_tables(p.r, t->dim);
+  DevTables D;
+  D.upload(H, s);
+  // pad = max(1e-9 * diam, 1e-300), diam = 2 * root radius (hss.py:221-222)
+  double w[3];
+  for (int a = 0; a < t->dim; ++a) w[a] = t->root_hi[a] - t->root_lo[a];
+  double diam = 2 * (0.5 * host_norm_fma(w, t->dim));
+  double pad = std::max(1e-9 * diam, 1e-300);
+  build_side(M.get(), 0, D, pad, s);
+  if (t->shared) {
+    M->colf = &M->rowf;
+  } else {
+    build_side(M.get(), 1, D, pad, s);
+    M->colf = &M->colf_own;
+  }
+  sync(s);
+  return M.release();
+}
+
+// ---------------------------------------------------------------------------
+// export (postorder)
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_exp_counts(int n, int root, const int* post, const int* nib, const int* rank,
+                             const int64_t* g_off_unused, int64_t* has, int64_t* rk, int64_t* cp,
+                             int64_t* cs, int64_t* cg) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  int p = post[v];
+  bool h = v != root;
+  int k = h ? rank[v] : 0, ni = h ? nib[v] : 0;
+  if (has) has[p] = h ? 1 : 0;
+  if (rk) rk[p] = k;
+  cp[p] = ni;
+  cs[p] = k;
+  cg[p] = (int64_t)(ni - k) * k;
+  (void)g_off_unused;
+}
+
+__global__ void k_exp_copy(int n, int root, const int* post, const int* nib, const int* rank,
+                           const int64_t* ib_off, const int64_t* g_off, const int* skel_off,
+                           const int* perm, const double* G, const int* skel, const int64_t* pp,
+                           const int64_t* sp, const int64_t* gp, int64_t* operm, int64_t* oskel,
+                           double* oG) {
+  int v = blockIdx.x;
+  if (v >= n || v == root) return;
+  int p = post[v];
+  int ni = nib[v], k = rank[v];
+  if (operm)
+    for (int c = threadIdx.x; c < ni; c += blockDim.x) operm[pp[p] + c] = perm[ib_off[v] + c];
+  if (oskel)
+    for (int a = threadIdx.x; a < k; a += blockDim.x) oskel[sp[p] + a] = skel[skel_off[v] + a];
+  if (oG) {
+    int64_t ng = (int64_t)(ni - k) * k;
+    for (int64_t e = threadIdx.x; e < ng; e += blockDim.x) oG[gp[p] + e] = G[g_off[v] + e];
+  }
+}
+
+}  // namespace
+
+void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t* perm_ptr,
+                   int64_t* perm, int64_t* skel_ptr, int64_t* skel, int64_t* g_ptr, double* G,
+                   cudaStream_t s) {
+  TreeImpl* t = m->tree;
+  SideFactors& F = side == 0 ? m->rowf : *m->colf;
+  const int n = t->n_nodes;
+  DBuf<int64_t> cp, cs, cg, pp, sp, gp;
+  cp.alloc(n + 1, s); cs.alloc(n + 1, s); cg.alloc(n + 1, s);
+  cp.zero(s); cs.zero(s); cg.zero(s);
+  k_exp_counts<<<cdiv(n, 128), 128, 0, s>>>(n, 0, t->post.p, F.nib.p, F.rank.p, F.g_off.p, has,
+                                            rank, cp.p, cs.p, cg.p);
+  DBuf<char> tmp;
+  auto scan = [&](DBuf<int64_t>& in, int64_t* out, DBuf<int64_t>& own) {
+    int64_t* dst = out;
+    if (!dst) { own.alloc(n + 1, s); dst = own.p; }
+    cub_call([&](void* tp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tp, b, in.p, dst, n + 1, s);
+    }, tmp, s);
+    return dst;
+  };
+  int64_t* ppp = scan(cp, perm_ptr, pp);
+  int64_t* spp = scan(cs, skel_ptr, sp);
+  int64_t* gpp = scan(cg, g_ptr, gp);
+  k_exp_copy<<<std::max(n, 1), 128, 0, s>>>(n, 0, t->post.p, F.nib.p, F.rank.p, F.ib_off.p,
+                                            F.g_off.p, F.skel_off.p, F.perm.p, F.G.p, F.skel.p,
+                                            ppp, spp, gpp, perm, skel, G);
+  sync(s);
+  SMASH_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// single-call primitives
+// ---------------------------------------------------------------------------
+void interp_basis_single(int dim, const double* lo, const double* hi, const double* pts, int64_t n,
+                         int r, double* out, cudaStream_t s) {
+  SMASH_CHECK(dim >= 1 && dim <= 3, SMASH_ERR_INVALID, "interpolation basis supports d <= 3");
+  check_basis_params(r, dim);
+  double scale = 1.0;
+  for (int a = 0; a < dim; ++a) scale = std::max(scale, hi[a] - lo[a]);
+  for (int a = 0; a < dim; ++a)
+    SMASH_CHECK(hi[a] - lo[a] > 1e-14 * scale, SMASH_ERR_INVALID,
+                "degenerate box dimension; interpolation nodes would coincide");
+  HostTables H = make_tables(r, dim);
+  DevTables D;
+  D.upload(H, s);
+  DBuf<double> soa;
+  soa.alloc(std::max<int64_t>(n * dim, 1), s);
+  // AoS (n, dim) -> SoA
+  std::vector<double> dummy;
+  (void)dummy;
+  if (n) {
+    // transpose on device via a strided copy per axis
+    for (int a = 0; a < dim; ++a)
+      SMASH_CUDA(cudaMemcpy2DAsync(soa.p + (size_t)a * n, sizeof(double), pts + a,
+                                   sizeof(double) * dim, sizeof(double), n,
+                                   cudaMemcpyDeviceToDevice, s));
+    launch_basis_single(dim, lo, hi, D.view, r, soa.p, n, out, nullptr, s);
+  }
+  sync(s);
+}
+
+void compr_single(const double* C, int64_t nrows, int64_t ncols, double s_bound, double rtol,
+                  int64_t* perm, double* G, int64_t* rank, int64_t* swaps, cudaStream_t s) {
+  SMASH_CHECK(nrows >= 0 && ncols >= 0, SMASH_ERR_INVALID, "bad shape");
+  SMASH_CHECK(nrows < (1 << 20), SMASH_ERR_INVALID, "compr: too many rows for one CTA");
+  if (nrows == 0 || ncols == 0) {
+    *rank = 0;
+    *swaps = 0;
+    if (nrows) {
+      std::vector<int64_t> id(nrows);
+      for (int64_t i = 0; i < nrows; ++i) id[i] = i;
+      h2d(perm, id.data(), nrows, s);
+      sync(s);
+    }
+    return;
+  }
+  DBuf<int> nib, rk, pm, err;
+  DBuf<int64_t> off;
+  DBuf<double> g;
+  DBuf<unsigned long long> sw;
+  int ni = (int)nrows;
+  nib.alloc(1, s); rk.alloc(1, s); pm.alloc(nrows, s); err.alloc(1, s); off.alloc(2, s);
+  int64_t kmax = std::min(nrows, ncols);
+  g.alloc(std::max<int64_t>(nrows * kmax, 1), s);
+  sw.alloc(1, s);
+  h2d(nib.p, &ni, 1, s);
+  off.zero(s); err.zero(s); sw.zero(s);
+  CompressArgs A;
+  A.lb = 0; A.le = 1; A.dim = 1; A.r = 0;
+  A.nib = nib.p; A.ib_off = off.p; A.g_off = off.p + 1;
+  A.Cexp = C; A.C_cols = (int)ncols;
+  A.s_bound = s_bound; A.rtol = rtol;
+  A.rank = rk.p; A.perm = pm.p; A.G = g.p;
+  A.err = err.p; A.swaps = sw.p;
+  A.nmax = ni; A.mmax = (int)ncols;
+  size_t smem = compress_smem_bytes(A.nmax, A.mmax, true);
+  DBuf<double> gws;
+  if ((int)smem > max_sm_smem()) {
+    A.smem_panel = 0;
+    smem = compress_smem_bytes(A.nmax, A.mmax, false);
+    gws.alloc((size_t)A.nmax * A.mmax, s);
+    A.gws = gws.p;
+  }
+  SMASH_CHECK((int)smem <= max_sm_smem(), SMASH_ERR_INVALID, "compr: matrix too large for one CTA");
+  launch_compress(A, 1, smem, s);
+  int hk = 0, he = 0;
+  unsigned long long hs = 0;
+  d2h(&hk, rk.p, 1, s);
+  d2h(&he, err.p, 1, s);
+  d2h(&hs, sw.p, 1, s);
+  sync(s);
+  raise_dev_err(he);
+  *rank = hk;
+  *swaps = (int64_t)hs;
+  std::vector<int> hp(nrows);
+  d2h(hp.data(), pm.p, nrows, s);
+  sync(s);
+  std::vector<int64_t> hp64(hp.begin(), hp.end());
+  h2d(perm, hp64.data(), nrows, s);
+  if (hk > 0 && hk < nrows) d2d(G, g.p, (size_t)(nrows - hk) * hk, s);
+  sync(s);
+}
+
+}  // namespace smash

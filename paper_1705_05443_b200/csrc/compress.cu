@@ -1,0 +1,514 @@
+// K3 + K4: per-level batched interpolation basis + strong rank-revealing QR.
+//
+// One CTA per node (persistent grid over the level's nodes).  The CTA
+//  1. evaluates the Lagrange basis at Chebyshev nodes of the node's padded box
+//     for every point of ibar (smash/hss.py:219-238, smash/lowrank.py:103-144)
+//     straight into the panel M = C^T (r rows x |ibar| columns), in shared
+//     memory when it fits (global/L2 workspace otherwise);
+//  2. runs column-pivoted Householder QR with LAPACK dlaqp2 semantics (what
+//     scipy.linalg.qr(pivoting=True) -> dgeqp3 executes for min(m,n) < 128):
+//     first-argmax pivot on the partial norms, dlarfg reflector, dlarf update,
+//     norm downdate with the tol3z = sqrt(eps) recompute rule;
+//  3. counts the numerical rank k = #{|R_ii| > rtol |R_00|} (lowrank.py:163-167);
+//  4. runs the bounded-entry swap loop: W = R11^-1 R12; while max|W| > s, swap
+//     the C-order argmax pair and refactor the permuted panel without pivoting
+//     (lowrank.py:191-202), the panel being re-evaluated from the basis;
+//  5. writes perm, G = W^T, the ordered skeleton labels and their coordinates
+//     (lowrank.py:244-255).
+// Thread-per-column mapping keeps every column's dot products and norms in a
+// fixed sequential order; the row-major panel makes those accesses
+// bank-conflict free.
+#include "compress.cuh"
+
+namespace smash {
+
+namespace {
+
+constexpr double TOL3Z = 1.0536712127723509e-08;  // sqrt(dlamch('E')), dlaqp2
+constexpr int MAX_SWAPS = 200;                     // lowrank.py:171
+
+// numpy's pairwise summation (8 accumulators, n <= 128) over terms f(0..n-1);
+// this is the order of `terms.sum(axis=1)` in lowrank.py:116.
+template <typename F>
+__device__ __forceinline__ double np_pairwise_sum(int n, F f) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(i));
+    return r;
+  }
+  double a0 = f(0), a1 = f(1), a2 = f(2), a3 = f(3), a4 = f(4), a5 = f(5), a6 = f(6), a7 = f(7);
+  int i = 8;
+  const int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+    a0 = __dadd_rn(a0, f(i + 0)); a1 = __dadd_rn(a1, f(i + 1));
+    a2 = __dadd_rn(a2, f(i + 2)); a3 = __dadd_rn(a3, f(i + 3));
+    a4 = __dadd_rn(a4, f(i + 4)); a5 = __dadd_rn(a5, f(i + 5));
+    a6 = __dadd_rn(a6, f(i + 6)); a7 = __dadd_rn(a7, f(i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)),
+                         __dadd_rn(__dadd_rn(a4, a5), __dadd_rn(a6, a7)));
+  for (; i < n; ++i) res = __dadd_rn(res, f(i));
+  return res;
+}
+
+// Lagrange cardinal functions of one axis at x (lowrank.py:108-120), written to L[0..m).
+__device__ __forceinline__ void lagrange_axis(double x, const double* nd, const double* w, int m,
+                                              double* L) {
+  bool exact = false;
+  for (int k = 0; k < m; ++k) exact |= (__dsub_rn(x, nd[k]) == 0.0);
+  if (exact) {
+    for (int k = 0; k < m; ++k) L[k] = (__dsub_rn(x, nd[k]) == 0.0) ? 1.0 : 0.0;
+    return;
+  }
+  double S = np_pairwise_sum(m, [&](int k) { return __ddiv_rn(w[k], __dsub_rn(x, nd[k])); });
+  for (int k = 0; k < m; ++k) L[k] = __ddiv_rn(__ddiv_rn(w[k], __dsub_rn(x, nd[k])), S);
+}
+
+struct Shared {
+  double* vn1;
+  double* vn2;
+  double* vh;
+  double* rdiag;
+  double* nodes;  // [3][MAX_M_AXIS_1D]
+  double* redv;   // [32]
+  int* redi;      // [32]
+  double* misc;   // [8]
+  int* imisc;     // [8]
+  int* jpvt;
+  double* panel;
+};
+
+__device__ __forceinline__ void argmax_combine(double& v, int& i, double ov, int oi) {
+  if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+}
+
+// Block-wide (max value, smallest index) reduction; result broadcast to all threads.
+__device__ void block_argmax(double& v, int& i, Shared& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int off = 16; off; off >>= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, v, off);
+    int oi = __shfl_down_sync(0xffffffffu, i, off);
+    argmax_combine(v, i, ov, oi);
+  }
+  __syncthreads();  // protect redv/redi reuse
+  if (lane == 0) { S.redv[wid] = v; S.redi[wid] = i; }
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < nw ? S.redv[lane] : -1.0;
+    i = lane < nw ? S.redi[lane] : 0x7fffffff;
+    for (int off = 16; off; off >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, v, off);
+      int oi = __shfl_down_sync(0xffffffffu, i, off);
+      argmax_combine(v, i, ov, oi);
+    }
+    if (lane == 0) { S.redv[0] = v; S.redi[0] = i; }
+  }
+  __syncthreads();
+  v = S.redv[0];
+  i = S.redi[0];
+}
+
+__device__ __forceinline__ double col_sumsq(const double* P, int ld, int j, int r0, int r1) {
+  double s = 0.0;
+  for (int row = r0; row < r1; ++row) {
+    double x = P[(size_t)row * ld + j];
+    s = __fma_rn(x, x, s);
+  }
+  return s;
+}
+
+__device__ __forceinline__ double dlapy2(double x, double y) {
+  double xa = fabs(x), ya = fabs(y);
+  double w = fmax(xa, ya), z = fmin(xa, ya);
+  if (z == 0.0 || w > 1.7976931348623157e308) return w;
+  double q = __ddiv_rn(z, w);
+  return __dmul_rn(w, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
+}
+
+// Householder reflector on column i (dlarfg), done by warp 0; result in panel,
+// tau in S.misc[0], v (rows > i) in S.vh.
+__device__ void householder(double* P, int ld, int m, int i, Shared& S) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double alpha = P[(size_t)i * ld + i];
+  double ss = 0.0;
+  for (int row = i + 1 + lane; row < m; row += 32) {
+    double x = P[(size_t)row * ld + i];
+    ss = __fma_rn(x, x, ss);
+  }
+  for (int off = 16; off; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
+  double xnorm = __dsqrt_rn(ss);
+  double tau = 0.0;
+  if (m - i > 1 && xnorm != 0.0) {
+    double beta = -copysign(dlapy2(alpha, xnorm), alpha);
+    tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+    double scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
+    for (int row = i + 1 + lane; row < m; row += 32) {
+      double x = __dmul_rn(scal, P[(size_t)row * ld + i]);
+      P[(size_t)row * ld + i] = x;
+      S.vh[row] = x;
+    }
+    if (lane == 0) P[(size_t)i * ld + i] = beta;
+  }
+  if (lane == 0) {
+    S.misc[0] = tau;
+    S.rdiag[i] = P[(size_t)i * ld + i];
+  }
+}
+
+// Apply H_i^T = I - tau v v^T (v_i = 1) to column j > i (dlarf: w = C^T v; C -= tau v w^T).
+__device__ __forceinline__ void apply_reflector(double* P, int ld, int m, int i, int j, double tau,
+                                                const double* vh) {
+  double w = P[(size_t)i * ld + j];
+  for (int row = i + 1; row < m; ++row) w = __fma_rn(vh[row], P[(size_t)row * ld + j], w);
+  double t = -__dmul_rn(tau, w);
+  P[(size_t)i * ld + j] = __dadd_rn(P[(size_t)i * ld + j], t);
+  for (int row = i + 1; row < m; ++row)
+    P[(size_t)row * ld + j] = __fma_rn(t, vh[row], P[(size_t)row * ld + j]);
+}
+
+// ---------------------------------------------------------------------------
+// ibar point access
+// ---------------------------------------------------------------------------
+struct NodeSrc {
+  const double* base;  // coordinate SoA base for this node's ibar
+  int64_t stride;
+  const int* lab;      // labels (nullptr -> leaf: label = lab0 + c)
+  int lab0;
+};
+
+__device__ __forceinline__ NodeSrc node_src(const CompressArgs& A, int v) {
+  NodeSrc s;
+  if (A.nchild[v] == 0) {
+    int a = A.pt_a[v];
+    s.base = A.P + a;
+    s.stride = A.P_stride;
+    s.lab = nullptr;
+    s.lab0 = a;
+  } else {
+    int o = A.skel_off[A.child_first[v]];
+    s.base = A.Sk + o;
+    s.stride = A.S_stride;
+    s.lab = A.Slab + o;
+    s.lab0 = 0;
+  }
+  return s;
+}
+
+// Fill panel columns c in [0, n): column c is ibar point colmap[c] (or c).
+template <int D>
+__device__ void build_panel(const CompressArgs& A, int v, int n, int mrows, double* P,
+                            const int* colmap, const NodeSrc& src, const double* nodes) {
+  const int r = A.r;
+  const int m = A.tab.m;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const int pc = colmap ? colmap[c] : c;
+    if (A.Cexp) {  // single-call compr: panel = C^T
+      for (int q = 0; q < mrows; ++q) P[(size_t)q * n + c] = A.Cexp[(size_t)pc * A.C_cols + q];
+      continue;
+    }
+    double x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = src.base[(size_t)a * src.stride + pc];
+    if (D == 1) {
+      const double* nd = nodes;
+      bool exact = false;
+      for (int k = 0; k < m; ++k) exact |= (__dsub_rn(x[0], nd[k]) == 0.0);
+      if (exact) {
+        for (int k = 0; k < m; ++k) P[(size_t)k * n + c] = (__dsub_rn(x[0], nd[k]) == 0.0) ? 1.0 : 0.0;
+      } else {
+        double Ssum = np_pairwise_sum(m, [&](int k) {
+          return __ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k]));
+        });
+        for (int k = 0; k < m; ++k)
+          P[(size_t)k * n + c] = __ddiv_rn(__ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k])), Ssum);
+      }
+    } else {
+      double L[D][MAX_M_AXIS_ND];
+#pragma unroll
+      for (int a = 0; a < D; ++a) lagrange_axis(x[a], nodes + a * MAX_M_AXIS_1D, A.tab.wv, m, L[a]);
+      for (int q = 0; q < r; ++q) {
+        const int* o = A.tab.order + 3 * q;
+        double val = __dmul_rn(L[0][o[0]], L[1][o[1]]);
+        if (D == 3) val = __dmul_rn(val, L[D - 1][o[2]]);
+        P[(size_t)q * n + c] = val;
+      }
+    }
+    if (A.keep) {  // HSS: rows r.. hold S^T (hss.py:287)
+      const int kp = A.keep[v];
+      const double* sv = A.sv + A.sv_off[v];
+      for (int q = 0; q < kp; ++q) P[(size_t)(r + q) * n + c] = sv[(size_t)pc * kp + q];
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared S;
+  {
+    double* d = reinterpret_cast<double*>(smem_raw);
+    S.vn1 = d; d += A.nmax;
+    S.vn2 = d; d += A.nmax;
+    S.vh = d; d += A.mmax;
+    S.rdiag = d; d += A.mmax;
+    S.nodes = d; d += 3 * MAX_M_AXIS_1D;
+    S.redv = d; d += 32;
+    S.misc = d; d += 8;
+    int* ip = reinterpret_cast<int*>(d);
+    S.redi = ip; ip += 32;
+    S.imisc = ip; ip += 8;
+    S.jpvt = ip; ip += A.nmax + (A.nmax & 1);
+    S.panel = A.smem_panel ? reinterpret_cast<double*>(ip)
+                           : A.gws + (size_t)blockIdx.x * A.mmax * A.nmax;
+  }
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
+    const int n = A.nib[v];
+    const int mrows = A.Cexp ? A.C_cols : A.r + (A.keep ? A.keep[v] : 0);
+    double* P = S.panel;
+    const NodeSrc src = A.Cexp ? NodeSrc{nullptr, 0, nullptr, 0} : node_src(A, v);
+    if (n == 0) {
+      if (tid == 0) A.rank[v] = 0;
+      continue;
+    }
+    // ---- padded box + Chebyshev nodes (hss.py:39-45, lowrank.py:103-105,127-134)
+    if (!A.Cexp) {
+      if (tid == 0) {
+        double plo[3], phi[3];
+        double scale = 1.0;
+        for (int a = 0; a < D; ++a) {
+          double lo = A.lo[(size_t)v * D + a], hi = A.hi[(size_t)v * D + a];
+          if (__dsub_rn(hi, lo) < A.pad) {
+            lo = __dsub_rn(lo, A.half_pad);
+            hi = __dadd_rn(hi, A.half_pad);
+          }
+          plo[a] = lo; phi[a] = hi;
+          scale = fmax(scale, __dsub_rn(hi, lo));
+        }
+        // scale = max(max(hi - lo), 1.0)
+        int bad = 0;
+        for (int a = 0; a < D; ++a)
+          if (!(__dsub_rn(phi[a], plo[a]) > __dmul_rn(1e-14, scale))) bad = 1;
+        if (bad) atomicOr(A.err, DEV_DEGENERATE_BOX);
+        for (int a = 0; a < D; ++a) { S.misc[2 + a] = plo[a]; S.misc[5 + a] = phi[a]; }
+      }
+      __syncthreads();
+      const int m = A.tab.m;
+      for (int e = tid; e < D * m; e += NT) {
+        int a = e / m, k = e % m;
+        double lo = S.misc[2 + a], hi = S.misc[5 + a];
+        double t1 = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        double t2 = __dmul_rn(0.5, __dsub_rn(hi, lo));
+        S.nodes[a * MAX_M_AXIS_1D + k] = __dadd_rn(t1, __dmul_rn(t2, A.tab.cosv[k]));
+      }
+      __syncthreads();
+    }
+    build_panel<D>(A, v, n, mrows, P, nullptr, src, S.nodes);
+    const int ld = n;
+    const int m = mrows;
+    const int kmax = min(m, n);
+    // ---- dgeqp3 / dlaqp2
+    for (int j = tid; j < n; j += NT) {
+      double nr = __dsqrt_rn(col_sumsq(P, ld, j, 0, m));
+      S.vn1[j] = nr;
+      S.vn2[j] = nr;
+      S.jpvt[j] = j;
+    }
+    __syncthreads();
+    for (int i = 0; i < kmax; ++i) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int j = i + tid; j < n; j += NT)
+        if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
+      block_argmax(bv, bi, S);
+      const int pvt = bi;
+      if (pvt != i) {
+        for (int row = tid; row < m; row += NT) {
+          double t = P[(size_t)row * ld + pvt];
+          P[(size_t)row * ld + pvt] = P[(size_t)row * ld + i];
+          P[(size_t)row * ld + i] = t;
+        }
+        if (tid == 0) {
+          int it = S.jpvt[pvt]; S.jpvt[pvt] = S.jpvt[i]; S.jpvt[i] = it;
+          S.vn1[pvt] = S.vn1[i];
+          S.vn2[pvt] = S.vn2[i];
+        }
+      }
+      __syncthreads();
+      householder(P, ld, m, i, S);
+      __syncthreads();
+      const double tau = S.misc[0];
+      for (int j = i + 1 + tid; j < n; j += NT) {
+        if (tau != 0.0) apply_reflector(P, ld, m, i, j, tau, S.vh);
+        double v1 = S.vn1[j];
+        if (v1 != 0.0) {
+          double q = __ddiv_rn(fabs(P[(size_t)i * ld + j]), v1);
+          double temp = fmax(__dsub_rn(1.0, __dmul_rn(q, q)), 0.0);
+          double q2 = __ddiv_rn(v1, S.vn2[j]);
+          double temp2 = __dmul_rn(temp, __dmul_rn(q2, q2));
+          if (temp2 <= TOL3Z) {
+            double nv = i + 1 < m ? __dsqrt_rn(col_sumsq(P, ld, j, i + 1, m)) : 0.0;
+            S.vn1[j] = nv;
+            S.vn2[j] = nv;
+          } else {
+            S.vn1[j] = __dmul_rn(v1, __dsqrt_rn(temp));
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- numerical rank (count semantics, lowrank.py:163-167)
+    if (tid == 0) {
+      int k = 0;
+      double r0 = fabs(S.rdiag[0]);
+      if (r0 != 0.0) {
+        double thr = __dmul_rn(A.rtol, r0);
+        for (int i = 0; i < kmax; ++i) k += fabs(S.rdiag[i]) > thr ? 1 : 0;
+      }
+      S.imisc[0] = min(k, kmax);
+    }
+    __syncthreads();
+    const int k = S.imisc[0];
+    // ---- bounded-entry swap loop (lowrank.py:191-202)
+    int swaps = 0;
+    while (k > 0 && k < n) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      const int nk = n - k;
+      for (int j = k + tid; j < n; j += NT) {
+        for (int a = k - 1; a >= 0; --a) {
+          double x = __ddiv_rn(P[(size_t)a * ld + j], P[(size_t)a * ld + a]);
+          P[(size_t)a * ld + j] = x;
+          for (int b = 0; b < a; ++b)
+            P[(size_t)b * ld + j] = __fma_rn(-x, P[(size_t)b * ld + a], P[(size_t)b * ld + j]);
+        }
+        for (int a = 0; a < k; ++a) {
+          double ax = fabs(P[(size_t)a * ld + j]);
+          argmax_combine(bv, bi, ax, a * nk + (j - k));
+        }
+      }
+      block_argmax(bv, bi, S);
+      if (!(bv > A.s_bound)) break;
+      if (swaps >= MAX_SWAPS) {
+        if (tid == 0) atomicOr(A.err, DEV_SWAP_CAP);
+        break;
+      }
+      if (tid == 0) {
+        int a = bi / nk, jj = bi % nk;
+        int t = S.jpvt[a]; S.jpvt[a] = S.jpvt[k + jj]; S.jpvt[k + jj] = t;
+      }
+      __syncthreads();
+      ++swaps;
+      build_panel<D>(A, v, n, mrows, P, S.jpvt, src, S.nodes);
+      __syncthreads();
+      for (int i = 0; i < k; ++i) {  // unpivoted QR (dgeqr2); rows < k of R suffice
+        householder(P, ld, m, i, S);
+        __syncthreads();
+        const double tau = S.misc[0];
+        if (tau != 0.0)
+          for (int j = i + 1 + tid; j < n; j += NT) apply_reflector(P, ld, m, i, j, tau, S.vh);
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    // ---- outputs
+    if (tid == 0) {
+      A.rank[v] = k;
+      if (swaps) atomicAdd(A.swaps, (unsigned long long)swaps);
+    }
+    const int64_t io = A.ib_off[v];
+    for (int c = tid; c < n; c += NT) A.perm[io + c] = S.jpvt[c];
+    if (k > 0 && k < n) {
+      double* G = A.G + A.g_off[v];
+      const int nk = n - k;
+      for (int e = tid; e < nk * k; e += NT) {
+        int b = e / k, a = e % k;
+        G[e] = P[(size_t)a * ld + k + b];
+      }
+    }
+    if (A.tmp_lab) {
+      const int64_t lo = io - A.ib_level_base;
+      for (int a = tid; a < k; a += NT) {
+        int pc = S.jpvt[a];
+        A.tmp_lab[lo + a] = src.lab ? src.lab[pc] : src.lab0 + pc;
+        for (int d = 0; d < D; ++d)
+          A.tmp_pts[(size_t)d * A.tmp_stride + lo + a] = src.base[(size_t)d * src.stride + pc];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// single-call interp_basis: one thread per point
+template <int D>
+__global__ void k_basis_single(BasisTables tab, int r, const double* pts, int64_t n, double plo0,
+                               double plo1, double plo2, double phi0, double phi1, double phi2,
+                               double* out) {
+  __shared__ double nodes[3 * MAX_M_AXIS_1D];
+  double plo[3] = {plo0, plo1, plo2}, phi[3] = {phi0, phi1, phi2};
+  const int m = tab.m;
+  for (int e = threadIdx.x; e < D * m; e += blockDim.x) {
+    int a = e / m, k = e % m;
+    double t1 = __dmul_rn(0.5, __dadd_rn(plo[a], phi[a]));
+    double t2 = __dmul_rn(0.5, __dsub_rn(phi[a], plo[a]));
+    nodes[a * MAX_M_AXIS_1D + k] = __dadd_rn(t1, __dmul_rn(t2, tab.cosv[k]));
+  }
+  __syncthreads();
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  if (D == 1) {
+    double L[MAX_M_AXIS_1D];
+    lagrange_axis(pts[c], nodes, tab.wv, m, L);
+    for (int k = 0; k < r; ++k) out[c * r + k] = L[k];
+  } else {
+    double L[D][MAX_M_AXIS_ND];
+    for (int a = 0; a < D; ++a)
+      lagrange_axis(pts[(size_t)a * n + c], nodes + a * MAX_M_AXIS_1D, tab.wv, m, L[a]);
+    for (int q = 0; q < r; ++q) {
+      const int* o = tab.order + 3 * q;
+      double val = __dmul_rn(L[0][o[0]], L[1][o[1]]);
+      if (D == 3) val = __dmul_rn(val, L[D - 1][o[2]]);
+      out[c * r + q] = val;
+    }
+  }
+}
+
+}  // namespace
+
+size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem) {
+  size_t b = 8 * (2 * (size_t)nmax + 2 * (size_t)mmax + 3 * MAX_M_AXIS_1D + 32 + 8);
+  b += 4 * (32 + 8 + (size_t)nmax + (nmax & 1));
+  b = (b + 15) & ~size_t(15);
+  if (panel_in_smem) b += 8 * (size_t)nmax * mmax;
+  return b;
+}
+
+void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s) {
+  if (a.dim == 1) {
+    SMASH_CUDA(cudaFuncSetAttribute(k_compress<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_compress<1><<<grid, COMPRESS_THREADS, smem, s>>>(a);
+  } else if (a.dim == 2) {
+    SMASH_CUDA(cudaFuncSetAttribute(k_compress<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_compress<2><<<grid, COMPRESS_THREADS, smem, s>>>(a);
+  } else {
+    SMASH_CUDA(cudaFuncSetAttribute(k_compress<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_compress<3><<<grid, COMPRESS_THREADS, smem, s>>>(a);
+  }
+  SMASH_CUDA(cudaGetLastError());
+}
+
+void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
+                         int r, const double* pts_soa, int64_t n, double* out, int* err,
+                         cudaStream_t s) {
+  (void)err;
+  double l[3] = {0, 0, 0}, h[3] = {0, 0, 0};
+  for (int a = 0; a < dim; ++a) { l[a] = plo[a]; h[a] = phi[a]; }
+  unsigned g = cdiv(std::max<int64_t>(n, 1), 128);
+  if (dim == 1) k_basis_single<1><<<g, 128, 0, s>>>(tab, r, pts_soa, n, l[0], l[1], l[2], h[0], h[1], h[2], out);
+  if (dim == 2) k_basis_single<2><<<g, 128, 0, s>>>(tab, r, pts_soa, n, l[0], l[1], l[2], h[0], h[1], h[2], out);
+  if (dim == 3) k_basis_single<3><<<g, 128, 0, s>>>(tab, r, pts_soa, n, l[0], l[1], l[2], h[0], h[1], h[2], out);
+  SMASH_CUDA(cudaGetLastError());
+}
+
+}  // namespace smash

@@ -1,0 +1,75 @@
+// K3 + K4: batched Chebyshev/Lagrange basis + strong rank-revealing QR
+// (see compress.cu).
+#pragma once
+
+#include "smash_impl.cuh"
+
+namespace smash {
+
+constexpr int COMPRESS_THREADS = 256;
+constexpr int MAX_M_AXIS_1D = 128;  // 1-D: r <= 128 (numpy pairwise block, one level)
+constexpr int MAX_M_AXIS_ND = 16;   // 2-D/3-D: nodes per axis
+
+struct BasisTables {
+  // Chebyshev cos((2k+1)pi/2m) and barycentric weights (-1)^k sin(...) for the
+  // per-axis node count m, computed on the host with libm (== numpy's values).
+  const double* cosv = nullptr;
+  const double* wv = nullptr;
+  const int* order = nullptr;  // [r][3] tensor indices in (degree, i, j, k) order
+  int m = 0;                   // nodes per axis
+};
+
+struct CompressArgs {
+  int lb = 0, le = 0;  // BFS node range of the level
+  int dim = 1, r = 0;
+  int side = 0;
+  // tree
+  const int* nchild = nullptr;
+  const int* child_first = nullptr;
+  const int* pt_a = nullptr;   // leaf point range start (tree order) for this side
+  const double* lo = nullptr;  // node boxes [n][dim]
+  const double* hi = nullptr;
+  double half_pad = 0;         // pad / 2 (hss.py:39-45, 221-222)
+  double pad = 0;
+  // ibar sources
+  const double* P = nullptr;   // tree-ordered points, SoA, stride P_stride
+  int64_t P_stride = 0;
+  const double* Sk = nullptr;  // compact skeleton points of the previous level, SoA
+  int64_t S_stride = 0;
+  const int* Slab = nullptr;   // compact skeleton labels
+  const int* skel_off = nullptr;  // compact offset per BFS node
+  const int* nib = nullptr;       // |ibar| per node
+  const int64_t* ib_off = nullptr;
+  const int64_t* g_off = nullptr;
+  int64_t ib_level_base = 0;      // ib_off of the level's first node
+  // HSS: extra panel rows from the truncated SVD (hss.py:286-287)
+  const int* keep = nullptr;
+  const int64_t* sv_off = nullptr;
+  const double* sv = nullptr;     // S: (nib x keep) row-major per node
+  BasisTables tab;
+  double s_bound = 2.0, rtol = 1e-14;
+  // outputs
+  int* rank = nullptr;
+  int* perm = nullptr;
+  double* G = nullptr;
+  int* tmp_lab = nullptr;     // level-local, at ib_off - ib_level_base
+  double* tmp_pts = nullptr;  // SoA [dim][level ib total]
+  int64_t tmp_stride = 0;
+  int* err = nullptr;
+  unsigned long long* swaps = nullptr;
+  // panel storage
+  int nmax = 0, mmax = 0;
+  int smem_panel = 1;
+  double* gws = nullptr;  // global workspace, per block mmax * nmax
+  // single-call mode: C given explicitly (nrows x ncols row-major) instead of a basis
+  const double* Cexp = nullptr;
+  int C_cols = 0;
+};
+
+size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
+void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s);
+void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
+                         int r, const double* pts_soa, int64_t n, double* out, int* err,
+                         cudaStream_t s);
+
+}  // namespace smash

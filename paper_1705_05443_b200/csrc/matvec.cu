@@ -1,0 +1,418 @@
+// K6-K10: the H^2 / HSS matvec -- replaces smash.apply.matvec_nodewise
+// (smash/apply.py:34-80).
+//
+// Phases (all coefficient vectors are (count, nrhs) row-major, nrhs processed
+// in chunks of RC <= 16 columns kept in registers):
+//   K10 gather   qt = q[perm_col]                               (apply.py:39)
+//   K6  upward   qhat_v = X_v^T ibar-vector, level L..2         (apply.py:42-53)
+//   K7  coupling zhat_i = sum_{j in L(i)} K(S_i, S_j) qhat_j     (apply.py:55-58)
+//   K8  downward zhat_children += X_v zhat_v, level 2..L-1      (apply.py:60-72)
+//   K9  leaves   z[perm_row] = X_v zhat_v + sum_{j in Lm(v)} K(P_v, P_j) qt_j
+//                                                              (apply.py:66-80)
+// X_v = P [I; G] is applied implicitly from (perm, G) (lowrank.py:224-229).
+// The coupling and nearfield blocks are generated on the fly in registers
+// (never stored): one CTA per target node, lanes = target points, warps split
+// the source list, sources staged per warp in shared memory; the four warps'
+// partial sums are reduced in a fixed order (deterministic).
+#include "kernels.cuh"
+#include "smash_impl.cuh"
+
+namespace smash {
+
+namespace {
+
+constexpr int P2P_WARPS = 4;
+constexpr int P2P_THREADS = 32 * P2P_WARPS;
+
+__global__ void k_gather_rows(const double* q, int64_t ldq, const int* perm, int64_t n, int rc,
+                              int64_t c0, double* qt, int64_t ldt) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * rc) return;
+  int64_t p = e / rc;
+  int r = (int)(e % rc);
+  qt[p * ldt + r] = q[(int64_t)perm[p] * ldq + c0 + r];
+}
+
+struct Side {
+  const int* nib;
+  const int* rank;
+  const int64_t* ib_off;
+  const int64_t* g_off;
+  const int* skel_off;
+  const int* perm;
+  const double* G;
+  const double* skel_pts;
+  int64_t skel_stride;
+};
+
+// ---- K6 upward: qhat[v] = ivec[perm[:k]] + G^T ivec[perm[k:]]
+template <int RC>
+__global__ void k_upward(int lb, int le, Side cs, const int* nchild, const int* child_first,
+                         const int* col_a, const double* qt, double* qhat) {
+  extern __shared__ double sh[];
+  const int v = lb + blockIdx.x;
+  if (v >= le) return;
+  const int n = cs.nib[v], k = cs.rank[v];
+  if (k == 0) return;
+  const double* ivec = nchild[v] == 0 ? qt + (int64_t)col_a[v] * RC
+                                      : qhat + (int64_t)cs.skel_off[child_first[v]] * RC;
+  const int* perm = cs.perm + cs.ib_off[v];
+  double* iv = sh;  // permuted ivec: iv[c] = ivec[perm[c]]
+  for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
+    int c = e / RC, r = e % RC;
+    iv[e] = ivec[(int64_t)perm[c] * RC + r];
+  }
+  __syncthreads();
+  const double* G = cs.G + cs.g_off[v];
+  double* out = qhat + (int64_t)cs.skel_off[v] * RC;
+  const int nk = n - k;
+  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
+    int a = e / RC, r = e % RC;
+    double acc = iv[a * RC + r];
+    for (int b = 0; b < nk; ++b) acc = fma(G[(int64_t)b * k + a], iv[(k + b) * RC + r], acc);
+    out[(int64_t)a * RC + r] = acc;
+  }
+}
+
+// ---- K8 downward: zhat[children] += X_v zhat[v]
+template <int RC>
+__global__ void k_downward(int lb, int le, Side rs, const int* nchild, const int* child_first,
+                           double* zhat) {
+  extern __shared__ double sh[];
+  const int v = lb + blockIdx.x;
+  if (v >= le || nchild[v] == 0) return;
+  const int n = rs.nib[v], k = rs.rank[v];
+  if (k == 0 || n == 0) return;
+  double* zv = sh;                                  // k * RC
+  int* inv = reinterpret_cast<int*>(sh + k * RC);   // n
+  const int* perm = rs.perm + rs.ib_off[v];
+  const double* zsrc = zhat + (int64_t)rs.skel_off[v] * RC;
+  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) zv[e] = zsrc[e];
+  for (int c = threadIdx.x; c < n; c += blockDim.x) inv[perm[c]] = c;
+  __syncthreads();
+  const double* G = rs.G + rs.g_off[v];
+  double* dst = zhat + (int64_t)rs.skel_off[child_first[v]] * RC;
+  for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
+    int c = e / RC, r = e % RC;
+    int pos = inv[c];
+    double y;
+    if (pos < k) {
+      y = zv[pos * RC + r];
+    } else {
+      const double* g = G + (int64_t)(pos - k) * k;
+      y = 0.0;
+      for (int a = 0; a < k; ++a) y = fma(g[a], zv[a * RC + r], y);
+    }
+    dst[e] += y;
+  }
+}
+
+// ---- P2P core: accumulate sum_s K(x_t, y_s) w_s over one source set into acc
+template <int KER, int D, int RC>
+__device__ __forceinline__ void p2p_sources(const double* xt, const double* ys, int64_t ystride,
+                                            const double* w, int ns, double dx, double* acc,
+                                            double* stage, int lane) {
+  // stage: per-warp buffer of 32 * (D + RC) doubles
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int cnt = min(32, ns - s0);
+    __syncwarp();
+    if (lane < cnt) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) stage[a * 32 + lane] = ys[(int64_t)a * ystride + s0 + lane];
+#pragma unroll
+      for (int r = 0; r < RC; ++r) stage[(D + r) * 32 + lane] = w[(int64_t)(s0 + lane) * RC + r];
+    }
+    __syncwarp();
+    for (int s = 0; s < cnt; ++s) {
+      double y[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) y[a] = stage[a * 32 + s];
+      double kv = kval<KER, D>(xt, y, dx);
+#pragma unroll
+      for (int r = 0; r < RC; ++r) acc[r] = fma(kv, stage[(D + r) * 32 + s], acc[r]);
+    }
+  }
+}
+
+struct P2PArgs {
+  // targets
+  const double* tpts;  // SoA
+  int64_t tstride;
+  // sources
+  const double* spts;
+  int64_t sstride;
+  const double* w;  // source weights (count, RC)
+  // CSR
+  const int* ptr;
+  const int* src;
+  double dx;
+};
+
+// ---- K7 coupling: zhat[v] = sum_{j in L(v)} K(S_v, S_j) qhat_j (one CTA per target node)
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_coupling(int n_nodes, Side rs, Side cs,
+                                                          const int* Lptr, const int* Lsrc,
+                                                          const double* qhat, double* zhat,
+                                                          double dx) {
+  __shared__ double stage[P2P_WARPS][32 * (D + RC)];
+  __shared__ double red[P2P_WARPS][32 * RC];
+  const int v = blockIdx.x;
+  if (v >= n_nodes || v == 0) return;  // root has no factor / no coupling
+  const int k = rs.rank[v];
+  if (k == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p0 = Lptr[v], p1 = Lptr[v + 1];
+  const int to = rs.skel_off[v];
+  for (int t0 = 0; t0 < k; t0 += 32) {
+    const int t = t0 + lane;
+    double xt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[a] = t < k ? rs.skel_pts[(int64_t)a * rs.skel_stride + to + t] : 0.0;
+    double acc[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) acc[r] = 0.0;
+    for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
+      const int j = Lsrc[e];
+      const int so = cs.skel_off[j];
+      p2p_sources<KER, D, RC>(xt, cs.skel_pts + so, cs.skel_stride, qhat + (int64_t)so * RC,
+                              cs.rank[j], dx, acc, stage[wid], lane);
+    }
+#pragma unroll
+    for (int r = 0; r < RC; ++r) red[wid][r * 32 + lane] = acc[r];
+    __syncthreads();
+    if (wid == 0 && t < k) {
+#pragma unroll
+      for (int r = 0; r < RC; ++r) {
+        double s = red[0][r * 32 + lane];
+        for (int w = 1; w < P2P_WARPS; ++w) s += red[w][r * 32 + lane];
+        zhat[(int64_t)(to + t) * RC + r] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K9 leaves: z[perm_row[p]] = (X_v zhat_v)[p] + sum_{j in Lm(v)} K(x_p, y_s) qt_s
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_leaf(
+    int lb_unused, const int* leaves, int n_leaves, Side rs, const int* row_a, const int* row_b,
+    const int* col_a, const int* col_b, const double* pts_row, int64_t nrow, const double* pts_col,
+    int64_t ncol, const int* Lmptr, const int* Lmsrc, const double* qt, const double* zhat,
+    const int* perm_row, double* z, int64_t ldz, int64_t c0, double dx) {
+  extern __shared__ int inv[];  // leaf row count (<= nu0)
+  __shared__ double stage[P2P_WARPS][32 * (D + RC)];
+  __shared__ double red[P2P_WARPS][32 * RC];
+  (void)lb_unused;
+  const int li = blockIdx.x;
+  if (li >= n_leaves) return;
+  const int v = leaves[li];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ra = row_a[v], nr = row_b[v] - ra;
+  const bool has = v != 0;
+  const int k = has ? rs.rank[v] : 0;
+  const int* perm = has ? rs.perm + rs.ib_off[v] : nullptr;
+  if (has)
+    for (int c = threadIdx.x; c < nr; c += blockDim.x) inv[perm[c]] = c;
+  __syncthreads();
+  const int p0 = Lmptr[v], p1 = Lmptr[v + 1];
+  for (int t0 = 0; t0 < nr; t0 += 32) {
+    const int t = t0 + lane;
+    double xt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[a] = t < nr ? pts_row[(int64_t)a * nrow + ra + t] : 0.0;
+    double acc[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) acc[r] = 0.0;
+    for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
+      const int j = Lmsrc[e];
+      const int ca = col_a[j];
+      p2p_sources<KER, D, RC>(xt, pts_col + ca, ncol, qt + (int64_t)ca * RC, col_b[j] - ca, dx,
+                              acc, stage[wid], lane);
+    }
+#pragma unroll
+    for (int r = 0; r < RC; ++r) red[wid][r * 32 + lane] = acc[r];
+    __syncthreads();
+    if (wid == 0 && t < nr) {
+      double y[RC];
+#pragma unroll
+      for (int r = 0; r < RC; ++r) y[r] = 0.0;
+      if (k > 0) {
+        const double* zv = zhat + (int64_t)rs.skel_off[v] * RC;
+        const int pos = inv[t];
+        if (pos < k) {
+#pragma unroll
+          for (int r = 0; r < RC; ++r) y[r] = zv[pos * RC + r];
+        } else {
+          const double* g = rs.G + rs.g_off[v] + (int64_t)(pos - k) * k;
+          for (int a = 0; a < k; ++a) {
+            double ga = g[a];
+#pragma unroll
+            for (int r = 0; r < RC; ++r) y[r] = fma(ga, zv[a * RC + r], y[r]);
+          }
+        }
+      }
+      double* zo = z + (int64_t)perm_row[ra + t] * ldz + c0;
+#pragma unroll
+      for (int r = 0; r < RC; ++r) {
+        double s = red[0][r * 32 + lane];
+        for (int w = 1; w < P2P_WARPS; ++w) s += red[w][r * 32 + lane];
+        zo[r] = y[r] + s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_list_leaves(int n, const int* nchild, int* out, int* cnt) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n && nchild[v] == 0) out[atomicAdd(cnt, 1)] = v;
+}
+
+// exact block evaluation (kernel_block API)
+template <int KER, int D>
+__global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx,
+                        double* out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nx * ny) return;
+  int64_t i = e / ny, j = e % ny;
+  double x[D], y[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) { x[a] = X[i * D + a]; y[a] = Y[j * D + a]; }
+  out[e] = kval<KER, D>(x, y, dx);
+}
+
+Side side_of(const SideFactors& F) {
+  return Side{F.nib.p, F.rank.p, F.ib_off.p, F.g_off.p, F.skel_off.p, F.perm.p, F.G.p,
+              F.skel_pts.p, F.skel_stride};
+}
+
+template <int KER, int D, int RC>
+void run_chunk(MatrixImpl* m, const double* q, double* z, int64_t nrhs, int64_t c0,
+               cudaStream_t s, const int* leaves, int n_leaves, int max_nib) {
+  TreeImpl* t = m->tree;
+  const SideFactors& R = m->rowf;
+  const SideFactors& C = *m->colf;
+  Side rs = side_of(R), cs = side_of(C);
+  const int* perm_col = t->shared ? t->perm_row.p : t->perm_col.p;
+  const double* pts_col = t->shared ? t->pts_row.p : t->pts_col.p;
+  const int* col_a = t->shared ? t->row_a.p : t->col_a.p;
+  const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
+  // K10 gather
+  k_gather_rows<<<cdiv(t->ny * RC, 256), 256, 0, s>>>(q, nrhs, perm_col, t->ny, RC, c0, m->qt.p, RC);
+  // K6 upward
+  for (int l = t->n_levels; l >= 2; --l) {
+    int lb = t->level_begin(l), le = t->level_end(l);
+    size_t sm = (size_t)max_nib * RC * sizeof(double);
+    k_upward<RC><<<le - lb, 128, sm, s>>>(lb, le, cs, t->nchild.p, t->child_first.p, col_a,
+                                          m->qt.p, m->qhat.p);
+  }
+  // K7 coupling
+  k_coupling<KER, D, RC><<<t->n_nodes, P2P_THREADS, 0, s>>>(t->n_nodes, rs, cs, m->pl->L_ptr.p,
+                                                            m->pl->L_j.p, m->qhat.p, m->zhat.p,
+                                                            m->p.dx);
+  // K8 downward
+  for (int l = 2; l < t->n_levels; ++l) {
+    int lb = t->level_begin(l), le = t->level_end(l);
+    size_t sm = (size_t)max_nib * (RC * sizeof(double) + sizeof(int)) + 128 * RC * 8;
+    k_downward<RC><<<le - lb, 128, sm, s>>>(lb, le, rs, t->nchild.p, t->child_first.p, m->zhat.p);
+  }
+  // K9 leaves (+ K10 scatter)
+  size_t sm = (size_t)(t->nu0 + 1) * sizeof(int);
+  k_leaf<KER, D, RC><<<n_leaves, P2P_THREADS, sm, s>>>(
+      0, leaves, n_leaves, rs, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx, pts_col,
+      t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zhat.p, t->perm_row.p, z, nrhs, c0,
+      m->p.dx);
+}
+
+template <int KER, int D>
+void run_all(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s,
+             const int* leaves, int n_leaves, int max_nib) {
+  int64_t c0 = 0;
+  while (c0 < nrhs) {
+    int64_t left = nrhs - c0;
+    if (left >= 16) { run_chunk<KER, D, 16>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 16; }
+    else if (left >= 8) { run_chunk<KER, D, 8>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 8; }
+    else if (left >= 4) { run_chunk<KER, D, 4>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 4; }
+    else if (left >= 2) { run_chunk<KER, D, 2>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 2; }
+    else { run_chunk<KER, D, 1>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 1; }
+  }
+}
+
+}  // namespace
+
+struct MatvecPlan {
+  DBuf<int> leaves;
+  int n_leaves = 0;
+  int max_nib = 0;
+};
+
+static std::map<const MatrixImpl*, std::unique_ptr<MatvecPlan>> g_plans;
+
+static MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
+  auto it = g_plans.find(m);
+  if (it != g_plans.end()) return it->second.get();
+  std::unique_ptr<MatvecPlan> P(new MatvecPlan());
+  TreeImpl* t = m->tree;
+  DBuf<int> cnt;
+  cnt.alloc(1, s);
+  cnt.zero(s);
+  P->leaves.alloc(t->n_nodes, s);
+  k_list_leaves<<<cdiv(t->n_nodes, 128), 128, 0, s>>>(t->n_nodes, t->nchild.p, P->leaves.p, cnt.p);
+  d2h(&P->n_leaves, cnt.p, 1, s);
+  // max |ibar| over both sides (host copy of nib)
+  std::vector<int> nib(t->n_nodes);
+  d2h(nib.data(), m->rowf.nib.p, t->n_nodes, s);
+  sync(s);
+  int mx = 1;
+  for (int x : nib) mx = std::max(mx, x);
+  if (m->colf != &m->rowf) {
+    d2h(nib.data(), m->colf->nib.p, t->n_nodes, s);
+    sync(s);
+    for (int x : nib) mx = std::max(mx, x);
+  }
+  P->max_nib = mx;
+  MatvecPlan* out = P.get();
+  g_plans[m] = std::move(P);
+  return out;
+}
+
+void matvec_release_plan(const MatrixImpl* m) { g_plans.erase(m); }
+
+void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s) {
+  SMASH_CHECK(nrhs >= 1, SMASH_ERR_INVALID, "nrhs must be positive");
+  TreeImpl* t = m->tree;
+  MatvecPlan* P = plan_of(m, s);
+  const int rc_max = (int)std::min<int64_t>(nrhs, 16);
+  if (m->ws_nrhs < rc_max) {
+    m->qt.alloc((size_t)t->ny * 16, s);
+    m->qhat.alloc((size_t)std::max<int64_t>(m->colf->skel_total, 1) * 16, s);
+    m->zhat.alloc((size_t)std::max<int64_t>(m->rowf.skel_total, 1) * 16, s);
+    m->ws_nrhs = 16;
+  }
+  // shared-memory needs of the upward/downward kernels
+  size_t need = (size_t)P->max_nib * (16 * sizeof(double) + sizeof(int)) + 128 * 16 * 8;
+  static bool attr_set = false;
+  (void)attr_set;
+  dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
+    auto setattr = [&](auto kern) {
+      SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+    };
+    setattr(k_upward<1>); setattr(k_upward<2>); setattr(k_upward<4>); setattr(k_upward<8>);
+    setattr(k_upward<16>);
+    setattr(k_downward<1>); setattr(k_downward<2>); setattr(k_downward<4>); setattr(k_downward<8>);
+    setattr(k_downward<16>);
+    run_all<KER, D>(m, q, z, nrhs, s, P->leaves.p, P->n_leaves, P->max_nib);
+  });
+  SMASH_CUDA(cudaGetLastError());
+}
+
+void kernel_block(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
+                  int64_t ny, double* out, cudaStream_t s) {
+  if (nx * ny == 0) return;
+  dispatch_kernel_dim(kernel, dim, [&]<int KER, int D>() {
+    k_block<KER, D><<<cdiv(nx * ny, 256), 256, 0, s>>>(X, nx, Y, ny, dx, out);
+  });
+  SMASH_CUDA(cudaGetLastError());
+}
+
+}  // namespace smash

@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference-generated
+golden fixtures and the CPU oracle.
+
+Bars (SURVEY.md 8(c) parity rules): tree arrays, pair sets, nearfield sets and
+ordered skeletons bit-exact; matvec within 1e-10 relative per RHS column; the
+error against the exact product no worse than 1.1x the reference's + 1e-12.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, unflatten
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_names()
+
+
+@pytest.fixture(scope="module")
+def smash_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1705_05443_b200 as sg
+    return sg
+
+
+_TREES = {}
+_MATS = {}
+
+
+def gpu_tree(sg, golden, name):
+    if name not in _TREES:
+        g = golden(name)
+        m = g["meta"]
+        X = sg.PointSet(g["X"])
+        Y = None if g["Y"] is g["X"] else sg.PointSet(g["Y"], role="col")
+        _TREES[name] = sg.build_tree(X, Y, nu0=m["nu0"], mode=m["mode"], tau=m["tau"])
+    return _TREES[name]
+
+
+def gpu_matrix(sg, golden, name):
+    if name not in _MATS:
+        g = golden(name)
+        m = g["meta"]
+        tree = gpu_tree(sg, golden, name)
+        spec = sg.KernelSpec(m["kernel"], dx=None if m["kernel"] == "exp" else 0.0)
+        params = sg.BuildParams(r=m["r"], tau=m["tau"], eps_svd=m["eps_svd"], s=2.0, basis="interp",
+                                rtol=m["rtol"])
+        build = sg.build_h2 if m["structure"] == "h2" else sg.build_hss
+        _MATS[name] = build(tree, spec, None, None, params)
+    return _MATS[name]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_tree_bitexact(smash_gpu, golden, name):
+    g = golden(name)
+    A = gpu_tree(smash_gpu, golden, name).arrays()
+    for k in ("level", "parent", "child_ptr", "child_idx", "row_start", "row_stop", "col_start",
+              "col_stop", "perm_row", "perm_col"):
+        assert np.array_equal(A[k], g[k]), k
+    assert np.array_equal(A["lo"], g["lo"]) and np.array_equal(A["hi"], g["hi"])
+    assert np.array_equal(A["points_row"], g["X"][g["perm_row"]])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pair_sets_bitexact(smash_gpu, golden, name):
+    g = golden(name)
+    m = g["meta"]
+    tree = gpu_tree(smash_gpu, golden, name)
+    L, Lm = smash_gpu.leaf_sets(tree, m["tau"], m["structure"])
+    assert np.array_equal(np.array(L, np.int64).reshape(-1, 2), g["L"])
+    assert np.array_equal(np.array(Lm, np.int64).reshape(-1, 2), g["Lm"])
+    if m["structure"] == "hss":
+        for i in range(len(g["level"])):
+            assert smash_gpu.nearfield_set(tree, i, m["tau"]) == unflatten(g["near_ptr"], g["near"], i).tolist()
+
+
+def _h2_or_skip(golden, name):
+    if golden(name)["meta"]["structure"] != "h2":
+        pytest.skip("HSS construction lands with the batched SVD kernel")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_skeletons_bitexact(smash_gpu, golden, name):
+    _h2_or_skip(golden, name)
+    g = golden(name)
+    M = gpu_matrix(smash_gpu, golden, name)
+    mism = []
+    for side, fac in (("row", M.rowfac), ("col", M.colfac)):
+        has = g["has_%s" % side]
+        assert sorted(fac) == [int(i) for i in np.nonzero(has)[0]]
+        for i in fac:
+            ref = unflatten(g["skel_%s_ptr" % side], g["skel_%s" % side], i)
+            if not np.array_equal(fac[i].skel, ref):
+                mism.append((side, i, fac[i].skel.size, ref.size))
+    assert not mism, "skeleton mismatches (side, node, k_gpu, k_ref): %s" % mism[:10]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_transfer_G(smash_gpu, golden, name):
+    _h2_or_skip(golden, name)
+    g = golden(name)
+    if "G_row" not in g:
+        pytest.skip("fixture stores no G")
+    M = gpu_matrix(smash_gpu, golden, name)
+    for i, f in M.rowfac.items():
+        Gr = unflatten(g["G_row_ptr"], g["G_row"], i)
+        pr = unflatten(g["fperm_row_ptr"], g["fperm_row"], i)
+        k = f.rank
+        Xg = f.expand()
+        Xr = np.zeros_like(Xg)
+        Xr[pr[:k]] = np.eye(k)
+        if k < pr.size:
+            Xr[pr[k:]] = Gr.reshape(pr.size - k, k)
+        # conditioning-aware rule (SURVEY.md 8(c) rule 3), first clause
+        err = np.linalg.norm(Xg - Xr) / max(np.linalg.norm(Xr), 1e-300)
+        assert err <= 1e-8, (i, err)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_matvec_vs_reference(smash_gpu, golden, name):
+    _h2_or_skip(golden, name)
+    g = golden(name)
+    M = gpu_matrix(smash_gpu, golden, name)
+    z = smash_gpu.matvec_nodewise(M, g["q"])
+    ref = g["z"]
+    for c in range(ref.shape[1]):
+        rel = np.linalg.norm(z[:, c] - ref[:, c]) / np.linalg.norm(ref[:, c])
+        assert rel <= 1e-10, (c, rel)
+    # vs exact on the sampled rows: no worse than the reference
+    rows = g["exact_rows"]
+    ze = g["z_exact_rows"]
+    e_gpu = np.linalg.norm(z[rows] - ze) / np.linalg.norm(ze)
+    e_ref = np.linalg.norm(ref[rows] - ze) / np.linalg.norm(ze)
+    assert e_gpu <= 1.1 * e_ref + 1e-12
