@@ -127,6 +127,11 @@ int smash_matrix_stats(smash_matrix_t m, int64_t* swaps_row, int64_t* swaps_col)
 /* ---- matvec: replaces smash.apply.matvec_nodewise (smash/apply.py:34-80) ----
  * q: (n_col, nrhs) row-major device, z: (n_row, nrhs) row-major device; caller order. */
 int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
+/* Matvec phase timing (CUDA events on the launch stream; synchronises each matvec while on).
+ * Returns the accumulated per-phase milliseconds since the last reset
+ * [gather, upward, coupling, downward, leaves] and the number of kernel launches; then
+ * enable = 1 turns profiling on and resets, 0 turns it off and resets, -1 leaves it as is. */
+int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int64_t* launches);
 int smash_matrix_free(smash_matrix_t m);
 
 /* ---- exact kernel entries: replaces smash.kernel.kernel_block (smash/kernel.py:278-310)

@@ -644,9 +644,17 @@ def build_hss(tree: OTree, kernel: str, r: int, tau: float, eps_svd: float, s: f
 # ---------------------------------------------------------------------------
 
 
-def matvec(M: OMatrix, q: np.ndarray) -> np.ndarray:
+def matvec(M: OMatrix, q: np.ndarray, cache: dict = None) -> np.ndarray:
     """Upward sweep, skeleton couplings, downward sweep, dense nearfield
-    (apply.py:34-80).  Blocks are evaluated on the fly (use_cache=False)."""
+    (apply.py:34-80).  Blocks are evaluated on the fly, or kept in ``cache``
+    across calls like the reference's use_cache=True (hss.py:138-162)."""
+    def block(key, fn):
+        if cache is None:
+            return fn()
+        b = cache.get(key)
+        if b is None:
+            b = cache[key] = fn()
+        return b
     tr = M.tree
     q = np.asarray(q, dtype=np.float64)
     single = q.ndim == 1
@@ -666,7 +674,7 @@ def matvec(M: OMatrix, q: np.ndarray) -> np.ndarray:
             qhat[i] = M.colfac[i].expand().T @ v
     zhat = {}
     for i, j in M.pairs_L:
-        blk = kernel_block(M.kernel, Xr[M.skel_row[i]], Xc[M.skel_col[j]], M.dx)
+        blk = block(("B", i, j), lambda: kernel_block(M.kernel, Xr[M.skel_row[i]], Xc[M.skel_col[j]], M.dx))
         e = blk @ qhat[j]
         zhat[i] = zhat[i] + e if i in zhat else e
     zt = np.zeros((tr.perm_row.size, nr))
@@ -685,7 +693,8 @@ def matvec(M: OMatrix, q: np.ndarray) -> np.ndarray:
                     zhat[c] = zhat[c] + y[off:off + k] if c in zhat else y[off:off + k]
                     off += k
     for i, j in M.pairs_Lm:
-        blk = kernel_block(M.kernel, Xr[tr.row_start[i]:tr.row_stop[i]], Xc[tr.col_start[j]:tr.col_stop[j]], M.dx)
+        blk = block(("NF", i, j), lambda: kernel_block(
+            M.kernel, Xr[tr.row_start[i]:tr.row_stop[i]], Xc[tr.col_start[j]:tr.col_stop[j]], M.dx))
         zt[tr.row_start[i]:tr.row_stop[i]] += blk @ qt[tr.col_start[j]:tr.col_stop[j]]
     z = np.empty_like(zt)
     z[tr.perm_row] = zt

@@ -32,12 +32,21 @@ def matvec_nodewise(M, q):
     if q.shape[0] != M.n_col:
         raise ValueError("vector length %d does not match matrix (%d)" % (q.shape[0], M.n_col))
     single = q.ndim == 1
-    Q = _lib.to_device(q)
+    pinned = is_torch and not q.is_cuda and q.is_pinned()
+    if pinned:  # host-pinned round trip: async copies on the current stream
+        Q = q.to(device="cuda", dtype=torch.float64, non_blocking=True)
+    else:
+        Q = _lib.to_device(q)
     if single:
         Q = Q.reshape(-1, 1)
     Z = matvec_device(M, Q)
     if single:
         Z = Z[:, 0]
+    if pinned:
+        out = torch.empty(Z.shape, dtype=torch.float64, pin_memory=True)
+        out.copy_(Z, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
     if is_torch:
         return Z.to(q.device)
     return Z.cpu().numpy()

@@ -22,28 +22,55 @@ __all__ = ["PointSet", "Box", "TreeNode", "ClusterTree", "build_tree", "well_sep
            "leaf_sets", "nearfield_set"]
 
 
-@dataclass
 class PointSet:
-    """(n, d) float64 coordinates plus a role tag (cluster.py:27-45)."""
+    """(n, d) float64 coordinates plus a role tag (cluster.py:27-45).
 
-    coords: np.ndarray
-    role: str = "row"
+    ``coords`` may be a numpy array or a torch tensor; a CUDA tensor stays on the
+    device (the tree build reads it in place) and is copied to the host only if
+    ``.coords`` is accessed."""
 
-    def __post_init__(self):
-        c = self.coords
-        if hasattr(c, "detach"):  # torch tensor
-            c = c.detach().cpu().numpy()
-        self.coords = np.atleast_2d(np.asarray(c, dtype=np.float64))
-        if self.coords.ndim != 2:
-            raise ValueError("coords must be a 2-d array")
+    def __init__(self, coords, role: str = "row"):
+        self.role = role
+        self._dev = None
+        self._coords = None
+        if hasattr(coords, "detach") and getattr(coords, "is_cuda", False):
+            import torch
+            t = coords.detach()
+            if t.dim() == 1:
+                t = t.reshape(1, -1)
+            if t.dim() != 2:
+                raise ValueError("coords must be a 2-d array")
+            self._dev = t.to(torch.float64).contiguous()
+        else:
+            if hasattr(coords, "detach"):
+                coords = coords.detach().cpu().numpy()
+            c = np.atleast_2d(np.asarray(coords, dtype=np.float64))
+            if c.ndim != 2:
+                raise ValueError("coords must be a 2-d array")
+            self._coords = c
+
+    @property
+    def coords(self) -> np.ndarray:
+        if self._coords is None:
+            self._coords = self._dev.cpu().numpy()
+        return self._coords
+
+    @property
+    def shape(self):
+        return tuple(self._dev.shape) if self._dev is not None else self._coords.shape
 
     @property
     def n(self) -> int:
-        return self.coords.shape[0]
+        return self.shape[0]
 
     @property
     def dim(self) -> int:
-        return self.coords.shape[1]
+        return self.shape[1]
+
+    def device_tensor(self):
+        if self._dev is None:
+            self._dev = _lib.to_device(self._coords)
+        return self._dev
 
 
 def _fma(a: float, b: float, c: float) -> float:
@@ -301,22 +328,21 @@ def build_tree(points_row: PointSet, points_col: PointSet = None, nu0: int = 50,
         raise ValueError("mode must be 'binary' or '2d'")
     if nu0 < 1:
         raise ValueError("nu0 must be positive")
-    X = points_row.coords
-    if X.shape[0] == 0:
+    nx, dim = points_row.shape
+    if nx == 0:
         raise ValueError("row point set is empty")
     shared = points_col is None or points_col is points_row
-    Y = X if shared else points_col.coords
-    if X.shape[1] != Y.shape[1]:
+    ny = nx if shared else points_col.shape[0]
+    if not shared and points_col.shape[1] != dim:
         raise ValueError("row/column point dimensions differ")
-    if not 1 <= X.shape[1] <= 3:
+    if not 1 <= dim <= 3:
         raise ValueError("points must have 1, 2 or 3 coordinates")
     lib = _lib.load()
-    dX = _lib.to_device(X)
-    dY = None if shared else _lib.to_device(Y)
+    dX = points_row.device_tensor()
+    dY = None if shared else points_col.device_tensor()
     h = ctypes.c_void_p()
-    _lib.check(lib.smash_tree_build(_lib.ptr(dX), X.shape[0], None if shared else _lib.ptr(dY),
-                                    Y.shape[0], X.shape[1], nu0, _lib.MODE[mode], _lib.stream_ptr(),
-                                    ctypes.byref(h)))
+    _lib.check(lib.smash_tree_build(_lib.ptr(dX), nx, None if shared else _lib.ptr(dY), ny, dim,
+                                    nu0, _lib.MODE[mode], _lib.stream_ptr(), ctypes.byref(h)))
     return ClusterTree(h, mode, nu0, tau)
 
 

@@ -186,6 +186,13 @@ int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, voi
   });
 }
 
+int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int64_t* launches) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
+    smash::matvec_profile(m->impl, enable, phase_ms, launches);
+  });
+}
+
 int smash_matrix_free(smash_matrix_t m) {
   return guarded([&] {
     if (!m) return;

@@ -105,6 +105,21 @@ inline void sync(cudaStream_t s) { SMASH_CUDA(cudaStreamSynchronize(s)); }
 
 inline unsigned cdiv(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
+// Keep freed stream-ordered allocations in the device pool (the default release
+// threshold of 0 hands memory back to the driver at every synchronisation,
+// which turns each per-level cudaMallocAsync into a real allocation).
+inline void init_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  SMASH_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  SMASH_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ULL;
+  SMASH_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = true;
+}
+
 // ---------------------------------------------------------------------------
 // exact geometry (smash/cluster.py:64-85)
 // ---------------------------------------------------------------------------

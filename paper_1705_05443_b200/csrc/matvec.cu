@@ -45,10 +45,19 @@ struct Side {
   int64_t skel_stride;
 };
 
+// Tile of G rows staged in shared memory (TB rows, <= 4096 doubles).
+__device__ __forceinline__ int g_tile_rows(int ks) { return max(1, min(64, 4096 / ks)); }
+
+constexpr int XFER_THREADS = 256;
+constexpr int XFER_MAXO = 8;  // outputs per thread in the upward kernel (k * RC <= 2048)
+
 // ---- K6 upward: qhat[v] = ivec[perm[:k]] + G^T ivec[perm[k:]]
+// One CTA per node: the permuted ibar-vector and row tiles of G are staged in
+// shared memory with coalesced loads; each thread owns <= 8 (a, r) outputs.
 template <int RC>
-__global__ void k_upward(int lb, int le, Side cs, const int* nchild, const int* child_first,
-                         const int* col_a, const double* qt, double* qhat) {
+__global__ void __launch_bounds__(XFER_THREADS) k_upward(int lb, int le, Side cs, const int* nchild,
+                                                         const int* child_first, const int* col_a,
+                                                         const double* qt, double* qhat) {
   extern __shared__ double sh[];
   const int v = lb + blockIdx.x;
   if (v >= le) return;
@@ -57,53 +66,91 @@ __global__ void k_upward(int lb, int le, Side cs, const int* nchild, const int* 
   const double* ivec = nchild[v] == 0 ? qt + (int64_t)col_a[v] * RC
                                       : qhat + (int64_t)cs.skel_off[child_first[v]] * RC;
   const int* perm = cs.perm + cs.ib_off[v];
-  double* iv = sh;  // permuted ivec: iv[c] = ivec[perm[c]]
+  double* iv = sh;               // n * RC: iv[c] = ivec[perm[c]]
+  double* gs = sh + n * RC;      // TB * k
   for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
     int c = e / RC, r = e % RC;
     iv[e] = ivec[(int64_t)perm[c] * RC + r];
   }
   __syncthreads();
+  const int nout = k * RC;
+  double acc[XFER_MAXO];
+#pragma unroll
+  for (int j = 0; j < XFER_MAXO; ++j) {
+    int e = threadIdx.x + j * blockDim.x;
+    acc[j] = e < nout ? iv[e] : 0.0;
+  }
   const double* G = cs.G + cs.g_off[v];
-  double* out = qhat + (int64_t)cs.skel_off[v] * RC;
   const int nk = n - k;
-  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
-    int a = e / RC, r = e % RC;
-    double acc = iv[a * RC + r];
-    for (int b = 0; b < nk; ++b) acc = fma(G[(int64_t)b * k + a], iv[(k + b) * RC + r], acc);
-    out[(int64_t)a * RC + r] = acc;
+  const int TB = g_tile_rows(k);
+  for (int b0 = 0; b0 < nk; b0 += TB) {
+    const int tb = min(TB, nk - b0);
+    const double* src = G + (int64_t)b0 * k;
+    for (int e = threadIdx.x; e < tb * k; e += blockDim.x) gs[e] = src[e];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < XFER_MAXO; ++j) {
+      int e = threadIdx.x + j * blockDim.x;
+      if (e < nout) {
+        int a = e / RC, r = e % RC;
+        double t = acc[j];
+        const double* ivb = iv + (k + b0) * RC + r;
+        for (int bb = 0; bb < tb; ++bb) t = fma(gs[bb * k + a], ivb[bb * RC], t);
+        acc[j] = t;
+      }
+    }
+    __syncthreads();
+  }
+  double* out = qhat + (int64_t)cs.skel_off[v] * RC;
+#pragma unroll
+  for (int j = 0; j < XFER_MAXO; ++j) {
+    int e = threadIdx.x + j * blockDim.x;
+    if (e < nout) out[e] = acc[j];
   }
 }
 
 // ---- K8 downward: zhat[children] += X_v zhat[v]
+// Skeleton rows add zhat directly; the other rows are dot products of staged G
+// rows (odd row stride -> conflict-free) with zhat_v.
 template <int RC>
-__global__ void k_downward(int lb, int le, Side rs, const int* nchild, const int* child_first,
-                           double* zhat) {
+__global__ void __launch_bounds__(XFER_THREADS) k_downward(int lb, int le, Side rs, const int* nchild,
+                                                           const int* child_first, double* zhat) {
   extern __shared__ double sh[];
   const int v = lb + blockIdx.x;
   if (v >= le || nchild[v] == 0) return;
   const int n = rs.nib[v], k = rs.rank[v];
   if (k == 0 || n == 0) return;
-  double* zv = sh;                                  // k * RC
-  int* inv = reinterpret_cast<int*>(sh + k * RC);   // n
+  const int ks = k | 1;
+  double* zv = sh;           // k * RC
+  double* gs = sh + k * RC;  // TB * ks
   const int* perm = rs.perm + rs.ib_off[v];
   const double* zsrc = zhat + (int64_t)rs.skel_off[v] * RC;
-  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) zv[e] = zsrc[e];
-  for (int c = threadIdx.x; c < n; c += blockDim.x) inv[perm[c]] = c;
-  __syncthreads();
-  const double* G = rs.G + rs.g_off[v];
   double* dst = zhat + (int64_t)rs.skel_off[child_first[v]] * RC;
-  for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
-    int c = e / RC, r = e % RC;
-    int pos = inv[c];
-    double y;
-    if (pos < k) {
-      y = zv[pos * RC + r];
-    } else {
-      const double* g = G + (int64_t)(pos - k) * k;
-      y = 0.0;
-      for (int a = 0; a < k; ++a) y = fma(g[a], zv[a * RC + r], y);
+  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
+    double x = zsrc[e];
+    zv[e] = x;
+    int a = e / RC, r = e % RC;
+    dst[(int64_t)perm[a] * RC + r] += x;
+  }
+  const double* G = rs.G + rs.g_off[v];
+  const int nk = n - k;
+  const int TB = g_tile_rows(ks);
+  for (int b0 = 0; b0 < nk; b0 += TB) {
+    const int tb = min(TB, nk - b0);
+    const double* src = G + (int64_t)b0 * k;
+    __syncthreads();
+    for (int e = threadIdx.x; e < tb * k; e += blockDim.x) {
+      int bb = e / k, a = e % k;
+      gs[bb * ks + a] = src[e];
     }
-    dst[e] += y;
+    __syncthreads();
+    for (int e = threadIdx.x; e < tb * RC; e += blockDim.x) {
+      int bb = e / RC, r = e % RC;
+      const double* g = gs + bb * ks;
+      double y = 0.0;
+      for (int a = 0; a < k; ++a) y = fma(g[a], zv[a * RC + r], y);
+      dst[(int64_t)perm[k + b0 + bb] * RC + r] += y;
+    }
   }
 }
 
@@ -263,6 +310,217 @@ __global__ void __launch_bounds__(P2P_THREADS) k_leaf(
   }
 }
 
+// ---------------------------------------------------------------------------
+// DMMA path (nrhs chunk RC = 8 or 16): the coupling / nearfield block is a real
+// dense contraction Z(t, r) += sum_s K(x_t, y_s) W(s, r), so the K tile is
+// generated in registers directly in the A-fragment layout of
+// mma.sync.m8n8k4.f64 (DMMA) and multiplied by the weights' B fragments.
+// Per warp: all target tiles (8 rows each) x a quarter of the source list;
+// the four warps' C fragments are summed in shared memory in a fixed order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct SrcSet {
+  const double* pts;  // SoA coordinates of the set's first point
+  int64_t stride;
+  const double* w;    // weights (count, RC)
+  int n;
+};
+
+template <int RC>
+constexpr int mma_mtmax() { return RC == 16 ? 8 : 16; }
+
+template <int D, int RC>
+constexpr int mma_smem_doubles() {
+  return P2P_WARPS * mma_mtmax<RC>() * 8 * RC > P2P_WARPS * 32 * (D + RC)
+             ? P2P_WARPS * mma_mtmax<RC>() * 8 * RC
+             : P2P_WARPS * 32 * (D + RC);
+}
+
+// Accumulate the block's sum over the source sets [p0, p1) for targets
+// [t0, t0 + nt) (nt <= 8 * MTMAX) into red[warp][t][r] (shared).
+template <int KER, int D, int RC, typename SrcF>
+__device__ __forceinline__ void p2p_mma_chunk(const double* tx, int64_t tstride, int nt, int p0,
+                                              int p1, SrcF src_of, double dx, double* stage,
+                                              double* red) {
+  constexpr int MTMAX = mma_mtmax<RC>();
+  constexpr int NT = RC / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int MT = (nt + 7) >> 3;
+  double xt[MTMAX][D];
+  bool tv[MTMAX];
+#pragma unroll
+  for (int m = 0; m < MTMAX; ++m) {
+    const int t = m * 8 + g;
+    tv[m] = t < nt;
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[m][a] = tv[m] ? tx[(int64_t)a * tstride + t] : 0.0;
+  }
+  double c[MTMAX][NT][2];
+#pragma unroll
+  for (int m = 0; m < MTMAX; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) c[m][n][0] = c[m][n][1] = 0.0;
+  double* sc = stage;            // [D][32]
+  double* sw = stage + D * 32;   // [32][RC]
+  for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
+    const SrcSet S = src_of(e);
+    for (int s0 = 0; s0 < S.n; s0 += 32) {
+      const int cnt = min(32, S.n - s0);
+      __syncwarp();
+#pragma unroll
+      for (int a = 0; a < D; ++a) sc[a * 32 + lane] = lane < cnt ? S.pts[(int64_t)a * S.stride + s0 + lane] : 0.0;
+      for (int i = lane; i < 32 * RC; i += 32) {
+        const int si = i / RC;
+        sw[i] = si < cnt ? S.w[(int64_t)(s0 + si) * RC + (i % RC)] : 0.0;
+      }
+      __syncwarp();
+      for (int kk = 0; kk < cnt; kk += 4) {
+        const int si = kk + q;
+        const bool sv = si < cnt;
+        double ys[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + si];
+        double b[NT];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) b[n] = sw[si * RC + n * 8 + g];
+#pragma unroll
+        for (int m = 0; m < MTMAX; ++m) {
+          if (m < MT) {
+            const double av = (sv && tv[m]) ? kval<KER, D>(xt[m], ys, dx) : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av, b[n]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();  // red aliases the warps' staging buffers
+  double* rw = red + wid * (MTMAX * 8 * RC);
+#pragma unroll
+  for (int m = 0; m < MTMAX; ++m) {
+    if (m < MT) {
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int t = m * 8 + g, r = n * 8 + 2 * q;
+        rw[t * RC + r] = c[m][n][0];
+        rw[t * RC + r + 1] = c[m][n][1];
+      }
+    }
+  }
+}
+
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_coupling_mma(int n_nodes, Side rs, Side cs,
+                                                              const int* Lptr, const int* Lsrc,
+                                                              const double* qhat, double* zhat,
+                                                              double dx) {
+  constexpr int MTMAX = mma_mtmax<RC>();
+  __shared__ double buf[mma_smem_doubles<D, RC>()];  // per-warp staging, then the warp sums
+  double* red = buf;
+  const int v = blockIdx.x;
+  if (v >= n_nodes || v == 0) return;
+  const int k = rs.rank[v];
+  if (k == 0) return;
+  const int wid = threadIdx.x >> 5;
+  const int p0 = Lptr[v], p1 = Lptr[v + 1];
+  const int to = rs.skel_off[v];
+  auto src_of = [&](int e) {
+    const int j = Lsrc[e];
+    const int so = cs.skel_off[j];
+    return SrcSet{cs.skel_pts + so, cs.skel_stride, qhat + (int64_t)so * RC, cs.rank[j]};
+  };
+  for (int t0 = 0; t0 < k; t0 += MTMAX * 8) {
+    const int nt = min(MTMAX * 8, k - t0);
+    __syncthreads();
+    p2p_mma_chunk<KER, D, RC>(rs.skel_pts + to + t0, rs.skel_stride, nt, p0, p1, src_of, dx,
+                              buf + wid * 32 * (D + RC), red);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * RC; e += blockDim.x) {
+      double sum = 0.0;
+      if (p1 > p0) {
+        sum = red[e];
+        for (int w = 1; w < P2P_WARPS; ++w) sum += red[w * (MTMAX * 8 * RC) + e];
+      }
+      zhat[(int64_t)(to + t0) * RC + e] = sum;
+    }
+  }
+}
+
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_leaf_mma(
+    const int* leaves, int n_leaves, Side rs, const int* row_a, const int* row_b, const int* col_a,
+    const int* col_b, const double* pts_row, int64_t nrow, const double* pts_col, int64_t ncol,
+    const int* Lmptr, const int* Lmsrc, const double* qt, const double* zhat, const int* perm_row,
+    double* z, int64_t ldz, int64_t c0, double dx) {
+  constexpr int MTMAX = mma_mtmax<RC>();
+  __shared__ double buf[mma_smem_doubles<D, RC>()];
+  double* red = buf;
+  extern __shared__ double dyn[];  // zhat_v (k * RC) then inv (nr ints)
+  const int li = blockIdx.x;
+  if (li >= n_leaves) return;
+  const int v = leaves[li];
+  const int wid = threadIdx.x >> 5;
+  const int ra = row_a[v], nr = row_b[v] - ra;
+  const bool has = v != 0;
+  const int k = has ? rs.rank[v] : 0;
+  double* zv = dyn;
+  int* inv = reinterpret_cast<int*>(dyn + k * RC);
+  if (has) {
+    const int* perm = rs.perm + rs.ib_off[v];
+    for (int c = threadIdx.x; c < nr; c += blockDim.x) inv[perm[c]] = c;
+    const double* zsrc = zhat + (int64_t)rs.skel_off[v] * RC;
+    for (int e = threadIdx.x; e < k * RC; e += blockDim.x) zv[e] = zsrc[e];
+  }
+  const int p0 = Lmptr[v], p1 = Lmptr[v + 1];
+  auto src_of = [&](int e) {
+    const int j = Lmsrc[e];
+    const int ca = col_a[j];
+    return SrcSet{pts_col + ca, ncol, qt + (int64_t)ca * RC, col_b[j] - ca};
+  };
+  const double* G = has ? rs.G + rs.g_off[v] : nullptr;
+  for (int t0 = 0; t0 < nr; t0 += MTMAX * 8) {
+    const int nt = min(MTMAX * 8, nr - t0);
+    __syncthreads();
+    p2p_mma_chunk<KER, D, RC>(pts_row + ra + t0, nrow, nt, p0, p1, src_of, dx,
+                              buf + wid * 32 * (D + RC), red);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * RC; e += blockDim.x) {
+      const int tl = e / RC, r = e % RC, t = t0 + tl;
+      double sum = 0.0;
+      if (p1 > p0) {
+        sum = red[e];
+        for (int w = 1; w < P2P_WARPS; ++w) sum += red[w * (MTMAX * 8 * RC) + e];
+      }
+      double y = 0.0;
+      if (k > 0) {
+        const int pos = inv[t];
+        if (pos < k) {
+          y = zv[pos * RC + r];
+        } else {
+          const double* gr = G + (int64_t)(pos - k) * k;
+          double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+          int a = 0;
+          for (; a + 3 < k; a += 4) {
+            y0 = fma(gr[a], zv[a * RC + r], y0);
+            y1 = fma(gr[a + 1], zv[(a + 1) * RC + r], y1);
+            y2 = fma(gr[a + 2], zv[(a + 2) * RC + r], y2);
+            y3 = fma(gr[a + 3], zv[(a + 3) * RC + r], y3);
+          }
+          for (; a < k; ++a) y0 = fma(gr[a], zv[a * RC + r], y0);
+          y = (y0 + y1) + (y2 + y3);
+        }
+      }
+      z[(int64_t)perm_row[ra + t] * ldz + c0 + r] = y + sum;
+    }
+  }
+}
+
 __global__ void k_list_leaves(int n, const int* nchild, int* out, int* cnt) {
   int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v < n && nchild[v] == 0) out[atomicAdd(cnt, 1)] = v;
@@ -288,7 +546,7 @@ Side side_of(const SideFactors& F) {
 
 template <int KER, int D, int RC>
 void run_chunk(MatrixImpl* m, const double* q, double* z, int64_t nrhs, int64_t c0,
-               cudaStream_t s, const int* leaves, int n_leaves, int max_nib) {
+               cudaStream_t s, const int* leaves, int n_leaves, int max_nib, int max_rank) {
   TreeImpl* t = m->tree;
   const SideFactors& R = m->rowf;
   const SideFactors& C = *m->colf;
@@ -297,44 +555,76 @@ void run_chunk(MatrixImpl* m, const double* q, double* z, int64_t nrhs, int64_t 
   const double* pts_col = t->shared ? t->pts_row.p : t->pts_col.p;
   const int* col_a = t->shared ? t->row_a.p : t->col_a.p;
   const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
+  auto mark = [&](int i) {
+    if (m->profile) SMASH_CUDA(cudaEventRecord(m->ev[i], s));
+  };
+  mark(0);
   // K10 gather
   k_gather_rows<<<cdiv(t->ny * RC, 256), 256, 0, s>>>(q, nrhs, perm_col, t->ny, RC, c0, m->qt.p, RC);
+  mark(1);
   // K6 upward
+  const size_t sm_up = ((size_t)max_nib * RC + 4096) * sizeof(double);
   for (int l = t->n_levels; l >= 2; --l) {
     int lb = t->level_begin(l), le = t->level_end(l);
-    size_t sm = (size_t)max_nib * RC * sizeof(double);
-    k_upward<RC><<<le - lb, 128, sm, s>>>(lb, le, cs, t->nchild.p, t->child_first.p, col_a,
-                                          m->qt.p, m->qhat.p);
+    k_upward<RC><<<le - lb, XFER_THREADS, sm_up, s>>>(lb, le, cs, t->nchild.p, t->child_first.p,
+                                                      col_a, m->qt.p, m->qhat.p);
   }
+  mark(2);
   // K7 coupling
-  k_coupling<KER, D, RC><<<t->n_nodes, P2P_THREADS, 0, s>>>(t->n_nodes, rs, cs, m->pl->L_ptr.p,
-                                                            m->pl->L_j.p, m->qhat.p, m->zhat.p,
-                                                            m->p.dx);
+  if constexpr (RC == 8 || RC == 16) {
+    k_coupling_mma<KER, D, RC><<<t->n_nodes, P2P_THREADS, 0, s>>>(
+        t->n_nodes, rs, cs, m->pl->L_ptr.p, m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx);
+  } else {
+    k_coupling<KER, D, RC><<<t->n_nodes, P2P_THREADS, 0, s>>>(t->n_nodes, rs, cs, m->pl->L_ptr.p,
+                                                              m->pl->L_j.p, m->qhat.p, m->zhat.p,
+                                                              m->p.dx);
+  }
+  mark(3);
   // K8 downward
+  const size_t sm_down = ((size_t)max_nib * RC + 4096 + 64) * sizeof(double);
   for (int l = 2; l < t->n_levels; ++l) {
     int lb = t->level_begin(l), le = t->level_end(l);
-    size_t sm = (size_t)max_nib * (RC * sizeof(double) + sizeof(int)) + 128 * RC * 8;
-    k_downward<RC><<<le - lb, 128, sm, s>>>(lb, le, rs, t->nchild.p, t->child_first.p, m->zhat.p);
+    k_downward<RC><<<le - lb, XFER_THREADS, sm_down, s>>>(lb, le, rs, t->nchild.p,
+                                                          t->child_first.p, m->zhat.p);
   }
+  mark(4);
   // K9 leaves (+ K10 scatter)
-  size_t sm = (size_t)(t->nu0 + 1) * sizeof(int);
-  k_leaf<KER, D, RC><<<n_leaves, P2P_THREADS, sm, s>>>(
-      0, leaves, n_leaves, rs, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx, pts_col,
-      t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zhat.p, t->perm_row.p, z, nrhs, c0,
-      m->p.dx);
+  if constexpr (RC == 8 || RC == 16) {
+    size_t smd = (size_t)max_rank * RC * sizeof(double) + (size_t)(t->nu0 + 1) * sizeof(int);
+    k_leaf_mma<KER, D, RC><<<n_leaves, P2P_THREADS, smd, s>>>(
+        leaves, n_leaves, rs, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx, pts_col,
+        t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zhat.p, t->perm_row.p, z, nrhs, c0,
+        m->p.dx);
+  } else {
+    size_t sm = (size_t)(t->nu0 + 1) * sizeof(int);
+    k_leaf<KER, D, RC><<<n_leaves, P2P_THREADS, sm, s>>>(
+        0, leaves, n_leaves, rs, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
+        pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zhat.p, t->perm_row.p, z, nrhs,
+        c0, m->p.dx);
+  }
+  mark(5);
+  m->launches += 3 + (t->n_levels - 1) + std::max(0, t->n_levels - 2);
+  if (m->profile) {
+    SMASH_CUDA(cudaEventSynchronize(m->ev[5]));
+    for (int i = 0; i < 5; ++i) {
+      float ms = 0;
+      SMASH_CUDA(cudaEventElapsedTime(&ms, m->ev[i], m->ev[i + 1]));
+      m->phase_ms[i] += ms;
+    }
+  }
 }
 
 template <int KER, int D>
 void run_all(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s,
-             const int* leaves, int n_leaves, int max_nib) {
+             const int* leaves, int n_leaves, int max_nib, int max_rank, int rc_cap) {
   int64_t c0 = 0;
   while (c0 < nrhs) {
-    int64_t left = nrhs - c0;
-    if (left >= 16) { run_chunk<KER, D, 16>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 16; }
-    else if (left >= 8) { run_chunk<KER, D, 8>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 8; }
-    else if (left >= 4) { run_chunk<KER, D, 4>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 4; }
-    else if (left >= 2) { run_chunk<KER, D, 2>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 2; }
-    else { run_chunk<KER, D, 1>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib); c0 += 1; }
+    int64_t left = std::min<int64_t>(nrhs - c0, rc_cap);
+    if (left >= 16) { run_chunk<KER, D, 16>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib, max_rank); c0 += 16; }
+    else if (left >= 8) { run_chunk<KER, D, 8>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib, max_rank); c0 += 8; }
+    else if (left >= 4) { run_chunk<KER, D, 4>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib, max_rank); c0 += 4; }
+    else if (left >= 2) { run_chunk<KER, D, 2>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib, max_rank); c0 += 2; }
+    else { run_chunk<KER, D, 1>(m, q, z, nrhs, c0, s, leaves, n_leaves, max_nib, max_rank); c0 += 1; }
   }
 }
 
@@ -344,6 +634,7 @@ struct MatvecPlan {
   DBuf<int> leaves;
   int n_leaves = 0;
   int max_nib = 0;
+  int max_rank = 0;
 };
 
 static std::map<const MatrixImpl*, std::unique_ptr<MatvecPlan>> g_plans;
@@ -365,12 +656,20 @@ static MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   sync(s);
   int mx = 1;
   for (int x : nib) mx = std::max(mx, x);
+  std::vector<int> rk(t->n_nodes);
+  d2h(rk.data(), m->rowf.rank.p, t->n_nodes, s);
+  sync(s);
+  int mr = 1;
+  for (int x : rk) mr = std::max(mr, x);
   if (m->colf != &m->rowf) {
     d2h(nib.data(), m->colf->nib.p, t->n_nodes, s);
+    d2h(rk.data(), m->colf->rank.p, t->n_nodes, s);
     sync(s);
     for (int x : nib) mx = std::max(mx, x);
+    for (int x : rk) mr = std::max(mr, x);
   }
   P->max_nib = mx;
+  P->max_rank = mr;
   MatvecPlan* out = P.get();
   g_plans[m] = std::move(P);
   return out;
@@ -390,7 +689,14 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
     m->ws_nrhs = 16;
   }
   // shared-memory needs of the upward/downward kernels
-  size_t need = (size_t)P->max_nib * (16 * sizeof(double) + sizeof(int)) + 128 * 16 * 8;
+  // largest nrhs chunk whose transfer-kernel shared memory and registers fit
+  int rc_cap = 16;
+  while (rc_cap > 1 && (((size_t)P->max_nib * rc_cap + 4096 + 64) * sizeof(double) > 200 * 1024 ||
+                        P->max_rank * rc_cap > XFER_THREADS * XFER_MAXO))
+    rc_cap /= 2;
+  size_t need = ((size_t)P->max_nib * rc_cap + 4096 + 64) * sizeof(double);
+  SMASH_CHECK(need <= 227 * 1024 && P->max_rank <= XFER_THREADS * XFER_MAXO, SMASH_ERR_INVALID,
+              "intermediate sets too large for the matvec");
   static bool attr_set = false;
   (void)attr_set;
   dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
@@ -401,9 +707,22 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
     setattr(k_upward<16>);
     setattr(k_downward<1>); setattr(k_downward<2>); setattr(k_downward<4>); setattr(k_downward<8>);
     setattr(k_downward<16>);
-    run_all<KER, D>(m, q, z, nrhs, s, P->leaves.p, P->n_leaves, P->max_nib);
+    run_all<KER, D>(m, q, z, nrhs, s, P->leaves.p, P->n_leaves, P->max_nib, P->max_rank, rc_cap);
   });
   SMASH_CUDA(cudaGetLastError());
+}
+
+void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launches) {
+  if (phase_ms)
+    for (int i = 0; i < 5; ++i) phase_ms[i] = m->phase_ms[i];
+  if (launches) *launches = m->launches;
+  if (enable >= 0) {
+    if (enable && !m->ev[0])
+      for (auto& e : m->ev) SMASH_CUDA(cudaEventCreate(&e));
+    m->profile = enable != 0;
+    for (double& x : m->phase_ms) x = 0;
+    m->launches = 0;
+  }
 }
 
 void kernel_block(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,

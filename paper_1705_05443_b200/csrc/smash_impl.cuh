@@ -98,6 +98,15 @@ struct MatrixImpl {
   // matvec workspaces
   DBuf<double> qt, qhat, zhat;
   int64_t ws_nrhs = 0;
+  // optional per-phase timing of the matvec (CUDA events on the launch stream)
+  bool profile = false;
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double phase_ms[5] = {0, 0, 0, 0, 0};  // gather, upward, coupling, downward, leaves
+  int64_t launches = 0;
+  ~MatrixImpl() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s);
@@ -105,6 +114,7 @@ void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t
                    int64_t* perm, int64_t* skel_ptr, int64_t* skel, int64_t* g_ptr, double* G,
                    cudaStream_t s);
 void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
+void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launches);
 
 void kernel_block(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
                   int64_t ny, double* out, cudaStream_t s);

@@ -331,6 +331,7 @@ TreeImpl* tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, i
   int64_t ntot = shared ? nx : nx + ny;
   SMASH_CHECK(ntot < (1LL << 30), SMASH_ERR_INVALID, "too many points for int32 indexing");
 
+  init_pool();
   std::unique_ptr<TreeImpl> T(new TreeImpl());
   T->dim = dim; T->mode = mode; T->nu0 = nu0; T->shared = shared;
   T->nx = nx; T->ny = ny; T->stream = s;
