@@ -197,67 +197,73 @@ int num_sms() {
 
 }  // namespace
 
-// Compress one side of the matrix, all levels.
-static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pad,
-                       cudaStream_t s) {
-  TreeImpl* t = M->tree;
-  SideFactors& F = side == 0 ? M->rowf : M->colf_own;
-  const int n = t->n_nodes, dim = t->dim, r = M->p.r;
-  const bool hss = M->p.structure == SMASH_STRUCT_HSS;
-  const int* pt_a = side == 0 ? t->row_a.p : t->col_a.p;
-  const int* pt_b = side == 0 ? t->row_b.p : t->col_b.p;
-  const double* P = side == 0 || t->shared ? t->pts_row.p : t->pts_col.p;
-  const int64_t Pn = side == 0 || t->shared ? t->nx : t->ny;
-
-  F.nib.alloc(n, s); F.rank.alloc(n, s); F.ib_off.alloc(n, s); F.g_off.alloc(n, s);
-  F.skel_off.alloc(n, s);
-  F.rank.zero(s); F.nib.zero(s); F.ib_off.zero(s); F.g_off.zero(s); F.skel_off.zero(s);
+// Level-synchronous compression state of one side (row or column factors).
+struct SideBuild {
+  MatrixImpl* M;
+  int side;
+  SideFactors* F;
+  const DevTables* tabs;
+  double pad;
+  cudaStream_t s;
+  const int* pt_a;
+  const int* pt_b;
+  const double* P;
+  int64_t Pn;
+  int64_t skel_cap = 0, skel_used = 0;
   DBuf<char> tmp;
-  DBuf<int64_t> kb;
-  kb.alloc(n + 1, s);
-  kb.zero(s);
-  const int root = 0;
-  // skeleton capacity: k_v <= min(rows, |points below v|); HSS rows are r + keep <= |ibar|
-  k_skel_bound<<<cdiv(n, 128), 128, 0, s>>>(n, root, pt_a, pt_b, hss ? (1 << 30) : r, kb.p);
-  DBuf<int64_t> kbs;
-  kbs.alloc(1, s);
-  cub_call([&](void* tp, size_t& b) { return cub::DeviceReduce::Sum(tp, b, kb.p, kbs.p, n, s); },
-           tmp, s);
-  int64_t skel_cap = 0;
-  d2h(&skel_cap, kbs.p, 1, s);
-  sync(s);
-  skel_cap = std::max<int64_t>(skel_cap, 1);
-  F.skel.alloc(skel_cap, s);
-  F.skel_pts.alloc((size_t)skel_cap * dim, s);
-  F.perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
-  F.G.alloc(std::max<int64_t>(Pn * 8, 1024), s);
-  F.level_skel_begin.assign(t->n_levels + 2, 0);
-
-  DBuf<int> err;
-  err.alloc(1, s);
-  err.zero(s);
+  DBuf<int> err, dmax;
   DBuf<unsigned long long> swaps;
-  swaps.alloc(1, s);
-  swaps.zero(s);
-  DBuf<int> dmax;
-  dmax.alloc(1, s);
-
-  const int smem_limit = max_sm_smem();
-  const int nsm = num_sms();
-  int64_t skel_used = 0;
   DBuf<double> gws;
-  NearSets* near = hss ? get_near(t, M->p.tau, s) : nullptr;
   SvdWorkspace svdws;
+  int smem_limit = 0, nsm = 0;
 
-  for (int l = t->n_levels; l >= 2; --l) {
+  void init() {
+    TreeImpl* t = M->tree;
+    const int n = t->n_nodes, dim = t->dim, r = M->p.r;
+    const bool hss = M->p.structure == SMASH_STRUCT_HSS;
+    const bool col = side == 1 && !t->shared;
+    pt_a = col ? t->col_a.p : t->row_a.p;
+    pt_b = col ? t->col_b.p : t->row_b.p;
+    P = col ? t->pts_col.p : t->pts_row.p;
+    Pn = col ? t->ny : t->nx;
+    F->nib.alloc(n, s); F->rank.alloc(n, s); F->ib_off.alloc(n, s); F->g_off.alloc(n, s);
+    F->skel_off.alloc(n, s);
+    F->rank.zero(s); F->nib.zero(s); F->ib_off.zero(s); F->g_off.zero(s); F->skel_off.zero(s);
+    // skeleton capacity: k_v <= min(rows, |points below v|); HSS rows r + keep are bounded by |ibar|
+    DBuf<int64_t> kb, kbs;
+    kb.alloc(n + 1, s);
+    kb.zero(s);
+    kbs.alloc(1, s);
+    k_skel_bound<<<cdiv(n, 128), 128, 0, s>>>(n, 0, pt_a, pt_b, hss ? (1 << 30) : r, kb.p);
+    cub_call([&](void* tp, size_t& b) { return cub::DeviceReduce::Sum(tp, b, kb.p, kbs.p, n, s); },
+             tmp, s);
+    d2h(&skel_cap, kbs.p, 1, s);
+    sync(s);
+    skel_cap = std::max<int64_t>(skel_cap, 1);
+    F->skel_stride = skel_cap;
+    F->skel.alloc(skel_cap, s);
+    F->skel_pts.alloc((size_t)skel_cap * dim, s);
+    F->perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
+    F->G.alloc(std::max<int64_t>(Pn * 8, 1024), s);
+    F->level_skel_begin.assign(t->n_levels + 2, 0);
+    err.alloc(1, s); err.zero(s);
+    swaps.alloc(1, s); swaps.zero(s);
+    dmax.alloc(1, s);
+    smem_limit = max_sm_smem();
+    nsm = num_sms();
+  }
+
+  void level(int l, NearSets* near) {
+    TreeImpl* t = M->tree;
+    const int dim = t->dim, r = M->p.r;
+    const bool hss = M->p.structure == SMASH_STRUCT_HSS;
     const int lb = t->level_begin(l), le = t->level_end(l), cnt = le - lb;
     DBuf<int64_t> ibc, gc, ibo, go;
     ibc.alloc(cnt + 1, s); gc.alloc(cnt + 1, s); ibo.alloc(cnt + 1, s); go.alloc(cnt + 1, s);
     SMASH_CUDA(cudaMemsetAsync(ibc.p + cnt, 0, 8, s));
     SMASH_CUDA(cudaMemsetAsync(gc.p + cnt, 0, 8, s));
-    // HSS: G capacity bound uses |ibar| (rows r + keep may exceed r)
     k_level_sizes<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a,
-                                                 pt_b, F.rank.p, F.nib.p, ibc.p, gc.p,
+                                                 pt_b, F->rank.p, F->nib.p, ibc.p, gc.p,
                                                  hss ? (1 << 30) : r);
     cub_call([&](void* tp, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(tp, b, ibc.p, ibo.p, cnt + 1, s);
@@ -266,7 +272,7 @@ static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pa
       return cub::DeviceScan::ExclusiveSum(tp, b, gc.p, go.p, cnt + 1, s);
     }, tmp, s);
     dmax.zero(s);
-    k_max_int<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(F.nib.p + lb, cnt, dmax.p);
+    k_max_int<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(F->nib.p + lb, cnt, dmax.p);
     int64_t tot[2];
     int nmax = 0;
     d2h(&tot[0], ibo.p + cnt, 1, s);
@@ -274,16 +280,14 @@ static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pa
     d2h(&nmax, dmax.p, 1, s);
     sync(s);
     const int64_t lvl_ib = tot[0], lvl_g = tot[1];
-    grow(F.perm, F.ib_total, F.ib_total + lvl_ib, s);
-    grow(F.G, F.g_total, F.g_total + lvl_g, s);
-    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, ibo.p, F.ib_total, F.ib_off.p);
-    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, go.p, F.g_total, F.g_off.p);
+    grow(F->perm, F->ib_total, F->ib_total + lvl_ib, s);
+    grow(F->G, F->g_total, F->g_total + lvl_g, s);
+    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, ibo.p, F->ib_total, F->ib_off.p);
+    k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, go.p, F->g_total, F->g_off.p);
 
     // ---- HSS nearfield SVD (hss.py:279-299)
     int max_keep = 0;
-    if (hss) {
-      max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s);
-    }
+    if (hss) max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s);
 
     DBuf<int> tmp_lab;
     DBuf<double> tmp_pts;
@@ -295,12 +299,12 @@ static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pa
     A.nchild = t->nchild.p; A.child_first = t->child_first.p; A.pt_a = pt_a;
     A.lo = t->lo.p; A.hi = t->hi.p; A.pad = pad; A.half_pad = pad / 2;
     A.P = P; A.P_stride = Pn;
-    A.Sk = F.skel_pts.p; A.S_stride = skel_cap; A.Slab = F.skel.p; A.skel_off = F.skel_off.p;
-    A.nib = F.nib.p; A.ib_off = F.ib_off.p; A.g_off = F.g_off.p; A.ib_level_base = F.ib_total;
+    A.Sk = F->skel_pts.p; A.S_stride = skel_cap; A.Slab = F->skel.p; A.skel_off = F->skel_off.p;
+    A.nib = F->nib.p; A.ib_off = F->ib_off.p; A.g_off = F->g_off.p; A.ib_level_base = F->ib_total;
     if (hss) { A.keep = svdws.keep.p; A.sv_off = svdws.sv_off.p; A.sv = svdws.sv.p; }
-    A.tab = tabs.view;
+    A.tab = tabs->view;
     A.s_bound = M->p.s; A.rtol = M->p.rtol;
-    A.rank = F.rank.p; A.perm = F.perm.p; A.G = F.G.p;
+    A.rank = F->rank.p; A.perm = F->perm.p; A.G = F->G.p;
     A.tmp_lab = tmp_lab.p; A.tmp_pts = tmp_pts.p; A.tmp_stride = std::max<int64_t>(lvl_ib, 1);
     A.err = err.p; A.swaps = swaps.p;
     A.nmax = std::max(nmax, 1);
@@ -327,7 +331,7 @@ static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pa
     DBuf<int> rc, ro;
     rc.alloc(cnt + 1, s); ro.alloc(cnt + 1, s);
     SMASH_CUDA(cudaMemsetAsync(rc.p + cnt, 0, 4, s));
-    k_rank_cnt<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, F.rank.p, rc.p);
+    k_rank_cnt<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, F->rank.p, rc.p);
     cub_call([&](void* tp, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(tp, b, rc.p, ro.p, cnt + 1, s);
     }, tmp, s);
@@ -337,24 +341,25 @@ static void build_side(MatrixImpl* M, int side, const DevTables& tabs, double pa
     sync(s);
     raise_dev_err(herr);
     SMASH_CHECK(skel_used + lvl_k <= skel_cap, SMASH_ERR_CUDA, "skeleton capacity exceeded");
-    F.level_skel_begin[l] = skel_used;
-    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F.rank.p, ro.p, (int)skel_used, F.ib_off.p,
-                                       F.ib_total, tmp_lab.p, tmp_pts.p, A.tmp_stride, dim,
-                                       F.skel_off.p, F.skel.p, F.skel_pts.p, skel_cap);
+    F->level_skel_begin[l] = skel_used;
+    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, (int)skel_used, F->ib_off.p,
+                                       F->ib_total, tmp_lab.p, tmp_pts.p, A.tmp_stride, dim,
+                                       F->skel_off.p, F->skel.p, F->skel_pts.p, skel_cap);
     skel_used += lvl_k;
-    F.ib_total += lvl_ib;
-    F.g_total += lvl_g;
+    F->ib_total += lvl_ib;
+    F->g_total += lvl_g;
   }
-  F.level_skel_begin[1] = skel_used;
-  F.skel_total = skel_used;
-  // keep the SoA stride == capacity (skel_pts rows are skel_cap apart)
-  F.skel_stride = skel_cap;
-  unsigned long long hs = 0;
-  d2h(&hs, swaps.p, 1, s);
-  sync(s);
-  F.swaps = (int64_t)hs;
-  SMASH_CUDA(cudaGetLastError());
-}
+
+  void finish() {
+    F->level_skel_begin[1] = skel_used;
+    F->skel_total = skel_used;
+    unsigned long long hs = 0;
+    d2h(&hs, swaps.p, 1, s);
+    sync(s);
+    F->swaps = (int64_t)hs;
+    SMASH_CUDA(cudaGetLastError());
+  }
+};
 
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s) {
   SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
@@ -367,6 +372,7 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
     SMASH_CHECK(t->mode == SMASH_MODE_2D || t->dim == 1, SMASH_ERR_INVALID,
                 "H2 construction expects a 2^d-mode tree");
   check_basis_params(p.r, t->dim);
+  init_pool();
   std::unique_ptr<MatrixImpl> M(new MatrixImpl());
   M->tree = t;
   M->p = p;
@@ -379,13 +385,28 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
   for (int a = 0; a < t->dim; ++a) w[a] = t->root_hi[a] - t->root_lo[a];
   double diam = 2 * (0.5 * host_norm_fma(w, t->dim));
   double pad = std::max(1e-9 * diam, 1e-300);
-  build_side(M.get(), 0, D, pad, s);
-  if (t->shared) {
-    M->colf = &M->rowf;
-  } else {
-    build_side(M.get(), 1, D, pad, s);
-    M->colf = &M->colf_own;
+  const bool hss = p.structure == SMASH_STRUCT_HSS;
+  // Shared points: H2 skeletons are kernel independent and HSS ones depend on the
+  // kernel only through the nearfield block, so the column factors equal the row
+  // factors whenever the kernel is symmetric (all but the Cauchy kernel).
+  const bool alias = t->shared && (!hss || p.kernel != SMASH_KERNEL_CAUCHY);
+  M->colf = alias ? &M->rowf : &M->colf_own;
+  NearSets* near = hss ? get_near(t, p.tau, s) : nullptr;
+  SideBuild rowb{M.get(), 0, &M->rowf, &D, pad, s};
+  rowb.init();
+  std::unique_ptr<SideBuild> colb;
+  if (!alias) {
+    colb.reset(new SideBuild{M.get(), 1, &M->colf_own, &D, pad, s});
+    colb->init();
   }
+  // row and column passes interleave per level: the HSS row pass at level l
+  // reads the column side's level-(l+1) skeletons and vice versa (hss.py:274-299)
+  for (int l = t->n_levels; l >= 2; --l) {
+    rowb.level(l, near);
+    if (colb) colb->level(l, near);
+  }
+  rowb.finish();
+  if (colb) colb->finish();
   sync(s);
   return M.release();
 }

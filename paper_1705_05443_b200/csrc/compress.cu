@@ -19,12 +19,14 @@
 // fixed sequential order; the row-major panel makes those accesses
 // bank-conflict free.
 #include "compress.cuh"
+#include "qr_device.cuh"
 
 namespace smash {
 
 namespace {
 
-constexpr double TOL3Z = 1.0536712127723509e-08;  // sqrt(dlamch('E')), dlaqp2
+using namespace qr;
+
 constexpr int MAX_SWAPS = 200;                     // lowrank.py:171
 
 // numpy's pairwise summation (8 accumulators, n <= 128) over terms f(0..n-1);
@@ -62,109 +64,6 @@ __device__ __forceinline__ void lagrange_axis(double x, const double* nd, const 
   }
   double S = np_pairwise_sum(m, [&](int k) { return __ddiv_rn(w[k], __dsub_rn(x, nd[k])); });
   for (int k = 0; k < m; ++k) L[k] = __ddiv_rn(__ddiv_rn(w[k], __dsub_rn(x, nd[k])), S);
-}
-
-struct Shared {
-  double* vn1;
-  double* vn2;
-  double* vh;
-  double* rdiag;
-  double* nodes;  // [3][MAX_M_AXIS_1D]
-  double* redv;   // [32]
-  int* redi;      // [32]
-  double* misc;   // [8]
-  int* imisc;     // [8]
-  int* jpvt;
-  double* panel;
-};
-
-__device__ __forceinline__ void argmax_combine(double& v, int& i, double ov, int oi) {
-  if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
-}
-
-// Block-wide (max value, smallest index) reduction; result broadcast to all threads.
-__device__ void block_argmax(double& v, int& i, Shared& S) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int off = 16; off; off >>= 1) {
-    double ov = __shfl_down_sync(0xffffffffu, v, off);
-    int oi = __shfl_down_sync(0xffffffffu, i, off);
-    argmax_combine(v, i, ov, oi);
-  }
-  __syncthreads();  // protect redv/redi reuse
-  if (lane == 0) { S.redv[wid] = v; S.redi[wid] = i; }
-  __syncthreads();
-  if (wid == 0) {
-    v = lane < nw ? S.redv[lane] : -1.0;
-    i = lane < nw ? S.redi[lane] : 0x7fffffff;
-    for (int off = 16; off; off >>= 1) {
-      double ov = __shfl_down_sync(0xffffffffu, v, off);
-      int oi = __shfl_down_sync(0xffffffffu, i, off);
-      argmax_combine(v, i, ov, oi);
-    }
-    if (lane == 0) { S.redv[0] = v; S.redi[0] = i; }
-  }
-  __syncthreads();
-  v = S.redv[0];
-  i = S.redi[0];
-}
-
-__device__ __forceinline__ double col_sumsq(const double* P, int ld, int j, int r0, int r1) {
-  double s = 0.0;
-  for (int row = r0; row < r1; ++row) {
-    double x = P[(size_t)row * ld + j];
-    s = __fma_rn(x, x, s);
-  }
-  return s;
-}
-
-__device__ __forceinline__ double dlapy2(double x, double y) {
-  double xa = fabs(x), ya = fabs(y);
-  double w = fmax(xa, ya), z = fmin(xa, ya);
-  if (z == 0.0 || w > 1.7976931348623157e308) return w;
-  double q = __ddiv_rn(z, w);
-  return __dmul_rn(w, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(q, q))));
-}
-
-// Householder reflector on column i (dlarfg), done by warp 0; result in panel,
-// tau in S.misc[0], v (rows > i) in S.vh.
-__device__ void householder(double* P, int ld, int m, int i, Shared& S) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  double alpha = P[(size_t)i * ld + i];
-  double ss = 0.0;
-  for (int row = i + 1 + lane; row < m; row += 32) {
-    double x = P[(size_t)row * ld + i];
-    ss = __fma_rn(x, x, ss);
-  }
-  for (int off = 16; off; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
-  double xnorm = __dsqrt_rn(ss);
-  double tau = 0.0;
-  if (m - i > 1 && xnorm != 0.0) {
-    double beta = -copysign(dlapy2(alpha, xnorm), alpha);
-    tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
-    double scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
-    for (int row = i + 1 + lane; row < m; row += 32) {
-      double x = __dmul_rn(scal, P[(size_t)row * ld + i]);
-      P[(size_t)row * ld + i] = x;
-      S.vh[row] = x;
-    }
-    if (lane == 0) P[(size_t)i * ld + i] = beta;
-  }
-  if (lane == 0) {
-    S.misc[0] = tau;
-    S.rdiag[i] = P[(size_t)i * ld + i];
-  }
-}
-
-// Apply H_i^T = I - tau v v^T (v_i = 1) to column j > i (dlarf: w = C^T v; C -= tau v w^T).
-__device__ __forceinline__ void apply_reflector(double* P, int ld, int m, int i, int j, double tau,
-                                                const double* vh) {
-  double w = P[(size_t)i * ld + j];
-  for (int row = i + 1; row < m; ++row) w = __fma_rn(vh[row], P[(size_t)row * ld + j], w);
-  double t = -__dmul_rn(tau, w);
-  P[(size_t)i * ld + j] = __dadd_rn(P[(size_t)i * ld + j], t);
-  for (int row = i + 1; row < m; ++row)
-    P[(size_t)row * ld + j] = __fma_rn(t, vh[row], P[(size_t)row * ld + j]);
 }
 
 // ---------------------------------------------------------------------------

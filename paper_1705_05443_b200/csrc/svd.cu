@@ -1,12 +1,481 @@
-// K5: HSS nearfield SVD (placeholder until the batched Jacobi kernel lands).
+// K5: HSS nearfield block-row assembly + batched truncated SVD -- replaces the
+// per-node `block(ibar, near columns)` + `truncated_svd` of build_hss
+// (smash/hss.py:279-299, smash/lowrank.py:265-276).
+//
+// One CTA per node.  A (|ibar| x n_near) is generated from the kernel into an
+// L2-resident workspace, then its left singular subspace is computed as
+//   A P = Q1 R      column-pivoted Householder QR, stopped once |R_ii| falls
+//                   to the fp64 noise floor (2^-53 |R_00|): the discarded block
+//                   perturbs the singular values by O(eps sigma_1), the same
+//                   order as LAPACK gesdd's own error;
+//   R_k^T = Q2 R2   unpivoted QR of the k' x n_near leading rows (transposed);
+//   R2 V = W        one-sided (Hestenes) Jacobi on the k' x k' triangle,
+//                   round-robin pair order, one warp per pair;
+// so sigma_j = ||W_j|| and U(A) = Q1[:, :k'] V.  keep = #{sigma >= eps sigma_1}
+// (lowrank.py:275) and S = U[:, kept] (descending sigma) is handed to the
+// compression kernel as extra panel rows.  Column order and signs of S do not
+// change the pivoted QR of [U_basis, S]^T in exact arithmetic.
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+#include "qr_device.cuh"
 #include "svd.cuh"
 
 namespace smash {
 
+namespace {
+
+using namespace qr;
+
+constexpr int SVD_THREADS = 256;
+constexpr int MAX_NEAR = 64;  // |N_i| cap (reference hist: |N_i| <= 2 on the HSS configs)
+
+struct IbarSide {
+  const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
+  const int* rank;
+  const int* pt_a;      // leaf point range start
+  const int* pt_b;
+  const double* P;      // tree-ordered points SoA
+  int64_t P_stride;
+  const double* Sk;     // compact skeleton points SoA
+  int64_t S_stride;
+  const int* skel_off;
+};
+
+struct SvdArgs {
+  int lb, le, dim, kernel;
+  double dx, eps_svd;
+  int transpose;  // 0: K(target, source) (row pass); 1: K(source, target) (column pass)
+  const int* nchild;
+  const int* child_first;
+  const int* near_ptr;
+  const int* near_idx;
+  IbarSide self, other;
+  // outputs
+  int* keep;
+  const int64_t* sv_off;
+  double* sv;
+  int* nn_out;
+  // workspace
+  double* gws;
+  int64_t gws_stride;  // doubles per CTA
+  int nmax, nnmax;
+  int* err;
+};
+
+__device__ __forceinline__ int ibar_size(const IbarSide& s, const int* nchild, const int* child_first,
+                                         int j) {
+  if (nchild[j] == 0) return s.pt_b[j] - s.pt_a[j];
+  int n = 0;
+  for (int c = 0; c < nchild[j]; ++c) n += s.rank[child_first[j] + c];
+  return n;
+}
+
+__device__ __forceinline__ const double* ibar_base(const IbarSide& s, const int* nchild,
+                                                   const int* child_first, int j, int64_t* stride) {
+  if (nchild[j] == 0) {
+    *stride = s.P_stride;
+    return s.P + s.pt_a[j];
+  }
+  *stride = s.S_stride;
+  return s.Sk + s.skel_off[child_first[j]];
+}
+
+__global__ void k_near_cols(SvdArgs A) {
+  int v = A.lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= A.le) return;
+  int nn = 0;
+  for (int e = A.near_ptr[v]; e < A.near_ptr[v + 1]; ++e)
+    nn += ibar_size(A.other, A.nchild, A.child_first, A.near_idx[e]);
+  A.nn_out[v - A.lb] = nn;
+}
+
+template <int KER, int D>
+__global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Shared S;
+  double* taus;
+  double* sig;
+  int* near_start;
+  const double** near_base;
+  int64_t* near_stride;
+  int* order;
+  {
+    double* d = reinterpret_cast<double*>(smem_raw);
+    S.vn1 = d; d += A.nnmax;
+    S.vn2 = d; d += A.nnmax;
+    S.vh = d; d += max(A.nmax, A.nnmax);
+    S.rdiag = d; d += max(A.nmax, A.nnmax);
+    taus = d; d += A.nmax;
+    sig = d; d += A.nmax;
+    S.nodes = nullptr;
+    S.redv = d; d += 32;
+    S.misc = d; d += 8;
+    near_base = reinterpret_cast<const double**>(d); d += MAX_NEAR;
+    near_stride = reinterpret_cast<int64_t*>(d); d += MAX_NEAR;
+    int* ip = reinterpret_cast<int*>(d);
+    S.redi = ip; ip += 32;
+    S.imisc = ip; ip += 8;
+    near_start = ip; ip += MAX_NEAR + 1;
+    order = ip; ip += A.nmax;
+    S.jpvt = ip; ip += A.nnmax;
+  }
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
+  double* W = A.gws + (size_t)blockIdx.x * A.gws_stride;
+  for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
+    const int n = A.self.nib[v];
+    const int e0 = A.near_ptr[v], e1 = A.near_ptr[v + 1];
+    if (tid == 0) {
+      int acc = 0, cnt = 0;
+      for (int e = e0; e < e1 && cnt < MAX_NEAR; ++e) {
+        const int j = A.near_idx[e];
+        const int sz = ibar_size(A.other, A.nchild, A.child_first, j);
+        if (sz == 0) continue;  // hss.py:283 drops empty neighbour sets
+        near_start[cnt] = acc;
+        near_base[cnt] = ibar_base(A.other, A.nchild, A.child_first, j, &near_stride[cnt]);
+        acc += sz;
+        ++cnt;
+      }
+      near_start[cnt] = acc;
+      S.imisc[0] = cnt;
+      S.imisc[1] = acc;
+      if (e1 - e0 > MAX_NEAR) atomicOr(A.err, DEV_CAPACITY);
+    }
+    __syncthreads();
+    const int nnear = S.imisc[0], nn = S.imisc[1];
+    if (n == 0 || nn == 0) {
+      if (tid == 0) A.keep[v] = 0;
+      __syncthreads();
+      continue;
+    }
+    // ---- assemble A (n x nn), row-major in W
+    int64_t ts;
+    const double* tb = ibar_base(A.self, A.nchild, A.child_first, v, &ts);
+    for (int e = tid; e < n * nn; e += NT) {
+      const int a = e / nn, b = e % nn;
+      int g = 0;
+      while (g + 1 < nnear && near_start[g + 1] <= b) ++g;
+      const int bl = b - near_start[g];
+      double x[D], y[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        x[d] = tb[(int64_t)d * ts + a];
+        y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
+      }
+      W[e] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
+    }
+    __syncthreads();
+    // ---- column-pivoted QR of A, truncated at the noise floor
+    double* P = W;
+    const int ld = nn;
+    const int kmax = min(n, nn);
+    for (int j = tid; j < nn; j += NT) {
+      double nr = __dsqrt_rn(col_sumsq(P, ld, j, 0, n));
+      S.vn1[j] = nr;
+      S.vn2[j] = nr;
+      S.jpvt[j] = j;
+    }
+    __syncthreads();
+    int kp = 0;
+    for (int i = 0; i < kmax; ++i) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int j = i + tid; j < nn; j += NT)
+        if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
+      block_argmax(bv, bi, S);
+      const int pvt = bi;
+      if (pvt != i) {
+        for (int row = tid; row < n; row += NT) {
+          double t = P[(size_t)row * ld + pvt];
+          P[(size_t)row * ld + pvt] = P[(size_t)row * ld + i];
+          P[(size_t)row * ld + i] = t;
+        }
+        if (tid == 0) {
+          S.vn1[pvt] = S.vn1[i];
+          S.vn2[pvt] = S.vn2[i];
+        }
+      }
+      __syncthreads();
+      householder(P, ld, n, i, S);
+      __syncthreads();
+      const double tau = S.misc[0];
+      if (tid == 0) taus[i] = tau;
+      const double r0 = fabs(S.rdiag[0]);
+      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > 0x1p-53 * r0)) break;  // noise floor reached
+      kp = i + 1;
+      for (int j = i + 1 + tid; j < nn; j += NT) {
+        if (tau != 0.0) apply_reflector(P, ld, n, i, j, tau, S.vh);
+        double v1 = S.vn1[j];
+        if (v1 != 0.0) {
+          double q = fabs(P[(size_t)i * ld + j]) / v1;
+          double temp = fmax(1.0 - q * q, 0.0);
+          double q2 = v1 / S.vn2[j];
+          if (temp * (q2 * q2) <= TOL3Z) {
+            double nv = i + 1 < n ? sqrt(col_sumsq(P, ld, j, i + 1, n)) : 0.0;
+            S.vn1[j] = nv;
+            S.vn2[j] = nv;
+          } else {
+            S.vn1[j] = v1 * sqrt(temp);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (kp == 0) {
+      if (tid == 0) A.keep[v] = 0;
+      __syncthreads();
+      continue;
+    }
+    // ---- B = R_k^T (nn x kp), unpivoted QR -> R2 (kp x kp)
+    double* B = W + (size_t)n * nn;
+    for (int e = tid; e < nn * kp; e += NT) {
+      const int b = e / kp, j = e % kp;
+      B[e] = b >= j ? P[(size_t)j * ld + b] : 0.0;
+    }
+    __syncthreads();
+    for (int i = 0; i < kp; ++i) {
+      householder(B, kp, nn, i, S);
+      __syncthreads();
+      const double tau = S.misc[0];
+      if (tau != 0.0)
+        for (int j = i + 1 + tid; j < kp; j += NT) apply_reflector(B, kp, nn, i, j, tau, S.vh);
+      __syncthreads();
+    }
+    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated
+    double* J = B + (size_t)nn * kp;
+    double* V = J + (size_t)kp * kp;
+    for (int e = tid; e < kp * kp; e += NT) {
+      const int c = e / kp, r = e % kp;
+      J[e] = r <= c ? B[(size_t)r * kp + c] : 0.0;
+      V[e] = r == c ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      if (tid == 0) S.imisc[2] = 0;
+      __syncthreads();
+      for (int rnd = 0; rnd < np - 1; ++rnd) {
+        for (int pr = wid; pr < np / 2; pr += nw) {
+          // circle method: position 0 fixed, others rotate
+          int a = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (np - 1);
+          int b = 1 + (np - 2 - pr + rnd) % (np - 1);
+          if (a >= kp || b >= kp) continue;
+          double* ja = J + (size_t)a * kp;
+          double* jb = J + (size_t)b * kp;
+          double al = 0, be = 0, ga = 0;
+          for (int r = lane; r < kp; r += 32) {
+            al = fma(ja[r], ja[r], al);
+            be = fma(jb[r], jb[r], be);
+            ga = fma(ja[r], jb[r], ga);
+          }
+          for (int off = 16; off; off >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, off);
+            be += __shfl_xor_sync(0xffffffffu, be, off);
+            ga += __shfl_xor_sync(0xffffffffu, ga, off);
+          }
+          if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+            double* va = V + (size_t)a * kp;
+            double* vb = V + (size_t)b * kp;
+            for (int r = lane; r < kp; r += 32) {
+              const double x = ja[r], y = jb[r];
+              ja[r] = c * x - s * y;
+              jb[r] = s * x + c * y;
+              const double p = va[r], q = vb[r];
+              va[r] = c * p - s * q;
+              vb[r] = s * p + c * q;
+            }
+            if (lane == 0) atomicAdd(&S.imisc[2], 1);
+          }
+        }
+        __syncthreads();
+      }
+      if (S.imisc[2] == 0) break;
+      __syncthreads();
+    }
+    // ---- singular values, keep count, descending order
+    for (int c = tid; c < kp; c += NT) {
+      double s2 = 0.0;
+      for (int r = 0; r < kp; ++r) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
+      sig[c] = sqrt(s2);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double smax = 0.0;
+      for (int c = 0; c < kp; ++c) smax = fmax(smax, sig[c]);
+      int keep = 0;
+      if (smax > 0.0) {
+        // selection of sigma >= eps * sigma_1 in descending order
+        for (int c = 0; c < kp; ++c) order[c] = c;
+        for (int c = 1; c < kp; ++c) {  // insertion sort by sigma descending (kp small)
+          int x = order[c];
+          int p = c - 1;
+          while (p >= 0 && sig[order[p]] < sig[x]) { order[p + 1] = order[p]; --p; }
+          order[p + 1] = x;
+        }
+        const double thr = A.eps_svd * smax;
+        for (int c = 0; c < kp; ++c) keep += sig[c] >= thr ? 1 : 0;
+      }
+      S.imisc[3] = keep;
+      A.keep[v] = keep;
+    }
+    __syncthreads();
+    const int keep = S.imisc[3];
+    if (keep == 0) continue;
+    // ---- U = Q1[:, :kp] V[:, kept]  (n x keep, row-major into sv)
+    double* Y = A.sv + A.sv_off[v];
+    for (int e = tid; e < n * keep; e += NT) {
+      const int a = e / keep, c = e % keep;
+      Y[e] = a < kp ? V[(size_t)order[c] * kp + a] : 0.0;
+    }
+    __syncthreads();
+    for (int i = kp - 1; i >= 0; --i) {
+      const double tau = taus[i];
+      if (tau == 0.0) continue;
+      for (int c = tid; c < keep; c += NT) {
+        double w = Y[(size_t)i * keep + c];
+        for (int row = i + 1; row < n; ++row) w = fma(P[(size_t)row * ld + i], Y[(size_t)row * keep + c], w);
+        const double t = -tau * w;
+        Y[(size_t)i * keep + c] += t;
+        for (int row = i + 1; row < n; ++row)
+          Y[(size_t)row * keep + c] = fma(t, P[(size_t)row * ld + i], Y[(size_t)row * keep + c]);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <typename F>
+void cub_call(F f, DBuf<char>& tmp, cudaStream_t s) {
+  size_t bytes = 0;
+  SMASH_CUDA(f((void*)nullptr, bytes));
+  if (bytes > tmp.n) tmp.alloc(bytes, s);
+  SMASH_CUDA(f((void*)tmp.p, bytes));
+}
+
+__global__ void k_sv_cap(int lb, int le, const int* nib, const int* nn, int64_t* cap) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= le) return;
+  int a = nib[v], b = nn[v - lb];
+  cap[v - lb] = (int64_t)a * min(a, b);
+}
+
+__global__ void k_sv_off(int lb, int le, const int64_t* loc, int64_t* off) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < le) off[v] = loc[v - lb];
+}
+
+__global__ void k_max_keep(int lb, int le, const int* keep, int* out) {
+  int m = 0;
+  for (int v = lb + blockIdx.x * blockDim.x + threadIdx.x; v < le; v += gridDim.x * blockDim.x)
+    m = max(m, keep[v]);
+  for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+IbarSide ibar_side(MatrixImpl* M, int side) {
+  TreeImpl* t = M->tree;
+  SideFactors& F = side == 0 ? M->rowf : *M->colf;
+  const bool col = side == 1 && !t->shared;
+  IbarSide s;
+  s.nib = F.nib.p;
+  s.rank = F.rank.p;
+  s.pt_a = col ? t->col_a.p : t->row_a.p;
+  s.pt_b = col ? t->col_b.p : t->row_b.p;
+  s.P = col ? t->pts_col.p : t->pts_row.p;
+  s.P_stride = col ? t->ny : t->nx;
+  s.Sk = F.skel_pts.p;
+  s.S_stride = F.skel_stride;
+  s.skel_off = F.skel_off.p;
+  return s;
+}
+
+}  // namespace
+
 int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, SvdWorkspace& ws,
                   cudaStream_t s) {
-  (void)M; (void)side; (void)level; (void)near; (void)nmax; (void)ws; (void)s;
-  throw Error(SMASH_ERR_INVALID, "HSS construction is not available in this build yet");
+  TreeImpl* t = M->tree;
+  const int n_nodes = t->n_nodes;
+  const int lb = t->level_begin(level), le = t->level_end(level), cnt = le - lb;
+  if (ws.keep.n < (size_t)n_nodes) {
+    ws.keep.alloc(n_nodes, s);
+    ws.keep.zero(s);
+    ws.sv_off.alloc(n_nodes, s);
+    ws.sv_off.zero(s);
+  }
+  SvdArgs A{};
+  A.lb = lb; A.le = le; A.dim = t->dim; A.kernel = M->p.kernel;
+  A.dx = M->p.kernel == SMASH_KERNEL_EXP ? 1.0 : M->p.dx;
+  A.eps_svd = M->p.eps_svd;
+  A.transpose = side;
+  A.nchild = t->nchild.p; A.child_first = t->child_first.p;
+  A.near_ptr = near->ptr.p; A.near_idx = near->idx.p;
+  A.self = ibar_side(M, side);
+  A.other = ibar_side(M, 1 - side);
+  A.keep = ws.keep.p;
+  DBuf<int> nn;
+  nn.alloc(cnt, s);
+  A.nn_out = nn.p;
+  k_near_cols<<<cdiv(cnt, 128), 128, 0, s>>>(A);
+  // S capacity: |ibar| x min(|ibar|, n_near) per node
+  DBuf<int64_t> cap, off;
+  cap.alloc(cnt + 1, s); off.alloc(cnt + 1, s);
+  SMASH_CUDA(cudaMemsetAsync(cap.p + cnt, 0, 8, s));
+  k_sv_cap<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, A.self.nib, nn.p, cap.p);
+  DBuf<char> tmp;
+  cub_call([&](void* tp, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(tp, b, cap.p, off.p, cnt + 1, s);
+  }, tmp, s);
+  DBuf<int> dmax;
+  dmax.alloc(1, s);
+  dmax.zero(s);
+  int64_t total = 0;
+  d2h(&total, off.p + cnt, 1, s);
+  std::vector<int> hnn(cnt);
+  d2h(hnn.data(), nn.p, cnt, s);
+  sync(s);
+  int nnmax = 1;
+  for (int x : hnn) nnmax = std::max(nnmax, x);
+  ws.sv.alloc(std::max<int64_t>(total, 1), s);
+  k_sv_off<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, off.p, ws.sv_off.p);
+  A.sv_off = ws.sv_off.p;
+  A.sv = ws.sv.p;
+  A.nmax = std::max(nmax, 1);
+  A.nnmax = nnmax;
+  const int kpmax = std::min(A.nmax, A.nnmax);
+  A.gws_stride = (int64_t)A.nmax * A.nnmax + (int64_t)A.nnmax * kpmax + 2 * (int64_t)kpmax * kpmax;
+  int dev = 0, nsm = 0;
+  SMASH_CUDA(cudaGetDevice(&dev));
+  SMASH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(cnt, nsm * 2);
+  DBuf<double> gws;
+  gws.alloc((size_t)grid * A.gws_stride, s);
+  A.gws = gws.p;
+  DBuf<int> err;
+  err.alloc(1, s);
+  err.zero(s);
+  A.err = err.p;
+  const int mx = std::max(A.nmax, A.nnmax);
+  size_t smem = 8 * ((size_t)2 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
+                4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64;
+  SMASH_CHECK(smem <= 200 * 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
+  dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
+    SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    k_svd<KER, D><<<grid, SVD_THREADS, smem, s>>>(A);
+  });
+  SMASH_CUDA(cudaGetLastError());
+  k_max_keep<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(lb, le, ws.keep.p, dmax.p);
+  int hk = 0, he = 0;
+  d2h(&hk, dmax.p, 1, s);
+  d2h(&he, err.p, 1, s);
+  sync(s);
+  SMASH_CHECK(he == 0, SMASH_ERR_INVALID, "nearfield set larger than the supported cap");
+  return hk;
 }
 
 }  // namespace smash
