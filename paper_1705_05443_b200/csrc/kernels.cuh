@@ -8,6 +8,22 @@
 
 namespace smash {
 
+// Branch-free fp64 1/sqrt: MUFU approximation (~2^-20) + two Newton steps
+// (measured max relative error 2.7e-16 vs 2.2e-16 for CUDA's rsqrt(), which
+// carries a special-case branch that breaks instruction-level parallelism
+// across the unrolled target tiles of the P2P kernels; tools/rsqrt_test.cu).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double h = x * y;
+    const double e = fma(-h, y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
 template <int KER, int D>
 __device__ __forceinline__ double kval(const double* x, const double* y, double dx) {
   if (KER == SMASH_KERNEL_CAUCHY) {
@@ -21,7 +37,10 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
     r2 = fma(t, t, r2);
   }
   if (KER == SMASH_KERNEL_LOG) return r2 == 0.0 ? dx : 0.5 * log(r2);
-  if (KER == SMASH_KERNEL_INV_R) return r2 == 0.0 ? dx : rsqrt(r2);
+  if (KER == SMASH_KERNEL_INV_R) {
+    const double v = rsqrt_nr(r2);
+    return r2 == 0.0 ? dx : v;
+  }
   // exp(-r): r = sqrt(r2); exp(0) = 1 on the diagonal
   return exp(-sqrt(r2));
 }

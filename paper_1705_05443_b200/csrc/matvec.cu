@@ -45,6 +45,26 @@ struct Side {
   int64_t skel_stride;
 };
 
+// Block-wide staging copy dst[e] = f(e), e < n: each thread issues U independent
+// global loads before its shared-memory stores so a whole tile is one memory
+// round trip instead of n / blockDim dependent ones.
+template <int U, typename F, typename S>
+__device__ __forceinline__ void stage_block(int n, F load, S store) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < n ? load(e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < n) store(e, v[u]);
+    }
+  }
+}
+
 // Tile of G rows staged in shared memory (TB rows, <= 4096 doubles).
 __device__ __forceinline__ int g_tile_rows(int ks) { return max(1, min(64, 4096 / ks)); }
 
@@ -68,10 +88,8 @@ __global__ void __launch_bounds__(XFER_THREADS) k_upward(int lb, int le, Side cs
   const int* perm = cs.perm + cs.ib_off[v];
   double* iv = sh;               // n * RC: iv[c] = ivec[perm[c]]
   double* gs = sh + n * RC;      // TB * k
-  for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
-    int c = e / RC, r = e % RC;
-    iv[e] = ivec[(int64_t)perm[c] * RC + r];
-  }
+  stage_block<8>(n * RC, [&](int e) { return ivec[(int64_t)perm[e / RC] * RC + e % RC]; },
+                 [&](int e, double x) { iv[e] = x; });
   __syncthreads();
   const int nout = k * RC;
   double acc[XFER_MAXO];
@@ -86,7 +104,7 @@ __global__ void __launch_bounds__(XFER_THREADS) k_upward(int lb, int le, Side cs
   for (int b0 = 0; b0 < nk; b0 += TB) {
     const int tb = min(TB, nk - b0);
     const double* src = G + (int64_t)b0 * k;
-    for (int e = threadIdx.x; e < tb * k; e += blockDim.x) gs[e] = src[e];
+    stage_block<16>(tb * k, [&](int e) { return src[e]; }, [&](int e, double x) { gs[e] = x; });
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < XFER_MAXO; ++j) {
@@ -139,10 +157,8 @@ __global__ void __launch_bounds__(XFER_THREADS) k_downward(int lb, int le, Side 
     const int tb = min(TB, nk - b0);
     const double* src = G + (int64_t)b0 * k;
     __syncthreads();
-    for (int e = threadIdx.x; e < tb * k; e += blockDim.x) {
-      int bb = e / k, a = e % k;
-      gs[bb * ks + a] = src[e];
-    }
+    stage_block<16>(tb * k, [&](int e) { return src[e]; },
+                    [&](int e, double x) { gs[(e / k) * ks + e % k] = x; });
     __syncthreads();
     for (int e = threadIdx.x; e < tb * RC; e += blockDim.x) {
       int bb = e / RC, r = e % RC;
@@ -162,13 +178,16 @@ __device__ __forceinline__ void p2p_sources(const double* xt, const double* ys, 
   // stage: per-warp buffer of 32 * (D + RC) doubles
   for (int s0 = 0; s0 < ns; s0 += 32) {
     const int cnt = min(32, ns - s0);
+    double vc[D], vw[RC];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = lane < cnt ? ys[(int64_t)a * ystride + s0 + lane] : 0.0;
+#pragma unroll
+    for (int r = 0; r < RC; ++r) vw[r] = lane < cnt ? w[(int64_t)(s0 + lane) * RC + r] : 0.0;
     __syncwarp();
-    if (lane < cnt) {
 #pragma unroll
-      for (int a = 0; a < D; ++a) stage[a * 32 + lane] = ys[(int64_t)a * ystride + s0 + lane];
+    for (int a = 0; a < D; ++a) stage[a * 32 + lane] = vc[a];
 #pragma unroll
-      for (int r = 0; r < RC; ++r) stage[(D + r) * 32 + lane] = w[(int64_t)(s0 + lane) * RC + r];
-    }
+    for (int r = 0; r < RC; ++r) stage[(D + r) * 32 + lane] = vw[r];
     __syncwarp();
     for (int s = 0; s < cnt; ++s) {
       double y[D];
@@ -324,94 +343,184 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-struct SrcSet {
-  const double* pts;  // SoA coordinates of the set's first point
-  int64_t stride;
-  const double* w;    // weights (count, RC)
-  int n;
-};
+constexpr int MMA_MTMAX = 8;      // target tiles (8 rows) per pass: 64 targets
+constexpr int MMA_WSTRIDE = 36;   // staged weight row stride (doubles): 4 (mod 16)
+constexpr int MMA_SEG_CAP = 512;  // source segments per table fill
 
-template <int RC>
-constexpr int mma_mtmax() { return RC == 16 ? 8 : 16; }
+template <int D, int RC>
+constexpr int mma_stage_doubles() { return 32 * D + MMA_WSTRIDE * RC; }
 
 template <int D, int RC>
 constexpr int mma_smem_doubles() {
-  return P2P_WARPS * mma_mtmax<RC>() * 8 * RC > P2P_WARPS * 32 * (D + RC)
-             ? P2P_WARPS * mma_mtmax<RC>() * 8 * RC
-             : P2P_WARPS * 32 * (D + RC);
+  return P2P_WARPS * MMA_MTMAX * 8 * RC > P2P_WARPS * mma_stage_doubles<D, RC>()
+             ? P2P_WARPS * MMA_MTMAX * 8 * RC
+             : P2P_WARPS * mma_stage_doubles<D, RC>();
 }
 
-// Accumulate the block's sum over the source sets [p0, p1) for targets
-// [t0, t0 + nt) (nt <= 8 * MTMAX) into red[warp][t][r] (shared).
-template <int KER, int D, int RC, typename SrcF>
-__device__ __forceinline__ void p2p_mma_chunk(const double* tx, int64_t tstride, int nt, int p0,
-                                              int p1, SrcF src_of, double dx, double* stage,
-                                              double* red) {
-  constexpr int MTMAX = mma_mtmax<RC>();
+struct SegTable {
+  int pre[MMA_SEG_CAP + 1];  // prefix of segment lengths
+  int off[MMA_SEG_CAP];      // segment start (row index into the source arrays)
+  int n;
+};
+
+// Source chunk (32 consecutive stream positions) -> registers of this lane.
+template <int D, int RC>
+__device__ __forceinline__ void mma_fetch(const SegTable& T, int p, int total, const double* spts,
+                                          int64_t sstride, const double* wts, double* vc,
+                                          double* vw) {
+  if (p < total) {
+    int lo = 0, hi = T.n - 1;  // last segment with pre <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (T.pre[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    const int row = T.off[lo] + (p - T.pre[lo]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = spts[(int64_t)a * sstride + row];
+    const double2* wp = reinterpret_cast<const double2*>(wts + (int64_t)row * RC);
+#pragma unroll
+    for (int u = 0; u < RC / 2; ++u) {
+      const double2 t = wp[u];
+      vw[2 * u] = t.x;
+      vw[2 * u + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = 0.0;
+#pragma unroll
+    for (int u = 0; u < RC; ++u) vw[u] = 0.0;
+  }
+}
+
+// One warp: accumulate sum over its share of the source stream for MTX target
+// tiles into the C fragments c.  Sources stream in chunks of 32 (lane = source)
+// across segment boundaries; the next chunk is fetched into registers while
+// the current one is consumed from shared memory.
+template <int KER, int D, int RC, int MTX>
+__device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double* spts,
+                                                int64_t sstride, const double* wts,
+                                                const double (&xt)[MTX][D], const bool (&tv)[MTX],
+                                                double dx, double* stage,
+                                                double (&c)[MTX][RC / 8][2]) {
   constexpr int NT = RC / 8;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int MT = (nt + 7) >> 3;
-  double xt[MTMAX][D];
-  bool tv[MTMAX];
+  const int total = T.pre[T.n];
+  const int nch = (total + 31) >> 5;
+  const int per = (nch + P2P_WARPS - 1) / P2P_WARPS;
+  const int c0 = wid * per, c1 = min(nch, c0 + per);
+  double* sc = stage;
+  double* sw = stage + D * 32;
+  double vc[D], vw[RC];
+  if (c0 < c1) mma_fetch<D, RC>(T, c0 * 32 + lane, total, spts, sstride, wts, vc, vw);
+  for (int ch = c0; ch < c1; ++ch) {
+    const int cnt = min(32, total - ch * 32);
+    __syncwarp();
 #pragma unroll
-  for (int m = 0; m < MTMAX; ++m) {
+    for (int a = 0; a < D; ++a) sc[a * 32 + lane] = vc[a];
+#pragma unroll
+    for (int u = 0; u < RC; ++u) sw[u * MMA_WSTRIDE + lane] = vw[u];
+    __syncwarp();
+    if (ch + 1 < c1) mma_fetch<D, RC>(T, (ch + 1) * 32 + lane, total, spts, sstride, wts, vc, vw);
+    for (int kk = 0; kk < cnt; kk += 4) {
+      const int si = kk + q;
+      const bool sv = si < cnt;
+      double ys[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + si];
+      double b[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = sw[(n * 8 + g) * MMA_WSTRIDE + si];
+      double av[MTX];
+#pragma unroll
+      for (int m = 0; m < MTX; ++m) {  // straight-line: padded entries selected to 0
+        const double kv = kval<KER, D>(xt[m], ys, dx);
+        av[m] = (sv && tv[m]) ? kv : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < MTX; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av[m], b[n]);
+    }
+  }
+}
+
+// Block: targets [0, nt) (nt <= 64) against the CSR source list [p0, p1);
+// seg(e) -> (row offset, count) of source set e.  Leaves the per-warp partial
+// sums in red[warp][t][r].
+template <int KER, int D, int RC, int MTX, typename SegF>
+__device__ __forceinline__ void mma_block(const double* tx, int64_t tstride, int nt, int p0,
+                                          int p1, SegF seg, const double* spts, int64_t sstride,
+                                          const double* wts, double dx, SegTable& T,
+                                          double* buf) {
+  constexpr int NT = RC / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double xt[MTX][D];
+  bool tv[MTX];
+#pragma unroll
+  for (int m = 0; m < MTX; ++m) {
     const int t = m * 8 + g;
     tv[m] = t < nt;
 #pragma unroll
     for (int a = 0; a < D; ++a) xt[m][a] = tv[m] ? tx[(int64_t)a * tstride + t] : 0.0;
   }
-  double c[MTMAX][NT][2];
+  double c[MTX][NT][2];
 #pragma unroll
-  for (int m = 0; m < MTMAX; ++m)
+  for (int m = 0; m < MTX; ++m)
 #pragma unroll
     for (int n = 0; n < NT; ++n) c[m][n][0] = c[m][n][1] = 0.0;
-  double* sc = stage;            // [D][32]
-  double* sw = stage + D * 32;   // [32][RC]
-  for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
-    const SrcSet S = src_of(e);
-    for (int s0 = 0; s0 < S.n; s0 += 32) {
-      const int cnt = min(32, S.n - s0);
-      __syncwarp();
-#pragma unroll
-      for (int a = 0; a < D; ++a) sc[a * 32 + lane] = lane < cnt ? S.pts[(int64_t)a * S.stride + s0 + lane] : 0.0;
-      for (int i = lane; i < 32 * RC; i += 32) {
-        const int si = i / RC;
-        sw[i] = si < cnt ? S.w[(int64_t)(s0 + si) * RC + (i % RC)] : 0.0;
-      }
-      __syncwarp();
-      for (int kk = 0; kk < cnt; kk += 4) {
-        const int si = kk + q;
-        const bool sv = si < cnt;
-        double ys[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + si];
-        double b[NT];
-#pragma unroll
-        for (int n = 0; n < NT; ++n) b[n] = sw[si * RC + n * 8 + g];
-#pragma unroll
-        for (int m = 0; m < MTMAX; ++m) {
-          if (m < MT) {
-            const double av = (sv && tv[m]) ? kval<KER, D>(xt[m], ys, dx) : 0.0;
-#pragma unroll
-            for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av, b[n]);
-          }
+  for (int e0 = p0; e0 < p1; e0 += MMA_SEG_CAP) {
+    const int ns = min(MMA_SEG_CAP, p1 - e0);
+    __syncthreads();
+    if (threadIdx.x == 0) T.n = ns;
+    for (int e = threadIdx.x; e < ns; e += blockDim.x) {
+      int2 oc = seg(e0 + e);
+      T.off[e] = oc.x;
+      T.pre[e + 1] = oc.y;  // lengths, prefix-summed below
+    }
+    __syncthreads();
+    if (wid == 0) {  // warp prefix sum of the lengths
+      int carry = 0;
+      for (int b0 = 0; b0 < ns; b0 += 32) {
+        int x = b0 + lane < ns ? T.pre[b0 + lane + 1] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
         }
+        if (b0 + lane < ns) T.pre[b0 + lane + 1] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
       }
+      if (lane == 0) T.pre[0] = 0;
     }
+    __syncthreads();
+    mma_warp_stream<KER, D, RC, MTX>(T, spts, sstride, wts, xt, tv, dx,
+                                     buf + wid * mma_stage_doubles<D, RC>(), c);
   }
-  __syncthreads();  // red aliases the warps' staging buffers
-  double* rw = red + wid * (MTMAX * 8 * RC);
+  __syncthreads();  // red aliases the staging buffers
+  double* rw = buf + wid * (MMA_MTMAX * 8 * RC);
 #pragma unroll
-  for (int m = 0; m < MTMAX; ++m) {
-    if (m < MT) {
+  for (int m = 0; m < MTX; ++m)
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const int t = m * 8 + g, r = n * 8 + 2 * q;
-        rw[t * RC + r] = c[m][n][0];
-        rw[t * RC + r + 1] = c[m][n][1];
-      }
+    for (int n = 0; n < NT; ++n) {
+      const int t = m * 8 + g, r = n * 8 + 2 * q;
+      rw[t * RC + r] = c[m][n][0];
+      rw[t * RC + r + 1] = c[m][n][1];
     }
+}
+
+// runtime tile count -> compile-time MTX
+template <int KER, int D, int RC, typename... Args>
+__device__ __forceinline__ void mma_block_dispatch(int mt, Args&&... args) {
+  switch (mt) {
+    case 1: mma_block<KER, D, RC, 1>(args...); break;
+    case 2: mma_block<KER, D, RC, 2>(args...); break;
+    case 3: mma_block<KER, D, RC, 3>(args...); break;
+    case 4: mma_block<KER, D, RC, 4>(args...); break;
+    case 5: mma_block<KER, D, RC, 5>(args...); break;
+    case 6: mma_block<KER, D, RC, 6>(args...); break;
+    case 7: mma_block<KER, D, RC, 7>(args...); break;
+    default: mma_block<KER, D, RC, 8>(args...); break;
   }
 }
 
@@ -420,32 +529,29 @@ __global__ void __launch_bounds__(P2P_THREADS) k_coupling_mma(int n_nodes, Side 
                                                               const int* Lptr, const int* Lsrc,
                                                               const double* qhat, double* zhat,
                                                               double dx) {
-  constexpr int MTMAX = mma_mtmax<RC>();
   __shared__ double buf[mma_smem_doubles<D, RC>()];  // per-warp staging, then the warp sums
-  double* red = buf;
+  __shared__ SegTable T;
   const int v = blockIdx.x;
   if (v >= n_nodes || v == 0) return;
   const int k = rs.rank[v];
   if (k == 0) return;
-  const int wid = threadIdx.x >> 5;
   const int p0 = Lptr[v], p1 = Lptr[v + 1];
   const int to = rs.skel_off[v];
-  auto src_of = [&](int e) {
+  auto seg = [&](int e) {
     const int j = Lsrc[e];
-    const int so = cs.skel_off[j];
-    return SrcSet{cs.skel_pts + so, cs.skel_stride, qhat + (int64_t)so * RC, cs.rank[j]};
+    return make_int2(cs.skel_off[j], cs.rank[j]);
   };
-  for (int t0 = 0; t0 < k; t0 += MTMAX * 8) {
-    const int nt = min(MTMAX * 8, k - t0);
+  for (int t0 = 0; t0 < k; t0 += MMA_MTMAX * 8) {
+    const int nt = min(MMA_MTMAX * 8, k - t0);
     __syncthreads();
-    p2p_mma_chunk<KER, D, RC>(rs.skel_pts + to + t0, rs.skel_stride, nt, p0, p1, src_of, dx,
-                              buf + wid * 32 * (D + RC), red);
+    mma_block_dispatch<KER, D, RC>((nt + 7) >> 3, rs.skel_pts + to + t0, rs.skel_stride, nt, p0,
+                                   p1, seg, cs.skel_pts, cs.skel_stride, qhat, dx, T, buf);
     __syncthreads();
     for (int e = threadIdx.x; e < nt * RC; e += blockDim.x) {
       double sum = 0.0;
       if (p1 > p0) {
-        sum = red[e];
-        for (int w = 1; w < P2P_WARPS; ++w) sum += red[w * (MTMAX * 8 * RC) + e];
+        sum = buf[e];
+        for (int w = 1; w < P2P_WARPS; ++w) sum += buf[w * (MMA_MTMAX * 8 * RC) + e];
       }
       zhat[(int64_t)(to + t0) * RC + e] = sum;
     }
@@ -458,14 +564,12 @@ __global__ void __launch_bounds__(P2P_THREADS) k_leaf_mma(
     const int* col_b, const double* pts_row, int64_t nrow, const double* pts_col, int64_t ncol,
     const int* Lmptr, const int* Lmsrc, const double* qt, const double* zhat, const int* perm_row,
     double* z, int64_t ldz, int64_t c0, double dx) {
-  constexpr int MTMAX = mma_mtmax<RC>();
   __shared__ double buf[mma_smem_doubles<D, RC>()];
-  double* red = buf;
+  __shared__ SegTable T;
   extern __shared__ double dyn[];  // zhat_v (k * RC) then inv (nr ints)
   const int li = blockIdx.x;
   if (li >= n_leaves) return;
   const int v = leaves[li];
-  const int wid = threadIdx.x >> 5;
   const int ra = row_a[v], nr = row_b[v] - ra;
   const bool has = v != 0;
   const int k = has ? rs.rank[v] : 0;
@@ -478,24 +582,23 @@ __global__ void __launch_bounds__(P2P_THREADS) k_leaf_mma(
     for (int e = threadIdx.x; e < k * RC; e += blockDim.x) zv[e] = zsrc[e];
   }
   const int p0 = Lmptr[v], p1 = Lmptr[v + 1];
-  auto src_of = [&](int e) {
+  auto seg = [&](int e) {
     const int j = Lmsrc[e];
-    const int ca = col_a[j];
-    return SrcSet{pts_col + ca, ncol, qt + (int64_t)ca * RC, col_b[j] - ca};
+    return make_int2(col_a[j], col_b[j] - col_a[j]);
   };
   const double* G = has ? rs.G + rs.g_off[v] : nullptr;
-  for (int t0 = 0; t0 < nr; t0 += MTMAX * 8) {
-    const int nt = min(MTMAX * 8, nr - t0);
+  for (int t0 = 0; t0 < nr; t0 += MMA_MTMAX * 8) {
+    const int nt = min(MMA_MTMAX * 8, nr - t0);
     __syncthreads();
-    p2p_mma_chunk<KER, D, RC>(pts_row + ra + t0, nrow, nt, p0, p1, src_of, dx,
-                              buf + wid * 32 * (D + RC), red);
+    mma_block_dispatch<KER, D, RC>((nt + 7) >> 3, pts_row + ra + t0, nrow, nt, p0, p1, seg,
+                                   pts_col, ncol, qt, dx, T, buf);
     __syncthreads();
     for (int e = threadIdx.x; e < nt * RC; e += blockDim.x) {
       const int tl = e / RC, r = e % RC, t = t0 + tl;
       double sum = 0.0;
       if (p1 > p0) {
-        sum = red[e];
-        for (int w = 1; w < P2P_WARPS; ++w) sum += red[w * (MTMAX * 8 * RC) + e];
+        sum = buf[e];
+        for (int w = 1; w < P2P_WARPS; ++w) sum += buf[w * (MMA_MTMAX * 8 * RC) + e];
       }
       double y = 0.0;
       if (k > 0) {
