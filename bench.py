@@ -243,7 +243,7 @@ def run_ours(args):
             e1.synchronize()
             mv_ms.append(e0.elapsed_time(e1))
         barrier()
-    phase = (ctypes.c_double * 5)()
+    phase = (ctypes.c_double * 7)()
     launches = ctypes.c_int64()
     lib.smash_matvec_profile(M._h, 0, phase, ctypes.byref(launches))
     t_mv = sum(mv_ms) / 1e3
@@ -296,11 +296,11 @@ def run_ours(args):
     I_near = float(np.sum(nr[Lmh[:, 0]] * ncl[Lmh[:, 1]])) if Lmh.size else 0.0
     per_int = C_K[c["kernel"]] + 2 * R
     ms_coup = phase[2] / args.steps
-    ms_leaf = phase[4] / args.steps
-    if ms_coup >= ms_leaf:
+    ms_near = phase[4] / args.steps
+    if ms_coup >= ms_near:
         dom, flops, ms = "k_coupling", I_coup * per_int, ms_coup
     else:
-        dom, flops, ms = "k_leaf", I_near * per_int, ms_leaf
+        dom, flops, ms = "k_near", I_near * per_int, ms_near
     achieved = flops / (ms / 1e3) / 1e12
     total_flops = (I_coup + I_near) * per_int
     roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
@@ -330,7 +330,9 @@ def run_ours(args):
             "config": workload_config(cfg, N, R),
             "build_s": statistics.median(build_ms) / 1e3,
             "phase_ms": {"gather": phase[0] / args.steps, "upward": phase[1] / args.steps,
-                         "coupling": ms_coup, "downward": phase[3] / args.steps, "leaves": ms_leaf},
+                         "coupling": ms_coup, "downward": phase[3] / args.steps,
+                         "nearfield_concurrent": ms_near, "leaf_farfield": phase[5] / args.steps,
+                         "matvec": phase[6] / args.steps},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gpoints/s", "h2d_bytes_per_step": int(q.nbytes),

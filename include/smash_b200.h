@@ -127,11 +127,27 @@ int smash_matrix_stats(smash_matrix_t m, int64_t* swaps_row, int64_t* swaps_col)
 /* ---- matvec: replaces smash.apply.matvec_nodewise (smash/apply.py:34-80) ----
  * q: (n_col, nrhs) row-major device, z: (n_row, nrhs) row-major device; caller order. */
 int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
-/* Matvec phase timing (CUDA events on the launch stream; synchronises each matvec while on).
- * Returns the accumulated per-phase milliseconds since the last reset
- * [gather, upward, coupling, downward, leaves] and the number of kernel launches; then
+/* Matvec phase timing (CUDA events on the launch streams; synchronises each matvec while on).
+ * Returns the accumulated per-phase milliseconds since the last reset into phase_ms[7] =
+ * [gather, upward, coupling, downward, nearfield (concurrent stream), leaf far-field, whole
+ * matvec] and the number of kernel launches; then
  * enable = 1 turns profiling on and resets, 0 turns it off and resets, -1 leaves it as is. */
 int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int64_t* launches);
+/* ---- sharded matvec (one rank of a multi-GPU job; NCCL is driven by the caller) ----
+ * Partition: own_nodes = the postorder ids of this rank's subtrees (frontier nodes and all
+ * their descendants), top_nodes = the ancestors of all frontier nodes (replicated work).
+ * Both are HOST arrays.  Stage 1: gather q and compute the coefficients qhat of the owned
+ * subtrees (all other coefficients zeroed); the caller then sums the coefficient buffer over
+ * ranks (the supports are disjoint, so this all-reduce is an all-gather of the skeleton
+ * coefficients).  Stage 2: top-level upward pass, coupling / downward /
+ * nearfield for the owned targets; writes only the owned rows of z.  nrhs: a power of two
+ * <= 16 (one chunk). */
+int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64_t n_own,
+                               const int64_t* top_nodes, int64_t n_top, void* stream);
+int smash_matvec_stage(smash_matrix_t m, int32_t stage, const double* q, double* z, int64_t nrhs,
+                       void* stream);
+/* device pointer of the coefficient buffer exchanged between stages: rows x nrhs doubles */
+int smash_matvec_coeffs(smash_matrix_t m, double** qhat, int64_t* rows);
 int smash_matrix_free(smash_matrix_t m);
 
 /* ---- exact kernel entries: replaces smash.kernel.kernel_block (smash/kernel.py:278-310)

@@ -45,6 +45,9 @@ SIGNATURES = {
     "smash_matrix_stats": (c_i32, [c_vp, P_i64, P_i64]),
     "smash_matvec": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "smash_matvec_profile": (c_i32, [c_vp, c_i32, P_dbl, P_i64]),
+    "smash_matvec_set_partition": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "smash_matvec_stage": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
+    "smash_matvec_coeffs": (c_i32, [c_vp, ctypes.POINTER(c_vp), P_i64]),
     "smash_matrix_free": (c_i32, [c_vp]),
     "smash_kernel_block": (c_i32, [c_i32, c_dbl, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "smash_interp_basis": (c_i32, [c_i32, P_dbl, P_dbl, c_vp, c_i64, c_i32, c_vp, c_vp]),

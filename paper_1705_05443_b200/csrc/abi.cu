@@ -186,6 +186,29 @@ int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, voi
   });
 }
 
+int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64_t n_own,
+                               const int64_t* top_nodes, int64_t n_top, void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
+    smash::matvec_set_partition(m->impl, own_nodes, n_own, top_nodes, n_top, st(stream));
+  });
+}
+
+int smash_matvec_stage(smash_matrix_t m, int32_t stage, const double* q, double* z, int64_t nrhs,
+                       void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
+    smash::matvec_stage(m->impl, stage, q, z, nrhs, st(stream));
+  });
+}
+
+int smash_matvec_coeffs(smash_matrix_t m, double** qhat, int64_t* rows) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl && qhat && rows, SMASH_ERR_INVALID, "null argument");
+    smash::matvec_coeffs(m->impl, qhat, rows);
+  });
+}
+
 int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int64_t* launches) {
   return guarded([&] {
     SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");

@@ -24,11 +24,70 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
+// Branch-free fp64 reciprocal: MUFU approximation + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+  }
+  return y;
+}
+
+// Branch-free natural log for positive normal x (the squared distances of the
+// log kernel): x = 2^e m, m in [sqrt(1/2), sqrt(2)), f = (m-1)/(m+1),
+// log m = 2 atanh f = 2f (1 + f^2/3 + f^4/5 + ...), |f| <= 0.1716 (11 terms).
+__device__ __forceinline__ double log_pos(double x) {
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  int e = (hi >> 20) - 1023;
+  int mh = (hi & 0x000fffff) | 0x3ff00000;
+  const bool big = mh > 0x3ff6a09e;  // m > sqrt(2) -> m / 2
+  mh = big ? mh - 0x00100000 : mh;
+  e = big ? e + 1 : e;
+  const double m = __hiloint2double(mh, lo);
+  const double f = (m - 1.0) * rcp_nr(m + 1.0);
+  const double s = f * f;
+  double p = 1.0 / 23;
+  p = fma(p, s, 1.0 / 21); p = fma(p, s, 1.0 / 19); p = fma(p, s, 1.0 / 17);
+  p = fma(p, s, 1.0 / 15); p = fma(p, s, 1.0 / 13); p = fma(p, s, 1.0 / 11);
+  p = fma(p, s, 1.0 / 9); p = fma(p, s, 1.0 / 7); p = fma(p, s, 1.0 / 5);
+  p = fma(p, s, 1.0 / 3);
+  const double f2 = f + f;
+  const double lm = fma(f2 * s, p, f2);
+  const double de = (double)e;
+  return fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, lm));
+}
+
+// Branch-free exp for x <= 0 (exp(-r) kernel): n = rint(x / ln2),
+// t = x - n ln2 (|t| <= 0.347, Cody-Waite), Taylor to degree 13, scale by 2^n.
+__device__ __forceinline__ double exp_neg(double x) {
+  const bool under = x < -708.0;
+  x = under ? -708.0 : x;
+  const double sh = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double kd = fma(x, 1.4426950408889634, sh);
+  const int n = __double2loint(kd);
+  const double nd = kd - sh;
+  double t = fma(-nd, 6.93147180369123816490e-01, x);
+  t = fma(-nd, 1.90821492927058770002e-10, t);
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = fma(p, t, 1.0 / 479001600.0); p = fma(p, t, 1.0 / 39916800.0);
+  p = fma(p, t, 1.0 / 3628800.0); p = fma(p, t, 1.0 / 362880.0);
+  p = fma(p, t, 1.0 / 40320.0); p = fma(p, t, 1.0 / 5040.0); p = fma(p, t, 1.0 / 720.0);
+  p = fma(p, t, 1.0 / 120.0); p = fma(p, t, 1.0 / 24.0); p = fma(p, t, 1.0 / 6.0);
+  p = fma(p, t, 0.5); p = fma(p, t, 1.0); p = fma(p, t, 1.0);
+  const double sc = __hiloint2double((n + 1023) << 20, 0);
+  return under ? 0.0 : p * sc;
+}
+
 template <int KER, int D>
 __device__ __forceinline__ double kval(const double* x, const double* y, double dx) {
   if (KER == SMASH_KERNEL_CAUCHY) {
-    double d = x[0] - y[0];
-    return d == 0.0 ? dx : 1.0 / d;
+    const double d = x[0] - y[0];
+    const double v = rcp_nr(d);
+    return d == 0.0 ? dx : v;
   }
   double r2 = 0.0;
 #pragma unroll
@@ -36,13 +95,17 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
     double t = x[a] - y[a];
     r2 = fma(t, t, r2);
   }
-  if (KER == SMASH_KERNEL_LOG) return r2 == 0.0 ? dx : 0.5 * log(r2);
+  if (KER == SMASH_KERNEL_LOG) {
+    const double v = 0.5 * log_pos(r2);
+    return r2 == 0.0 ? dx : v;
+  }
   if (KER == SMASH_KERNEL_INV_R) {
     const double v = rsqrt_nr(r2);
     return r2 == 0.0 ? dx : v;
   }
-  // exp(-r): r = sqrt(r2); exp(0) = 1 on the diagonal
-  return exp(-sqrt(r2));
+  // exp(-r): r = r2 * rsqrt(r2) (0 on the diagonal, exp(0) = 1)
+  const double r = r2 * rsqrt_nr(r2);
+  return exp_neg(r2 == 0.0 ? 0.0 : -r);
 }
 
 // runtime dispatch helper: f.template operator()<KER, D>()

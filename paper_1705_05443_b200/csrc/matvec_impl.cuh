@@ -1,0 +1,136 @@
+// Shared device code and launch interfaces of the matvec (K6-K10), split over
+// several translation units so the per-kernel P2P instantiations compile in
+// parallel (p2p_<kernel>.cu), see matvec.cu for the phase structure.
+#pragma once
+
+#include "kernels.cuh"
+#include "smash_impl.cuh"
+
+namespace smash {
+namespace mv {
+
+constexpr int P2P_WARPS = 4;
+constexpr int P2P_THREADS = 32 * P2P_WARPS;
+constexpr int XFER_THREADS = 256;
+constexpr int XFER_MAXO = 8;  // outputs per thread in the upward kernel (k * RC <= 2048)
+
+struct Side {
+  const int* nib;
+  const int* rank;
+  const int64_t* ib_off;
+  const int64_t* g_off;
+  const int* skel_off;
+  const int* perm;
+  const double* G;
+  const double* skel_pts;
+  int64_t skel_stride;
+};
+
+inline Side side_of(const SideFactors& F) {
+  return Side{F.nib.p, F.rank.p, F.ib_off.p, F.g_off.p, F.skel_off.p, F.perm.p, F.G.p,
+              F.skel_pts.p, F.skel_stride};
+}
+
+// coupling: zhat[v] = sum_{j in L(v)} K(S_v, S_j) qhat_j, for every non-root node
+struct CouplingArgs {
+  int n_nodes;        // number of targets (list length, or all nodes when list == nullptr)
+  const int* list;    // optional target node list (BFS ids)
+  Side rs, cs;
+  const int* Lptr;
+  const int* Lsrc;
+  const double* qhat;
+  double* zhat;
+  double dx;
+};
+
+// nearfield: z[perm_row[p]] = sum_{j in Lm(v)} K(x_p, y_s) qt_s for the rows of every leaf v
+struct NearArgs {
+  const int* leaves;
+  int n_leaves;
+  const int* row_a;
+  const int* row_b;
+  const int* col_a;
+  const int* col_b;
+  const double* pts_row;
+  int64_t nrow;
+  const double* pts_col;
+  int64_t ncol;
+  const int* Lmptr;
+  const int* Lmsrc;
+  const double* qt;
+  const int* perm_row;
+  double* z;
+  int64_t ldz;
+  int64_t c0;
+  double dx;
+};
+
+template <int KER, int D, int RC>
+void launch_coupling(const CouplingArgs& a, cudaStream_t s);
+template <int KER, int D, int RC>
+void launch_near(const NearArgs& a, cudaStream_t s);
+template <int KER, int D>
+void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx, double* out,
+                  cudaStream_t s);
+
+// transfer passes (matvec_xfer.cu)
+struct XferPlan {
+  DBuf<int> up_order;    // non-root nodes, deepest level first
+  DBuf<int> down_order;  // internal non-root nodes, shallowest level first
+  DBuf<int> leaves;
+  DBuf<unsigned char> inset_all;  // membership of the whole-tree passes (all ones)
+  DBuf<unsigned> done;   // per node epoch flags
+  DBuf<unsigned> counters;  // [0] upward tickets, [1] downward tickets
+  int n_up = 0, n_down = 0, n_leaves = 0;
+  int max_nib = 0, max_rank = 0;
+  unsigned epoch = 0;
+};
+
+struct XferArgs {
+  const int* nchild;
+  const int* child_first;
+  const int* parent;
+  const int* pt_a;  // leaf point range start (column side for the upward pass)
+  const double* qt;
+  double* qhat;
+  double* zhat;
+  Side side;
+};
+
+template <int RC>
+void launch_gather(const double* q, int64_t ldq, const int* perm, int64_t n, int64_t c0,
+                   double* qt, cudaStream_t s);
+// inset[v] != 0: v is processed by this launch (its flag must be waited for)
+template <int RC>
+void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
+                   const unsigned char* inset, cudaStream_t s);
+template <int RC>
+void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
+                     const unsigned char* inset, cudaStream_t s);
+template <int RC>
+void launch_leaf_add(const XferArgs& a, const XferPlan& P, const int* leaves, int n_leaves,
+                     const int* row_a, const int* row_b, const int* perm_row, double* z,
+                     int64_t ldz, int64_t c0, int nu0, cudaStream_t s);
+
+// Block-wide staging copy dst[e] = f(e), e < n: each thread issues U independent
+// global loads before its shared-memory stores, so a whole tile is one memory
+// round trip instead of n / blockDim dependent ones.
+template <int U, typename F, typename S>
+__device__ __forceinline__ void stage_block(int n, F load, S store) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < n ? load(e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < n) store(e, v[u]);
+    }
+  }
+}
+
+}  // namespace mv
+}  // namespace smash

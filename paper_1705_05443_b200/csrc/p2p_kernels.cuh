@@ -1,0 +1,394 @@
+// K7 / K9 point-to-point kernels: coupling and nearfield blocks generated on the
+// fly in registers (never stored) -- smash/apply.py:55-58 (coupling, with the
+// B(i, j) accessor smash/hss.py:138-148) and smash/apply.py:74-76 (nearfield,
+// NF(i, j) smash/hss.py:150-162).
+//
+// One CTA per target node (coupling: skeleton points; nearfield: leaf points).
+//  * RC = 8 / 16 right-hand-side columns: the block product is a real dense
+//    contraction, so each K tile is produced directly in the A-fragment layout of
+//    mma.sync.m8n8k4.f64 (DMMA) and multiplied by the weights' B fragments.  The
+//    source points of all partner nodes form one stream (segments = partner
+//    nodes), consumed by the 4 warps in 32-point chunks (lane = source) with a
+//    register prefetch of the next chunk; the number of 8-row target tiles is a
+//    compile-time constant per CTA (runtime switch), so the kernel evaluations
+//    of all tiles are straight-line code.
+//  * RC < 8: DFMA path, lane = target, warps split the partner list.
+// The four warps' partial sums are added in a fixed order (deterministic).
+#pragma once
+
+#include "matvec_impl.cuh"
+
+namespace smash {
+namespace mv {
+
+// ---------------------------------------------------------------------------
+// DFMA path
+// ---------------------------------------------------------------------------
+template <int KER, int D, int RC>
+__device__ __forceinline__ void p2p_sources(const double* xt, const double* ys, int64_t ystride,
+                                            const double* w, int ns, double dx, double* acc,
+                                            double* stage, int lane) {
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int cnt = min(32, ns - s0);
+    double vc[D], vw[RC];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = lane < cnt ? ys[(int64_t)a * ystride + s0 + lane] : 0.0;
+#pragma unroll
+    for (int r = 0; r < RC; ++r) vw[r] = lane < cnt ? w[(int64_t)(s0 + lane) * RC + r] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < D; ++a) stage[a * 32 + lane] = vc[a];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) stage[(D + r) * 32 + lane] = vw[r];
+    __syncwarp();
+    for (int s = 0; s < cnt; ++s) {
+      double y[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) y[a] = stage[a * 32 + s];
+      const double kv = kval<KER, D>(xt, y, dx);
+#pragma unroll
+      for (int r = 0; r < RC; ++r) acc[r] = fma(kv, stage[(D + r) * 32 + s], acc[r]);
+    }
+  }
+}
+
+// Block: lane = target (chunks of 32), warps split [p0, p1); sums into red[warp][r][32]
+// and hands (target, r, sum) to `out`.
+template <int KER, int D, int RC, typename SegF, typename OutF>
+__device__ __forceinline__ void dfma_block(const double* tx, int64_t tstride, int nt, int p0,
+                                           int p1, SegF seg, const double* spts, int64_t sstride,
+                                           const double* wts, double dx, OutF out) {
+  __shared__ double stage[P2P_WARPS][32 * (D + RC)];
+  __shared__ double red[P2P_WARPS][32 * RC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t0 = 0; t0 < nt; t0 += 32) {
+    const int t = t0 + lane;
+    double xt[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[a] = t < nt ? tx[(int64_t)a * tstride + t] : 0.0;
+    double acc[RC];
+#pragma unroll
+    for (int r = 0; r < RC; ++r) acc[r] = 0.0;
+    for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
+      const int2 oc = seg(e);
+      p2p_sources<KER, D, RC>(xt, spts + oc.x, sstride, wts + (int64_t)oc.x * RC, oc.y, dx, acc,
+                              stage[wid], lane);
+    }
+#pragma unroll
+    for (int r = 0; r < RC; ++r) red[wid][r * 32 + lane] = acc[r];
+    __syncthreads();
+    if (wid == 0 && t < nt) {
+#pragma unroll
+      for (int r = 0; r < RC; ++r) {
+        double sm = red[0][r * 32 + lane];
+        for (int w = 1; w < P2P_WARPS; ++w) sm += red[w][r * 32 + lane];
+        out(t, r, sm);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA path
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int MMA_MTMAX = 8;      // target tiles (8 rows) per pass: 64 targets
+constexpr int MMA_WSTRIDE = 36;   // staged weight row stride (doubles): 4 (mod 16) -> B reads conflict-free
+constexpr int MMA_SEG_CAP = 512;  // source segments per table fill
+
+template <int D, int RC>
+constexpr int mma_stage_doubles() { return 32 * D + MMA_WSTRIDE * RC; }
+
+template <int D, int RC>
+constexpr int mma_smem_doubles() {
+  return P2P_WARPS * MMA_MTMAX * 8 * RC > P2P_WARPS * mma_stage_doubles<D, RC>()
+             ? P2P_WARPS * MMA_MTMAX * 8 * RC
+             : P2P_WARPS * mma_stage_doubles<D, RC>();
+}
+
+struct SegTable {
+  int pre[MMA_SEG_CAP + 1];  // prefix of segment lengths
+  int off[MMA_SEG_CAP];      // segment start row in the source arrays
+  int n;
+};
+
+template <int D, int RC>
+__device__ __forceinline__ void mma_fetch(const SegTable& T, int p, int total, const double* spts,
+                                          int64_t sstride, const double* wts, double* vc,
+                                          double* vw) {
+  if (p < total) {
+    int lo = 0, hi = T.n - 1;  // last segment with pre <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (T.pre[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    const int row = T.off[lo] + (p - T.pre[lo]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = spts[(int64_t)a * sstride + row];
+    const double2* wp = reinterpret_cast<const double2*>(wts + (int64_t)row * RC);
+#pragma unroll
+    for (int u = 0; u < RC / 2; ++u) {
+      const double2 t = wp[u];
+      vw[2 * u] = t.x;
+      vw[2 * u + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < D; ++a) vc[a] = 0.0;
+#pragma unroll
+    for (int u = 0; u < RC; ++u) vw[u] = 0.0;
+  }
+}
+
+template <int KER, int D, int RC, int MTX>
+__device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double* spts,
+                                                int64_t sstride, const double* wts,
+                                                const double (&xt)[MTX][D], const bool (&tv)[MTX],
+                                                double dx, double* stage,
+                                                double (&c)[MTX][RC / 8][2]) {
+  constexpr int NT = RC / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int total = T.pre[T.n];
+  const int nch = (total + 31) >> 5;
+  const int per = (nch + P2P_WARPS - 1) / P2P_WARPS;
+  const int c0 = wid * per, c1 = min(nch, c0 + per);
+  double* sc = stage;
+  double* sw = stage + D * 32;
+  double vc[D], vw[RC];
+  if (c0 < c1) mma_fetch<D, RC>(T, c0 * 32 + lane, total, spts, sstride, wts, vc, vw);
+  for (int ch = c0; ch < c1; ++ch) {
+    const int cnt = min(32, total - ch * 32);
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < D; ++a) sc[a * 32 + lane] = vc[a];
+#pragma unroll
+    for (int u = 0; u < RC; ++u) sw[u * MMA_WSTRIDE + lane] = vw[u];
+    __syncwarp();
+    if (ch + 1 < c1) mma_fetch<D, RC>(T, (ch + 1) * 32 + lane, total, spts, sstride, wts, vc, vw);
+    for (int kk = 0; kk < cnt; kk += 4) {
+      const int si = kk + q;
+      const bool sv = si < cnt;
+      double ys[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + si];
+      double b[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = sw[(n * 8 + g) * MMA_WSTRIDE + si];
+      double av[MTX];
+#pragma unroll
+      for (int m = 0; m < MTX; ++m) {  // straight-line: padded entries selected to 0
+        const double kv = kval<KER, D>(xt[m], ys, dx);
+        av[m] = (sv && tv[m]) ? kv : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < MTX; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av[m], b[n]);
+    }
+  }
+}
+
+// Targets [0, nt) (nt <= 64) against the CSR source list [p0, p1); seg(e) ->
+// (row offset, count) of source set e.  Leaves per-warp partial sums in
+// buf[warp][t][r].
+template <int KER, int D, int RC, int MTX, typename SegF>
+__device__ __forceinline__ void mma_block(const double* tx, int64_t tstride, int nt, int p0,
+                                          int p1, SegF seg, const double* spts, int64_t sstride,
+                                          const double* wts, double dx, SegTable& T,
+                                          double* buf) {
+  constexpr int NT = RC / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double xt[MTX][D];
+  bool tv[MTX];
+#pragma unroll
+  for (int m = 0; m < MTX; ++m) {
+    const int t = m * 8 + g;
+    tv[m] = t < nt;
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[m][a] = tv[m] ? tx[(int64_t)a * tstride + t] : 0.0;
+  }
+  double c[MTX][NT][2];
+#pragma unroll
+  for (int m = 0; m < MTX; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) c[m][n][0] = c[m][n][1] = 0.0;
+  for (int e0 = p0; e0 < p1; e0 += MMA_SEG_CAP) {
+    const int ns = min(MMA_SEG_CAP, p1 - e0);
+    __syncthreads();
+    if (threadIdx.x == 0) T.n = ns;
+    for (int e = threadIdx.x; e < ns; e += blockDim.x) {
+      const int2 oc = seg(e0 + e);
+      T.off[e] = oc.x;
+      T.pre[e + 1] = oc.y;
+    }
+    __syncthreads();
+    if (wid == 0) {  // prefix sum of the segment lengths
+      int carry = 0;
+      for (int b0 = 0; b0 < ns; b0 += 32) {
+        int x = b0 + lane < ns ? T.pre[b0 + lane + 1] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (b0 + lane < ns) T.pre[b0 + lane + 1] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) T.pre[0] = 0;
+    }
+    __syncthreads();
+    mma_warp_stream<KER, D, RC, MTX>(T, spts, sstride, wts, xt, tv, dx,
+                                     buf + wid * mma_stage_doubles<D, RC>(), c);
+  }
+  __syncthreads();  // the sums alias the staging buffers
+  double* rw = buf + wid * (MMA_MTMAX * 8 * RC);
+#pragma unroll
+  for (int m = 0; m < MTX; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int t = m * 8 + g, r = n * 8 + 2 * q;
+      rw[t * RC + r] = c[m][n][0];
+      rw[t * RC + r + 1] = c[m][n][1];
+    }
+}
+
+template <int KER, int D, int RC, typename... Args>
+__device__ __forceinline__ void mma_block_dispatch(int mt, Args&&... args) {
+  switch (mt) {
+    case 1: mma_block<KER, D, RC, 1>(args...); break;
+    case 2: mma_block<KER, D, RC, 2>(args...); break;
+    case 3: mma_block<KER, D, RC, 3>(args...); break;
+    case 4: mma_block<KER, D, RC, 4>(args...); break;
+    case 5: mma_block<KER, D, RC, 5>(args...); break;
+    case 6: mma_block<KER, D, RC, 6>(args...); break;
+    case 7: mma_block<KER, D, RC, 7>(args...); break;
+    default: mma_block<KER, D, RC, 8>(args...); break;
+  }
+}
+
+// Targets [0, nt) in 64-row passes; out(t, r, value).
+template <int KER, int D, int RC, typename SegF, typename OutF>
+__device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int nt, int p0, int p1,
+                                          SegF seg, const double* spts, int64_t sstride,
+                                          const double* wts, double dx, OutF out) {
+  if constexpr (RC == 8 || RC == 16) {
+    __shared__ double buf[mma_smem_doubles<D, RC>()];
+    __shared__ SegTable T;
+    for (int t0 = 0; t0 < nt; t0 += MMA_MTMAX * 8) {
+      const int n = min(MMA_MTMAX * 8, nt - t0);
+      __syncthreads();
+      mma_block_dispatch<KER, D, RC>((n + 7) >> 3, tx + t0, tstride, n, p0, p1, seg, spts, sstride,
+                                     wts, dx, T, buf);
+      __syncthreads();
+      for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
+        double sm = 0.0;
+        if (p1 > p0) {
+          sm = buf[e];
+          for (int w = 1; w < P2P_WARPS; ++w) sm += buf[w * (MMA_MTMAX * 8 * RC) + e];
+        }
+        out(t0 + e / RC, e % RC, sm);
+      }
+    }
+  } else {
+    dfma_block<KER, D, RC>(tx, tstride, nt, p0, p1, seg, spts, sstride, wts, dx, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_coupling(CouplingArgs A) {
+  if ((int)blockIdx.x >= A.n_nodes) return;
+  const int v = A.list ? A.list[blockIdx.x] : (int)blockIdx.x;
+  if (v == 0) return;  // the root has no factor and no coupling
+  const int k = A.rs.rank[v];
+  if (k == 0) return;
+  const int to = A.rs.skel_off[v];
+  const Side cs = A.cs;
+  const int* Lsrc = A.Lsrc;
+  auto seg = [&](int e) {
+    const int j = Lsrc[e];
+    return make_int2(cs.skel_off[j], cs.rank[j]);
+  };
+  double* zo = A.zhat + (int64_t)to * RC;
+  p2p_block<KER, D, RC>(A.rs.skel_pts + to, A.rs.skel_stride, k, A.Lptr[v], A.Lptr[v + 1], seg,
+                        cs.skel_pts, cs.skel_stride, A.qhat, A.dx,
+                        [&](int t, int r, double val) { zo[(int64_t)t * RC + r] = val; });
+}
+
+template <int KER, int D, int RC>
+__global__ void __launch_bounds__(P2P_THREADS) k_near(NearArgs A) {
+  const int li = blockIdx.x;
+  if (li >= A.n_leaves) return;
+  const int v = A.leaves[li];
+  const int ra = A.row_a[v], nr = A.row_b[v] - ra;
+  const int* col_a = A.col_a;
+  const int* col_b = A.col_b;
+  const int* Lmsrc = A.Lmsrc;
+  auto seg = [&](int e) {
+    const int j = Lmsrc[e];
+    return make_int2(col_a[j], col_b[j] - col_a[j]);
+  };
+  const int* pr = A.perm_row + ra;
+  double* z = A.z;
+  const int64_t ldz = A.ldz, c0 = A.c0;
+  p2p_block<KER, D, RC>(A.pts_row + ra, A.nrow, nr, A.Lmptr[v], A.Lmptr[v + 1], seg, A.pts_col,
+                        A.ncol, A.qt, A.dx,
+                        [&](int t, int r, double val) { z[(int64_t)pr[t] * ldz + c0 + r] = val; });
+}
+
+template <int KER, int D>
+__global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx,
+                        double* out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nx * ny) return;
+  int64_t i = e / ny, j = e % ny;
+  double x[D], y[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) { x[a] = X[i * D + a]; y[a] = Y[j * D + a]; }
+  out[e] = kval<KER, D>(x, y, dx);
+}
+
+// ---------------------------------------------------------------------------
+// launchers (explicitly instantiated per kernel in p2p_<kernel>.cu)
+// ---------------------------------------------------------------------------
+template <int KER, int D, int RC>
+void launch_coupling(const CouplingArgs& a, cudaStream_t s) {
+  if (a.n_nodes > 0) k_coupling<KER, D, RC><<<a.n_nodes, P2P_THREADS, 0, s>>>(a);
+}
+
+template <int KER, int D, int RC>
+void launch_near(const NearArgs& a, cudaStream_t s) {
+  if (a.n_leaves > 0) k_near<KER, D, RC><<<a.n_leaves, P2P_THREADS, 0, s>>>(a);
+}
+
+template <int KER, int D>
+void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx, double* out,
+                  cudaStream_t s) {
+  if (nx * ny > 0) k_block<KER, D><<<cdiv(nx * ny, 256), 256, 0, s>>>(X, nx, Y, ny, dx, out);
+}
+
+#define SMASH_P2P_INSTANTIATE(KER, D)                                                 \
+  template void launch_coupling<KER, D, 1>(const CouplingArgs&, cudaStream_t);        \
+  template void launch_coupling<KER, D, 2>(const CouplingArgs&, cudaStream_t);        \
+  template void launch_coupling<KER, D, 4>(const CouplingArgs&, cudaStream_t);        \
+  template void launch_coupling<KER, D, 8>(const CouplingArgs&, cudaStream_t);        \
+  template void launch_coupling<KER, D, 16>(const CouplingArgs&, cudaStream_t);       \
+  template void launch_near<KER, D, 1>(const NearArgs&, cudaStream_t);                \
+  template void launch_near<KER, D, 2>(const NearArgs&, cudaStream_t);                \
+  template void launch_near<KER, D, 4>(const NearArgs&, cudaStream_t);                \
+  template void launch_near<KER, D, 8>(const NearArgs&, cudaStream_t);                \
+  template void launch_near<KER, D, 16>(const NearArgs&, cudaStream_t);               \
+  template void launch_block<KER, D>(const double*, int64_t, const double*, int64_t,  \
+                                     double, double*, cudaStream_t);
+
+}  // namespace mv
+}  // namespace smash

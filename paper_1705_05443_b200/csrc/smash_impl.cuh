@@ -98,14 +98,20 @@ struct MatrixImpl {
   // matvec workspaces
   DBuf<double> qt, qhat, zhat;
   int64_t ws_nrhs = 0;
-  // optional per-phase timing of the matvec (CUDA events on the launch stream)
+  // optional per-phase timing of the matvec (CUDA events on the launch streams)
   bool profile = false;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  double phase_ms[5] = {0, 0, 0, 0, 0};  // gather, upward, coupling, downward, leaves
+  cudaEvent_t ev[9] = {};
+  double phase_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // gather, up, coupling, down, near, leaf-add, total
   int64_t launches = 0;
+  // nearfield stream (runs concurrently with the far-field chain) + fork/join events
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   ~MatrixImpl() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s2) cudaStreamDestroy(s2);
   }
 };
 
@@ -115,6 +121,11 @@ void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t
                    cudaStream_t s);
 void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
 void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launches);
+void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
+                          const int64_t* top_post, int64_t n_top, cudaStream_t s);
+void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t nrhs,
+                  cudaStream_t s);
+void matvec_coeffs(MatrixImpl* m, double** qhat, int64_t* rows);
 
 void kernel_block(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
                   int64_t ny, double* out, cudaStream_t s);
