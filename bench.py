@@ -15,9 +15,10 @@ host (pinned) buffers and the host<->device copies inside the timed region.
 Usage:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config C] [--nrhs R] [--N n]
-For N > 1 run under torchrun: every rank builds and applies its own replica
-(the path is replicated), value = sum over ranks,
-time = max over ranks.
+For N > 1 run under torchrun: every rank builds the (replicated) matrix; the
+matvec is sharded by subtree (shard.py) with one NCCL exchange of the skeleton
+coefficients per matvec -- strong scaling of the fixed problem; time = max over
+ranks, value = N * nrhs / time.
 """
 
 from __future__ import annotations
@@ -151,7 +152,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "SMASH build time + H^2 matvec Gpoints/s (fp64), 1/2/4/8 B200, % roofline",
         "value": val, "unit": "Gpoints/s", "n_gpus": args.gpus, "steps": steps, "warmup": 1,
-        "ms_per_step": t_mv * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_mv * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
         "config": workload_config(cfg, N, args.nrhs),
         "build_s": t_build,
@@ -225,10 +226,22 @@ def run_ours(args):
         build_ms.append(e0.elapsed_time(e1))
     barrier()
 
-    # ---- matvec: W warm-up + K timed, L2 flushed between timed matvecs
+    # ---- matvec: W warm-up + K timed, L2 flushed between timed matvecs.
+    # N > 1: the sharded matvec (strong scaling of the fixed problem): every rank
+    # holds the replicated matrix and q, computes its owned rows, and the skeleton
+    # coefficients are exchanged once per matvec over NCCL (shard.py).
     out = torch.empty((M.n_row, R), dtype=torch.float64, device=dev)
+    if ws > 1:
+        from paper_1705_05443_b200.shard import ShardedMatvec
+        sm = ShardedMatvec(M)
+
+        def apply():
+            return sm(dQ, gather_output=False)
+    else:
+        def apply():
+            return sg.matvec_device(M, dQ, out)
     for _ in range(args.warmup):
-        sg.matvec_device(M, dQ, out)
+        apply()
     lib = _lib.load()
     import ctypes
     lib.smash_matvec_profile(M._h, 1, None, None)
@@ -237,12 +250,15 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
+            barrier() if ws > 1 else None
             e0.record()
-            sg.matvec_device(M, dQ, out)
+            res = apply()
             e1.record()
             e1.synchronize()
             mv_ms.append(e0.elapsed_time(e1))
         barrier()
+    if ws > 1:
+        out = res
     phase = (ctypes.c_double * 7)()
     launches = ctypes.c_int64()
     lib.smash_matvec_profile(M._h, 0, phase, ctypes.byref(launches))
@@ -252,7 +268,7 @@ def run_ours(args):
         t = torch.tensor([t_mv, max(build_ms)], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_mv = float(t[0])
-    value = ws * args.steps * M.n_row * R / t_mv / 1e9
+    value = args.steps * M.n_row * R / t_mv / 1e9
 
     # ---- e2e through the public API with pinned host buffers
     q_pin = torch.from_numpy(q).pin_memory()
@@ -261,7 +277,13 @@ def run_ours(args):
     for i in range(args.warmup + args.steps):
         flush.zero_()
         e0.record()
-        z = sg.matvec_nodewise(M, q_pin)
+        if ws > 1:
+            zg = sm(q_pin.to(dev, non_blocking=True), gather_output=True)
+            z = torch.empty(zg.shape, dtype=torch.float64, pin_memory=True)
+            z.copy_(zg, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            z = sg.matvec_nodewise(M, q_pin)
         e1.record()
         e1.synchronize()
         if i >= args.warmup:
@@ -276,11 +298,21 @@ def run_ours(args):
         e1.synchronize()
         if i >= args.warmup:
             e2e_build.append(e0.elapsed_time(e1))
-    e2e_val = ws * M.n_row * R / (np.mean(e2e_mv) / 1e3) / 1e9
+    t_e2e = float(np.mean(e2e_mv)) / 1e3
+    if ws > 1:
+        t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t[0])
+    e2e_val = M.n_row * R / t_e2e / 1e9
 
     # ---- parity spot check of the timed output (device result vs public-API result)
-    zd = out.cpu().numpy()
-    assert np.allclose(zd, z.numpy(), rtol=0, atol=0), "device and e2e results differ"
+    if ws == 1:
+        zd = out.cpu().numpy()
+        assert np.allclose(zd, z.numpy(), rtol=0, atol=0), "device and e2e results differ"
+    else:  # sharded (full, gathered) vs the single-GPU matvec
+        zf = sg.matvec_device(M, dQ).cpu().numpy()
+        rel = np.linalg.norm(z.numpy() - zf) / np.linalg.norm(zf)
+        assert rel <= 1e-12, "sharded matvec differs from the single-GPU one: %g" % rel
 
     # ---- roofline of the dominant kernel (coupling or leaf P2P)
     L, Lm = sg.leaf_sets(M.tree, c["tau"], c["structure"])
@@ -309,7 +341,7 @@ def run_ours(args):
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "flops_per_launch": flops, "ms_per_launch": ms,
                 "c_K": C_K[c["kernel"]], "interactions_coupling": I_coup, "interactions_near": I_near,
-                "matvec_total_frac": total_flops / (t_mv / (ws * args.steps)) / 1e12 / FP64_PEAK_TFLOPS}
+                "matvec_total_frac": total_flops / (t_mv / args.steps) / 1e12 / (ws * FP64_PEAK_TFLOPS)}
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0, N = 1 only
     cpu = None
@@ -325,7 +357,7 @@ def run_ours(args):
         line = {
             "metric": "SMASH build time + H^2 matvec Gpoints/s (fp64), 1/2/4/8 B200, % roofline",
             "value": value, "unit": "Gpoints/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_mv * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_mv * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
             "config": workload_config(cfg, N, R),
             "build_s": statistics.median(build_ms) / 1e3,
