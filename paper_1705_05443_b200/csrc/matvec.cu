@@ -12,6 +12,7 @@
 //   near stream:  K9a nearfield z[perm_row] = sum_{j in Lm(v)} K(P_v, P_j) qt_j (apply.py:74-80)
 // The nearfield only needs qt, so it overlaps the whole far-field chain.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 
 #include "matvec_impl.cuh"
@@ -47,6 +48,21 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   }
   P->max_nib = mx;
   P->max_rank = mr;
+  {  // largest leaf |ibar| over both sides (the leaf upward kernel's shared memory)
+    std::vector<int> nl(n);
+    int ml = 1;
+    d2h(nl.data(), m->rowf.nib.p, n, s);
+    sync(s);
+    for (int v = 0; v < n; ++v)
+      if (nchild[v] == 0) ml = std::max(ml, nl[v]);
+    if (m->colf != &m->rowf) {
+      d2h(nl.data(), m->colf->nib.p, n, s);
+      sync(s);
+      for (int v = 0; v < n; ++v)
+        if (nchild[v] == 0) ml = std::max(ml, nl[v]);
+    }
+    P->max_leaf_nib = ml;
+  }
   // ticket orders: BFS ids are level-major, so deepest level first = descending
   // level blocks; within a level any order works.
   std::vector<int> up, down, leaves;
@@ -66,6 +82,18 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   h2d(P->up_order.p, up.data(), up.size(), s);
   h2d(P->down_order.p, down.data(), down.size(), s);
   h2d(P->leaves.p, leaves.data(), leaves.size(), s);
+  std::vector<int> up_int;
+  std::vector<unsigned char> in_int(n, 0);
+  for (int v : up)
+    if (nchild[v] > 0) {
+      up_int.push_back(v);
+      in_int[v] = 1;
+    }
+  P->n_up_int = (int)up_int.size();
+  P->up_int.alloc(std::max<size_t>(up_int.size(), 1), s);
+  h2d(P->up_int.p, up_int.data(), up_int.size(), s);
+  P->inset_int.alloc(n, s);
+  h2d(P->inset_int.p, in_int.data(), n, s);
   P->done.alloc(n, s);
   P->done.zero(s);
   P->inset_all.alloc(n, s);
@@ -81,7 +109,8 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
 struct PhaseSets {
   bool gather = true;
   bool zero_qhat = false;                 // shard: unowned coefficients must be 0 for the all-reduce
-  const int* up = nullptr; int n_up = 0;  // upward order (deepest level first)
+  const int* up_leaves = nullptr; int n_up_leaves = 0;  // leaves (independent, one CTA each)
+  const int* up = nullptr; int n_up = 0;  // internal upward order (deepest level first)
   const unsigned char* up_in = nullptr;   // membership of the upward / downward sets
   const unsigned char* down_in = nullptr;
   bool far = true;                        // run coupling / downward / nearfield / leaf far field
@@ -92,7 +121,7 @@ struct PhaseSets {
 
 template <int KER, int D, int RC>
 void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q, double* z,
-               int64_t nrhs, int64_t c0, cudaStream_t s) {
+               int64_t nrhs, int64_t c0, cudaStream_t s, cudaEvent_t* ev, int* nlaunch) {
   TreeImpl* t = m->tree;
   const SideFactors& R = m->rowf;
   const SideFactors& C = *m->colf;
@@ -103,8 +132,8 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
   static const bool serial = getenv("SMASH_MATVEC_SERIAL") != nullptr;  // profiling aid
   cudaStream_t sn = serial ? s : m->s2;
-  auto mark = [&](int i, cudaStream_t st) {
-    if (m->profile) SMASH_CUDA(cudaEventRecord(m->ev[i], st));
+  auto mark = [&](int i, cudaStream_t st) {  // external record: a timing node in the graph
+    if (ev) SMASH_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
   };
   int launches = 0;
   mark(0, s);
@@ -123,14 +152,17 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     mark(6, sn);
     NearArgs na{S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
                 pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, t->perm_row.p, z, nrhs,
-                c0, m->p.dx};
+                c0, m->p.dx, t->nu0};
     launch_near<KER, D, RC>(na, sn);
     ++launches;
     mark(7, sn);
     SMASH_CUDA(cudaEventRecord(m->join, sn));
   }
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, m->qt.p, m->qhat.p, m->zhat.p, cs};
-  ++P.epoch;
+  if (S.n_up_leaves) {
+    launch_upward_leaves<RC>(up, P, S.up_leaves, S.n_up_leaves, s);
+    launches += 1;
+  }
   if (S.n_up) {
     launch_upward<RC>(up, P, S.up, S.n_up, S.up_in, s);
     launches += 2;
@@ -138,13 +170,12 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   mark(2, s);
   if (S.far) {
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
-                    m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx};
+                    m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
     launch_coupling<KER, D, RC>(ca, s);
     ++launches;
     mark(3, s);
     XferArgs down{t->nchild.p, t->child_first.p, t->parent.p, t->row_a.p, m->qt.p, m->qhat.p,
                   m->zhat.p, rs};
-    ++P.epoch;
     if (S.n_down) {
       launch_downward<RC>(down, P, S.down, S.n_down, S.down_in, s);
       launches += 2;
@@ -157,29 +188,101 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     ++launches;
   }
   mark(5, s);
-  m->launches += launches;
-  if (m->profile && S.far) {
-    SMASH_CUDA(cudaEventSynchronize(m->ev[5]));
-    const int pairs[7][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {6, 7}, {8, 5}, {0, 5}};
-    for (int i = 0; i < 7; ++i) {
-      float ms = 0;
-      SMASH_CUDA(cudaEventElapsedTime(&ms, m->ev[pairs[i][0]], m->ev[pairs[i][1]]));
-      m->phase_ms[i] += ms;
-    }
+  *nlaunch += launches;
+}
+
+// chunk sizes of an nrhs split (largest power of two <= 16 and <= rc_cap first)
+std::vector<int> chunks_of(int64_t nrhs, int rc_cap) {
+  std::vector<int> out;
+  int64_t left = nrhs;
+  while (left > 0) {
+    int c = 16;
+    while (c > 1 && (c > left || c > rc_cap)) c >>= 1;
+    out.push_back(c);
+    left -= c;
   }
+  return out;
 }
 
 template <int KER, int D>
 void run_all(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q, double* z,
-             int64_t nrhs, int rc_cap, cudaStream_t s) {
+             int64_t nrhs, int rc_cap, cudaStream_t s, std::vector<std::array<cudaEvent_t, 9>>* evs,
+             int* nlaunch) {
   int64_t c0 = 0;
-  while (c0 < nrhs) {
-    const int64_t left = std::min<int64_t>(nrhs - c0, rc_cap);
-    if (left >= 16) { run_chunk<KER, D, 16>(m, P, S, q, z, nrhs, c0, s); c0 += 16; }
-    else if (left >= 8) { run_chunk<KER, D, 8>(m, P, S, q, z, nrhs, c0, s); c0 += 8; }
-    else if (left >= 4) { run_chunk<KER, D, 4>(m, P, S, q, z, nrhs, c0, s); c0 += 4; }
-    else if (left >= 2) { run_chunk<KER, D, 2>(m, P, S, q, z, nrhs, c0, s); c0 += 2; }
-    else { run_chunk<KER, D, 1>(m, P, S, q, z, nrhs, c0, s); c0 += 1; }
+  int ci = 0;
+  for (int c : chunks_of(nrhs, rc_cap)) {
+    cudaEvent_t* ev = evs ? (*evs)[ci].data() : nullptr;
+    if (c == 16) run_chunk<KER, D, 16>(m, P, S, q, z, nrhs, c0, s, ev, nlaunch);
+    else if (c == 8) run_chunk<KER, D, 8>(m, P, S, q, z, nrhs, c0, s, ev, nlaunch);
+    else if (c == 4) run_chunk<KER, D, 4>(m, P, S, q, z, nrhs, c0, s, ev, nlaunch);
+    else if (c == 2) run_chunk<KER, D, 2>(m, P, S, q, z, nrhs, c0, s, ev, nlaunch);
+    else run_chunk<KER, D, 1>(m, P, S, q, z, nrhs, c0, s, ev, nlaunch);
+    c0 += c;
+    ++ci;
+  }
+}
+
+// Captured matvec: one CUDA graph per (q, z, nrhs, stage); replays cost one launch.
+struct GraphEntry {
+  const double* q = nullptr;
+  double* z = nullptr;
+  int64_t nrhs = 0;
+  int stage = 0;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<std::array<cudaEvent_t, 9>> ev;
+  bool far = true;
+  int launches = 0;
+  ~GraphEntry() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto& a : ev)
+      for (auto e : a)
+        if (e) cudaEventDestroy(e);
+  }
+};
+std::map<const MatrixImpl*, std::vector<std::unique_ptr<GraphEntry>>> g_graphs;
+
+template <typename F>
+GraphEntry* graph_for(MatrixImpl* m, const double* q, double* z, int64_t nrhs, int stage,
+                      int n_chunks, bool far, F record) {
+  cudaStream_t s = m->sc;  // captured work is recorded on the capture stream
+  auto& L = g_graphs[m];
+  for (auto& e : L)
+    if (e->q == q && e->z == z && e->nrhs == nrhs && e->stage == stage) return e.get();
+  std::unique_ptr<GraphEntry> E(new GraphEntry());
+  E->q = q; E->z = z; E->nrhs = nrhs; E->stage = stage; E->far = far;
+  E->ev.resize(n_chunks);
+  for (auto& a : E->ev)
+    for (auto& e : a) SMASH_CUDA(cudaEventCreate(&e));
+  cudaGraph_t g = nullptr;
+  SMASH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  try {
+    record(&E->ev, &E->launches);
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  SMASH_CUDA(cudaStreamEndCapture(s, &g));
+  SMASH_CUDA(cudaGraphInstantiate(&E->exec, g, 0));
+  SMASH_CUDA(cudaGraphDestroy(g));
+  if (L.size() >= 8) L.erase(L.begin());
+  L.push_back(std::move(E));
+  return L.back().get();
+}
+
+void replay(MatrixImpl* m, GraphEntry* E, cudaStream_t s) {
+  SMASH_CUDA(cudaGraphLaunch(E->exec, s));
+  m->launches += E->launches;
+  if (m->profile && E->far) {
+    const int pairs[7][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {6, 7}, {8, 5}, {0, 5}};
+    for (auto& ev : E->ev) {
+      SMASH_CUDA(cudaEventSynchronize(ev[5]));
+      for (int i = 0; i < 7; ++i) {
+        float ms = 0;
+        SMASH_CUDA(cudaEventElapsedTime(&ms, ev[pairs[i][0]], ev[pairs[i][1]]));
+        m->phase_ms[i] += ms;
+      }
+    }
   }
 }
 
@@ -193,6 +296,7 @@ int prepare(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
   TreeImpl* t = m->tree;
   if (!m->s2) {
     SMASH_CUDA(cudaStreamCreateWithFlags(&m->s2, cudaStreamNonBlocking));
+    SMASH_CUDA(cudaStreamCreateWithFlags(&m->sc, cudaStreamNonBlocking));
     SMASH_CUDA(cudaEventCreateWithFlags(&m->fork, cudaEventDisableTiming));
     SMASH_CUDA(cudaEventCreateWithFlags(&m->join, cudaEventDisableTiming));
   }
@@ -204,10 +308,12 @@ int prepare(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
   }
   // largest nrhs chunk whose transfer-kernel shared memory and registers fit
   int rc_cap = 16;
-  while (rc_cap > 1 && (((size_t)P->max_nib * rc_cap + 4096 + 64) * sizeof(double) > 200 * 1024 ||
-                        P->max_rank * rc_cap > XFER_THREADS * XFER_MAXO))
+  auto xfer_smem = [&](int rc) {
+    return ((size_t)P->max_rank * rc + (size_t)P->max_nib * (2 * rc + 1) + 4096 + 64) * sizeof(double);
+  };
+  while (rc_cap > 1 && (xfer_smem(rc_cap) > 200 * 1024 || P->max_rank * rc_cap > XFER_THREADS * XFER_MAXO))
     rc_cap /= 2;
-  SMASH_CHECK(((size_t)P->max_nib * rc_cap + 4096 + 64) * sizeof(double) <= 227 * 1024 &&
+  SMASH_CHECK(xfer_smem(rc_cap) <= 227 * 1024 &&
                   P->max_rank <= XFER_THREADS * XFER_MAXO,
               SMASH_ERR_INVALID, "intermediate sets too large for the matvec");
   return rc_cap;
@@ -229,13 +335,19 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
   MatvecPlan* P = plan_of(m, s);
   const int rc_cap = prepare(m, P, s);
   PhaseSets S;
-  S.up = P->up_order.p; S.n_up = P->n_up;
-  S.up_in = S.down_in = P->inset_all.p;
+  S.up_leaves = P->leaves.p; S.n_up_leaves = P->n_leaves;
+  S.up = P->up_int.p; S.n_up = P->n_up_int;
+  S.up_in = P->inset_int.p;
+  S.down_in = P->inset_all.p;
   S.down = P->down_order.p; S.n_down = P->n_down;
   S.leaves = P->leaves.p; S.n_leaves = P->n_leaves;
-  dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
-    run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, s);
+  const int nch = (int)chunks_of(nrhs, rc_cap).size();
+  GraphEntry* E = graph_for(m, q, z, nrhs, 0, nch, true, [&](auto* evs, int* nl) {
+    dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
+      run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, m->sc, evs, nl);
+    });
   });
+  replay(m, E, s);
   SMASH_CUDA(cudaGetLastError());
 }
 
@@ -259,7 +371,9 @@ void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
     return out;
   };
   std::vector<int> own = to_bfs(own_post, n_own), top = to_bfs(top_post, n_top);
-  std::vector<int> own_up = own, top_up = top, coup = own, down, leaves;
+  std::vector<int> own_up, top_up = top, coup = own, down, leaves;
+  for (int v : own)
+    if (nchild[v] > 0) own_up.push_back(v);  // owned leaves go through the leaf kernel
   std::sort(own_up.rbegin(), own_up.rend());  // BFS is level-major: descending = deepest first
   std::sort(top_up.rbegin(), top_up.rend());
   coup.insert(coup.end(), top.begin(), top.end());
@@ -290,6 +404,10 @@ void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
   member(S->down_in, down);
   sync(s);
   g_shards[m] = std::move(S);
+  auto& L = g_graphs[m];  // stage graphs captured for an older partition are stale
+  L.erase(std::remove_if(L.begin(), L.end(), [](const std::unique_ptr<GraphEntry>& e) {
+            return e->stage != 0;
+          }), L.end());
 }
 
 void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t nrhs,
@@ -306,6 +424,7 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
   PhaseSets S;
   if (stage == 1) {  // local upward of the owned subtrees; unowned coefficients 0
     S.zero_qhat = true;
+    S.up_leaves = H.leaves.p; S.n_up_leaves = H.n_leaves;
     S.up = H.own_up.p; S.n_up = H.n_own_up; S.up_in = H.own_in.p;
     S.far = false;
   } else {  // after the coefficient exchange: top upward, then owned far/near field
@@ -315,9 +434,12 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
     S.down = H.down.p; S.n_down = H.n_down; S.down_in = H.down_in.p;
     S.leaves = H.leaves.p; S.n_leaves = H.n_leaves;
   }
-  dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
-    run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, s);
+  GraphEntry* E = graph_for(m, q, z, nrhs, stage, 1, stage == 2, [&](auto* evs, int* nl) {
+    dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
+      run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, m->sc, evs, nl);
+    });
   });
+  replay(m, E, s);
   SMASH_CUDA(cudaGetLastError());
 }
 
@@ -327,6 +449,7 @@ void matvec_coeffs(MatrixImpl* m, double** qhat, int64_t* rows) {
 }
 
 void matvec_release_plan(const MatrixImpl* m) {
+  g_graphs.erase(m);
   g_plans.erase(m);
   g_shards.erase(m);
 }

@@ -41,6 +41,7 @@ struct CouplingArgs {
   const double* qhat;
   double* zhat;
   double dx;
+  int max_targets;  // largest target set (skeleton rank) -> CTA size of the DMMA path
 };
 
 // nearfield: z[perm_row[p]] = sum_{j in Lm(v)} K(x_p, y_s) qt_s for the rows of every leaf v
@@ -63,6 +64,7 @@ struct NearArgs {
   int64_t ldz;
   int64_t c0;
   double dx;
+  int max_targets;  // largest leaf row count
 };
 
 template <int KER, int D, int RC>
@@ -82,7 +84,10 @@ struct XferPlan {
   DBuf<unsigned> done;   // per node epoch flags
   DBuf<unsigned> counters;  // [0] upward tickets, [1] downward tickets
   int n_up = 0, n_down = 0, n_leaves = 0;
-  int max_nib = 0, max_rank = 0;
+  int max_nib = 0, max_rank = 0, max_leaf_nib = 0;
+  DBuf<int> up_int;                 // internal non-root nodes, deepest level first
+  DBuf<unsigned char> inset_int;    // 1 for internal non-root nodes
+  int n_up_int = 0;
   unsigned epoch = 0;
 };
 
@@ -104,6 +109,9 @@ void launch_gather(const double* q, int64_t ldq, const int* perm, int64_t n, int
 template <int RC>
 void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
                    const unsigned char* inset, cudaStream_t s);
+template <int RC>
+void launch_upward_leaves(const XferArgs& a, const XferPlan& P, const int* leaves, int n,
+                          cudaStream_t s);
 template <int RC>
 void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
                      const unsigned char* inset, cudaStream_t s);

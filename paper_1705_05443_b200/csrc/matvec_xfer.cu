@@ -6,7 +6,7 @@
 // launch per level (the small top levels are pure latency), each pass is ONE
 // persistent launch: CTAs take node tickets from an atomic counter in level
 // order (deepest first upward, shallowest first downward) and spin on the
-// producers' epoch flags, which were necessarily handed out earlier to CTAs
+// producers' done flags, which were necessarily handed out earlier to CTAs
 // that are already running -- so the wait cannot deadlock.  Cross-CTA data is
 // published with __threadfence() + a release flag and read with __ldcg (L2).
 // X_v = P [I; G] is applied implicitly; G row tiles are staged in shared memory
@@ -53,13 +53,102 @@ __device__ __forceinline__ void publish(unsigned* done, int v, unsigned epoch) {
 }
 
 // qhat[v] = ivec[perm[:k]] + G^T ivec[perm[k:]]
+// The node's ibar-vector is ONE contiguous block (leaf: its qt rows; internal:
+// its children's coefficient rows), so it is staged in the same batched load as
+// the permutation and the first G tile: one memory round trip per node.
+template <int RC>
+__device__ __forceinline__ void up_node(const XferArgs& A, int v, double* sh) {
+  const Side& cs = A.side;
+  const int nc = A.nchild[v];
+    const int ni = cs.nib[v], k = cs.rank[v];
+    if (k > 0) {
+      const bool leaf = nc == 0;
+      const double* ivec = leaf ? A.qt + (int64_t)A.pt_a[v] * RC
+                                : A.qhat + (int64_t)cs.skel_off[A.child_first[v]] * RC;
+      const int* perm = cs.perm + cs.ib_off[v];
+      const double* G = cs.G + cs.g_off[v];
+      const int nk = ni - k;
+      const int TB = g_tile_rows(k);
+      double* iv = sh;                 // ni * RC, unpermuted
+      double* pm = iv + ni * RC;       // ni permutation entries (as doubles)
+      double* gs = pm + ni;            // TB * k
+      const int n_iv = ni * RC, n_g0 = min(TB, nk) * k;
+      stage_block<16>(n_iv + ni + n_g0,
+                      [&](int e) {
+                        return e < n_iv ? __ldcg(ivec + e)
+                                        : e < n_iv + ni ? (double)perm[e - n_iv]
+                                                        : G[e - n_iv - ni];
+                      },
+                      [&](int e, double x) { iv[e] = x; });
+      __syncthreads();
+      // gather the permuted ibar rows once: ivp[c] = iv[perm[c]] (after gs, reusing pm's slot
+      // would alias; ivp lives after the G tile)
+      double* ivp = gs + TB * k;
+      for (int e = threadIdx.x; e < ni * RC; e += blockDim.x)
+        ivp[e] = iv[(int)pm[e / RC] * RC + e % RC];
+      __syncthreads();
+      // register tile: TA rows (a) x TR columns (r) per thread
+      constexpr int TR = RC < 4 ? RC : 4;
+      constexpr int TA = 2;
+      const int na = (k + TA - 1) / TA, nrq = RC / TR;
+      const int items = na * nrq;
+      for (int it0 = 0; it0 < items; it0 += blockDim.x) {
+        const int it = it0 + threadIdx.x;
+        const bool ok = it < items;
+        const int a0 = ok ? (it / nrq) * TA : 0, r0 = ok ? (it % nrq) * TR : 0;
+        double acc[TA][TR];
+#pragma unroll
+        for (int i = 0; i < TA; ++i)
+#pragma unroll
+          for (int j = 0; j < TR; ++j)
+            acc[i][j] = (ok && a0 + i < k) ? ivp[(a0 + i) * RC + r0 + j] : 0.0;
+        for (int b0 = 0; b0 < nk; b0 += TB) {
+          const int tb = min(TB, nk - b0);
+          if (b0 > 0) {
+            __syncthreads();
+            const double* src = G + (int64_t)b0 * k;
+            stage_block<16>(tb * k, [&](int e) { return src[e]; }, [&](int e, double x) { gs[e] = x; });
+            __syncthreads();
+          }
+          if (ok) {
+            const double* wb = ivp + (k + b0) * RC + r0;
+            for (int bb = 0; bb < tb; ++bb) {
+              double g[TA], w[TR];
+#pragma unroll
+              for (int i = 0; i < TA; ++i) g[i] = a0 + i < k ? gs[bb * k + a0 + i] : 0.0;
+#pragma unroll
+              for (int j = 0; j < TR; ++j) w[j] = wb[bb * RC + j];
+#pragma unroll
+              for (int i = 0; i < TA; ++i)
+#pragma unroll
+                for (int j = 0; j < TR; ++j) acc[i][j] = fma(g[i], w[j], acc[i][j]);
+            }
+          }
+        }
+        if (ok) {
+          double* out = A.qhat + (int64_t)cs.skel_off[v] * RC;
+#pragma unroll
+          for (int i = 0; i < TA; ++i)
+            if (a0 + i < k)
+#pragma unroll
+              for (int j = 0; j < TR; ++j) out[(int64_t)(a0 + i) * RC + r0 + j] = acc[i][j];
+        }
+        if (it0 + blockDim.x < items && nk > TB) {  // the G tiles must be restaged
+          __syncthreads();
+          const int tb0 = min(TB, nk);
+          stage_block<16>(tb0 * k, [&](int e) { return G[e]; }, [&](int e, double x) { gs[e] = x; });
+          __syncthreads();
+        }
+      }
+    }
+}
+
 template <int RC>
 __global__ void __launch_bounds__(XFER_THREADS) k_upward(XferArgs A, const int* order, int n,
                                                          const unsigned char* inset,
                                                          unsigned* counter, unsigned* done,
                                                          unsigned epoch) {
   extern __shared__ double sh[];
-  const Side cs = A.side;
   for (;;) {
     const int tk = next_ticket(counter);
     if (tk >= n) break;
@@ -67,62 +156,29 @@ __global__ void __launch_bounds__(XFER_THREADS) k_upward(XferArgs A, const int* 
     const int nc = A.nchild[v];
     if (threadIdx.x < nc) {
       const int c = A.child_first[v] + threadIdx.x;
-      if (inset[c])  // producers outside this launch are final already (sharded stages)
+      if (inset[c])  // producers outside this launch are final already
         while (ld_acquire(&done[c]) != epoch) __nanosleep(40);
     }
     __syncthreads();
-    const int ni = cs.nib[v], k = cs.rank[v];
-    if (k > 0) {
-      const bool leaf = nc == 0;
-      const double* ivec = leaf ? A.qt + (int64_t)A.pt_a[v] * RC
-                                : A.qhat + (int64_t)cs.skel_off[A.child_first[v]] * RC;
-      const int* perm = cs.perm + cs.ib_off[v];
-      double* iv = sh;           // ni * RC
-      double* gs = sh + ni * RC;  // TB * k
-      stage_block<8>(ni * RC,
-                     [&](int e) { return __ldcg(ivec + (int64_t)perm[e / RC] * RC + e % RC); },
-                     [&](int e, double x) { iv[e] = x; });
-      __syncthreads();
-      const int nout = k * RC;
-      double acc[XFER_MAXO];
-#pragma unroll
-      for (int j = 0; j < XFER_MAXO; ++j) {
-        const int e = threadIdx.x + j * blockDim.x;
-        acc[j] = e < nout ? iv[e] : 0.0;
-      }
-      const double* G = cs.G + cs.g_off[v];
-      const int nk = ni - k;
-      const int TB = g_tile_rows(k);
-      for (int b0 = 0; b0 < nk; b0 += TB) {
-        const int tb = min(TB, nk - b0);
-        const double* src = G + (int64_t)b0 * k;
-        stage_block<16>(tb * k, [&](int e) { return src[e]; }, [&](int e, double x) { gs[e] = x; });
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < XFER_MAXO; ++j) {
-          const int e = threadIdx.x + j * blockDim.x;
-          if (e < nout) {
-            const int a = e / RC, r = e % RC;
-            double t = acc[j];
-            const double* ivb = iv + (k + b0) * RC + r;
-            for (int bb = 0; bb < tb; ++bb) t = fma(gs[bb * k + a], ivb[bb * RC], t);
-            acc[j] = t;
-          }
-        }
-        __syncthreads();
-      }
-      double* out = A.qhat + (int64_t)cs.skel_off[v] * RC;
-#pragma unroll
-      for (int j = 0; j < XFER_MAXO; ++j) {
-        const int e = threadIdx.x + j * blockDim.x;
-        if (e < nout) out[e] = acc[j];
-      }
-    }
+    up_node<RC>(A, v, sh);
     publish(done, v, epoch);
   }
 }
 
-// zhat[children] += X_v zhat[v] (internal non-root nodes, after the coupling)
+// Leaves have no producers: one CTA per leaf, no tickets, no flags.
+template <int RC>
+__global__ void __launch_bounds__(64) k_upward_leaves(XferArgs A, const int* leaves, int n) {
+  extern __shared__ double sh[];
+  if ((int)blockIdx.x >= n) return;
+  const int v = leaves[blockIdx.x];
+  if (v == 0) return;  // a leaf root has no factor
+  up_node<RC>(A, v, sh);
+}
+
+// zhat[children] += X_v zhat[v] (internal non-root nodes, after the coupling).
+// zhat_v, the children's contiguous coefficient block, the permutation and the
+// first G tile are staged in one batched load; the block is updated in shared
+// memory and written back coalesced.
 template <int RC>
 __global__ void __launch_bounds__(XFER_THREADS) k_downward(XferArgs A, const int* order, int n,
                                                            const unsigned char* inset,
@@ -141,42 +197,80 @@ __global__ void __launch_bounds__(XFER_THREADS) k_downward(XferArgs A, const int
     const int ni = rs.nib[v], k = rs.rank[v];
     if (k > 0 && ni > 0) {
       const int ks = k | 1;
-      double* zv = sh;           // k * RC
-      double* gs = sh + k * RC;  // TB * ks
       const int* perm = rs.perm + rs.ib_off[v];
       const double* zsrc = A.zhat + (int64_t)rs.skel_off[v] * RC;
       double* dst = A.zhat + (int64_t)rs.skel_off[A.child_first[v]] * RC;
-      for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
-        const double x = __ldcg(zsrc + e);
-        zv[e] = x;
-        const int a = e / RC, r = e % RC;
-        double* d = dst + (int64_t)perm[a] * RC + r;
-        *d = __ldcg(d) + x;
-      }
       const double* G = rs.G + rs.g_off[v];
       const int nk = ni - k;
       const int TB = g_tile_rows(ks);
+      double* zv = sh;             // k * RC
+      double* db = zv + k * RC;    // ni * RC: the children's block
+      double* pm = db + ni * RC;   // ni
+      double* gs = pm + ni;        // TB * ks
+      const int n_z = k * RC, n_d = ni * RC, tb0 = min(TB, nk);
+      stage_block<16>(n_z + n_d + ni + tb0 * k,
+                      [&](int e) {
+                        return e < n_z ? __ldcg(zsrc + e)
+                               : e < n_z + n_d ? __ldcg(dst + (e - n_z))
+                               : e < n_z + n_d + ni ? (double)perm[e - n_z - n_d]
+                                                    : G[e - n_z - n_d - ni];
+                      },
+                      [&](int e, double x) {
+                        if (e < n_z + n_d + ni) {
+                          zv[e] = x;
+                        } else {
+                          const int g = e - n_z - n_d - ni;
+                          gs[(g / k) * ks + g % k] = x;
+                        }
+                      });
+      __syncthreads();
+      for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
+        const int a = e / RC, r = e % RC;
+        db[(int)pm[a] * RC + r] += zv[e];
+      }
+      constexpr int TR = RC < 4 ? RC : 4;
+      constexpr int TB2 = 2;
       for (int b0 = 0; b0 < nk; b0 += TB) {
         const int tb = min(TB, nk - b0);
-        const double* src = G + (int64_t)b0 * k;
-        __syncthreads();
-        stage_block<16>(tb * k, [&](int e) { return src[e]; },
-                        [&](int e, double x) { gs[(e / k) * ks + e % k] = x; });
-        __syncthreads();
-        for (int e = threadIdx.x; e < tb * RC; e += blockDim.x) {
-          const int bb = e / RC, r = e % RC;
-          const double* g = gs + bb * ks;
-          double y0 = 0.0, y1 = 0.0;
-          int a = 0;
-          for (; a + 1 < k; a += 2) {
-            y0 = fma(g[a], zv[a * RC + r], y0);
-            y1 = fma(g[a + 1], zv[(a + 1) * RC + r], y1);
+        if (b0 > 0) {
+          const double* src = G + (int64_t)b0 * k;
+          __syncthreads();
+          stage_block<16>(tb * k, [&](int e) { return src[e]; },
+                          [&](int e, double x) { gs[(e / k) * ks + e % k] = x; });
+          __syncthreads();
+        }
+        const int nb = (tb + TB2 - 1) / TB2, nrq = RC / TR;
+        for (int it = threadIdx.x; it < nb * nrq; it += blockDim.x) {
+          const int bl = (it / nrq) * TB2, r0 = (it % nrq) * TR;
+          double y[TB2][TR];
+#pragma unroll
+          for (int i = 0; i < TB2; ++i)
+#pragma unroll
+            for (int j = 0; j < TR; ++j) y[i][j] = 0.0;
+          const double* g0 = gs + bl * ks;
+          const bool two = bl + 1 < tb;
+          for (int a = 0; a < k; ++a) {
+            double w[TR];
+#pragma unroll
+            for (int j = 0; j < TR; ++j) w[j] = zv[a * RC + r0 + j];
+            const double ga = g0[a], gb = two ? g0[ks + a] : 0.0;
+#pragma unroll
+            for (int j = 0; j < TR; ++j) {
+              y[0][j] = fma(ga, w[j], y[0][j]);
+              y[1][j] = fma(gb, w[j], y[1][j]);
+            }
           }
-          if (a < k) y0 = fma(g[a], zv[a * RC + r], y0);
-          double* d = dst + (int64_t)perm[k + b0 + bb] * RC + r;
-          *d = __ldcg(d) + (y0 + y1);
+#pragma unroll
+          for (int i = 0; i < TB2; ++i)
+            if (bl + i < tb) {
+              double* d = db + (int)pm[k + b0 + bl + i] * RC + r0;
+#pragma unroll
+              for (int j = 0; j < TR; ++j) d[j] += y[i][j];
+            }
         }
       }
+      __syncthreads();
+      for (int e = threadIdx.x; e < ni * RC; e += blockDim.x) dst[e] = db[e];
     }
     publish(done, v, epoch);
   }
@@ -251,24 +345,37 @@ template <int RC>
 void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
                    const unsigned char* inset, cudaStream_t s) {
   if (!n) return;
-  const size_t smem = ((size_t)P.max_nib * RC + 4096) * sizeof(double);
+  const size_t smem = ((size_t)P.max_nib * (2 * RC + 1) + 4096) * sizeof(double);
   SMASH_CUDA(cudaFuncSetAttribute(k_upward<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // flags and ticket counter are reset on the stream (graph-replay safe)
   SMASH_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(unsigned), s));
+  SMASH_CUDA(cudaMemsetAsync(P.done.p, 0, P.done.n * sizeof(unsigned), s));
   const int grid = std::min(n, xfer_grid(smem));
-  k_upward<RC><<<grid, XFER_THREADS, smem, s>>>(a, order, n, inset, P.counters.p, P.done.p,
-                                                P.epoch);
+  k_upward<RC><<<grid, XFER_THREADS, smem, s>>>(a, order, n, inset, P.counters.p, P.done.p, 1u);
+}
+
+template <int RC>
+void launch_upward_leaves(const XferArgs& a, const XferPlan& P, const int* leaves, int n,
+                          cudaStream_t s) {
+  if (!n) return;
+  const size_t smem = ((size_t)P.max_leaf_nib * (2 * RC + 1) + 4096) * sizeof(double);
+  SMASH_CUDA(cudaFuncSetAttribute(k_upward_leaves<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  k_upward_leaves<RC><<<n, 64, smem, s>>>(a, leaves, n);
 }
 
 template <int RC>
 void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
                      const unsigned char* inset, cudaStream_t s) {
   if (!n) return;
-  const size_t smem = ((size_t)P.max_rank * RC + 4096 + 64) * sizeof(double);
+  const size_t smem = ((size_t)P.max_rank * RC + (size_t)P.max_nib * (RC + 1) + 4096 + 64) *
+                       sizeof(double);
   SMASH_CUDA(cudaFuncSetAttribute(k_downward<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SMASH_CUDA(cudaMemsetAsync(P.counters.p + 1, 0, sizeof(unsigned), s));
+  SMASH_CUDA(cudaMemsetAsync(P.done.p, 0, P.done.n * sizeof(unsigned), s));
   const int grid = std::min(n, xfer_grid(smem));
   k_downward<RC><<<grid, XFER_THREADS, smem, s>>>(a, order, n, inset, P.counters.p + 1, P.done.p,
-                                                  P.epoch, 0);
+                                                  1u, 0);
 }
 
 template <int RC>
@@ -287,6 +394,8 @@ void launch_leaf_add(const XferArgs& a, const XferPlan& P, const int* leaves, in
                                   cudaStream_t);                                               \
   template void launch_upward<RC>(const XferArgs&, XferPlan&, const int*, int,                  \
                                   const unsigned char*, cudaStream_t);                          \
+  template void launch_upward_leaves<RC>(const XferArgs&, const XferPlan&, const int*, int,      \
+                                         cudaStream_t);                                         \
   template void launch_downward<RC>(const XferArgs&, XferPlan&, const int*, int,                \
                                     const unsigned char*, cudaStream_t);                        \
   template void launch_leaf_add<RC>(const XferArgs&, const XferPlan&, const int*, int,          \

@@ -105,6 +105,7 @@ struct MatrixImpl {
   int64_t launches = 0;
   // nearfield stream (runs concurrently with the far-field chain) + fork/join events
   cudaStream_t s2 = nullptr;
+  cudaStream_t sc = nullptr;  // graph capture origin (the caller's stream may be the legacy one)
   cudaEvent_t fork = nullptr, join = nullptr;
   ~MatrixImpl() {
     for (auto& e : ev)
@@ -112,6 +113,7 @@ struct MatrixImpl {
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
     if (s2) cudaStreamDestroy(s2);
+    if (sc) cudaStreamDestroy(sc);
   }
 };
 
