@@ -1,0 +1,361 @@
+"""The reference's hot-path unit tests (pkg/tests/test_cluster.py, test_lowrank.py,
+test_h2.py, test_apply.py), ported to the GPU drop-in package.
+
+Adaptations (documented in DESIGN.md): the Taylor basis and the complex 2-D
+Cauchy kernel are out of scope, so the H^2 cases use the Chebyshev basis with
+the BASELINE real kernels; everything else keeps the reference's assertions.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sg():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1705_05443_b200 as s
+    return s
+
+
+def uniform_1d(sg, n, lo=0.0, hi=1.0):
+    pts = lo + (hi - lo) * (np.arange(n) + 0.5) / n
+    return sg.PointSet(pts.reshape(-1, 1))
+
+
+def grid_points(sg, m):
+    g = (np.arange(m) + 0.5) / m
+    xx, yy = np.meshgrid(g, g, indexing="ij")
+    return sg.PointSet(np.column_stack([xx.ravel(), yy.ravel()]))
+
+
+# ---------------------------------------------------------------- build_tree (test_cluster.py)
+
+def test_eight_points_capacity_three(sg):
+    tree = sg.build_tree(uniform_1d(sg, 8), nu0=3)
+    assert tree.n_levels == 3
+    leaves = tree.leaves()
+    assert len(leaves) == 4 and all(tree.nodes[i].n_row == 2 for i in leaves)
+    tree.verify()
+
+
+def test_capacity_larger_than_n_single_node(sg):
+    tree = sg.build_tree(uniform_1d(sg, 10), nu0=50)
+    assert tree.n_levels == 1 and tree.is_leaf(tree.root) and len(tree.nodes) == 1
+
+
+def test_clustered_points_shrink_and_stay_binary(sg):
+    tree = sg.build_tree(sg.PointSet((np.arange(8) / 16.0).reshape(-1, 1)), nu0=2)
+    assert tree.n_levels == 3
+    for nd in tree.nodes:
+        assert nd.box.hi[0] <= 0.5 + 1e-12
+        if not nd.is_leaf:
+            assert len(nd.children) == 2
+    tree.verify()
+
+
+def test_uneven_density_leaves_at_different_depths(sg):
+    pts = np.concatenate([np.linspace(0.0, 0.1, 12), [0.8, 0.9]])
+    tree = sg.build_tree(sg.PointSet(pts.reshape(-1, 1)), nu0=2)
+    assert len({tree.nodes[i].level for i in tree.leaves()}) > 1
+    tree.verify()
+
+
+def test_2d_mode_discards_empty_quadrants(sg):
+    pts = np.linspace(0.0, 1.0, 16)
+    tree = sg.build_tree(sg.PointSet(np.column_stack([pts, pts])), nu0=3, mode="2d")
+    assert {len(nd.children) for nd in tree.nodes if not nd.is_leaf} == {2}
+    tree.verify()
+
+
+def test_2d_mode_full_grid_four_way(sg):
+    tree = sg.build_tree(grid_points(sg, 8), nu0=5, mode="2d")
+    assert any(len(nd.children) == 4 for nd in tree.nodes if not nd.is_leaf)
+    tree.verify()
+
+
+def test_leaf_capacity_per_role(sg):
+    rng = np.random.default_rng(3)
+    tree = sg.build_tree(sg.PointSet(rng.random((100, 1))), sg.PointSet(rng.random((100, 1)), role="col"), nu0=7)
+    for i in tree.leaves():
+        assert max(tree.nodes[i].n_row, tree.nodes[i].n_col) <= 7
+    tree.verify()
+
+
+def test_postorder_sibling_ranges(sg):
+    tree = sg.build_tree(uniform_1d(sg, 32), nu0=4)
+    for nd in tree.nodes:
+        if nd.is_leaf:
+            continue
+        stops = [tree.nodes[c].row_stop for c in nd.children]
+        starts = [tree.nodes[c].row_start for c in nd.children]
+        assert starts[0] == nd.row_start and stops[-1] == nd.row_stop
+        assert all(a == b for a, b in zip(stops, starts[1:]))
+
+
+def test_invalid_input_rejected(sg):
+    with pytest.raises(ValueError):
+        sg.build_tree(sg.PointSet(np.empty((0, 1))))
+    with pytest.raises(ValueError):
+        sg.build_tree(uniform_1d(sg, 4), nu0=0)
+    with pytest.raises(ValueError):
+        sg.build_tree(uniform_1d(sg, 4), mode="quad")
+
+
+def test_coincident_points_cannot_be_separated(sg):
+    # more coincident points than nu0: the reference raises after its shrink cap
+    with pytest.raises(RuntimeError):
+        sg.build_tree(sg.PointSet(np.full((10, 2), 0.25)), nu0=3, mode="2d")
+
+
+# ---------------------------------------------------------------- nearfield / leaf_sets
+
+def test_nearfield_root_and_root_children(sg):
+    tree = sg.build_tree(uniform_1d(sg, 32), nu0=4, tau=0.5)
+    assert sg.nearfield_set(tree, tree.root) == []
+    c1, c2 = tree.nodes[tree.root].children
+    assert sg.nearfield_set(tree, c1, tau=0.5) == [c2]
+    assert sg.nearfield_set(tree, c2, tau=0.5) == [c1]
+
+
+def test_nearfield_small_and_actually_near(sg):
+    tree = sg.build_tree(uniform_1d(sg, 64), nu0=2, tau=0.5)
+    for nd in tree.nodes:
+        near = sg.nearfield_set(tree, nd.index, tau=0.5)
+        assert len(near) <= 2
+        for k in near:
+            assert not sg.well_separated(nd.box, tree.nodes[k].box, 0.5)
+
+
+def test_hss_leaf_sets(sg):
+    tree = sg.build_tree(uniform_1d(sg, 32), nu0=4)
+    L, Lm = sg.leaf_sets(tree, structure="hss")
+    sib = set()
+    for nd in tree.nodes:
+        if not nd.is_leaf:
+            c1, c2 = nd.children
+            sib |= {(c1, c2), (c2, c1)}
+    assert set(L) == sib and set(Lm) == {(i, i) for i in tree.leaves()}
+
+
+def test_h2_depth_two_all_dense(sg):
+    tree = sg.build_tree(uniform_1d(sg, 8), nu0=4, tau=0.5)
+    L, Lm = sg.leaf_sets(tree, tau=0.5, structure="h2")
+    kids = tree.nodes[tree.root].children
+    assert L == [] and set(Lm) == {(i, j) for i in kids for j in kids}
+
+
+def brute_force_h2(sg, tree, tau):
+    nodes = tree.nodes
+    sep = {(a.index, b.index): sg.well_separated(a.box, b.box, tau) for a in nodes for b in nodes}
+    L, Lm = [], []
+    for a in nodes:
+        for b in nodes:
+            i, j = a.index, b.index
+            pi, pj = a.parent, b.parent
+            if sep[i, j]:
+                same = a.level == b.level and pi >= 0 and pj >= 0 and not sep[pi, pj]
+                il = a.is_leaf and b.level > a.level and pj >= 0 and not sep[i, pj]
+                jl = b.is_leaf and a.level > b.level and pi >= 0 and not sep[pi, j]
+                if same or il or jl:
+                    L.append((i, j))
+            elif a.is_leaf and b.is_leaf:
+                Lm.append((i, j))
+    return L, Lm
+
+
+def test_h2_leaf_sets_brute_force_tiling_symmetry(sg):
+    tree = sg.build_tree(uniform_1d(sg, 16), nu0=2, tau=0.5)
+    L, Lm = sg.leaf_sets(tree, tau=0.5, structure="h2")
+    Lb, Lmb = brute_force_h2(sg, tree, 0.5)
+    assert set(L) == set(Lb) and set(Lm) == set(Lmb)
+    assert all((j, i) in set(L) for i, j in L)
+    tree = sg.build_tree(uniform_1d(sg, 32), nu0=4, tau=0.5)
+    for structure in ("hss", "h2"):
+        L, Lm = sg.leaf_sets(tree, tau=0.5, structure=structure)
+        cover = np.zeros((32, 32), int)
+        for i, j in list(L) + list(Lm):
+            r, c = tree.nodes[i], tree.nodes[j]
+            cover[r.row_start:r.row_stop, c.col_start:c.col_stop] += 1
+        assert np.all(cover == 1)
+
+
+def test_hss_structure_requires_binary_tree(sg):
+    tree = sg.build_tree(grid_points(sg, 8), nu0=5, mode="2d")
+    with pytest.raises(ValueError):
+        sg.leaf_sets(tree, structure="hss")
+
+
+# ---------------------------------------------------------------- lowrank (test_lowrank.py)
+
+def test_interpolation_partition_of_unity_and_nodes(sg):
+    box = sg.Box.of((0.0,), (2.0,))
+    pts = np.random.default_rng(0).uniform(0, 2, 40).reshape(-1, 1)
+    np.testing.assert_allclose(sg.interp_basis(box, pts, 9).sum(axis=1), 1.0, atol=1e-10)
+    k = np.arange(7)
+    nodes = (1.0 + np.cos((2 * k + 1) * np.pi / 14)).reshape(-1, 1)
+    np.testing.assert_allclose(sg.interp_basis(box, nodes, 7), np.eye(7), atol=1e-12)
+
+
+def test_interpolation_reproduces_polynomials(sg):
+    box = sg.Box.of((-1.0,), (1.0,))
+    r = 8
+    k = np.arange(r)
+    nodes = np.cos((2 * k + 1) * np.pi / (2 * r))
+    pts = np.linspace(-1, 1, 33).reshape(-1, 1)
+    U = sg.interp_basis(box, pts, r)
+    np.testing.assert_allclose(U @ (nodes ** (r - 1) * 0.37), pts[:, 0] ** (r - 1) * 0.37, atol=1e-12)
+
+
+def test_planar_and_3d_interpolation_shapes(sg):
+    pts = np.random.default_rng(1).random((10, 2))
+    box = sg.Box.of((0.0, 0.0), (1.0, 1.0))
+    for r in (4, 9, 22):
+        assert sg.interp_basis(box, pts, r).shape == (10, r)
+    np.testing.assert_allclose(sg.interp_basis(box, pts, 9).sum(axis=1), 1.0, atol=1e-10)
+    box3 = sg.Box.of((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    p3 = np.random.default_rng(2).random((12, 3))
+    np.testing.assert_allclose(sg.interp_basis(box3, p3, 27).sum(axis=1), 1.0, atol=1e-10)
+
+
+def test_compr_properties(sg):
+    rng = np.random.default_rng(2)
+    C = rng.standard_normal((5, 5)) + 5 * np.eye(5)
+    f = sg.compr(C, np.array([10, 20, 30, 40, 50]))
+    assert f.rank == 5 and set(f.skel) == {10, 20, 30, 40, 50}
+    np.testing.assert_allclose(f.expand() @ C[f.skel_local], C, atol=1e-10)
+    v = np.array([[1.0, 2.0, 3.0]])
+    f = sg.compr(np.vstack([v, 2 * v]), np.array([0, 1]))
+    assert f.rank == 1 and f.G.shape == (1, 1)
+    assert abs(f.G[0, 0]) in (pytest.approx(2.0), pytest.approx(0.5))
+    for seed in range(20):
+        r = np.random.default_rng(seed)
+        kk = 1 + seed % 8
+        C = r.standard_normal((50, kk)) @ r.standard_normal((kk, 8))
+        f = sg.compr(C, np.arange(50))
+        assert f.rank <= min(kk, 8)
+        assert np.linalg.norm(C - f.expand() @ C[f.skel_local]) <= 1e-10 * np.linalg.norm(C)
+        if f.G.size:
+            assert np.max(np.abs(f.G)) <= 2.0 + 1e-12
+    f = sg.compr(np.zeros((6, 4)), np.arange(6))
+    assert f.rank == 0
+    with pytest.raises(ValueError):
+        sg.compr(np.zeros((4, 2)), np.arange(3))
+
+
+def test_compr_matches_oracle_pivots(sg):
+    """Same skeleton order as LAPACK dgeqp3 on random tall panels."""
+    from oracle import smash_oracle as orc
+    for seed in range(30):
+        r = np.random.default_rng(100 + seed)
+        C = r.standard_normal((40, 12)) @ np.diag(10.0 ** -np.arange(12))
+        f = sg.compr(C, np.arange(40), rtol=1e-8)
+        o = orc.compr(C, np.arange(40), rtol=1e-8)
+        assert np.array_equal(f.skel, o.skel), seed
+
+
+# ---------------------------------------------------------------- H^2 / matvec (test_h2.py, test_apply.py)
+
+@pytest.fixture(scope="module")
+def grid_h2(sg):
+    X = grid_points(sg, 20)
+    spec = sg.KernelSpec("log", dx=0.0)
+    tree = sg.build_tree(X, nu0=50, mode="2d", tau=0.65)
+    M = sg.build_h2(tree, spec, X, X, sg.BuildParams(r=64, tau=0.65, basis="interp", rtol=1e-14))
+    return M, spec, X
+
+
+def dense(sg, spec, X, Y=None):
+    Y = X if Y is None else Y
+    return sg.kernel_block(spec, X, Y, np.arange(X.n), np.arange(Y.n))
+
+
+def test_blocks_hold_exact_kernel_entries(sg, grid_h2):
+    from oracle import smash_oracle as orc
+    M, spec, X = grid_h2
+    A = orc.kernel_block("log", X.coords, X.coords, 0.0)
+    tr = M.tree
+    for i, j in M.pairs_Lm[:20]:
+        ref = A[np.ix_(tr.perm_row[tr.row_range(i)], tr.perm_col[tr.col_range(j)])]
+        np.testing.assert_allclose(M.NF(i, j), ref, rtol=1e-14, atol=1e-15)
+    for i, j in M.pairs_L[:20]:
+        ref = A[np.ix_(tr.perm_row[M.skel_row[i]], tr.perm_col[M.skel_col[j]])]
+        np.testing.assert_allclose(M.B(i, j), ref, rtol=1e-14, atol=1e-15)
+
+
+def test_grid_matvec_and_reconstruction(sg, grid_h2):
+    M, spec, X = grid_h2
+    A = dense(sg, spec, X)
+    q = np.random.default_rng(5).random(X.n)
+    z = sg.matvec_nodewise(M, q)
+    assert np.linalg.norm(z - A @ q) <= 1e-9 * np.linalg.norm(A @ q)
+    Ad = M.todense()
+    for j in np.random.default_rng(9).integers(0, X.n, 4):
+        e = np.zeros(X.n)
+        e[j] = 1.0
+        np.testing.assert_allclose(sg.matvec_nodewise(M, e), Ad[:, j], rtol=0, atol=1e-12 * np.abs(Ad).max())
+
+
+def test_matvec_zero_linear_multirhs_length(sg, grid_h2):
+    M, spec, X = grid_h2
+    np.testing.assert_array_equal(sg.matvec_nodewise(M, np.zeros(X.n)), np.zeros(X.n))
+    rng = np.random.default_rng(4)
+    q1, q2 = rng.random(X.n), rng.random(X.n)
+    np.testing.assert_allclose(sg.matvec_nodewise(M, -1.7 * q1 + 0.3 * q2),
+                               -1.7 * sg.matvec_nodewise(M, q1) + 0.3 * sg.matvec_nodewise(M, q2),
+                               rtol=1e-12, atol=1e-12)
+    Q = rng.random((X.n, 3))
+    Z = sg.matvec_nodewise(M, Q)
+    assert Z.shape == (X.n, 3)
+    for j in range(3):
+        np.testing.assert_allclose(Z[:, j], sg.matvec_nodewise(M, Q[:, j]), rtol=1e-13, atol=1e-14)
+    with pytest.raises(ValueError):
+        sg.matvec_nodewise(M, np.ones(X.n - 1))
+
+
+def test_no_admissible_pairs_is_dense(sg):
+    rng = np.random.default_rng(0)
+    X = sg.PointSet(np.vstack([rng.random((6, 2)) * 0.5, rng.random((6, 2)) * 0.5 + 0.5]))
+    tree = sg.build_tree(X, nu0=6, mode="2d", tau=0.5)
+    spec = sg.KernelSpec("inv_r", dx=1.0)
+    M = sg.build_h2(tree, spec, X, X, sg.BuildParams(r=4, tau=0.5, basis="interp"))
+    assert M.pairs_L == []
+    np.testing.assert_allclose(M.todense(), dense(sg, spec, X), rtol=0, atol=0)
+
+
+def test_adaptive_cross_level_pairs(sg):
+    rng = np.random.default_rng(3)
+    X = sg.PointSet(np.vstack([rng.random((64, 2)) * 0.08, rng.random((24, 2)) * 0.9 + 0.1]))
+    tree = sg.build_tree(X, nu0=4, mode="2d", tau=0.6)
+    spec = sg.KernelSpec("log", dx=0.0)
+    M = sg.build_h2(tree, spec, X, X, sg.BuildParams(r=16, tau=0.6, basis="interp"))
+    assert any(tree.nodes[i].level != tree.nodes[j].level for i, j in M.pairs_L)
+    A = dense(sg, spec, X)
+    q = rng.random(X.n)
+    assert np.linalg.norm(sg.matvec_nodewise(M, q) - A @ q) <= 1e-6 * np.linalg.norm(A @ q)
+
+
+def test_1d_binary_h2_with_cauchy(sg):
+    rng = np.random.default_rng(2)
+    x = np.sort(rng.random(200)).reshape(-1, 1)
+    X = sg.PointSet(x)
+    Y = sg.PointSet(x + 1e-7 * rng.random((200, 1)), role="col")
+    tree = sg.build_tree(X, Y, nu0=16, tau=0.5)
+    spec = sg.KernelSpec("cauchy")
+    M = sg.build_h2(tree, spec, X, Y, sg.BuildParams(r=15, tau=0.5, basis="interp"))
+    A = dense(sg, spec, X, Y)
+    q = rng.random(200)
+    assert np.linalg.norm(sg.matvec_nodewise(M, q) - A @ q) <= 1e-7 * np.linalg.norm(A @ q)
+    assert any(i != j for i, j in M.pairs_Lm)
+
+
+def test_h2_requires_2d_tree_and_supported_basis(sg):
+    X = sg.PointSet(np.random.default_rng(1).random((64, 2)))
+    with pytest.raises(ValueError):
+        sg.build_h2(sg.build_tree(X, nu0=8, mode="binary"), sg.KernelSpec("log"), X, X)
+    tree = sg.build_tree(X, nu0=8, mode="2d")
+    with pytest.raises(NotImplementedError):
+        sg.build_h2(tree, sg.KernelSpec("cauchy", dx=0.0), X, X, sg.BuildParams(basis=None))
