@@ -103,7 +103,7 @@ __device__ void build_panel(const CompressArgs& A, int v, int n, int mrows, doub
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     const int pc = colmap ? colmap[c] : c;
     if (A.Cexp) {  // single-call compr: panel = C^T
-      for (int q = 0; q < mrows; ++q) P[(size_t)q * n + c] = A.Cexp[(size_t)pc * A.C_cols + q];
+      for (int q = 0; q < mrows; ++q) P[q * n + c] = A.Cexp[(size_t)pc * A.C_cols + q];
       continue;
     }
     double x[D];
@@ -114,13 +114,13 @@ __device__ void build_panel(const CompressArgs& A, int v, int n, int mrows, doub
       bool exact = false;
       for (int k = 0; k < m; ++k) exact |= (__dsub_rn(x[0], nd[k]) == 0.0);
       if (exact) {
-        for (int k = 0; k < m; ++k) P[(size_t)k * n + c] = (__dsub_rn(x[0], nd[k]) == 0.0) ? 1.0 : 0.0;
+        for (int k = 0; k < m; ++k) P[k * n + c] = (__dsub_rn(x[0], nd[k]) == 0.0) ? 1.0 : 0.0;
       } else {
         double Ssum = np_pairwise_sum(m, [&](int k) {
           return __ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k]));
         });
         for (int k = 0; k < m; ++k)
-          P[(size_t)k * n + c] = __ddiv_rn(__ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k])), Ssum);
+          P[k * n + c] = __ddiv_rn(__ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k])), Ssum);
       }
     } else {
       double L[D][MAX_M_AXIS_ND];
@@ -130,18 +130,18 @@ __device__ void build_panel(const CompressArgs& A, int v, int n, int mrows, doub
         const int* o = A.tab.order + 3 * q;
         double val = __dmul_rn(L[0][o[0]], L[1][o[1]]);
         if (D == 3) val = __dmul_rn(val, L[D - 1][o[2]]);
-        P[(size_t)q * n + c] = val;
+        P[q * n + c] = val;
       }
     }
     if (A.keep) {  // HSS: rows r.. hold S^T (hss.py:287)
       const int kp = A.keep[v];
       const double* sv = A.sv + A.sv_off[v];
-      for (int q = 0; q < kp; ++q) P[(size_t)(r + q) * n + c] = sv[(size_t)pc * kp + q];
+      for (int q = 0; q < kp; ++q) P[(r + q) * n + c] = sv[(size_t)pc * kp + q];
     }
   }
 }
 
-template <int D>
+template <int D, bool SM>
 __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared S;
@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
     S.redi = ip; ip += 32;
     S.imisc = ip; ip += 8;
     S.jpvt = ip; ip += A.nmax + (A.nmax & 1);
-    S.panel = A.smem_panel ? reinterpret_cast<double*>(ip)
-                           : A.gws + (size_t)blockIdx.x * A.mmax * A.nmax;
+    // SM: the panel lives in shared memory (the compiler then emits LDS/STS with
+    // 32-bit addresses); otherwise in this CTA's slice of the global workspace
+    S.panel = SM ? reinterpret_cast<double*>(ip) : A.gws + (size_t)blockIdx.x * A.mmax * A.nmax;
   }
   const int tid = threadIdx.x, NT = blockDim.x;
   for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
@@ -224,9 +225,9 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
       const int pvt = bi;
       if (pvt != i) {
         for (int row = tid; row < m; row += NT) {
-          double t = P[(size_t)row * ld + pvt];
-          P[(size_t)row * ld + pvt] = P[(size_t)row * ld + i];
-          P[(size_t)row * ld + i] = t;
+          double t = P[row * ld + pvt];
+          P[row * ld + pvt] = P[row * ld + i];
+          P[row * ld + i] = t;
         }
         if (tid == 0) {
           int it = S.jpvt[pvt]; S.jpvt[pvt] = S.jpvt[i]; S.jpvt[i] = it;
@@ -242,10 +243,11 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
         if (tau != 0.0) apply_reflector(P, ld, m, i, j, tau, S.vh);
         double v1 = S.vn1[j];
         if (v1 != 0.0) {
-          double q = __ddiv_rn(fabs(P[(size_t)i * ld + j]), v1);
-          double temp = fmax(__dsub_rn(1.0, __dmul_rn(q, q)), 0.0);
-          double q2 = __ddiv_rn(v1, S.vn2[j]);
-          double temp2 = __dmul_rn(temp, __dmul_rn(q2, q2));
+          const double rv1 = 1.0 / v1;
+          double q = fabs(P[i * ld + j]) * rv1;
+          double temp = fmax(1.0 - q * q, 0.0);
+          double q2 = v1 / S.vn2[j];
+          double temp2 = temp * (q2 * q2);
           if (temp2 <= TOL3Z) {
             double nv = i + 1 < m ? __dsqrt_rn(col_sumsq(P, ld, j, i + 1, m)) : 0.0;
             S.vn1[j] = nv;
@@ -277,13 +279,13 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
       const int nk = n - k;
       for (int j = k + tid; j < n; j += NT) {
         for (int a = k - 1; a >= 0; --a) {
-          double x = __ddiv_rn(P[(size_t)a * ld + j], P[(size_t)a * ld + a]);
-          P[(size_t)a * ld + j] = x;
+          double x = __ddiv_rn(P[a * ld + j], P[a * ld + a]);
+          P[a * ld + j] = x;
           for (int b = 0; b < a; ++b)
-            P[(size_t)b * ld + j] = __fma_rn(-x, P[(size_t)b * ld + a], P[(size_t)b * ld + j]);
+            P[b * ld + j] = __fma_rn(-x, P[b * ld + a], P[b * ld + j]);
         }
         for (int a = 0; a < k; ++a) {
-          double ax = fabs(P[(size_t)a * ld + j]);
+          double ax = fabs(P[a * ld + j]);
           argmax_combine(bv, bi, ax, a * nk + (j - k));
         }
       }
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
       const int nk = n - k;
       for (int e = tid; e < nk * k; e += NT) {
         int b = e / k, a = e % k;
-        G[e] = P[(size_t)a * ld + k + b];
+        G[e] = P[a * ld + k + b];
       }
     }
     if (A.tmp_lab) {
@@ -384,15 +386,18 @@ size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem) {
 }
 
 void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s) {
-  if (a.dim == 1) {
-    SMASH_CUDA(cudaFuncSetAttribute(k_compress<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_compress<1><<<grid, COMPRESS_THREADS, smem, s>>>(a);
-  } else if (a.dim == 2) {
-    SMASH_CUDA(cudaFuncSetAttribute(k_compress<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_compress<2><<<grid, COMPRESS_THREADS, smem, s>>>(a);
+  auto go = [&](auto kern) {
+    SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, COMPRESS_THREADS, smem, s>>>(a);
+  };
+  if (a.smem_panel) {
+    if (a.dim == 1) go(k_compress<1, true>);
+    else if (a.dim == 2) go(k_compress<2, true>);
+    else go(k_compress<3, true>);
   } else {
-    SMASH_CUDA(cudaFuncSetAttribute(k_compress<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_compress<3><<<grid, COMPRESS_THREADS, smem, s>>>(a);
+    if (a.dim == 1) go(k_compress<1, false>);
+    else if (a.dim == 2) go(k_compress<2, false>);
+    else go(k_compress<3, false>);
   }
   SMASH_CUDA(cudaGetLastError());
 }

@@ -28,7 +28,8 @@ namespace {
 using namespace qr;
 
 constexpr int SVD_THREADS = 256;
-constexpr int MAX_NEAR = 64;  // |N_i| cap (reference hist: |N_i| <= 2 on the HSS configs)
+constexpr int MAX_NEAR = 64;
+constexpr int SVD_JV_MAX = 64;  // Jacobi factors in shared memory up to this rank  // |N_i| cap (reference hist: |N_i| <= 2 on the HSS configs)
 
 struct IbarSide {
   const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
   const double** near_base;
   int64_t* near_stride;
   int* order;
+  double* jv_smem;
   {
     double* d = reinterpret_cast<double*>(smem_raw);
     S.vn1 = d; d += A.nnmax;
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     near_start = ip; ip += MAX_NEAR + 1;
     order = ip; ip += A.nmax;
     S.jpvt = ip; ip += A.nnmax;
+    jv_smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ip) + 15) & ~uintptr_t(15));
   }
   const int tid = threadIdx.x, NT = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
@@ -243,9 +246,13 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
         for (int j = i + 1 + tid; j < kp; j += NT) apply_reflector(B, kp, nn, i, j, tau, S.vh);
       __syncthreads();
     }
-    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated
-    double* J = B + (size_t)nn * kp;
+    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated.
+    // J and V live in shared memory when kp <= SVD_JV_MAX.  Column norms are kept
+    // up to date through the rotation (one dot product per pair) and refreshed
+    // exactly at every sweep.
+    double* J = kp <= SVD_JV_MAX ? jv_smem : B + (size_t)nn * kp;
     double* V = J + (size_t)kp * kp;
+    double* nrm = sig;  // squared column norms (reuses the sigma scratch)
     for (int e = tid; e < kp * kp; e += NT) {
       const int c = e / kp, r = e % kp;
       J[e] = r <= c ? B[(size_t)r * kp + c] : 0.0;
@@ -254,6 +261,12 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     __syncthreads();
     const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
     for (int sweep = 0; sweep < 40; ++sweep) {
+      for (int c = wid; c < kp; c += nw) {  // exact squared norms
+        double s2 = 0.0;
+        for (int r = lane; r < kp; r += 32) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
+        for (int off = 16; off; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+        if (lane == 0) nrm[c] = s2;
+      }
       if (tid == 0) S.imisc[2] = 0;
       __syncthreads();
       for (int rnd = 0; rnd < np - 1; ++rnd) {
@@ -264,17 +277,10 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
           if (a >= kp || b >= kp) continue;
           double* ja = J + (size_t)a * kp;
           double* jb = J + (size_t)b * kp;
-          double al = 0, be = 0, ga = 0;
-          for (int r = lane; r < kp; r += 32) {
-            al = fma(ja[r], ja[r], al);
-            be = fma(jb[r], jb[r], be);
-            ga = fma(ja[r], jb[r], ga);
-          }
-          for (int off = 16; off; off >>= 1) {
-            al += __shfl_xor_sync(0xffffffffu, al, off);
-            be += __shfl_xor_sync(0xffffffffu, be, off);
-            ga += __shfl_xor_sync(0xffffffffu, ga, off);
-          }
+          double ga = 0;
+          for (int r = lane; r < kp; r += 32) ga = fma(ja[r], jb[r], ga);
+          for (int off = 16; off; off >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, off);
+          const double al = nrm[a], be = nrm[b];
           if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
             const double zeta = (be - al) / (2.0 * ga);
             const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -289,7 +295,12 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
               va[r] = c * p - s * q;
               vb[r] = s * p + c * q;
             }
-            if (lane == 0) atomicAdd(&S.imisc[2], 1);
+            __syncwarp();
+            if (lane == 0) {
+              nrm[a] = fmax(al - t * ga, 0.0);
+              nrm[b] = be + t * ga;
+              atomicAdd(&S.imisc[2], 1);
+            }
           }
         }
         __syncthreads();
@@ -461,7 +472,8 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.err = err.p;
   const int mx = std::max(A.nmax, A.nnmax);
   size_t smem = 8 * ((size_t)2 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
-                4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64;
+                4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64 + 16 +
+                8 * (size_t)2 * SVD_JV_MAX * SVD_JV_MAX;
   SMASH_CHECK(smem <= 200 * 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
     SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
