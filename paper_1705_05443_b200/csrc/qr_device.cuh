@@ -57,7 +57,7 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, Shared& S) {
 __device__ __forceinline__ double col_sumsq(const double* P, int ld, int j, int r0, int r1) {
   double s = 0.0;
   for (int row = r0; row < r1; ++row) {
-    double x = P[(size_t)row * ld + j];
+    double x = P[row * ld + j];
     s = __fma_rn(x, x, s);
   }
   return s;
@@ -76,10 +76,10 @@ __device__ __forceinline__ double dlapy2(double x, double y) {
 __device__ __forceinline__ void householder(double* P, int ld, int m, int i, Shared& S) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  double alpha = P[(size_t)i * ld + i];
+  double alpha = P[i * ld + i];
   double ss = 0.0;
   for (int row = i + 1 + lane; row < m; row += 32) {
-    double x = P[(size_t)row * ld + i];
+    double x = P[row * ld + i];
     ss = __fma_rn(x, x, ss);
   }
   for (int off = 16; off; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
@@ -90,27 +90,27 @@ __device__ __forceinline__ void householder(double* P, int ld, int m, int i, Sha
     tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
     double scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
     for (int row = i + 1 + lane; row < m; row += 32) {
-      double x = __dmul_rn(scal, P[(size_t)row * ld + i]);
-      P[(size_t)row * ld + i] = x;
+      double x = __dmul_rn(scal, P[row * ld + i]);
+      P[row * ld + i] = x;
       S.vh[row] = x;
     }
-    if (lane == 0) P[(size_t)i * ld + i] = beta;
+    if (lane == 0) P[i * ld + i] = beta;
   }
   if (lane == 0) {
     S.misc[0] = tau;
-    S.rdiag[i] = P[(size_t)i * ld + i];
+    S.rdiag[i] = P[i * ld + i];
   }
 }
 
 // Apply H_i^T = I - tau v v^T (v_i = 1) to column j > i (dlarf: w = C^T v; C -= tau v w^T).
 __device__ __forceinline__ void apply_reflector(double* P, int ld, int m, int i, int j, double tau,
                                                 const double* vh) {
-  double w = P[(size_t)i * ld + j];
-  for (int row = i + 1; row < m; ++row) w = __fma_rn(vh[row], P[(size_t)row * ld + j], w);
+  double w = P[i * ld + j];
+  for (int row = i + 1; row < m; ++row) w = __fma_rn(vh[row], P[row * ld + j], w);
   double t = -__dmul_rn(tau, w);
-  P[(size_t)i * ld + j] = __dadd_rn(P[(size_t)i * ld + j], t);
+  P[i * ld + j] = __dadd_rn(P[i * ld + j], t);
   for (int row = i + 1; row < m; ++row)
-    P[(size_t)row * ld + j] = __fma_rn(t, vh[row], P[(size_t)row * ld + j]);
+    P[row * ld + j] = __fma_rn(t, vh[row], P[row * ld + j]);
 }
 
 
