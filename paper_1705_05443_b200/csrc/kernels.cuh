@@ -8,32 +8,33 @@
 
 namespace smash {
 
-// Branch-free fp64 1/sqrt: MUFU approximation (~2^-20) + two Newton steps
-// (measured max relative error 2.7e-16 vs 2.2e-16 for CUDA's rsqrt(), which
-// carries a special-case branch that breaks instruction-level parallelism
-// across the unrolled target tiles of the P2P kernels; tools/rsqrt_test.cu).
+// Branch-free fp64 1/sqrt: MUFU.RSQ64H approximation (max rel. error 9.2e-7),
+// one residual e = 1 - x y0^2 and the quadratic correction
+// y = y0 (1 + e/2 + 3e^2/8) (truncation ~(5/16)e^3 < 2^-60): 5 FP64 ops instead
+// of the 8 of two Newton steps, measured max rel. error 2.65e-16 (CUDA's
+// rsqrt(): 2.2e-16, but with a special-case branch that breaks the ILP across
+// the unrolled target tiles of the P2P kernels; tools/rsqrt_test.cu).
 __device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double h = x * y;
-    const double e = fma(-h, y, 1.0);
-    y = fma(0.5 * y, e, y);
-  }
-  return y;
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  const double h = x * y0;
+  const double e = fma(-h, y0, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  return fma(y0 * e, p, y0);
 }
 
-// Branch-free fp64 reciprocal: MUFU approximation + two Newton steps.
+// Branch-free fp64 reciprocal: MUFU.RCP64H approximation, e = 1 - x y0,
+// y = y0 (1 + e + e^2) (truncation e^3 < 2^-59).
 __device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-  }
-  return y;
+  double y0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  const double e = fma(-x, y0, 1.0);
+  return fma(y0, fma(e, e, e), y0);
+}
+
+// x == +-0.0 tested on the integer pipe (keeps DSETP off the FP64 pipe)
+__device__ __forceinline__ bool is_zero(double x) {
+  return ((__double2hiint(x) & 0x7fffffff) | __double2loint(x)) == 0;
 }
 
 // Branch-free natural log for positive normal x (the squared distances of the
@@ -87,7 +88,7 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
   if (KER == SMASH_KERNEL_CAUCHY) {
     const double d = x[0] - y[0];
     const double v = rcp_nr(d);
-    return d == 0.0 ? dx : v;
+    return is_zero(d) ? dx : v;
   }
   double r2 = 0.0;
 #pragma unroll
@@ -97,15 +98,15 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
   }
   if (KER == SMASH_KERNEL_LOG) {
     const double v = 0.5 * log_pos(r2);
-    return r2 == 0.0 ? dx : v;
+    return is_zero(r2) ? dx : v;
   }
   if (KER == SMASH_KERNEL_INV_R) {
     const double v = rsqrt_nr(r2);
-    return r2 == 0.0 ? dx : v;
+    return is_zero(r2) ? dx : v;
   }
   // exp(-r): r = r2 * rsqrt(r2) (0 on the diagonal, exp(0) = 1)
   const double r = r2 * rsqrt_nr(r2);
-  return exp_neg(r2 == 0.0 ? 0.0 : -r);
+  return exp_neg(is_zero(r2) ? 0.0 : -r);
 }
 
 // runtime dispatch helper: f.template operator()<KER, D>()

@@ -6,10 +6,11 @@
 //   main stream:  K10 gather qt = q[perm_col]                     (apply.py:39)
 //                 K6  upward  qhat_v = X_v^T ibar-vector, one persistent launch (apply.py:42-53)
 //                 K7  coupling zhat_i = sum_{j in L(i)} K(S_i, S_j) qhat_j   (apply.py:55-58)
-//                 K8  downward zhat_children += X_v zhat_v, one persistent launch (apply.py:60-72)
+//                 K8  downward zhat_children += X_v zhat_v and, for leaves, the far-field
+//                     rows zf = X_v zhat_v, one persistent launch            (apply.py:60-72)
 //                 --- join ---
-//                 K9b leaf far field z[perm_row] += X_v zhat_v               (apply.py:66-71)
-//   near stream:  K9a nearfield z[perm_row] = sum_{j in Lm(v)} K(P_v, P_j) qt_j (apply.py:74-80)
+//                 K10 combine z[perm_row] = zn + zf                          (apply.py:78-80)
+//   near stream:  K9  nearfield zn = sum_{j in Lm(v)} K(P_v, P_j) qt_j       (apply.py:74-76)
 // The nearfield only needs qt, so it overlaps the whole far-field chain.
 #include <algorithm>
 #include <array>
@@ -48,31 +49,25 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   }
   P->max_nib = mx;
   P->max_rank = mr;
-  {  // largest leaf |ibar| over both sides (the leaf upward kernel's shared memory)
-    std::vector<int> nl(n);
-    int ml = 1;
-    d2h(nl.data(), m->rowf.nib.p, n, s);
-    sync(s);
-    for (int v = 0; v < n; ++v)
-      if (nchild[v] == 0) ml = std::max(ml, nl[v]);
-    if (m->colf != &m->rowf) {
-      d2h(nl.data(), m->colf->nib.p, n, s);
+  {  // largest |ibar| - k over both sides (G rows per node)
+    int mk = 0;
+    for (SideFactors* F : {&m->rowf, m->colf}) {
+      d2h(nib.data(), F->nib.p, n, s);
+      d2h(rk.data(), F->rank.p, n, s);
       sync(s);
-      for (int v = 0; v < n; ++v)
-        if (nchild[v] == 0) ml = std::max(ml, nl[v]);
+      for (int v = 0; v < n; ++v) mk = std::max(mk, nib[v] - rk[v]);
     }
-    P->max_leaf_nib = ml;
+    P->max_nk = mk;
   }
   // ticket orders: BFS ids are level-major, so deepest level first = descending
-  // level blocks; within a level any order works.
+  // ids; leaves ride along in their level (they have no producers upward and
+  // only their parent downward).
   std::vector<int> up, down, leaves;
-  for (int l = t->n_levels; l >= 2; --l)
-    for (int v = t->level_begin(l); v < t->level_end(l); ++v) up.push_back(v);
-  for (int l = 2; l <= t->n_levels; ++l)
-    for (int v = t->level_begin(l); v < t->level_end(l); ++v)
-      if (nchild[v] > 0) down.push_back(v);
+  for (int v = n - 1; v >= 1; --v) up.push_back(v);
+  for (int v = 1; v < n; ++v) down.push_back(v);
   for (int v = 0; v < n; ++v)
     if (nchild[v] == 0) leaves.push_back(v);
+  if (n == 1) down.push_back(0);  // a root leaf: its (zero) far-field rows
   P->n_up = (int)up.size();
   P->n_down = (int)down.size();
   P->n_leaves = (int)leaves.size();
@@ -82,18 +77,6 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   h2d(P->up_order.p, up.data(), up.size(), s);
   h2d(P->down_order.p, down.data(), down.size(), s);
   h2d(P->leaves.p, leaves.data(), leaves.size(), s);
-  std::vector<int> up_int;
-  std::vector<unsigned char> in_int(n, 0);
-  for (int v : up)
-    if (nchild[v] > 0) {
-      up_int.push_back(v);
-      in_int[v] = 1;
-    }
-  P->n_up_int = (int)up_int.size();
-  P->up_int.alloc(std::max<size_t>(up_int.size(), 1), s);
-  h2d(P->up_int.p, up_int.data(), up_int.size(), s);
-  P->inset_int.alloc(n, s);
-  h2d(P->inset_int.p, in_int.data(), n, s);
   P->done.alloc(n, s);
   P->done.zero(s);
   P->inset_all.alloc(n, s);
@@ -109,14 +92,13 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
 struct PhaseSets {
   bool gather = true;
   bool zero_qhat = false;                 // shard: unowned coefficients must be 0 for the all-reduce
-  const int* up_leaves = nullptr; int n_up_leaves = 0;  // leaves (independent, one CTA each)
-  const int* up = nullptr; int n_up = 0;  // internal upward order (deepest level first)
+  const int* up = nullptr; int n_up = 0;  // upward order (deepest level first, leaves included)
   const unsigned char* up_in = nullptr;   // membership of the upward / downward sets
   const unsigned char* down_in = nullptr;
-  bool far = true;                        // run coupling / downward / nearfield / leaf far field
+  bool far = true;                        // run coupling / downward / nearfield / combine
   const int* coup = nullptr; int n_coup = -1;  // coupling targets (nullptr + -1: all nodes)
-  const int* down = nullptr; int n_down = 0;
-  const int* leaves = nullptr; int n_leaves = 0;
+  const int* down = nullptr; int n_down = 0;   // downward order (shallowest first, leaves included)
+  const int* leaves = nullptr; int n_leaves = 0;  // nearfield / combine rows
 };
 
 template <int KER, int D, int RC>
@@ -151,18 +133,14 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     SMASH_CUDA(cudaStreamWaitEvent(sn, m->fork, 0));
     mark(6, sn);
     NearArgs na{S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
-                pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, t->perm_row.p, z, nrhs,
-                c0, m->p.dx, t->nu0};
+                pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zn.p, m->p.dx, t->nu0};
     launch_near<KER, D, RC>(na, sn);
     ++launches;
     mark(7, sn);
     SMASH_CUDA(cudaEventRecord(m->join, sn));
   }
-  XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, m->qt.p, m->qhat.p, m->zhat.p, cs};
-  if (S.n_up_leaves) {
-    launch_upward_leaves<RC>(up, P, S.up_leaves, S.n_up_leaves, s);
-    launches += 1;
-  }
+  XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
+              m->zhat.p, cs};
   if (S.n_up) {
     launch_upward<RC>(up, P, S.up, S.n_up, S.up_in, s);
     launches += 2;
@@ -174,17 +152,17 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     launch_coupling<KER, D, RC>(ca, s);
     ++launches;
     mark(3, s);
-    XferArgs down{t->nchild.p, t->child_first.p, t->parent.p, t->row_a.p, m->qt.p, m->qhat.p,
-                  m->zhat.p, rs};
+    XferArgs down{t->nchild.p, t->child_first.p, t->parent.p, t->row_a.p, t->row_b.p, m->qt.p,
+                  m->qhat.p, m->zhat.p, rs};
     if (S.n_down) {
-      launch_downward<RC>(down, P, S.down, S.n_down, S.down_in, s);
+      launch_downward<RC>(down, P, S.down, S.n_down, S.down_in, m->zf.p, s);
       launches += 2;
     }
     mark(4, s);
     SMASH_CUDA(cudaStreamWaitEvent(s, m->join, 0));
     mark(8, s);
-    launch_leaf_add<RC>(down, P, S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, t->perm_row.p, z,
-                        nrhs, c0, t->nu0, s);
+    launch_combine<RC>(S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, t->perm_row.p, m->zn.p,
+                       m->zf.p, z, nrhs, c0, s);
     ++launches;
   }
   mark(5, s);
@@ -304,18 +282,20 @@ int prepare(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
     m->qt.alloc((size_t)t->ny * 16, s);
     m->qhat.alloc((size_t)std::max<int64_t>(m->colf->skel_total, 1) * 16, s);
     m->zhat.alloc((size_t)std::max<int64_t>(m->rowf.skel_total, 1) * 16, s);
+    m->zn.alloc((size_t)t->nx * 16, s);
+    m->zf.alloc((size_t)t->nx * 16, s);
     m->ws_nrhs = 16;
   }
-  // largest nrhs chunk whose transfer-kernel shared memory and registers fit
-  int rc_cap = 16;
-  auto xfer_smem = [&](int rc) {
-    return ((size_t)P->max_rank * rc + (size_t)P->max_nib * (2 * rc + 1) + 4096 + 64) * sizeof(double);
+  // largest nrhs chunk whose transfer-kernel tiles and shared memory fit
+  auto fits = [&](int rc) {
+    const XferGeom G = xfer_geom(P->max_nib, P->max_rank, P->max_nk, rc);
+    const int tiles = ((P->max_rank + 7) / 8) * ((rc + 7) / 8);
+    return tiles <= 8 * XFER_MAXT && xfer_smem_up(G) <= 200 * 1024 &&
+           xfer_smem_down(G) <= 200 * 1024;
   };
-  while (rc_cap > 1 && (xfer_smem(rc_cap) > 200 * 1024 || P->max_rank * rc_cap > XFER_THREADS * XFER_MAXO))
-    rc_cap /= 2;
-  SMASH_CHECK(xfer_smem(rc_cap) <= 227 * 1024 &&
-                  P->max_rank <= XFER_THREADS * XFER_MAXO,
-              SMASH_ERR_INVALID, "intermediate sets too large for the matvec");
+  int rc_cap = 16;
+  while (rc_cap > 1 && !fits(rc_cap)) rc_cap /= 2;
+  SMASH_CHECK(fits(rc_cap), SMASH_ERR_INVALID, "intermediate sets too large for the matvec");
   return rc_cap;
 }
 
@@ -335,9 +315,8 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
   MatvecPlan* P = plan_of(m, s);
   const int rc_cap = prepare(m, P, s);
   PhaseSets S;
-  S.up_leaves = P->leaves.p; S.n_up_leaves = P->n_leaves;
-  S.up = P->up_int.p; S.n_up = P->n_up_int;
-  S.up_in = P->inset_int.p;
+  S.up = P->up_order.p; S.n_up = P->n_up;
+  S.up_in = P->inset_all.p;
   S.down_in = P->inset_all.p;
   S.down = P->down_order.p; S.n_down = P->n_down;
   S.leaves = P->leaves.p; S.n_leaves = P->n_leaves;
@@ -371,16 +350,13 @@ void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
     return out;
   };
   std::vector<int> own = to_bfs(own_post, n_own), top = to_bfs(top_post, n_top);
-  std::vector<int> own_up, top_up = top, coup = own, down, leaves;
-  for (int v : own)
-    if (nchild[v] > 0) own_up.push_back(v);  // owned leaves go through the leaf kernel
+  std::vector<int> own_up = own, top_up = top, coup = own, down, leaves;
   std::sort(own_up.rbegin(), own_up.rend());  // BFS is level-major: descending = deepest first
   std::sort(top_up.rbegin(), top_up.rend());
   coup.insert(coup.end(), top.begin(), top.end());
   std::sort(coup.begin(), coup.end());
+  down = coup;  // ascending = shallowest first; leaves write their far-field rows
   for (int v : coup)
-    if (nchild[v] > 0) down.push_back(v);  // ascending = shallowest first
-  for (int v : own)
     if (nchild[v] == 0) leaves.push_back(v);
   std::unique_ptr<ShardSets> S(new ShardSets());
   auto up = [&](DBuf<int>& d, const std::vector<int>& h, int& cnt) {
@@ -424,7 +400,6 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
   PhaseSets S;
   if (stage == 1) {  // local upward of the owned subtrees; unowned coefficients 0
     S.zero_qhat = true;
-    S.up_leaves = H.leaves.p; S.n_up_leaves = H.n_leaves;
     S.up = H.own_up.p; S.n_up = H.n_own_up; S.up_in = H.own_in.p;
     S.far = false;
   } else {  // after the coefficient exchange: top upward, then owned far/near field

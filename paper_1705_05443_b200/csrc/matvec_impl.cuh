@@ -12,7 +12,7 @@ namespace mv {
 constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 constexpr int XFER_THREADS = 256;
-constexpr int XFER_MAXO = 8;  // outputs per thread in the upward kernel (k * RC <= 2048)
+constexpr int XFER_MAXT = 4;  // upward output tiles per warp: ceil(k / 8) * ceil(RC / 8) <= 32
 
 struct Side {
   const int* nib;
@@ -44,7 +44,7 @@ struct CouplingArgs {
   int max_targets;  // largest target set (skeleton rank) -> CTA size of the DMMA path
 };
 
-// nearfield: z[perm_row[p]] = sum_{j in Lm(v)} K(x_p, y_s) qt_s for the rows of every leaf v
+// nearfield: zn[p] = sum_{j in Lm(v)} K(x_p, y_s) qt_s for the rows p of every listed leaf v
 struct NearArgs {
   const int* leaves;
   int n_leaves;
@@ -59,10 +59,7 @@ struct NearArgs {
   const int* Lmptr;
   const int* Lmsrc;
   const double* qt;
-  const int* perm_row;
-  double* z;
-  int64_t ldz;
-  int64_t c0;
+  double* zn;       // tree-ordered nearfield rows (RC per row)
   double dx;
   int max_targets;  // largest leaf row count
 };
@@ -77,30 +74,38 @@ void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, doub
 
 // transfer passes (matvec_xfer.cu)
 struct XferPlan {
-  DBuf<int> up_order;    // non-root nodes, deepest level first
-  DBuf<int> down_order;  // internal non-root nodes, shallowest level first
+  DBuf<int> up_order;    // non-root nodes, deepest level first (BFS ids descending)
+  DBuf<int> down_order;  // non-root nodes, shallowest level first (BFS ids ascending)
   DBuf<int> leaves;
   DBuf<unsigned char> inset_all;  // membership of the whole-tree passes (all ones)
-  DBuf<unsigned> done;   // per node epoch flags
+  DBuf<unsigned> done;   // per node flags (reset before each pass)
   DBuf<unsigned> counters;  // [0] upward tickets, [1] downward tickets
   int n_up = 0, n_down = 0, n_leaves = 0;
-  int max_nib = 0, max_rank = 0, max_leaf_nib = 0;
-  DBuf<int> up_int;                 // internal non-root nodes, deepest level first
-  DBuf<unsigned char> inset_int;    // 1 for internal non-root nodes
-  int n_up_int = 0;
-  unsigned epoch = 0;
+  int max_nib = 0, max_rank = 0, max_nk = 0;
 };
 
 struct XferArgs {
   const int* nchild;
   const int* child_first;
   const int* parent;
-  const int* pt_a;  // leaf point range start (column side for the upward pass)
+  const int* pt_a;  // leaf point range [pt_a, pt_b) (column side upward, row side downward)
+  const int* pt_b;
   const double* qt;
   double* qhat;
   double* zhat;
   Side side;
 };
+
+// shared-memory geometry of the transfer kernels (from the plan maxima)
+struct XferGeom {
+  int ks;   // G row stride in shared memory (>= max rank, = 4 mod 8)
+  int rcs;  // row stride of staged coefficient rows
+  int tb;   // G rows per staged chunk
+  int max_nib, max_rank;
+};
+XferGeom xfer_geom(int max_nib, int max_rank, int max_nk, int rc);
+size_t xfer_smem_up(const XferGeom& G);
+size_t xfer_smem_down(const XferGeom& G);
 
 template <int RC>
 void launch_gather(const double* q, int64_t ldq, const int* perm, int64_t n, int64_t c0,
@@ -110,35 +115,12 @@ template <int RC>
 void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
                    const unsigned char* inset, cudaStream_t s);
 template <int RC>
-void launch_upward_leaves(const XferArgs& a, const XferPlan& P, const int* leaves, int n,
-                          cudaStream_t s);
-template <int RC>
 void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
-                     const unsigned char* inset, cudaStream_t s);
+                     const unsigned char* inset, double* zf, cudaStream_t s);
 template <int RC>
-void launch_leaf_add(const XferArgs& a, const XferPlan& P, const int* leaves, int n_leaves,
-                     const int* row_a, const int* row_b, const int* perm_row, double* z,
-                     int64_t ldz, int64_t c0, int nu0, cudaStream_t s);
-
-// Block-wide staging copy dst[e] = f(e), e < n: each thread issues U independent
-// global loads before its shared-memory stores, so a whole tile is one memory
-// round trip instead of n / blockDim dependent ones.
-template <int U, typename F, typename S>
-__device__ __forceinline__ void stage_block(int n, F load, S store) {
-  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      v[u] = e < n ? load(e) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < n) store(e, v[u]);
-    }
-  }
-}
+void launch_combine(const int* leaves, int n_leaves, const int* row_a, const int* row_b,
+                    const int* perm_row, const double* zn, const double* zf, double* z,
+                    int64_t ldz, int64_t c0, cudaStream_t s);
 
 }  // namespace mv
 }  // namespace smash

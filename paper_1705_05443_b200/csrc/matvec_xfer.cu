@@ -1,16 +1,26 @@
 // K6 / K8 / K10: permutation gather, upward and downward transfer passes and
-// the leaf far-field epilogue of the matvec (smash/apply.py:39-53, 60-72, 78-80).
+// the final far + near combine of the matvec (smash/apply.py:39-53, 60-72, 78-80).
 //
 // The transfer passes are level-ordered dataflow: a node's upward projection
-// needs its children's, its downward step needs its parent's.  Instead of one
-// launch per level (the small top levels are pure latency), each pass is ONE
-// persistent launch: CTAs take node tickets from an atomic counter in level
-// order (deepest first upward, shallowest first downward) and spin on the
-// producers' done flags, which were necessarily handed out earlier to CTAs
-// that are already running -- so the wait cannot deadlock.  Cross-CTA data is
-// published with __threadfence() + a release flag and read with __ldcg (L2).
-// X_v = P [I; G] is applied implicitly; G row tiles are staged in shared memory
-// with batched loads.
+// needs its children's, its downward step needs its parent's.  Each pass is ONE
+// persistent launch over all its nodes (leaves included): CTAs take node
+// tickets from an atomic counter in level order (deepest first upward,
+// shallowest first downward) and spin on the producers' done flags, which were
+// necessarily handed out earlier to CTAs that are already running -- so the
+// wait cannot deadlock.  Cross-CTA data is published with __threadfence() + a
+// release flag and read through L2 (cp.async.cg / ld.cg).
+//
+// Per node the work is a small GEMM with the interpolative factor
+// X_v = P [I; G] (G: (|ibar| - k) x k row-major):
+//   upward    qhat_v          = in[perm[:k]] + G^T in[perm[k:]]    (in: children's
+//                                coefficients, or the leaf's qt rows)
+//   downward  out[perm[:k]]  += zhat_v,  out[perm[k:]] += G zhat_v (out: children's
+//                                zhat, or the leaf's far-field rows zf)
+// G and the permutation are read-only, so their cp.async staging is issued
+// before the producer wait; the producer rows follow in one more asynchronous
+// batch.  The GEMM runs on the FP64 tensor cores (mma.sync m8n8k4 DMMA) with
+// operands read from shared memory at bank-conflict-free strides (row strides
+// = 4 mod 8 doubles), one 8x8 output tile per warp and item.
 #include "matvec_impl.cuh"
 
 namespace smash {
@@ -36,291 +46,277 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ int g_tile_rows(int ks) { return max(1, min(64, 4096 / ks)); }
-
-__device__ __forceinline__ int next_ticket(unsigned* counter) {
-  __shared__ int s_t;
-  __syncthreads();
-  if (threadIdx.x == 0) s_t = (int)atomicAdd(counter, 1u);
-  __syncthreads();
-  return s_t;
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 
-__device__ __forceinline__ void publish(unsigned* done, int v, unsigned epoch) {
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_commit_wait() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// RC doubles of a coherent (written by other CTAs of this launch) row -> shared
+template <int RC>
+__device__ __forceinline__ void row_l2(double* dst, const double* src) {
+  if constexpr (RC % 2 == 0) {
+#pragma unroll
+    for (int u = 0; u < RC / 2; ++u) cp_async16_cg(dst + 2 * u, src + 2 * u);
+  } else {
+#pragma unroll
+    for (int u = 0; u < RC; ++u) dst[u] = __ldcg(src + u);
+  }
+}
+
+// Read-only G rows [r0, r0 + nr) (row length k) -> shared rows of stride ks.
+__device__ __forceinline__ void stage_g(const double* G, int k, int r0, int nr, double* gs, int ks) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = wid; row < nr; row += nw) {
+    const double* src = G + (int64_t)(r0 + row) * k;
+    for (int c = lane; c < k; c += 32) cp_async8(gs + row * ks + c, src + c);
+  }
+}
+
+__device__ __forceinline__ void publish(unsigned* done, int v) {
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) st_release(&done[v], epoch);
+  if (threadIdx.x == 0) st_release(&done[v], 1u);
 }
 
-// qhat[v] = ivec[perm[:k]] + G^T ivec[perm[k:]]
-// The node's ibar-vector is ONE contiguous block (leaf: its qt rows; internal:
-// its children's coefficient rows), so it is staged in the same batched load as
-// the permutation and the first G tile: one memory round trip per node.
+// qhat_v = in[perm[:k]] + G^T in[perm[k:]] for every node of `order`.
 template <int RC>
-__device__ __forceinline__ void up_node(const XferArgs& A, int v, double* sh) {
-  const Side& cs = A.side;
-  const int nc = A.nchild[v];
-    const int ni = cs.nib[v], k = cs.rank[v];
+__global__ void __launch_bounds__(XFER_THREADS) k_upward(XferArgs A, XferGeom Gm, const int* order,
+                                                         int n, const unsigned char* inset,
+                                                         unsigned* counter, unsigned* done) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ int s_tk;
+  const int ks = Gm.ks, rcs = Gm.rcs;
+  double* gs = sh;                        // tb x ks   (G chunk)
+  double* ivp = sh + Gm.tb * ks;          // (max_nib + 8) x rcs (permuted ibar rows)
+  const Side cs = A.side;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  constexpr int NR = (RC + 7) / 8;
+  if (tid == 0) s_tk = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  int tk = s_tk;
+  while (tk < n) {
+    const int v = order[tk];
+    __syncthreads();  // s_tk consumed; the previous node's shared memory is free
+    if (tid == 0) s_tk = (int)atomicAdd(counter, 1u);  // prefetch the next ticket
+    const int ni = cs.nib[v], k = cs.rank[v], nc = A.nchild[v];
+    const int nk = ni - k, nk4 = (nk + 3) & ~3;
     if (k > 0) {
-      const bool leaf = nc == 0;
-      const double* ivec = leaf ? A.qt + (int64_t)A.pt_a[v] * RC
-                                : A.qhat + (int64_t)cs.skel_off[A.child_first[v]] * RC;
-      const int* perm = cs.perm + cs.ib_off[v];
       const double* G = cs.G + cs.g_off[v];
-      const int nk = ni - k;
-      const int TB = g_tile_rows(k);
-      double* iv = sh;                 // ni * RC, unpermuted
-      double* pm = iv + ni * RC;       // ni permutation entries (as doubles)
-      double* gs = pm + ni;            // TB * k
-      const int n_iv = ni * RC, n_g0 = min(TB, nk) * k;
-      stage_block<16>(n_iv + ni + n_g0,
-                      [&](int e) {
-                        return e < n_iv ? __ldcg(ivec + e)
-                                        : e < n_iv + ni ? (double)perm[e - n_iv]
-                                                        : G[e - n_iv - ni];
-                      },
-                      [&](int e, double x) { iv[e] = x; });
+      const int* perm = cs.perm + cs.ib_off[v];
+      const double* in = nc == 0 ? A.qt + (int64_t)A.pt_a[v] * RC
+                                 : A.qhat + (int64_t)cs.skel_off[A.child_first[v]] * RC;
+      const int tb0 = min(Gm.tb, nk);
+      stage_g(G, k, 0, tb0, gs, ks);  // read-only: in flight during the producer wait
+      for (int e = tid; e < (nk4 - nk) * k; e += blockDim.x) {  // K padding rows (nk <= tb)
+        if (nk4 <= Gm.tb) gs[(nk + e / k) * ks + e % k] = 0.0;
+      }
+      for (int e = tid; e < (nk4 - nk) * rcs; e += blockDim.x) ivp[ni * rcs + e] = 0.0;
+      if (tid < nc) {
+        const int c = A.child_first[v] + tid;
+        if (inset[c])  // producers outside this launch are final already
+          while (ld_acquire(&done[c]) == 0u) __nanosleep(32);
+      }
       __syncthreads();
-      // gather the permuted ibar rows once: ivp[c] = iv[perm[c]] (after gs, reusing pm's slot
-      // would alias; ivp lives after the G tile)
-      double* ivp = gs + TB * k;
-      for (int e = threadIdx.x; e < ni * RC; e += blockDim.x)
-        ivp[e] = iv[(int)pm[e / RC] * RC + e % RC];
+      for (int j = tid; j < ni; j += blockDim.x) row_l2<RC>(ivp + j * rcs, in + (int64_t)perm[j] * RC);
+      cp_commit_wait();
       __syncthreads();
-      // register tile: TA rows (a) x TR columns (r) per thread
-      constexpr int TR = RC < 4 ? RC : 4;
-      constexpr int TA = 2;
-      const int na = (k + TA - 1) / TA, nrq = RC / TR;
-      const int items = na * nrq;
-      for (int it0 = 0; it0 < items; it0 += blockDim.x) {
-        const int it = it0 + threadIdx.x;
-        const bool ok = it < items;
-        const int a0 = ok ? (it / nrq) * TA : 0, r0 = ok ? (it % nrq) * TR : 0;
-        double acc[TA][TR];
+      const int NA = (k + 7) >> 3, T = NA * NR;
+      double c[XFER_MAXT][2];
 #pragma unroll
-        for (int i = 0; i < TA; ++i)
+      for (int i = 0; i < XFER_MAXT; ++i) c[i][0] = c[i][1] = 0.0;
+      for (int cb = 0;;) {
+        const int tbc = min(Gm.tb, nk - cb);
+        const int steps = (tbc + 3) >> 2;
 #pragma unroll
-          for (int j = 0; j < TR; ++j)
-            acc[i][j] = (ok && a0 + i < k) ? ivp[(a0 + i) * RC + r0 + j] : 0.0;
-        for (int b0 = 0; b0 < nk; b0 += TB) {
-          const int tb = min(TB, nk - b0);
-          if (b0 > 0) {
-            __syncthreads();
-            const double* src = G + (int64_t)b0 * k;
-            stage_block<16>(tb * k, [&](int e) { return src[e]; }, [&](int e, double x) { gs[e] = x; });
-            __syncthreads();
-          }
-          if (ok) {
-            const double* wb = ivp + (k + b0) * RC + r0;
-            for (int bb = 0; bb < tb; ++bb) {
-              double g[TA], w[TR];
-#pragma unroll
-              for (int i = 0; i < TA; ++i) g[i] = a0 + i < k ? gs[bb * k + a0 + i] : 0.0;
-#pragma unroll
-              for (int j = 0; j < TR; ++j) w[j] = wb[bb * RC + j];
-#pragma unroll
-              for (int i = 0; i < TA; ++i)
-#pragma unroll
-                for (int j = 0; j < TR; ++j) acc[i][j] = fma(g[i], w[j], acc[i][j]);
-            }
+        for (int i = 0; i < XFER_MAXT; ++i) {
+          const int t = wid + 8 * i;
+          if (t < T) {
+            const int a0 = (t / NR) * 8, r0 = (t % NR) * 8;
+            const double* ga = gs + q * ks + a0 + g;
+            const double* bb = ivp + (k + cb + q) * rcs + r0 + g;
+#pragma unroll 4
+            for (int s = 0; s < steps; ++s) dmma(c[i][0], c[i][1], ga[s * 4 * ks], bb[s * 4 * rcs]);
           }
         }
-        if (ok) {
-          double* out = A.qhat + (int64_t)cs.skel_off[v] * RC;
+        cb += tbc;
+        if (cb >= nk) break;
+        __syncthreads();
+        const int tbn = min(Gm.tb, nk - cb);
+        stage_g(G, k, cb, tbn, gs, ks);
+        for (int e = tid; e < (nk4 - nk) * k; e += blockDim.x)
+          if (cb + tbn == nk && tbn + (nk4 - nk) <= Gm.tb) gs[(tbn + e / k) * ks + e % k] = 0.0;
+        cp_commit_wait();
+        __syncthreads();
+      }
+      double* out = A.qhat + (int64_t)cs.skel_off[v] * RC;
 #pragma unroll
-          for (int i = 0; i < TA; ++i)
-            if (a0 + i < k)
-#pragma unroll
-              for (int j = 0; j < TR; ++j) out[(int64_t)(a0 + i) * RC + r0 + j] = acc[i][j];
-        }
-        if (it0 + blockDim.x < items && nk > TB) {  // the G tiles must be restaged
-          __syncthreads();
-          const int tb0 = min(TB, nk);
-          stage_block<16>(tb0 * k, [&](int e) { return G[e]; }, [&](int e, double x) { gs[e] = x; });
-          __syncthreads();
+      for (int i = 0; i < XFER_MAXT; ++i) {
+        const int t = wid + 8 * i;
+        if (t < T) {
+          const int a = (t / NR) * 8 + g, r = (t % NR) * 8 + 2 * q;
+          if (a < k) {
+            if (r < RC) out[(int64_t)a * RC + r] = c[i][0] + ivp[a * rcs + r];
+            if (r + 1 < RC) out[(int64_t)a * RC + r + 1] = c[i][1] + ivp[a * rcs + r + 1];
+          }
         }
       }
     }
-}
-
-template <int RC>
-__global__ void __launch_bounds__(XFER_THREADS) k_upward(XferArgs A, const int* order, int n,
-                                                         const unsigned char* inset,
-                                                         unsigned* counter, unsigned* done,
-                                                         unsigned epoch) {
-  extern __shared__ double sh[];
-  for (;;) {
-    const int tk = next_ticket(counter);
-    if (tk >= n) break;
-    const int v = order[tk];
-    const int nc = A.nchild[v];
-    if (threadIdx.x < nc) {
-      const int c = A.child_first[v] + threadIdx.x;
-      if (inset[c])  // producers outside this launch are final already
-        while (ld_acquire(&done[c]) != epoch) __nanosleep(40);
-    }
-    __syncthreads();
-    up_node<RC>(A, v, sh);
-    publish(done, v, epoch);
+    publish(done, v);
+    tk = s_tk;
   }
 }
 
-// Leaves have no producers: one CTA per leaf, no tickets, no flags.
+// Downward: for internal nodes out = the children's zhat block (read-modify-
+// write), for leaves out = the leaf's rows of the far-field buffer zf (store).
 template <int RC>
-__global__ void __launch_bounds__(64) k_upward_leaves(XferArgs A, const int* leaves, int n) {
-  extern __shared__ double sh[];
-  if ((int)blockIdx.x >= n) return;
-  const int v = leaves[blockIdx.x];
-  if (v == 0) return;  // a leaf root has no factor
-  up_node<RC>(A, v, sh);
-}
-
-// zhat[children] += X_v zhat[v] (internal non-root nodes, after the coupling).
-// zhat_v, the children's contiguous coefficient block, the permutation and the
-// first G tile are staged in one batched load; the block is updated in shared
-// memory and written back coalesced.
-template <int RC>
-__global__ void __launch_bounds__(XFER_THREADS) k_downward(XferArgs A, const int* order, int n,
+__global__ void __launch_bounds__(XFER_THREADS) k_downward(XferArgs A, XferGeom Gm,
+                                                           const int* order, int n,
                                                            const unsigned char* inset,
                                                            unsigned* counter, unsigned* done,
-                                                           unsigned epoch, int root) {
-  extern __shared__ double sh[];
+                                                           double* zf) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ int s_tk;
+  const int ks = Gm.ks, rcs = Gm.rcs;
+  double* gs = sh;                             // tb x ks
+  double* zv = sh + Gm.tb * ks;                // (max_rank + 8) x rcs
+  int* pm = reinterpret_cast<int*>(zv + (Gm.max_rank + 8) * rcs);  // max_nib
   const Side rs = A.side;
-  for (;;) {
-    const int tk = next_ticket(counter);
-    if (tk >= n) break;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  constexpr int NR = (RC + 7) / 8;
+  if (tid == 0) s_tk = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  int tk = s_tk;
+  while (tk < n) {
     const int v = order[tk];
-    const int p = A.parent[v];
-    if (threadIdx.x == 0 && p != root && inset[p])
-      while (ld_acquire(&done[p]) != epoch) __nanosleep(40);
     __syncthreads();
-    const int ni = rs.nib[v], k = rs.rank[v];
-    if (k > 0 && ni > 0) {
-      const int ks = k | 1;
-      const int* perm = rs.perm + rs.ib_off[v];
-      const double* zsrc = A.zhat + (int64_t)rs.skel_off[v] * RC;
-      double* dst = A.zhat + (int64_t)rs.skel_off[A.child_first[v]] * RC;
-      const double* G = rs.G + rs.g_off[v];
-      const int nk = ni - k;
-      const int TB = g_tile_rows(ks);
-      double* zv = sh;             // k * RC
-      double* db = zv + k * RC;    // ni * RC: the children's block
-      double* pm = db + ni * RC;   // ni
-      double* gs = pm + ni;        // TB * ks
-      const int n_z = k * RC, n_d = ni * RC, tb0 = min(TB, nk);
-      stage_block<16>(n_z + n_d + ni + tb0 * k,
-                      [&](int e) {
-                        return e < n_z ? __ldcg(zsrc + e)
-                               : e < n_z + n_d ? __ldcg(dst + (e - n_z))
-                               : e < n_z + n_d + ni ? (double)perm[e - n_z - n_d]
-                                                    : G[e - n_z - n_d - ni];
-                      },
-                      [&](int e, double x) {
-                        if (e < n_z + n_d + ni) {
-                          zv[e] = x;
-                        } else {
-                          const int g = e - n_z - n_d - ni;
-                          gs[(g / k) * ks + g % k] = x;
-                        }
-                      });
-      __syncthreads();
-      for (int e = threadIdx.x; e < k * RC; e += blockDim.x) {
-        const int a = e / RC, r = e % RC;
-        db[(int)pm[a] * RC + r] += zv[e];
+    if (tid == 0) s_tk = (int)atomicAdd(counter, 1u);
+    const int ni = rs.nib[v], k = rs.rank[v], nc = A.nchild[v];
+    const bool leaf = nc == 0;
+    const int nk = ni - k, k4 = (k + 3) & ~3;
+    if (k == 0) {
+      if (leaf) {  // no factor (a root leaf): the far field is zero
+        const int ra = A.pt_a[v], nr = A.pt_b[v] - ra;
+        for (int e = tid; e < nr * RC; e += blockDim.x) zf[(int64_t)ra * RC + e] = 0.0;
       }
-      constexpr int TR = RC < 4 ? RC : 4;
-      constexpr int TB2 = 2;
-      for (int b0 = 0; b0 < nk; b0 += TB) {
-        const int tb = min(TB, nk - b0);
-        if (b0 > 0) {
-          const double* src = G + (int64_t)b0 * k;
-          __syncthreads();
-          stage_block<16>(tb * k, [&](int e) { return src[e]; },
-                          [&](int e, double x) { gs[(e / k) * ks + e % k] = x; });
-          __syncthreads();
-        }
-        const int nb = (tb + TB2 - 1) / TB2, nrq = RC / TR;
-        for (int it = threadIdx.x; it < nb * nrq; it += blockDim.x) {
-          const int bl = (it / nrq) * TB2, r0 = (it % nrq) * TR;
-          double y[TB2][TR];
-#pragma unroll
-          for (int i = 0; i < TB2; ++i)
-#pragma unroll
-            for (int j = 0; j < TR; ++j) y[i][j] = 0.0;
-          const double* g0 = gs + bl * ks;
-          const bool two = bl + 1 < tb;
-          for (int a = 0; a < k; ++a) {
-            double w[TR];
-#pragma unroll
-            for (int j = 0; j < TR; ++j) w[j] = zv[a * RC + r0 + j];
-            const double ga = g0[a], gb = two ? g0[ks + a] : 0.0;
-#pragma unroll
-            for (int j = 0; j < TR; ++j) {
-              y[0][j] = fma(ga, w[j], y[0][j]);
-              y[1][j] = fma(gb, w[j], y[1][j]);
+    } else {
+      const double* G = rs.G + rs.g_off[v];
+      const int* perm = rs.perm + rs.ib_off[v];
+      const int tb0 = min(Gm.tb, nk);
+      stage_g(G, k, 0, tb0, gs, ks);
+      for (int e = tid; e < tb0 * (k4 - k); e += blockDim.x) {  // K padding columns
+        const int d = k4 - k;
+        gs[(e / d) * ks + k + e % d] = 0.0;
+      }
+      for (int j = tid; j < ni; j += blockDim.x) pm[j] = perm[j];
+      for (int e = tid; e < (k4 - k) * rcs; e += blockDim.x) zv[k * rcs + e] = 0.0;
+      const int p = A.parent[v];
+      if (tid == 0 && p > 0 && inset[p])
+        while (ld_acquire(&done[p]) == 0u) __nanosleep(32);
+      __syncthreads();
+      const double* zsrc = A.zhat + (int64_t)rs.skel_off[v] * RC;
+      for (int a = tid; a < k; a += blockDim.x) row_l2<RC>(zv + a * rcs, zsrc + (int64_t)a * RC);
+      cp_commit_wait();
+      __syncthreads();
+      double* dst = leaf ? zf + (int64_t)A.pt_a[v] * RC
+                         : A.zhat + (int64_t)rs.skel_off[A.child_first[v]] * RC;
+      // identity rows: out[perm[a]] (+)= zhat_v[a]
+      for (int e = tid; e < k * RC; e += blockDim.x) {
+        const int a = e / RC, r = e - a * RC;
+        double* d = dst + (int64_t)pm[a] * RC + r;
+        const double x = zv[a * rcs + r];
+        *d = leaf ? x : __ldcg(d) + x;
+      }
+      const int ksteps = k4 >> 2;
+      for (int cb = 0; cb < nk;) {
+        const int tbc = min(Gm.tb, nk - cb);
+        const int T = ((tbc + 7) >> 3) * NR;
+        for (int t0 = wid; t0 < T; t0 += 16) {  // two independent tiles per warp pass
+          double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          const int t1 = t0 + 8;
+          const int b00 = (t0 / NR) * 8, r00 = (t0 % NR) * 8;
+          const int b01 = (t1 / NR) * 8, r01 = (t1 % NR) * 8;
+          const double* ga0 = gs + (b00 + g) * ks + q;
+          const double* ga1 = gs + (b01 + g) * ks + q;
+          const double* zb0 = zv + q * rcs + r00 + g;
+          const double* zb1 = zv + q * rcs + r01 + g;
+          if (t1 < T) {
+#pragma unroll 4
+            for (int s = 0; s < ksteps; ++s) {
+              dmma(c[0][0], c[0][1], ga0[4 * s], zb0[4 * s * rcs]);
+              dmma(c[1][0], c[1][1], ga1[4 * s], zb1[4 * s * rcs]);
             }
+          } else {
+#pragma unroll 4
+            for (int s = 0; s < ksteps; ++s) dmma(c[0][0], c[0][1], ga0[4 * s], zb0[4 * s * rcs]);
           }
 #pragma unroll
-          for (int i = 0; i < TB2; ++i)
-            if (bl + i < tb) {
-              double* d = db + (int)pm[k + b0 + bl + i] * RC + r0;
-#pragma unroll
-              for (int j = 0; j < TR; ++j) d[j] += y[i][j];
+          for (int i = 0; i < 2; ++i) {
+            const int t = i ? t1 : t0;
+            if (t >= T) break;
+            const int b = (t / NR) * 8 + g, r = (t % NR) * 8 + 2 * q;
+            if (b < tbc) {
+              double* d = dst + (int64_t)pm[k + cb + b] * RC + r;
+              if (leaf) {
+                if (r < RC) d[0] = c[i][0];
+                if (r + 1 < RC) d[1] = c[i][1];
+              } else {
+                if (r < RC) d[0] = __ldcg(d) + c[i][0];
+                if (r + 1 < RC) d[1] = __ldcg(d + 1) + c[i][1];
+              }
             }
+          }
         }
+        cb += tbc;
+        if (cb >= nk) break;
+        __syncthreads();
+        const int tbn = min(Gm.tb, nk - cb);
+        stage_g(G, k, cb, tbn, gs, ks);
+        for (int e = tid; e < tbn * (k4 - k); e += blockDim.x) {
+          const int d = k4 - k;
+          gs[(e / d) * ks + k + e % d] = 0.0;
+        }
+        cp_commit_wait();
+        __syncthreads();
       }
-      __syncthreads();
-      for (int e = threadIdx.x; e < ni * RC; e += blockDim.x) dst[e] = db[e];
     }
-    publish(done, v, epoch);
+    if (!leaf) publish(done, v);  // (no consumer waits on a leaf)
+    else __syncthreads();          // s_tk written by thread 0 above
+    tk = s_tk;
   }
 }
 
-// z[perm_row[p]] += (X_v zhat_v)[p] for the rows of every non-root leaf
+// z[perm_row[p], c0 + r] = zn[p, r] + zf[p, r] for the rows of the listed leaves
+// (one warp per leaf).
 template <int RC>
-__global__ void __launch_bounds__(XFER_THREADS) k_leaf_add(XferArgs A, const int* leaves,
-                                                           int n_leaves, const int* row_a,
-                                                           const int* row_b, const int* perm_row,
-                                                           double* z, int64_t ldz, int64_t c0,
-                                                           int root) {
-  extern __shared__ double sh[];
-  const int li = blockIdx.x;
-  if (li >= n_leaves) return;
-  const int v = leaves[li];
-  if (v == root) return;
-  const Side rs = A.side;
-  const int k = rs.rank[v];
-  if (k == 0) return;
+__global__ void k_combine(const int* leaves, int n_leaves, const int* row_a, const int* row_b,
+                          const int* perm_row, const double* zn, const double* zf, double* z,
+                          int64_t ldz, int64_t c0) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n_leaves) return;
+  const int v = leaves[w];
   const int ra = row_a[v], nr = row_b[v] - ra;
-  double* zv = sh;
-  int* inv = reinterpret_cast<int*>(sh + k * RC);
-  const int* perm = rs.perm + rs.ib_off[v];
-  const double* zsrc = A.zhat + (int64_t)rs.skel_off[v] * RC;
-  for (int c = threadIdx.x; c < nr; c += blockDim.x) inv[perm[c]] = c;
-  for (int e = threadIdx.x; e < k * RC; e += blockDim.x) zv[e] = zsrc[e];
-  __syncthreads();
-  const double* G = rs.G + rs.g_off[v];
-  for (int e = threadIdx.x; e < nr * RC; e += blockDim.x) {
-    const int t = e / RC, r = e % RC;
-    const int pos = inv[t];
-    double y;
-    if (pos < k) {
-      y = zv[pos * RC + r];
-    } else {
-      const double* gr = G + (int64_t)(pos - k) * k;
-      double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-      int a = 0;
-      for (; a + 3 < k; a += 4) {
-        y0 = fma(gr[a], zv[a * RC + r], y0);
-        y1 = fma(gr[a + 1], zv[(a + 1) * RC + r], y1);
-        y2 = fma(gr[a + 2], zv[(a + 2) * RC + r], y2);
-        y3 = fma(gr[a + 3], zv[(a + 3) * RC + r], y3);
-      }
-      for (; a < k; ++a) y0 = fma(gr[a], zv[a * RC + r], y0);
-      y = (y0 + y1) + (y2 + y3);
-    }
-    double* zo = z + (int64_t)perm_row[ra + t] * ldz + c0 + r;
-    *zo += y;
+  for (int e = lane; e < nr * RC; e += 32) {
+    const int t = e / RC, r = e - t * RC;
+    const int64_t p = ra + t;
+    z[(int64_t)perm_row[p] * ldz + c0 + r] = zn[p * RC + r] + zf[p * RC + r];
   }
 }
 
@@ -328,11 +324,32 @@ int xfer_grid(size_t smem) {
   int dev = 0, nsm = 0;
   SMASH_CUDA(cudaGetDevice(&dev));
   SMASH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  int per = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / (smem + 2048)));
+  int per = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smem + 1024)));
   return nsm * per;
 }
 
 }  // namespace
+
+XferGeom xfer_geom(int max_nib, int max_rank, int max_nk, int rc) {
+  XferGeom G;
+  G.ks = (max_rank + 3) & ~3;
+  if (G.ks % 8 == 0) G.ks += 4;  // row stride = 4 (mod 8) doubles: conflict-free fragments
+  G.rcs = rc < 8 ? rc : rc + 4;
+  const int cap = std::max(8, ((64 * 1024) / (G.ks * 8)) & ~7);
+  G.tb = std::min(cap, std::max(8, (max_nk + 7) & ~7));
+  G.max_nib = max_nib;
+  G.max_rank = max_rank;
+  return G;
+}
+
+size_t xfer_smem_up(const XferGeom& G) {
+  return ((size_t)G.tb * G.ks + (size_t)(G.max_nib + 8) * G.rcs) * sizeof(double);
+}
+
+size_t xfer_smem_down(const XferGeom& G) {
+  return ((size_t)G.tb * G.ks + (size_t)(G.max_rank + 8) * G.rcs) * sizeof(double) +
+         (size_t)G.max_nib * sizeof(int);
+}
 
 template <int RC>
 void launch_gather(const double* q, int64_t ldq, const int* perm, int64_t n, int64_t c0,
@@ -345,48 +362,37 @@ template <int RC>
 void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
                    const unsigned char* inset, cudaStream_t s) {
   if (!n) return;
-  const size_t smem = ((size_t)P.max_nib * (2 * RC + 1) + 4096) * sizeof(double);
+  const XferGeom G = xfer_geom(P.max_nib, P.max_rank, P.max_nk, RC);
+  const size_t smem = xfer_smem_up(G);
   SMASH_CUDA(cudaFuncSetAttribute(k_upward<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // flags and ticket counter are reset on the stream (graph-replay safe)
   SMASH_CUDA(cudaMemsetAsync(P.counters.p, 0, sizeof(unsigned), s));
   SMASH_CUDA(cudaMemsetAsync(P.done.p, 0, P.done.n * sizeof(unsigned), s));
   const int grid = std::min(n, xfer_grid(smem));
-  k_upward<RC><<<grid, XFER_THREADS, smem, s>>>(a, order, n, inset, P.counters.p, P.done.p, 1u);
-}
-
-template <int RC>
-void launch_upward_leaves(const XferArgs& a, const XferPlan& P, const int* leaves, int n,
-                          cudaStream_t s) {
-  if (!n) return;
-  const size_t smem = ((size_t)P.max_leaf_nib * (2 * RC + 1) + 4096) * sizeof(double);
-  SMASH_CUDA(cudaFuncSetAttribute(k_upward_leaves<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-  k_upward_leaves<RC><<<n, 64, smem, s>>>(a, leaves, n);
+  k_upward<RC><<<grid, XFER_THREADS, smem, s>>>(a, G, order, n, inset, P.counters.p, P.done.p);
 }
 
 template <int RC>
 void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
-                     const unsigned char* inset, cudaStream_t s) {
+                     const unsigned char* inset, double* zf, cudaStream_t s) {
   if (!n) return;
-  const size_t smem = ((size_t)P.max_rank * RC + (size_t)P.max_nib * (RC + 1) + 4096 + 64) *
-                       sizeof(double);
+  const XferGeom G = xfer_geom(P.max_nib, P.max_rank, P.max_nk, RC);
+  const size_t smem = xfer_smem_down(G);
   SMASH_CUDA(cudaFuncSetAttribute(k_downward<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SMASH_CUDA(cudaMemsetAsync(P.counters.p + 1, 0, sizeof(unsigned), s));
   SMASH_CUDA(cudaMemsetAsync(P.done.p, 0, P.done.n * sizeof(unsigned), s));
   const int grid = std::min(n, xfer_grid(smem));
-  k_downward<RC><<<grid, XFER_THREADS, smem, s>>>(a, order, n, inset, P.counters.p + 1, P.done.p,
-                                                  1u, 0);
+  k_downward<RC><<<grid, XFER_THREADS, smem, s>>>(a, G, order, n, inset, P.counters.p + 1,
+                                                  P.done.p, zf);
 }
 
 template <int RC>
-void launch_leaf_add(const XferArgs& a, const XferPlan& P, const int* leaves, int n_leaves,
-                     const int* row_a, const int* row_b, const int* perm_row, double* z,
-                     int64_t ldz, int64_t c0, int nu0, cudaStream_t s) {
+void launch_combine(const int* leaves, int n_leaves, const int* row_a, const int* row_b,
+                    const int* perm_row, const double* zn, const double* zf, double* z,
+                    int64_t ldz, int64_t c0, cudaStream_t s) {
   if (!n_leaves) return;
-  const size_t smem = (size_t)P.max_rank * RC * sizeof(double) + (size_t)(nu0 + 1) * sizeof(int);
-  SMASH_CUDA(cudaFuncSetAttribute(k_leaf_add<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_leaf_add<RC><<<n_leaves, XFER_THREADS, smem, s>>>(a, leaves, n_leaves, row_a, row_b, perm_row,
-                                                      z, ldz, c0, 0);
+  k_combine<RC><<<cdiv((int64_t)n_leaves * 32, 256), 256, 0, s>>>(leaves, n_leaves, row_a, row_b,
+                                                                  perm_row, zn, zf, z, ldz, c0);
 }
 
 #define SMASH_XFER_INSTANTIATE(RC)                                                              \
@@ -394,13 +400,11 @@ void launch_leaf_add(const XferArgs& a, const XferPlan& P, const int* leaves, in
                                   cudaStream_t);                                               \
   template void launch_upward<RC>(const XferArgs&, XferPlan&, const int*, int,                  \
                                   const unsigned char*, cudaStream_t);                          \
-  template void launch_upward_leaves<RC>(const XferArgs&, const XferPlan&, const int*, int,      \
-                                         cudaStream_t);                                         \
   template void launch_downward<RC>(const XferArgs&, XferPlan&, const int*, int,                \
-                                    const unsigned char*, cudaStream_t);                        \
-  template void launch_leaf_add<RC>(const XferArgs&, const XferPlan&, const int*, int,          \
-                                    const int*, const int*, const int*, double*, int64_t,       \
-                                    int64_t, int, cudaStream_t);
+                                    const unsigned char*, double*, cudaStream_t);               \
+  template void launch_combine<RC>(const int*, int, const int*, const int*, const int*,         \
+                                   const double*, const double*, double*, int64_t, int64_t,     \
+                                   cudaStream_t);
 SMASH_XFER_INSTANTIATE(1)
 SMASH_XFER_INSTANTIATE(2)
 SMASH_XFER_INSTANTIATE(4)

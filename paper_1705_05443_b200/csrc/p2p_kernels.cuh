@@ -305,7 +305,7 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
 // kernels
 // ---------------------------------------------------------------------------
 template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS) k_coupling(CouplingArgs A) {
+__global__ void __launch_bounds__(P2P_THREADS, 4) k_coupling(CouplingArgs A) {
   if ((int)blockIdx.x >= A.n_nodes) return;
   const int v = A.list ? A.list[blockIdx.x] : (int)blockIdx.x;
   if (v == 0) return;  // the root has no factor and no coupling
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(P2P_THREADS) k_coupling(CouplingArgs A) {
 }
 
 template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS) k_near(NearArgs A) {
+__global__ void __launch_bounds__(P2P_THREADS, 4) k_near(NearArgs A) {
   const int li = blockIdx.x;
   if (li >= A.n_leaves) return;
   const int v = A.leaves[li];
@@ -337,12 +337,10 @@ __global__ void __launch_bounds__(P2P_THREADS) k_near(NearArgs A) {
     const int j = Lmsrc[e];
     return make_int2(col_a[j], col_b[j] - col_a[j]);
   };
-  const int* pr = A.perm_row + ra;
-  double* z = A.z;
-  const int64_t ldz = A.ldz, c0 = A.c0;
+  double* zn = A.zn + (int64_t)ra * RC;
   p2p_block<KER, D, RC>(A.pts_row + ra, A.nrow, nr, A.Lmptr[v], A.Lmptr[v + 1], seg, A.pts_col,
                         A.ncol, A.qt, A.dx,
-                        [&](int t, int r, double val) { z[(int64_t)pr[t] * ldz + c0 + r] = val; });
+                        [&](int t, int r, double val) { zn[(int64_t)t * RC + r] = val; });
 }
 
 template <int KER, int D>

@@ -17,6 +17,15 @@ template <int IT> __device__ __forceinline__ double rsqrt_nr(double x) {
   }
   return y;
 }
+// one residual + polynomial correction: y0 (1 + e/2 + 3e^2/8 [+ 5e^3/16]), e = 1 - x y0^2
+template <int DEG> __device__ __forceinline__ double rsqrt_poly(double x) {
+  const double y0 = rsqrt_approx(x);
+  const double h = x * y0;
+  const double e = fma(-h, y0, 1.0);
+  double p = DEG == 3 ? fma(e, 0.3125, 0.375) : 0.375;
+  p = fma(p, e, 0.5);
+  return fma(y0 * e, p, y0);
+}
 __global__ void acc(const double* x, int n, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -25,30 +34,36 @@ __global__ void acc(const double* x, int n, double* out) {
   out[4 * i + 1] = (rsqrt_nr<1>(x[i]) - r) / r;
   out[4 * i + 2] = (rsqrt_nr<2>(x[i]) - r) / r;
   out[4 * i + 3] = (rsqrt(x[i]) - r) / r;
+  out[4 * n + 2 * i] = (rsqrt_poly<2>(x[i]) - r) / r;
+  out[4 * n + 2 * i + 1] = (rsqrt_poly<3>(x[i]) - r) / r;
 }
 template <int M> __global__ void thr(double* o, int it) {
   double x[4], a[4] = {0, 0, 0, 0};
   for (int c = 0; c < 4; ++c) x[c] = 0.5 + threadIdx.x * 1e-5 + c * 0.1;
   for (int k = 0; k < it; ++k)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { a[c] += (M == 0 ? rsqrt(x[c]) : rsqrt_nr<2>(x[c])); x[c] += 1e-7; }
+    for (int c = 0; c < 4; ++c) { a[c] += (M == 0 ? rsqrt(x[c]) : M == 1 ? rsqrt_nr<2>(x[c]) : rsqrt_poly<2>(x[c])); x[c] += 1e-7; }
   if (a[0] + a[1] + a[2] + a[3] == 1.2345) o[0] = 1;
 }
 int main() {
   const int n = 1 << 20;
-  double *x, *o; cudaMallocManaged(&x, n * 8); cudaMallocManaged(&o, 4 * n * 8);
+  double *x, *o; cudaMallocManaged(&x, n * 8); cudaMallocManaged(&o, 6 * n * 8);
   unsigned long long s = 88172645463325252ULL;
   for (int i = 0; i < n; ++i) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; x[i] = pow(10.0, -8.0 + 10.0 * (double)(s % 1000003) / 1000003.0); }
   acc<<<n / 256, 256>>>(x, n, o); cudaDeviceSynchronize();
   double mx[4] = {0, 0, 0, 0};
   for (int i = 0; i < n; ++i) for (int k = 0; k < 4; ++k) mx[k] = fmax(mx[k], fabs(o[4 * i + k]));
+  double mp[2] = {0, 0};
+  for (int i = 0; i < n; ++i) for (int k = 0; k < 2; ++k) mp[k] = fmax(mp[k], fabs(o[4 * n + 2 * i + k]));
+  printf("poly2 %.3e poly3 %.3e\n", mp[0], mp[1]);
   printf("max rel err: approx %.3e  nr1 %.3e  nr2 %.3e  cuda rsqrt %.3e  (eps %.3e)\n", mx[0], mx[1], mx[2], mx[3], 0x1p-53);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b); float ms;
-  for (int m = 0; m < 2; ++m) {
-    if (m == 0) thr<0><<<148 * 8, 256>>>(o, 16); else thr<1><<<148 * 8, 256>>>(o, 16);
+  for (int m = 0; m < 3; ++m) {
+    auto f = m == 0 ? thr<0> : m == 1 ? thr<1> : thr<2>;
+    f<<<148 * 8, 256>>>(o, 16);
     cudaEventRecord(a);
-    if (m == 0) thr<0><<<148 * 8, 256>>>(o, 4096); else thr<1><<<148 * 8, 256>>>(o, 4096);
+    f<<<148 * 8, 256>>>(o, 4096);
     cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-    printf("%s: %.1f Geval/s\n", m == 0 ? "cuda rsqrt" : "rsqrt_nr<2>", 4.0 * 4096 * 148 * 8 * 256 / ms / 1e6);
+    printf("%s: %.1f Geval/s\n", m == 0 ? "cuda rsqrt" : m == 1 ? "rsqrt_nr<2>" : "rsqrt_poly<2>", 4.0 * 4096 * 148 * 8 * 256 / ms / 1e6);
   }
 }
