@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsmash_b200.so")
+LIB_PATH = os.environ.get("SMASH_LIB") or os.path.join(HERE, "libsmash_b200.so")
 
 SMASH_OK, SMASH_ERR_INVALID, SMASH_ERR_NUMERICAL, SMASH_ERR_CUDA = 0, 2, 3, 4
 MODE = {"binary": 0, "2d": 1, "2^d": 1}

@@ -6,10 +6,10 @@
 //   main stream:  K10 gather qt = q[perm_col]                     (apply.py:39)
 //                 K6  upward  qhat_v = X_v^T ibar-vector, one persistent launch (apply.py:42-53)
 //                 K7  coupling zhat_i = sum_{j in L(i)} K(S_i, S_j) qhat_j   (apply.py:55-58)
-//                 K8  downward zhat_children += X_v zhat_v and, for leaves, the far-field
-//                     rows zf = X_v zhat_v, one persistent launch            (apply.py:60-72)
+//                 K8  downward zhat_children += X_v zhat_v, one persistent launch (apply.py:60-72)
 //                 --- join ---
-//                 K10 combine z[perm_row] = zn + zf                          (apply.py:78-80)
+//                 K8b leaf far field fused with the combine
+//                     z[perm_row] = zn + X_v zhat_v                          (apply.py:66-80)
 //   near stream:  K9  nearfield zn = sum_{j in Lm(v)} K(P_v, P_j) qt_j       (apply.py:74-76)
 // The nearfield only needs qt, so it overlaps the whole far-field chain.
 #include <algorithm>
@@ -59,15 +59,16 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
     }
     P->max_nk = mk;
   }
-  // ticket orders: BFS ids are level-major, so deepest level first = descending
-  // ids; leaves ride along in their level (they have no producers upward and
-  // only their parent downward).
+  // ticket orders of the internal non-root nodes: BFS ids are level-major, so
+  // deepest level first = descending ids (leaves go through the warp-per-leaf
+  // launches before / after the persistent passes).
   std::vector<int> up, down, leaves;
-  for (int v = n - 1; v >= 1; --v) up.push_back(v);
-  for (int v = 1; v < n; ++v) down.push_back(v);
+  for (int v = n - 1; v >= 1; --v)
+    if (nchild[v] > 0) up.push_back(v);
+  for (int v = 1; v < n; ++v)
+    if (nchild[v] > 0) down.push_back(v);
   for (int v = 0; v < n; ++v)
     if (nchild[v] == 0) leaves.push_back(v);
-  if (n == 1) down.push_back(0);  // a root leaf: its (zero) far-field rows
   P->n_up = (int)up.size();
   P->n_down = (int)down.size();
   P->n_leaves = (int)leaves.size();
@@ -77,10 +78,21 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   h2d(P->up_order.p, up.data(), up.size(), s);
   h2d(P->down_order.p, down.data(), down.size(), s);
   h2d(P->leaves.p, leaves.data(), leaves.size(), s);
+  {  // membership of the internal passes (leaf producers are final before them)
+    std::vector<unsigned char> in(n, 0);
+    for (int v : up) in[v] = 1;
+    P->inset_int.alloc(n, s);
+    h2d(P->inset_int.p, in.data(), n, s);
+  }
+  P->up_pos.alloc(std::max<int64_t>(m->colf->skel_total, 1), s);
+  launch_up_pos(side_of(*m->colf), t->nchild.p, t->child_first.p, n, P->up_pos.p,
+                m->colf->skel_total, s);
+  P->slot_of.alloc(std::max<int64_t>(t->nx, 1), s);
+  P->zrow.alloc(std::max<int64_t>(t->nx, 1), s);
+  launch_leaf_slots(side_of(m->rowf), P->leaves.p, P->n_leaves, t->row_a.p, t->row_b.p,
+                    t->perm_row.p, P->slot_of.p, P->zrow.p, s);
   P->done.alloc(n, s);
   P->done.zero(s);
-  P->inset_all.alloc(n, s);
-  SMASH_CUDA(cudaMemsetAsync(P->inset_all.p, 1, n, s));
   P->counters.alloc(2, s);
   sync(s);
   MatvecPlan* out = P.get();
@@ -92,14 +104,29 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
 struct PhaseSets {
   bool gather = true;
   bool zero_qhat = false;                 // shard: unowned coefficients must be 0 for the all-reduce
-  const int* up = nullptr; int n_up = 0;  // upward order (deepest level first, leaves included)
+  const int* up_leaves = nullptr; int n_up_leaves = 0;  // leaves of the upward pass
+  const int* up = nullptr; int n_up = 0;  // internal upward order (deepest level first)
   const unsigned char* up_in = nullptr;   // membership of the upward / downward sets
   const unsigned char* down_in = nullptr;
   bool far = true;                        // run coupling / downward / nearfield / combine
   const int* coup = nullptr; int n_coup = -1;  // coupling targets (nullptr + -1: all nodes)
-  const int* down = nullptr; int n_down = 0;   // downward order (shallowest first, leaves included)
-  const int* leaves = nullptr; int n_leaves = 0;  // nearfield / combine rows
+  const int* down = nullptr; int n_down = 0;   // internal downward order (shallowest first)
+  const int* leaves = nullptr; int n_leaves = 0;  // nearfield / far-field + combine rows
 };
+
+// SMASH_DEBUG_SYNC=1: eager (uncaptured) matvec with a synchronize + error
+// check after every launch, naming the failing phase (debug aid).
+bool debug_sync() {
+  static const bool on = getenv("SMASH_DEBUG_SYNC") != nullptr;
+  return on;
+}
+
+void check_phase(const char* name, cudaStream_t st) {
+  if (!debug_sync()) return;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess)
+    throw Error(SMASH_ERR_CUDA, std::string("matvec phase ") + name + ": " + cudaGetErrorString(e));
+}
 
 template <int KER, int D, int RC>
 void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q, double* z,
@@ -112,7 +139,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   const double* pts_col = t->shared ? t->pts_row.p : t->pts_col.p;
   const int* col_a = t->shared ? t->row_a.p : t->col_a.p;
   const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
-  static const bool serial = getenv("SMASH_MATVEC_SERIAL") != nullptr;  // profiling aid
+  static const bool serial = getenv("SMASH_MATVEC_SERIAL") != nullptr || debug_sync();
   cudaStream_t sn = serial ? s : m->s2;
   auto mark = [&](int i, cudaStream_t st) {  // external record: a timing node in the graph
     if (ev) SMASH_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
@@ -121,10 +148,11 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   mark(0, s);
   if (S.gather) {
     launch_gather<RC>(q, nrhs, perm_col, t->ny, c0, m->qt.p, s);
+    check_phase("gather", s);
     ++launches;
   }
   if (S.zero_qhat) {
-    SMASH_CUDA(cudaMemsetAsync(m->qhat.p, 0, (size_t)std::max<int64_t>(C.skel_total, 1) * RC * 8, s));
+    SMASH_CUDA(cudaMemsetAsync(m->qhat.p, 0, 2 * (size_t)std::max<int64_t>(C.skel_total, 1) * RC * 8, s));
     ++launches;
   }
   mark(1, s);
@@ -133,16 +161,25 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     SMASH_CUDA(cudaStreamWaitEvent(sn, m->fork, 0));
     mark(6, sn);
     NearArgs na{S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
-                pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, m->zn.p, m->p.dx, t->nu0};
+                pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, P.slot_of.p, m->zn.p,
+                m->p.dx, t->nu0};
     launch_near<KER, D, RC>(na, sn);
+    check_phase("near", sn);
     ++launches;
     mark(7, sn);
     SMASH_CUDA(cudaEventRecord(m->join, sn));
   }
+  double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;  // second half of qhat
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
-              m->zhat.p, cs};
+              qp, P.up_pos.p, m->zhat.p, m->zd.p, cs};
+  if (S.n_up_leaves) {
+    launch_up_leaves<RC>(up, S.up_leaves, S.n_up_leaves, s);
+    check_phase("upward leaves", s);
+    ++launches;
+  }
   if (S.n_up) {
     launch_upward<RC>(up, P, S.up, S.n_up, S.up_in, s);
+    check_phase("upward", s);
     launches += 2;
   }
   mark(2, s);
@@ -150,19 +187,21 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
                     m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
     launch_coupling<KER, D, RC>(ca, s);
+    check_phase("coupling", s);
     ++launches;
     mark(3, s);
     XferArgs down{t->nchild.p, t->child_first.p, t->parent.p, t->row_a.p, t->row_b.p, m->qt.p,
-                  m->qhat.p, m->zhat.p, rs};
+                  m->qhat.p, qp, P.up_pos.p, m->zhat.p, m->zd.p, rs};
     if (S.n_down) {
-      launch_downward<RC>(down, P, S.down, S.n_down, S.down_in, m->zf.p, s);
+      launch_downward<RC>(down, P, S.down, S.n_down, S.down_in, s);
+      check_phase("downward", s);
       launches += 2;
     }
     mark(4, s);
     SMASH_CUDA(cudaStreamWaitEvent(s, m->join, 0));
     mark(8, s);
-    launch_combine<RC>(S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, t->perm_row.p, m->zn.p,
-                       m->zf.p, z, nrhs, c0, s);
+    launch_down_leaves<RC>(down, S.leaves, S.n_leaves, P.zrow.p, m->zn.p, z, nrhs, c0, s);
+    check_phase("downward leaves", s);
     ++launches;
   }
   mark(5, s);
@@ -280,17 +319,17 @@ int prepare(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
   }
   if (m->ws_nrhs < 16) {
     m->qt.alloc((size_t)t->ny * 16, s);
-    m->qhat.alloc((size_t)std::max<int64_t>(m->colf->skel_total, 1) * 16, s);
+    m->qhat.alloc(2 * (size_t)std::max<int64_t>(m->colf->skel_total, 1) * 16, s);  // qhat | qp
     m->zhat.alloc((size_t)std::max<int64_t>(m->rowf.skel_total, 1) * 16, s);
+    m->zd.alloc((size_t)std::max<int64_t>(m->rowf.skel_total, 1) * 16, s);
     m->zn.alloc((size_t)t->nx * 16, s);
-    m->zf.alloc((size_t)t->nx * 16, s);
     m->ws_nrhs = 16;
   }
   // largest nrhs chunk whose transfer-kernel tiles and shared memory fit
   auto fits = [&](int rc) {
     const XferGeom G = xfer_geom(P->max_nib, P->max_rank, P->max_nk, rc);
     const int tiles = ((P->max_rank + 7) / 8) * ((rc + 7) / 8);
-    return tiles <= 8 * XFER_MAXT && xfer_smem_up(G) <= 200 * 1024 &&
+    return tiles <= 16 && xfer_smem_up(G) <= 200 * 1024 &&  // upward: <= 2 tiles per warp
            xfer_smem_down(G) <= 200 * 1024;
   };
   int rc_cap = 16;
@@ -315,12 +354,20 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
   MatvecPlan* P = plan_of(m, s);
   const int rc_cap = prepare(m, P, s);
   PhaseSets S;
+  S.up_leaves = P->leaves.p; S.n_up_leaves = P->n_leaves;
   S.up = P->up_order.p; S.n_up = P->n_up;
-  S.up_in = P->inset_all.p;
-  S.down_in = P->inset_all.p;
+  S.up_in = P->inset_int.p;
+  S.down_in = P->inset_int.p;
   S.down = P->down_order.p; S.n_down = P->n_down;
   S.leaves = P->leaves.p; S.n_leaves = P->n_leaves;
   const int nch = (int)chunks_of(nrhs, rc_cap).size();
+  if (debug_sync()) {
+    int nl = 0;
+    dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
+      run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, s, nullptr, &nl);
+    });
+    return;
+  }
   GraphEntry* E = graph_for(m, q, z, nrhs, 0, nch, true, [&](auto* evs, int* nl) {
     dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
       run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, m->sc, evs, nl);
@@ -350,13 +397,16 @@ void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
     return out;
   };
   std::vector<int> own = to_bfs(own_post, n_own), top = to_bfs(top_post, n_top);
-  std::vector<int> own_up = own, top_up = top, coup = own, down, leaves;
+  std::vector<int> own_up, top_up = top, coup = own, down, leaves;
+  for (int v : own)
+    if (nchild[v] > 0) own_up.push_back(v);  // owned leaves go through the leaf launches
   std::sort(own_up.rbegin(), own_up.rend());  // BFS is level-major: descending = deepest first
   std::sort(top_up.rbegin(), top_up.rend());
   coup.insert(coup.end(), top.begin(), top.end());
   std::sort(coup.begin(), coup.end());
-  down = coup;  // ascending = shallowest first; leaves write their far-field rows
   for (int v : coup)
+    if (nchild[v] > 0) down.push_back(v);  // ascending = shallowest first
+  for (int v : own)
     if (nchild[v] == 0) leaves.push_back(v);
   std::unique_ptr<ShardSets> S(new ShardSets());
   auto up = [&](DBuf<int>& d, const std::vector<int>& h, int& cnt) {
@@ -400,6 +450,7 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
   PhaseSets S;
   if (stage == 1) {  // local upward of the owned subtrees; unowned coefficients 0
     S.zero_qhat = true;
+    S.up_leaves = H.leaves.p; S.n_up_leaves = H.n_leaves;
     S.up = H.own_up.p; S.n_up = H.n_own_up; S.up_in = H.own_in.p;
     S.far = false;
   } else {  // after the coefficient exchange: top upward, then owned far/near field
@@ -419,8 +470,8 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
 }
 
 void matvec_coeffs(MatrixImpl* m, double** qhat, int64_t* rows) {
-  *qhat = m->qhat.p;
-  *rows = std::max<int64_t>(m->colf->skel_total, 1);
+  *qhat = m->qhat.p;  // qhat | qp (both exchanged between the stages)
+  *rows = 2 * std::max<int64_t>(m->colf->skel_total, 1);
 }
 
 void matvec_release_plan(const MatrixImpl* m) {

@@ -12,7 +12,7 @@ namespace mv {
 constexpr int P2P_WARPS = 4;
 constexpr int P2P_THREADS = 32 * P2P_WARPS;
 constexpr int XFER_THREADS = 256;
-constexpr int XFER_MAXT = 4;  // upward output tiles per warp: ceil(k / 8) * ceil(RC / 8) <= 32
+constexpr int XFER_MAXT = 4;  // leaf upward: a-tiles per warp pass
 
 struct Side {
   const int* nib;
@@ -59,7 +59,8 @@ struct NearArgs {
   const int* Lmptr;
   const int* Lmsrc;
   const double* qt;
-  double* zn;       // tree-ordered nearfield rows (RC per row)
+  const int* slot_of;  // tree row -> its slot in the leaf's ibar order
+  double* zn;          // nearfield rows in leaf ibar order (RC per row)
   double dx;
   int max_targets;  // largest leaf row count
 };
@@ -74,14 +75,16 @@ void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, doub
 
 // transfer passes (matvec_xfer.cu)
 struct XferPlan {
-  DBuf<int> up_order;    // non-root nodes, deepest level first (BFS ids descending)
-  DBuf<int> down_order;  // non-root nodes, shallowest level first (BFS ids ascending)
+  DBuf<int> up_order;    // internal non-root nodes, deepest level first (BFS ids descending)
+  DBuf<int> down_order;  // internal non-root nodes, shallowest level first (BFS ids ascending)
   DBuf<int> leaves;
-  DBuf<unsigned char> inset_all;  // membership of the whole-tree passes (all ones)
+  DBuf<unsigned char> inset_int;  // membership of the whole-tree internal passes
   DBuf<unsigned> done;   // per node flags (reset before each pass)
   DBuf<unsigned> counters;  // [0] upward tickets, [1] downward tickets
   int n_up = 0, n_down = 0, n_leaves = 0;
   int max_nib = 0, max_rank = 0, max_nk = 0;
+  DBuf<int> up_pos;
+  DBuf<int> slot_of, zrow;  // row side, see launch_leaf_slots  // column side, see launch_up_pos
 };
 
 struct XferArgs {
@@ -92,7 +95,10 @@ struct XferArgs {
   const int* pt_b;
   const double* qt;
   double* qhat;
-  double* zhat;
+  double* qp;          // coefficient rows in their parent's ibar order (upward input)
+  const int* up_pos;   // per skeleton row: its row in qp (-1 below the root)
+  double* zhat;        // coupling result
+  double* zd;          // contributions of the parent (downward)
   Side side;
 };
 
@@ -107,6 +113,9 @@ XferGeom xfer_geom(int max_nib, int max_rank, int max_nk, int rc);
 size_t xfer_smem_up(const XferGeom& G);
 size_t xfer_smem_down(const XferGeom& G);
 
+// up_pos[x] = row of skeleton row x in its parent's ibar order (-1 below the root)
+void launch_up_pos(const Side& cs, const int* nchild, const int* child_first, int n, int* up_pos,
+                   int64_t rows, cudaStream_t s);
 template <int RC>
 void launch_gather(const double* q, int64_t ldq, const int* perm, int64_t n, int64_t c0,
                    double* qt, cudaStream_t s);
@@ -116,11 +125,14 @@ void launch_upward(const XferArgs& a, XferPlan& P, const int* order, int n,
                    const unsigned char* inset, cudaStream_t s);
 template <int RC>
 void launch_downward(const XferArgs& a, XferPlan& P, const int* order, int n,
-                     const unsigned char* inset, double* zf, cudaStream_t s);
+                     const unsigned char* inset, cudaStream_t s);
 template <int RC>
-void launch_combine(const int* leaves, int n_leaves, const int* row_a, const int* row_b,
-                    const int* perm_row, const double* zn, const double* zf, double* z,
-                    int64_t ldz, int64_t c0, cudaStream_t s);
+void launch_up_leaves(const XferArgs& a, const int* leaves, int n, cudaStream_t s);
+template <int RC>
+void launch_down_leaves(const XferArgs& a, const int* leaves, int n, const int* zrow,
+                        const double* zn, double* z, int64_t ldz, int64_t c0, cudaStream_t s);
+void launch_leaf_slots(const Side& rs, const int* leaves, int n, const int* row_a, const int* row_b,
+                       const int* perm_row, int* slot_of, int* zrow, cudaStream_t s);
 
 }  // namespace mv
 }  // namespace smash

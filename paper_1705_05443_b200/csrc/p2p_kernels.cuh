@@ -99,11 +99,14 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 constexpr int MMA_MTMAX = 8;      // target tiles (8 rows) per pass: 64 targets
-constexpr int MMA_WSTRIDE = 36;   // staged weight row stride (doubles): 4 (mod 16) -> B reads conflict-free
+// staged weights are row-major (source x RC) with row stride RC + 4 = 4 (mod 8)
+// doubles: the B-fragment reads (4 rows x 8 consecutive) are conflict-free
+template <int RC>
+constexpr int mma_wstride() { return RC + 4; }
 constexpr int MMA_SEG_CAP = 512;  // source segments per table fill
 
 template <int D, int RC>
-constexpr int mma_stage_doubles() { return 32 * D + MMA_WSTRIDE * RC; }
+constexpr int mma_stage_doubles() { return 2 * (32 * D + 32 * mma_wstride<RC>()); }  // 2 buffers
 
 template <int D, int RC>
 constexpr int mma_smem_doubles() {
@@ -118,32 +121,44 @@ struct SegTable {
   int n;
 };
 
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(valid ? 16 : 0) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src),
+               "r"(valid ? 8 : 0) : "memory");
+}
+
+// Stage source p (this lane's slot of one 32-source chunk) asynchronously:
+// coordinates SoA sc[a][lane], weights row-major sw[lane][RC]; slots past the
+// end are zero-filled (their kernel values are selected to 0, and 0 * stale
+// NaN would not be).
 template <int D, int RC>
-__device__ __forceinline__ void mma_fetch(const SegTable& T, int p, int total, const double* spts,
-                                          int64_t sstride, const double* wts, double* vc,
-                                          double* vw) {
-  if (p < total) {
+__device__ __forceinline__ void mma_issue(const SegTable& T, int p, int total, const double* spts,
+                                          int64_t sstride, const double* wts, double* sc,
+                                          double* sw) {
+  const int lane = threadIdx.x & 31;
+  const bool ok = p < total;
+  int row = 0;
+  if (ok) {
     int lo = 0, hi = T.n - 1;  // last segment with pre <= p
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (T.pre[mid] <= p) lo = mid; else hi = mid - 1;
     }
-    const int row = T.off[lo] + (p - T.pre[lo]);
-#pragma unroll
-    for (int a = 0; a < D; ++a) vc[a] = spts[(int64_t)a * sstride + row];
-    const double2* wp = reinterpret_cast<const double2*>(wts + (int64_t)row * RC);
-#pragma unroll
-    for (int u = 0; u < RC / 2; ++u) {
-      const double2 t = wp[u];
-      vw[2 * u] = t.x;
-      vw[2 * u + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int a = 0; a < D; ++a) vc[a] = 0.0;
-#pragma unroll
-    for (int u = 0; u < RC; ++u) vw[u] = 0.0;
+    row = T.off[lo] + (p - T.pre[lo]);
   }
+#pragma unroll
+  for (int a = 0; a < D; ++a) cp_async8z(sc + a * 32 + lane, spts + (int64_t)a * sstride + row, ok);
+  double* dw = sw + lane * mma_wstride<RC>();
+  const double* w = wts + (int64_t)row * RC;
+#pragma unroll
+  for (int u = 0; u < RC / 2; ++u) cp_async16z(dw + 2 * u, w + 2 * u, ok);
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <int KER, int D, int RC, int MTX>
@@ -153,25 +168,27 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
                                                 double dx, double* stage,
                                                 double (&c)[MTX][RC / 8][2]) {
   constexpr int NT = RC / 8;
+  constexpr int WS = mma_wstride<RC>();
+  constexpr int BUF = 32 * D + 32 * WS;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int total = T.pre[T.n];
   const int nch = (total + 31) >> 5;
   const int per = (nch + P2P_WARPS - 1) / P2P_WARPS;
   const int c0 = wid * per, c1 = min(nch, c0 + per);
-  double* sc = stage;
-  double* sw = stage + D * 32;
-  double vc[D], vw[RC];
-  if (c0 < c1) mma_fetch<D, RC>(T, c0 * 32 + lane, total, spts, sstride, wts, vc, vw);
+  if (c0 < c1) mma_issue<D, RC>(T, c0 * 32 + lane, total, spts, sstride, wts, stage, stage + 32 * D);
   for (int ch = c0; ch < c1; ++ch) {
+    double* sc = stage + ((ch - c0) & 1) * BUF;
+    double* sw = sc + 32 * D;
+    if (ch + 1 < c1) {  // double buffering: the next chunk streams in during this one
+      double* nc = stage + ((ch + 1 - c0) & 1) * BUF;
+      mma_issue<D, RC>(T, (ch + 1) * 32 + lane, total, spts, sstride, wts, nc, nc + 32 * D);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
     const int cnt = min(32, total - ch * 32);
-    __syncwarp();
-#pragma unroll
-    for (int a = 0; a < D; ++a) sc[a * 32 + lane] = vc[a];
-#pragma unroll
-    for (int u = 0; u < RC; ++u) sw[u * MMA_WSTRIDE + lane] = vw[u];
-    __syncwarp();
-    if (ch + 1 < c1) mma_fetch<D, RC>(T, (ch + 1) * 32 + lane, total, spts, sstride, wts, vc, vw);
     for (int kk = 0; kk < cnt; kk += 4) {
       const int si = kk + q;
       const bool sv = si < cnt;
@@ -180,7 +197,7 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
       for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + si];
       double b[NT];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) b[n] = sw[(n * 8 + g) * MMA_WSTRIDE + si];
+      for (int n = 0; n < NT; ++n) b[n] = sw[si * WS + n * 8 + g];
       double av[MTX];
 #pragma unroll
       for (int m = 0; m < MTX; ++m) {  // straight-line: padded entries selected to 0
@@ -192,6 +209,7 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
 #pragma unroll
         for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av[m], b[n]);
     }
+    __syncwarp();  // this buffer is refilled two chunks later
   }
 }
 
@@ -279,8 +297,9 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
                                           SegF seg, const double* spts, int64_t sstride,
                                           const double* wts, double dx, OutF out) {
   if constexpr (RC == 8 || RC == 16) {
-    __shared__ double buf[mma_smem_doubles<D, RC>()];
-    __shared__ SegTable T;
+    extern __shared__ __align__(16) double p2p_dyn[];  // see p2p_smem_bytes
+    double* buf = p2p_dyn;
+    SegTable& T = *reinterpret_cast<SegTable*>(p2p_dyn + mma_smem_doubles<D, RC>());
     for (int t0 = 0; t0 < nt; t0 += MMA_MTMAX * 8) {
       const int n = min(MMA_MTMAX * 8, nt - t0);
       __syncthreads();
@@ -305,7 +324,7 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
 // kernels
 // ---------------------------------------------------------------------------
 template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS, 4) k_coupling(CouplingArgs A) {
+__global__ void __launch_bounds__(P2P_THREADS, 3) k_coupling(CouplingArgs A) {
   if ((int)blockIdx.x >= A.n_nodes) return;
   const int v = A.list ? A.list[blockIdx.x] : (int)blockIdx.x;
   if (v == 0) return;  // the root has no factor and no coupling
@@ -325,7 +344,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 4) k_coupling(CouplingArgs A) {
 }
 
 template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS, 4) k_near(NearArgs A) {
+__global__ void __launch_bounds__(P2P_THREADS, 3) k_near(NearArgs A) {
   const int li = blockIdx.x;
   if (li >= A.n_leaves) return;
   const int v = A.leaves[li];
@@ -337,10 +356,11 @@ __global__ void __launch_bounds__(P2P_THREADS, 4) k_near(NearArgs A) {
     const int j = Lmsrc[e];
     return make_int2(col_a[j], col_b[j] - col_a[j]);
   };
-  double* zn = A.zn + (int64_t)ra * RC;
+  const int* slot = A.slot_of + ra;
+  double* zn = A.zn;
   p2p_block<KER, D, RC>(A.pts_row + ra, A.nrow, nr, A.Lmptr[v], A.Lmptr[v + 1], seg, A.pts_col,
                         A.ncol, A.qt, A.dx,
-                        [&](int t, int r, double val) { zn[(int64_t)t * RC + r] = val; });
+                        [&](int t, int r, double val) { zn[(int64_t)slot[t] * RC + r] = val; });
 }
 
 template <int KER, int D>
@@ -358,14 +378,38 @@ __global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny
 // ---------------------------------------------------------------------------
 // launchers (explicitly instantiated per kernel in p2p_<kernel>.cu)
 // ---------------------------------------------------------------------------
+template <int D, int RC>
+constexpr size_t p2p_smem_bytes() {
+  return RC >= 8 ? mma_smem_doubles<D, RC>() * sizeof(double) + sizeof(SegTable) : 0;
+}
+
 template <int KER, int D, int RC>
 void launch_coupling(const CouplingArgs& a, cudaStream_t s) {
-  if (a.n_nodes > 0) k_coupling<KER, D, RC><<<a.n_nodes, P2P_THREADS, 0, s>>>(a);
+  constexpr size_t smem = p2p_smem_bytes<D, RC>();
+  static const bool attr = [] {
+    SMASH_CUDA(cudaFuncSetAttribute(k_coupling<KER, D, RC>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SMASH_CUDA(cudaFuncSetAttribute(k_coupling<KER, D, RC>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+    return true;
+  }();
+  (void)attr;
+  if (a.n_nodes > 0) k_coupling<KER, D, RC><<<a.n_nodes, P2P_THREADS, smem, s>>>(a);
 }
 
 template <int KER, int D, int RC>
 void launch_near(const NearArgs& a, cudaStream_t s) {
-  if (a.n_leaves > 0) k_near<KER, D, RC><<<a.n_leaves, P2P_THREADS, 0, s>>>(a);
+  constexpr size_t smem = p2p_smem_bytes<D, RC>();
+  static const bool attr = [] {
+    SMASH_CUDA(cudaFuncSetAttribute(k_near<KER, D, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    SMASH_CUDA(cudaFuncSetAttribute(k_near<KER, D, RC>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+    return true;
+  }();
+  (void)attr;
+  if (a.n_leaves > 0) k_near<KER, D, RC><<<a.n_leaves, P2P_THREADS, smem, s>>>(a);
 }
 
 template <int KER, int D>

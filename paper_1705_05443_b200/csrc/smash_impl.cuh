@@ -96,8 +96,8 @@ struct MatrixImpl {
   SideFactors rowf, colf_own;
   SideFactors* colf = nullptr;  // == &rowf when the points are shared
   // matvec workspaces
-  DBuf<double> qt, qhat, zhat;
-  DBuf<double> zn, zf;  // tree-ordered nearfield / leaf far-field rows of one chunk
+  DBuf<double> qt, qhat, zhat, zd;
+  DBuf<double> zn;  // tree-ordered nearfield rows of one chunk
   int64_t ws_nrhs = 0;
   // optional per-phase timing of the matvec (CUDA events on the launch streams)
   bool profile = false;
