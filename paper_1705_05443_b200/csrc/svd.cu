@@ -17,6 +17,9 @@
 // change the pivoted QR of [U_basis, S]^T in exact arithmetic.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "qr_device.cuh"
 #include "svd.cuh"
@@ -29,7 +32,8 @@ using namespace qr;
 
 constexpr int SVD_THREADS = 256;
 constexpr int MAX_NEAR = 64;
-constexpr int SVD_JV_MAX = 64;  // Jacobi factors in shared memory up to this rank  // |N_i| cap (reference hist: |N_i| <= 2 on the HSS configs)
+constexpr int SVD_JV_MAX = 64;  // Jacobi factors in shared memory up to this rank
+constexpr int SVD_Y_MAX = 128 * 65;  // shared-memory back-transform area (doubles), >= 2 * 64 * 64
 
 struct IbarSide {
   const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
@@ -62,6 +66,7 @@ struct SvdArgs {
   int64_t gws_stride;  // doubles per CTA
   int nmax, nnmax;
   int* err;
+  long long* dbg;  // SMASH_SVD_DBG: phase cycle counts of block 0's first nodes
 };
 
 __device__ __forceinline__ int ibar_size(const IbarSide& s, const int* nchild, const int* child_first,
@@ -89,6 +94,53 @@ __global__ void k_near_cols(SvdArgs A) {
   for (int e = A.near_ptr[v]; e < A.near_ptr[v + 1]; ++e)
     nn += ibar_size(A.other, A.nchild, A.child_first, A.near_idx[e]);
   A.nn_out[v - A.lb] = nn;
+}
+
+// Reflector application / column norms on the L2-resident panel with the row
+// loads batched 16 at a time (independent L2 loads in flight instead of one
+// dependent round trip per row) and four partial sums.
+constexpr int GB = 16;
+
+__device__ __forceinline__ double col_sumsq_g(const double* P, int ld, int j, int r0, int r1) {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int row = r0;
+  for (; row + GB <= r1; row += GB) {
+    double x[GB];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) s[q & 3] = fma(x[q], x[q], s[q & 3]);
+  }
+  for (; row < r1; ++row) {
+    const double x = P[(size_t)row * ld + j];
+    s[0] = fma(x, x, s[0]);
+  }
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+__device__ __forceinline__ void apply_reflector_g(double* P, int ld, int m, int i, int j, double tau,
+                                                  const double* vh) {
+  double w[4] = {P[(size_t)i * ld + j], 0.0, 0.0, 0.0};
+  int row = i + 1;
+  for (; row + GB <= m; row += GB) {
+    double x[GB];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) w[q & 3] = fma(vh[row + q], x[q], w[q & 3]);
+  }
+  for (; row < m; ++row) w[0] = fma(vh[row], P[(size_t)row * ld + j], w[0]);
+  const double t = -tau * ((w[0] + w[1]) + (w[2] + w[3]));
+  P[(size_t)i * ld + j] += t;
+  row = i + 1;
+  for (; row + GB <= m; row += GB) {
+    double x[GB];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
+#pragma unroll
+    for (int q = 0; q < GB; ++q) P[(size_t)(row + q) * ld + j] = fma(t, vh[row + q], x[q]);
+  }
+  for (; row < m; ++row) P[(size_t)row * ld + j] = fma(t, vh[row], P[(size_t)row * ld + j]);
 }
 
 template <int KER, int D>
@@ -126,6 +178,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
   const int tid = threadIdx.x, NT = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
   double* W = A.gws + (size_t)blockIdx.x * A.gws_stride;
+  int dbg_n = 0;
   for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
     const int n = A.self.nib[v];
     const int e0 = A.near_ptr[v], e1 = A.near_ptr[v + 1];
@@ -152,6 +205,9 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       __syncthreads();
       continue;
     }
+    const bool dbg = A.dbg && blockIdx.x == 0 && tid == 0 && dbg_n < 4;
+    long long tsv[6];
+    if (dbg) tsv[0] = clock64();
     // ---- assemble A (n x nn), row-major in W
     int64_t ts;
     const double* tb = ibar_base(A.self, A.nchild, A.child_first, v, &ts);
@@ -169,12 +225,13 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       W[e] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
     }
     __syncthreads();
+    if (dbg) tsv[1] = clock64();
     // ---- column-pivoted QR of A, truncated at the noise floor
     double* P = W;
     const int ld = nn;
     const int kmax = min(n, nn);
     for (int j = tid; j < nn; j += NT) {
-      double nr = __dsqrt_rn(col_sumsq(P, ld, j, 0, n));
+      double nr = __dsqrt_rn(col_sumsq_g(P, ld, j, 0, n));
       S.vn1[j] = nr;
       S.vn2[j] = nr;
       S.jpvt[j] = j;
@@ -208,14 +265,14 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       if (r0 == 0.0 || !(fabs(S.rdiag[i]) > 0x1p-53 * r0)) break;  // noise floor reached
       kp = i + 1;
       for (int j = i + 1 + tid; j < nn; j += NT) {
-        if (tau != 0.0) apply_reflector(P, ld, n, i, j, tau, S.vh);
+        if (tau != 0.0) apply_reflector_g(P, ld, n, i, j, tau, S.vh);
         double v1 = S.vn1[j];
         if (v1 != 0.0) {
           double q = fabs(P[(size_t)i * ld + j]) / v1;
           double temp = fmax(1.0 - q * q, 0.0);
           double q2 = v1 / S.vn2[j];
           if (temp * (q2 * q2) <= TOL3Z) {
-            double nv = i + 1 < n ? sqrt(col_sumsq(P, ld, j, i + 1, n)) : 0.0;
+            double nv = i + 1 < n ? sqrt(col_sumsq_g(P, ld, j, i + 1, n)) : 0.0;
             S.vn1[j] = nv;
             S.vn2[j] = nv;
           } else {
@@ -231,6 +288,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       __syncthreads();
       continue;
     }
+    if (dbg) tsv[2] = clock64();
     // ---- B = R_k^T (nn x kp), unpivoted QR -> R2 (kp x kp)
     double* B = W + (size_t)n * nn;
     for (int e = tid; e < nn * kp; e += NT) {
@@ -243,7 +301,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       __syncthreads();
       const double tau = S.misc[0];
       if (tau != 0.0)
-        for (int j = i + 1 + tid; j < kp; j += NT) apply_reflector(B, kp, nn, i, j, tau, S.vh);
+        for (int j = i + 1 + tid; j < kp; j += NT) apply_reflector_g(B, kp, nn, i, j, tau, S.vh);
       __syncthreads();
     }
     // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated.
@@ -260,17 +318,22 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     }
     __syncthreads();
     const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
+    if (dbg) tsv[3] = clock64();
+    // 8-lane groups: one column pair (or column) per group, kp <= 64 -> <= 8
+    // elements per lane, 3 shuffle levels per reduction
+    const int g8 = tid >> 3, gl = tid & 7, ngr = NT >> 3;
+    const unsigned gm = 0xffu << (lane & ~7);
     for (int sweep = 0; sweep < 40; ++sweep) {
-      for (int c = wid; c < kp; c += nw) {  // exact squared norms
+      for (int c = g8; c < kp; c += ngr) {  // exact squared norms
         double s2 = 0.0;
-        for (int r = lane; r < kp; r += 32) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
-        for (int off = 16; off; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
-        if (lane == 0) nrm[c] = s2;
+        for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
+        for (int off = 4; off; off >>= 1) s2 += __shfl_xor_sync(gm, s2, off);
+        if (gl == 0) nrm[c] = s2;
       }
       if (tid == 0) S.imisc[2] = 0;
       __syncthreads();
       for (int rnd = 0; rnd < np - 1; ++rnd) {
-        for (int pr = wid; pr < np / 2; pr += nw) {
+        for (int pr = g8; pr < np / 2; pr += ngr) {
           // circle method: position 0 fixed, others rotate
           int a = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (np - 1);
           int b = 1 + (np - 2 - pr + rnd) % (np - 1);
@@ -278,8 +341,8 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
           double* ja = J + (size_t)a * kp;
           double* jb = J + (size_t)b * kp;
           double ga = 0;
-          for (int r = lane; r < kp; r += 32) ga = fma(ja[r], jb[r], ga);
-          for (int off = 16; off; off >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, off);
+          for (int r = gl; r < kp; r += 8) ga = fma(ja[r], jb[r], ga);
+          for (int off = 4; off; off >>= 1) ga += __shfl_xor_sync(gm, ga, off);
           const double al = nrm[a], be = nrm[b];
           if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
             const double zeta = (be - al) / (2.0 * ga);
@@ -287,7 +350,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
             const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
             double* va = V + (size_t)a * kp;
             double* vb = V + (size_t)b * kp;
-            for (int r = lane; r < kp; r += 32) {
+            for (int r = gl; r < kp; r += 8) {
               const double x = ja[r], y = jb[r];
               ja[r] = c * x - s * y;
               jb[r] = s * x + c * y;
@@ -295,8 +358,8 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
               va[r] = c * p - s * q;
               vb[r] = s * p + c * q;
             }
-            __syncwarp();
-            if (lane == 0) {
+            __syncwarp(gm);
+            if (gl == 0) {
               nrm[a] = fmax(al - t * ga, 0.0);
               nrm[b] = be + t * ga;
               atomicAdd(&S.imisc[2], 1);
@@ -308,6 +371,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       if (S.imisc[2] == 0) break;
       __syncthreads();
     }
+    if (dbg) tsv[4] = clock64();
     // ---- singular values, keep count, descending order
     for (int c = tid; c < kp; c += NT) {
       double s2 = 0.0;
@@ -337,26 +401,63 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     __syncthreads();
     const int keep = S.imisc[3];
     if (keep == 0) continue;
-    // ---- U = Q1[:, :kp] V[:, kept]  (n x keep, row-major into sv)
-    double* Y = A.sv + A.sv_off[v];
-    for (int e = tid; e < n * keep; e += NT) {
-      const int a = e / keep, c = e % keep;
-      Y[e] = a < kp ? V[(size_t)order[c] * kp + a] : 0.0;
+    // ---- U = Q1[:, :kp] V[:, kept]  (n x keep): Y staged in shared memory (over
+    // the J/V area, through registers) when it fits, reflectors applied by
+    // 8-lane groups per column
+    double* Yg = A.sv + A.sv_off[v];
+    const bool ysm = kp <= SVD_JV_MAX && n * (keep | 1) <= SVD_Y_MAX;
+    double* Y = ysm ? jv_smem : Yg;
+    const int ldy = ysm ? (keep | 1) : keep;
+    if (ysm) {
+      constexpr int STG = SVD_JV_MAX * SVD_JV_MAX / SVD_THREADS;
+      double stg[STG];
+      const int cnt = kp * keep;
+#pragma unroll
+      for (int q = 0; q < STG; ++q) {
+        const int e = tid + q * NT;
+        stg[q] = e < cnt ? V[(size_t)order[e % keep] * kp + e / keep] : 0.0;
+      }
+      __syncthreads();
+      for (int e = tid; e < n * ldy; e += NT) Y[e] = 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < STG; ++q) {
+        const int e = tid + q * NT;
+        if (e < cnt) Y[(e / keep) * ldy + e % keep] = stg[q];
+      }
+    } else {
+      for (int e = tid; e < n * keep; e += NT) {
+        const int a = e / keep, c = e % keep;
+        Y[e] = a < kp ? V[(size_t)order[c] * kp + a] : 0.0;
+      }
     }
     __syncthreads();
     for (int i = kp - 1; i >= 0; --i) {
       const double tau = taus[i];
       if (tau == 0.0) continue;
-      for (int c = tid; c < keep; c += NT) {
-        double w = Y[(size_t)i * keep + c];
-        for (int row = i + 1; row < n; ++row) w = fma(P[(size_t)row * ld + i], Y[(size_t)row * keep + c], w);
+      for (int row = i + 1 + tid; row < n; row += NT) S.vh[row] = P[(size_t)row * ld + i];
+      __syncthreads();
+      for (int c = g8; c < keep; c += ngr) {
+        double w = 0.0;
+        for (int row = i + gl; row < n; row += 8)
+          w = fma(row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c], w);
+        for (int off = 4; off; off >>= 1) w += __shfl_xor_sync(gm, w, off);
         const double t = -tau * w;
-        Y[(size_t)i * keep + c] += t;
-        for (int row = i + 1; row < n; ++row)
-          Y[(size_t)row * keep + c] = fma(t, P[(size_t)row * ld + i], Y[(size_t)row * keep + c]);
+        for (int row = i + gl; row < n; row += 8)
+          Y[(size_t)row * ldy + c] = fma(t, row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c]);
       }
       __syncthreads();
     }
+    if (ysm) {
+      for (int e = tid; e < n * keep; e += NT) Yg[e] = Y[(e / keep) * ldy + e % keep];
+      __syncthreads();
+    }
+    if (dbg) {
+      tsv[5] = clock64();
+      for (int q = 0; q < 5; ++q) A.dbg[dbg_n * 8 + q] = tsv[q + 1] - tsv[q];
+      A.dbg[dbg_n * 8 + 5] = kp; A.dbg[dbg_n * 8 + 6] = keep; A.dbg[dbg_n * 8 + 7] = n * 1000 + nn;
+    }
+    ++dbg_n;
   }
 }
 
@@ -470,10 +571,18 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   err.alloc(1, s);
   err.zero(s);
   A.err = err.p;
+  static const bool svd_dbg = getenv("SMASH_SVD_DBG") != nullptr;
+  DBuf<long long> dbgbuf;
+  A.dbg = nullptr;
+  if (svd_dbg) {
+    dbgbuf.alloc(32, s);
+    dbgbuf.zero(s);
+    A.dbg = dbgbuf.p;
+  }
   const int mx = std::max(A.nmax, A.nnmax);
   size_t smem = 8 * ((size_t)2 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
                 4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64 + 16 +
-                8 * (size_t)2 * SVD_JV_MAX * SVD_JV_MAX;
+                8 * (size_t)SVD_Y_MAX;
   SMASH_CHECK(smem <= 200 * 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
     SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,6 +596,16 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   d2h(&he, err.p, 1, s);
   sync(s);
   SMASH_CHECK(he == 0, SMASH_ERR_INVALID, "nearfield set larger than the supported cap");
+  if (svd_dbg) {
+    long long h[32];
+    d2h(h, dbgbuf.p, 32, s);
+    sync(s);
+    fprintf(stderr, "svd level %d side %d cnt %d:", level, side, cnt);
+    for (int q = 0; q < 4; ++q)
+      fprintf(stderr, " [asm %lld qr %lld qr2 %lld jac %lld back %lld kp %lld keep %lld n.nn %lld]", h[q * 8], h[q * 8 + 1],
+              h[q * 8 + 2], h[q * 8 + 3], h[q * 8 + 4], h[q * 8 + 5], h[q * 8 + 6], h[q * 8 + 7]);
+    fprintf(stderr, "\n");
+  }
   return hk;
 }
 
