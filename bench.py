@@ -43,6 +43,8 @@ FP64_PEAK_TFLOPS = 34.1
 # counted by ncu on k_block -- profiles/ckernel_r01.txt); 2*nrhs flops per interaction added.
 C_K = {"inv_r": 14.0, "log": 51.0, "exp": 52.0, "cauchy": 11.0}
 L2_FLUSH_BYTES = 256 << 20
+# dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full, profiles/coupling_r01.txt)
+NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6}
 
 
 def parse():
@@ -335,13 +337,40 @@ def run_ours(args):
         dom, flops, ms = "k_near", I_near * per_int, ms_near
     achieved = flops / (ms / 1e3) / 1e12
     total_flops = (I_coup + I_near) * per_int
+    # DRAM traffic per launch of the dominant kernel from one ncu --set full capture
+    # (profiles/coupling_r01.txt; only measured for the default cfg2 / 16-RHS workload)
+    traffic = NCU_TRAFFIC.get((cfg, R, dom))
     roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "peak_source": "measured DFMA microbenchmark (profiles/fp64_peak_r01.txt); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "flops_per_launch": flops, "ms_per_launch": ms,
                 "c_K": C_K[c["kernel"]], "interactions_coupling": I_coup, "interactions_near": I_near,
                 "matvec_total_frac": total_flops / (t_mv / args.steps) / 1e12 / (ws * FP64_PEAK_TFLOPS)}
+
+    # ---- construction roofline: algorithmic FP64 work of the batched sRRQR
+    # (per compr call on an m x n panel, sum_{i<min(m,n)} 4(m-i)(n-i-1)
+    # for the pivoted QR plus k^2 (n-k) for G = (R11^-1 R12)^T), one side when the
+    # column factors alias the row factors, over the whole build time
+    build_flops = 0.0
+    sides = [Er] if (Y is X and c["structure"] == "h2") else [Er, Ec]
+    for E in sides:
+        nib = np.diff(E["perm_ptr"]).astype(np.float64)
+        kk = E["rank"].astype(np.float64)
+        m_rows = float(c["r"])
+        for nv, kv in zip(nib, kk):
+            if nv <= 0:
+                continue
+            steps = int(min(m_rows, nv))
+            i = np.arange(steps, dtype=np.float64)
+            build_flops += float(np.sum(4.0 * (m_rows - i) * np.maximum(nv - i - 1.0, 0.0)))
+            build_flops += kv * kv * (nv - kv)
+    b_s = statistics.median(build_ms) / 1e3
+    build_roofline = {"bound": "fp64", "flops": build_flops, "achieved": build_flops / b_s / 1e12,
+                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                      "frac": build_flops / b_s / 1e12 / FP64_PEAK_TFLOPS,
+                      "note": "algorithmic sRRQR flops (QR + G solve) over the whole build time "
+                              "(tree + pair lists + basis + sRRQR)"}
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0, N = 1 only
     cpu = None
@@ -366,6 +395,7 @@ def run_ours(args):
                          "nearfield_concurrent": ms_near, "leaf_farfield": phase[5] / args.steps,
                          "matvec": phase[6] / args.steps},
             "roofline": roofline,
+            "build_roofline": build_roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gpoints/s", "h2d_bytes_per_step": int(q.nbytes),
                     "d2h_bytes_per_step": int(M.n_row * R * 8),

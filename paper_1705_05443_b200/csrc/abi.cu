@@ -143,7 +143,15 @@ int smash_matrix_sizes(smash_matrix_t m, int32_t side, int64_t* has_total, int64
     SMASH_CHECK(side == 0 || side == 1, SMASH_ERR_INVALID, "side must be 0 or 1");
     const smash::SideFactors& F = side == 0 ? m->impl->rowf : *m->impl->colf;
     if (has_total) *has_total = m->impl->tree->n_nodes - 1;
-    if (ibar_total) *ibar_total = F.ib_total;
+    if (ibar_total) {  // exact sum of |ibar| (the device layout may hold capacity gaps)
+      int n = m->impl->tree->n_nodes;
+      std::vector<int> nib(n);
+      smash::d2h(nib.data(), F.nib.p, n, 0);
+      smash::sync(0);
+      int64_t t = 0;
+      for (int v = 1; v < n; ++v) t += nib[v];
+      *ibar_total = t;
+    }
     if (skel_total) *skel_total = F.skel_total;
     if (g_total) {
       // exact G count = sum (nib - k) * k ; computed at export; report capacity-free value

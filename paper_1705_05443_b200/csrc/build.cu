@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "compress.cuh"
 #include "svd.cuh"
@@ -55,6 +56,23 @@ __global__ void k_level_sizes(int lb, int le, const int* nchild, const int* chil
   gcnt[v - lb] = (int64_t)n * min(n, mrows_bound);
 }
 
+__global__ void k_level_nib(int lb, int le, const int* nchild, const int* child_first,
+                            const int* pt_a, const int* pt_b, const int* rank, int* nib) {
+  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= le) return;
+  int n;
+  if (nchild[v] == 0) {
+    n = pt_b[v] - pt_a[v];
+  } else {
+    n = 0;
+    for (int c = 0; c < nchild[v]; ++c) n += rank[child_first[v] + c];
+  }
+  nib[v] = n;
+}
+
+// device-resident running skeleton count: compaction base of the next level
+__global__ void k_skel_bump(int* used, const int* level_off, int cnt) { *used += level_off[cnt]; }
+
 __global__ void k_add_base(int lb, int le, const int64_t* loc, int64_t base, int64_t* glob) {
   int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
   if (v < le) glob[v] = base + loc[v - lb];
@@ -66,12 +84,12 @@ __global__ void k_rank_cnt(int lb, int le, const int* rank, int* cnt) {
 }
 
 __global__ void k_skel_compact(int lb, int le, const int* rank, const int* loc_off, int base,
-                               const int64_t* ib_off, int64_t ib_level_base, const int* tmp_lab,
-                               const double* tmp_pts, int64_t tmp_stride, int dim, int* skel_off,
-                               int* skel, double* skel_pts, int64_t skel_stride) {
+                               const int* base_dev, const int64_t* ib_off, int64_t ib_level_base,
+                               const int* tmp_lab, const double* tmp_pts, int64_t tmp_stride, int dim,
+                               int* skel_off, int* skel, double* skel_pts, int64_t skel_stride) {
   int v = lb + blockIdx.x;
   if (v >= le) return;
-  int o = base + loc_off[v - lb];
+  int o = (base_dev ? *base_dev : base) + loc_off[v - lb];
   if (threadIdx.x == 0) skel_off[v] = o;
   int k = rank[v];
   int64_t src = ib_off[v] - ib_level_base;
@@ -216,6 +234,14 @@ struct SideBuild {
   DBuf<double> gws;
   SvdWorkspace svdws;
   int smem_limit = 0, nsm = 0;
+  // H2: every size of the level loop comes from host-side bounds computed once
+  // from the tree (|ibar_v| <= sum_c min(r, |ibar_c|), leaves: their points), so
+  // the whole sweep is enqueued without a host round trip; the device keeps the
+  // running skeleton count.  HSS needs the SVD keep counts on the host.
+  bool async = false;
+  std::vector<int64_t> lvl_ib_b, lvl_g_b, lvl_ib_base;
+  std::vector<int> lvl_nmax_b;
+  DBuf<int> d_used;
 
   void init() {
     TreeImpl* t = M->tree;
@@ -251,9 +277,119 @@ struct SideBuild {
     dmax.alloc(1, s);
     smem_limit = max_sm_smem();
     nsm = num_sms();
+    async = !hss && getenv("SMASH_BUILD_SYNC") == nullptr;
+    if (async) plan_bounds();
+  }
+
+  void plan_bounds() {
+    TreeImpl* t = M->tree;
+    const int n = t->n_nodes, r = M->p.r, L = t->n_levels;
+    std::vector<int> nch(n), cf(n), a(n), b(n);
+    d2h(nch.data(), t->nchild.p, n, s);
+    d2h(cf.data(), t->child_first.p, n, s);
+    d2h(a.data(), pt_a, n, s);
+    d2h(b.data(), pt_b, n, s);
+    sync(s);
+    std::vector<int64_t> bib(n, 0), bk(n, 0);
+    for (int v = n - 1; v >= 0; --v) {  // BFS ids: children after their parent
+      int64_t ib = 0;
+      if (nch[v] == 0) ib = b[v] - a[v];
+      else for (int c = 0; c < nch[v]; ++c) ib += bk[cf[v] + c];
+      bib[v] = ib;
+      bk[v] = std::min<int64_t>(ib, r);
+    }
+    std::vector<int64_t> ibo(n, 0), go(n, 0);
+    lvl_ib_b.assign(L + 2, 0); lvl_g_b.assign(L + 2, 0); lvl_ib_base.assign(L + 2, 0);
+    lvl_nmax_b.assign(L + 2, 1);
+    int64_t ib_acc = 0, g_acc = 0;
+    for (int l = L; l >= 2; --l) {
+      lvl_ib_base[l] = ib_acc;
+      for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
+        ibo[v] = ib_acc;
+        go[v] = g_acc;
+        ib_acc += bib[v];
+        // (|ibar| - k) k with k <= min(r, |ibar|)
+        const int64_t nb = bib[v];
+        g_acc += 2 * std::min<int64_t>(nb, r) >= nb ? (nb / 2) * (nb - nb / 2) : (nb - r) * r;
+        lvl_nmax_b[l] = std::max<int>(lvl_nmax_b[l], (int)bib[v]);
+      }
+      lvl_ib_b[l] = ib_acc - lvl_ib_base[l];
+    }
+    F->perm.alloc(std::max<int64_t>(ib_acc, 1), s);
+    F->G.alloc(std::max<int64_t>(g_acc, 1), s);
+    h2d(F->ib_off.p, ibo.data(), n, s);
+    h2d(F->g_off.p, go.data(), n, s);
+    F->ib_total = ib_acc;
+    F->g_total = g_acc;
+    d_used.alloc(1, s);
+    d_used.zero(s);
+  }
+
+  void level_async(int l) {
+    TreeImpl* t = M->tree;
+    const int dim = t->dim, r = M->p.r;
+    const int lb = t->level_begin(l), le = t->level_end(l), cnt = le - lb;
+    k_level_nib<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a, pt_b,
+                                               F->rank.p, F->nib.p);
+    const int64_t lvl_ib = std::max<int64_t>(lvl_ib_b[l], 1);
+    DBuf<int> tmp_lab;
+    DBuf<double> tmp_pts;
+    tmp_lab.alloc(lvl_ib, s);
+    tmp_pts.alloc((size_t)lvl_ib * dim, s);
+    CompressArgs A;
+    A.lb = lb; A.le = le; A.dim = dim; A.r = r; A.side = side;
+    A.nchild = t->nchild.p; A.child_first = t->child_first.p; A.pt_a = pt_a;
+    A.lo = t->lo.p; A.hi = t->hi.p; A.pad = pad; A.half_pad = pad / 2;
+    A.P = P; A.P_stride = Pn;
+    A.Sk = F->skel_pts.p; A.S_stride = skel_cap; A.Slab = F->skel.p; A.skel_off = F->skel_off.p;
+    A.nib = F->nib.p; A.ib_off = F->ib_off.p; A.g_off = F->g_off.p; A.ib_level_base = lvl_ib_base[l];
+    A.tab = tabs->view;
+    A.s_bound = M->p.s; A.rtol = M->p.rtol;
+    A.rank = F->rank.p; A.perm = F->perm.p; A.G = F->G.p;
+    A.tmp_lab = tmp_lab.p; A.tmp_pts = tmp_pts.p; A.tmp_stride = lvl_ib;
+    A.err = err.p; A.swaps = swaps.p;
+    A.nmax = std::max(lvl_nmax_b[l], 1);
+    A.mmax = r;
+    launch_level(A, cnt);
+    // ---- compact this level's skeletons (offsets stay on the device)
+    DBuf<int> rc, ro;
+    rc.alloc(cnt + 1, s); ro.alloc(cnt + 1, s);
+    SMASH_CUDA(cudaMemsetAsync(rc.p + cnt, 0, 4, s));
+    k_rank_cnt<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, F->rank.p, rc.p);
+    cub_call([&](void* tp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tp, b, rc.p, ro.p, cnt + 1, s);
+    }, tmp, s);
+    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, 0, d_used.p, F->ib_off.p,
+                                       lvl_ib_base[l], tmp_lab.p, tmp_pts.p, lvl_ib, dim,
+                                       F->skel_off.p, F->skel.p, F->skel_pts.p, skel_cap);
+    k_skel_bump<<<1, 1, 0, s>>>(d_used.p, ro.p, cnt);
+  }
+
+  void launch_level(CompressArgs& A, int cnt) {
+    size_t smem_full = compress_smem_bytes(A.nmax, A.mmax, true);
+    size_t smem;
+    int grid;
+    if ((int)smem_full <= smem_limit) {
+      A.smem_panel = 1;
+      smem = smem_full;
+      int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, (228 * 1024) / (smem + 1024)));
+      grid = std::min(cnt, nsm * per_sm);
+    } else {
+      A.smem_panel = 0;
+      smem = compress_smem_bytes(A.nmax, A.mmax, false);
+      grid = std::min(cnt, nsm * 2);
+      size_t need = (size_t)grid * A.mmax * A.nmax;
+      if (gws.n < need) gws.alloc(need, s);
+      A.gws = gws.p;
+    }
+    launch_compress(A, grid, smem, s);
   }
 
   void level(int l, NearSets* near) {
+    if (async) {
+      level_async(l);
+      return;
+    }
     TreeImpl* t = M->tree;
     const int dim = t->dim, r = M->p.r;
     const bool hss = M->p.structure == SMASH_STRUCT_HSS;
@@ -342,7 +478,7 @@ struct SideBuild {
     raise_dev_err(herr);
     SMASH_CHECK(skel_used + lvl_k <= skel_cap, SMASH_ERR_CUDA, "skeleton capacity exceeded");
     F->level_skel_begin[l] = skel_used;
-    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, (int)skel_used, F->ib_off.p,
+    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, (int)skel_used, nullptr, F->ib_off.p,
                                        F->ib_total, tmp_lab.p, tmp_pts.p, A.tmp_stride, dim,
                                        F->skel_off.p, F->skel.p, F->skel_pts.p, skel_cap);
     skel_used += lvl_k;
@@ -351,11 +487,17 @@ struct SideBuild {
   }
 
   void finish() {
+    unsigned long long hs = 0;
+    int used = 0, herr = 0;
+    d2h(&hs, swaps.p, 1, s);
+    d2h(&herr, err.p, 1, s);
+    if (async) d2h(&used, d_used.p, 1, s);
+    sync(s);
+    raise_dev_err(herr);
+    if (async) skel_used = used;
+    SMASH_CHECK(skel_used <= skel_cap, SMASH_ERR_CUDA, "skeleton capacity exceeded");
     F->level_skel_begin[1] = skel_used;
     F->skel_total = skel_used;
-    unsigned long long hs = 0;
-    d2h(&hs, swaps.p, 1, s);
-    sync(s);
     F->swaps = (int64_t)hs;
     SMASH_CUDA(cudaGetLastError());
   }
