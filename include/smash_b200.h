@@ -109,6 +109,18 @@ typedef struct {
 
 int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream,
                        smash_matrix_t* out);
+/* Sharded H2 construction (replaces the level loop of smash/h2.py:44-53
+ * when one process per GPU builds its share).  Phase 1 compresses rank's contiguous node
+ * ranges of the levels at and below the cut level (cut_level < 2: the shallowest level with
+ * >= 8 nodes per rank); the caller then sums every buffer listed by
+ * smash_matrix_exchange_buffers over the ranks (all-reduce, in place; dtype 0 int32,
+ * 1 float64, 2 int64), and phase 2 compacts the cut levels and compresses the top levels
+ * on every rank.  The result equals smash_matrix_build's bit for bit. */
+int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                             int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out);
+int smash_matrix_exchange_buffers(smash_matrix_t m, int64_t capacity, int64_t* n, void** ptrs,
+                                  int64_t* counts, int32_t* dtypes);
+int smash_matrix_build_finish(smash_matrix_t m, void* stream);
 /* side: 0 = row factors (rowfac), 1 = column factors (colfac).  Host outputs:
  * n_factors (nodes with a factor = non-root), total |ibar|, total skeleton, total G entries. */
 int smash_matrix_sizes(smash_matrix_t m, int32_t side, int64_t* has_total, int64_t* ibar_total,

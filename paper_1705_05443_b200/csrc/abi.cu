@@ -136,6 +136,38 @@ int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream
   });
 }
 
+int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                             int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out) {
+  return guarded([&] {
+    SMASH_CHECK(t && t->impl && p && out, SMASH_ERR_INVALID, "null argument");
+    smash::MatrixImpl* m = smash::matrix_build_local(t->impl, *p, rank, world, cut_level, st(stream));
+    *out = new smash_matrix_s{m};
+  });
+}
+
+int smash_matrix_exchange_buffers(smash_matrix_t m, int64_t capacity, int64_t* n, void** ptrs,
+                                  int64_t* counts, int32_t* dtypes) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl && n, SMASH_ERR_INVALID, "null argument");
+    std::vector<smash::ExchangeBuf> b;
+    smash::matrix_exchange_buffers(m->impl, b);
+    *n = (int64_t)b.size();
+    SMASH_CHECK(capacity >= (int64_t)b.size(), SMASH_ERR_INVALID, "exchange list capacity too small");
+    for (size_t i = 0; i < b.size(); ++i) {
+      ptrs[i] = b[i].ptr;
+      counts[i] = b[i].count;
+      dtypes[i] = b[i].dtype;
+    }
+  });
+}
+
+int smash_matrix_build_finish(smash_matrix_t m, void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
+    smash::matrix_build_finish(m->impl, st(stream));
+  });
+}
+
 int smash_matrix_sizes(smash_matrix_t m, int32_t side, int64_t* has_total, int64_t* ibar_total,
                        int64_t* skel_total, int64_t* g_total) {
   return guarded([&] {

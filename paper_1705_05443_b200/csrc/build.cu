@@ -325,17 +325,16 @@ struct SideBuild {
     d_used.zero(s);
   }
 
-  void level_async(int l) {
+  // compress nodes [lb, le) of level l (a rank's owned range, or the whole
+  // level); tmp_lab / tmp_pts receive the ordered skeleton labels / coordinates
+  // at ib_off - lvl_ib_base[l] (row stride tmp_stride)
+  void compress_range(int l, int lb, int le, int* tmp_lab, double* tmp_pts, int64_t tmp_stride) {
     TreeImpl* t = M->tree;
     const int dim = t->dim, r = M->p.r;
-    const int lb = t->level_begin(l), le = t->level_end(l), cnt = le - lb;
+    const int cnt = le - lb;
+    if (cnt <= 0) return;
     k_level_nib<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a, pt_b,
                                                F->rank.p, F->nib.p);
-    const int64_t lvl_ib = std::max<int64_t>(lvl_ib_b[l], 1);
-    DBuf<int> tmp_lab;
-    DBuf<double> tmp_pts;
-    tmp_lab.alloc(lvl_ib, s);
-    tmp_pts.alloc((size_t)lvl_ib * dim, s);
     CompressArgs A;
     A.lb = lb; A.le = le; A.dim = dim; A.r = r; A.side = side;
     A.nchild = t->nchild.p; A.child_first = t->child_first.p; A.pt_a = pt_a;
@@ -346,12 +345,25 @@ struct SideBuild {
     A.tab = tabs->view;
     A.s_bound = M->p.s; A.rtol = M->p.rtol;
     A.rank = F->rank.p; A.perm = F->perm.p; A.G = F->G.p;
-    A.tmp_lab = tmp_lab.p; A.tmp_pts = tmp_pts.p; A.tmp_stride = lvl_ib;
+    A.tmp_lab = tmp_lab; A.tmp_pts = tmp_pts; A.tmp_stride = tmp_stride;
     A.err = err.p; A.swaps = swaps.p;
     A.nmax = std::max(lvl_nmax_b[l], 1);
     A.mmax = r;
     launch_level(A, cnt);
-    // ---- compact this level's skeletons (offsets stay on the device)
+  }
+
+  // compact level l's ordered skeletons (offsets stay on the device)
+  void compact_level(int l, const int* tmp_lab, const double* tmp_pts, int64_t tmp_stride) {
+    TreeImpl* t = M->tree;
+    compact_range(l, t->level_begin(l), t->level_end(l), tmp_lab, tmp_pts, tmp_stride, d_used.p);
+  }
+
+  // compaction of nodes [lb, le) of level l at the device-resident base *used
+  void compact_range(int l, int lb, int le, const int* tmp_lab, const double* tmp_pts,
+                     int64_t tmp_stride, int* used) {
+    TreeImpl* t = M->tree;
+    const int cnt = le - lb;
+    if (cnt <= 0) return;
     DBuf<int> rc, ro;
     rc.alloc(cnt + 1, s); ro.alloc(cnt + 1, s);
     SMASH_CUDA(cudaMemsetAsync(rc.p + cnt, 0, 4, s));
@@ -359,10 +371,21 @@ struct SideBuild {
     cub_call([&](void* tp, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(tp, b, rc.p, ro.p, cnt + 1, s);
     }, tmp, s);
-    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, 0, d_used.p, F->ib_off.p,
-                                       lvl_ib_base[l], tmp_lab.p, tmp_pts.p, lvl_ib, dim,
+    k_skel_compact<<<cnt, 128, 0, s>>>(lb, le, F->rank.p, ro.p, 0, used, F->ib_off.p,
+                                       lvl_ib_base[l], tmp_lab, tmp_pts, tmp_stride, t->dim,
                                        F->skel_off.p, F->skel.p, F->skel_pts.p, skel_cap);
-    k_skel_bump<<<1, 1, 0, s>>>(d_used.p, ro.p, cnt);
+    k_skel_bump<<<1, 1, 0, s>>>(used, ro.p, cnt);
+  }
+
+  void level_async(int l) {
+    TreeImpl* t = M->tree;
+    const int64_t lvl_ib = std::max<int64_t>(lvl_ib_b[l], 1);
+    DBuf<int> tmp_lab;
+    DBuf<double> tmp_pts;
+    tmp_lab.alloc(lvl_ib, s);
+    tmp_pts.alloc((size_t)lvl_ib * t->dim, s);
+    compress_range(l, t->level_begin(l), t->level_end(l), tmp_lab.p, tmp_pts.p, lvl_ib);
+    compact_level(l, tmp_lab.p, tmp_pts.p, lvl_ib);
   }
 
   void launch_level(CompressArgs& A, int cnt) {
@@ -551,6 +574,152 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
   if (colb) colb->finish();
   sync(s);
   return M.release();
+}
+
+// ---------------------------------------------------------------------------
+// Sharded construction: levels are stored level-major, so the
+// subtrees under a contiguous range of cut-level nodes occupy one contiguous
+// node range at every deeper level.  Rank r compresses its ranges of levels
+// L..cut with no data movement (the host-side capacity layout gives every node
+// a fixed slot in perm / G / the skeleton temporaries), the caller sums the
+// disjoint, zero-initialised buffers over the ranks (one all-reduce each), and
+// finish() compacts the cut levels and compresses the few top levels
+// redundantly on every rank.
+// ---------------------------------------------------------------------------
+struct ShardState {
+  DevTables D;
+  std::unique_ptr<SideBuild> rowb;
+  int cut = 0, rank = 0, world = 1;
+  std::vector<int> own_lb, own_le;  // per level l (>= cut): owned BFS range
+  DBuf<int> tmp_lab;                // ordered skeleton labels of levels L..cut (perm layout)
+  DBuf<double> tmp_pts;             // [dim][tmp_len]
+  int64_t tmp_len = 1, perm_len = 1, g_len = 1;
+  DBuf<long long> swaps64;          // exchanged counters
+  DBuf<int> err32;
+};
+
+MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int rank, int world,
+                               int cut_level, cudaStream_t s) {
+  SMASH_CHECK(p.structure == SMASH_STRUCT_H2, SMASH_ERR_INVALID,
+              "sharded construction supports the H2 structure");
+  SMASH_CHECK(world >= 1 && rank >= 0 && rank < world, SMASH_ERR_INVALID, "bad rank / world size");
+  SMASH_CHECK(t->mode == SMASH_MODE_2D || t->dim == 1, SMASH_ERR_INVALID,
+              "H2 construction expects a 2^d-mode tree");
+  SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
+              "unknown kernel kind");
+  check_basis_params(p.r, t->dim);
+  init_pool();
+  std::unique_ptr<MatrixImpl> M(new MatrixImpl());
+  M->tree = t;
+  M->p = p;
+  M->pl = get_pairs(t, p.tau, p.structure, s);
+  std::shared_ptr<ShardState> st(new ShardState());
+  st->D.upload(make_tables(p.r, t->dim), s);
+  double w[3];
+  for (int a = 0; a < t->dim; ++a) w[a] = t->root_hi[a] - t->root_lo[a];
+  const double pad = std::max(1e-9 * (2 * (0.5 * host_norm_fma(w, t->dim))), 1e-300);
+  M->colf = t->shared ? &M->rowf : &M->colf_own;
+  SMASH_CHECK(t->shared, SMASH_ERR_INVALID, "sharded construction expects shared row/column points");
+  st->rowb.reset(new SideBuild{M.get(), 0, &M->rowf, &st->D, pad, s});
+  st->rowb->init();  // H2 -> capacity layout (async path)
+  SideBuild& B = *st->rowb;
+  SMASH_CHECK(B.async, SMASH_ERR_INVALID, "sharded construction needs the capacity layout");
+  const int L = t->n_levels;
+  // cut level: the shallowest level with >= 8 nodes per rank (else the leaves' level)
+  int cut = L;
+  for (int l = 2; l <= L; ++l)
+    if (t->level_end(l) - t->level_begin(l) >= 8 * world) { cut = l; break; }
+  if (cut_level >= 2 && cut_level <= L) cut = cut_level;
+  st->cut = cut;
+  st->rank = rank;
+  st->world = world;
+  // balance contiguous cut-level ranges by subtree point counts
+  const int n = t->n_nodes;
+  std::vector<int> ra(n), rb(n), par(n);
+  d2h(ra.data(), t->row_a.p, n, s);
+  d2h(rb.data(), t->row_b.p, n, s);
+  d2h(par.data(), t->parent.p, n, s);
+  sync(s);
+  const int cb = t->level_begin(cut), ce = t->level_end(cut);
+  std::vector<int> owner(n, -1);
+  int64_t total = 0;
+  for (int v = cb; v < ce; ++v) total += rb[v] - ra[v];
+  int64_t acc = 0;
+  for (int v = cb; v < ce; ++v) {
+    const double mid = acc + 0.5 * (rb[v] - ra[v]);
+    owner[v] = std::min(world - 1, (int)(mid * world / std::max<int64_t>(total, 1)));
+    acc += rb[v] - ra[v];
+  }
+  st->own_lb.assign(L + 2, 0);
+  st->own_le.assign(L + 2, 0);
+  for (int l = cut; l <= L; ++l) {
+    if (l > cut)  // inherit the owner of the parent (parents at level l - 1)
+      for (int v = t->level_begin(l); v < t->level_end(l); ++v) owner[v] = owner[par[v]];
+    int lo = -1, hi = -1;
+    for (int v = t->level_begin(l); v < t->level_end(l); ++v)
+      if (owner[v] == rank) { if (lo < 0) lo = v; hi = v + 1; }
+    st->own_lb[l] = lo < 0 ? 0 : lo;
+    st->own_le[l] = lo < 0 ? 0 : hi;
+  }
+  // exchanged buffers: zero them (owned slots are written, the rest stays 0)
+  st->perm_len = std::max<int64_t>(B.lvl_ib_base[cut] + B.lvl_ib_b[cut], 1);
+  st->g_len = std::max<int64_t>(M->rowf.g_total, 1);  // whole G (top levels are zero too)
+  st->tmp_len = st->perm_len;
+  st->tmp_lab.alloc(st->tmp_len, s);
+  st->tmp_pts.alloc((size_t)st->tmp_len * t->dim, s);
+  st->tmp_lab.zero(s);
+  st->tmp_pts.zero(s);
+  SMASH_CUDA(cudaMemsetAsync(M->rowf.perm.p, 0, 4 * (size_t)st->perm_len, s));
+  SMASH_CUDA(cudaMemsetAsync(M->rowf.G.p, 0, 8 * (size_t)st->g_len, s));
+  // local compaction of the owned ranges (parents read their children's skeletons
+  // from the compact arrays); finish() rebuilds the global compact layout
+  DBuf<int> used_loc;
+  used_loc.alloc(1, s);
+  used_loc.zero(s);
+  for (int l = L; l >= cut; --l) {
+    B.compress_range(l, st->own_lb[l], st->own_le[l], st->tmp_lab.p + B.lvl_ib_base[l],
+                     st->tmp_pts.p + B.lvl_ib_base[l], st->tmp_len);
+    B.compact_range(l, st->own_lb[l], st->own_le[l], st->tmp_lab.p + B.lvl_ib_base[l],
+                    st->tmp_pts.p + B.lvl_ib_base[l], st->tmp_len, used_loc.p);
+  }
+  st->swaps64.alloc(1, s);
+  st->err32.alloc(1, s);
+  SMASH_CUDA(cudaMemcpyAsync(st->swaps64.p, B.swaps.p, 8, cudaMemcpyDeviceToDevice, s));
+  SMASH_CUDA(cudaMemcpyAsync(st->err32.p, B.err.p, 4, cudaMemcpyDeviceToDevice, s));
+  sync(s);
+  M->pending = st;
+  return M.release();
+}
+
+void matrix_exchange_buffers(MatrixImpl* m, std::vector<ExchangeBuf>& out) {
+  SMASH_CHECK(m->pending, SMASH_ERR_INVALID, "matrix has no pending sharded build");
+  ShardState* st = static_cast<ShardState*>(m->pending.get());
+  const int n = m->tree->n_nodes;
+  out.clear();
+  out.push_back({m->rowf.rank.p, (int64_t)n, 0});
+  out.push_back({m->rowf.nib.p, (int64_t)n, 0});
+  out.push_back({m->rowf.perm.p, st->perm_len, 0});
+  out.push_back({st->tmp_lab.p, st->tmp_len, 0});
+  out.push_back({st->err32.p, 1, 0});
+  out.push_back({m->rowf.G.p, st->g_len, 1});
+  out.push_back({st->tmp_pts.p, st->tmp_len * m->tree->dim, 1});
+  out.push_back({st->swaps64.p, 1, 2});
+}
+
+void matrix_build_finish(MatrixImpl* m, cudaStream_t s) {
+  SMASH_CHECK(m->pending, SMASH_ERR_INVALID, "matrix has no pending sharded build");
+  ShardState* st = static_cast<ShardState*>(m->pending.get());
+  SideBuild& B = *st->rowb;
+  B.s = s;
+  SMASH_CUDA(cudaMemcpyAsync(B.swaps.p, st->swaps64.p, 8, cudaMemcpyDeviceToDevice, s));
+  SMASH_CUDA(cudaMemcpyAsync(B.err.p, st->err32.p, 4, cudaMemcpyDeviceToDevice, s));
+  const int L = m->tree->n_levels;
+  for (int l = L; l >= st->cut; --l)
+    B.compact_level(l, st->tmp_lab.p + B.lvl_ib_base[l], st->tmp_pts.p + B.lvl_ib_base[l], st->tmp_len);
+  for (int l = st->cut - 1; l >= 2; --l) B.level(l, nullptr);
+  B.finish();
+  sync(s);
+  m->pending.reset();
 }
 
 // ---------------------------------------------------------------------------

@@ -90,6 +90,7 @@ struct SideFactors {
 };
 
 struct MatrixImpl {
+  std::shared_ptr<void> pending;  // state of a sharded build between its phases
   TreeImpl* tree = nullptr;
   smash_build_params p{};
   PairLists* pl = nullptr;
@@ -119,6 +120,16 @@ struct MatrixImpl {
 };
 
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s);
+// sharded construction (build.cu): local levels, buffers to sum over ranks, finish
+struct ExchangeBuf {
+  void* ptr;
+  int64_t count;
+  int dtype;  // 0 int32, 1 float64, 2 int64
+};
+MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int rank, int world,
+                               int cut_level, cudaStream_t s);
+void matrix_exchange_buffers(MatrixImpl* m, std::vector<ExchangeBuf>& out);
+void matrix_build_finish(MatrixImpl* m, cudaStream_t s);
 void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t* perm_ptr,
                    int64_t* perm, int64_t* skel_ptr, int64_t* skel, int64_t* g_ptr, double* G,
                    cudaStream_t s);
