@@ -171,6 +171,12 @@ int smash_kernel_block(int32_t kernel, double dx, int32_t dim, const double* X, 
 /* ---- single-call primitives (smash/lowrank.py) ----
  * interp_basis (lowrank.py:123-144): lo/hi HOST float64[dim]; pts (n, dim) device;
  * out (n, r) row-major device.  dim 3 is this library's tensor extension. */
+/* Exact product z = K(X, Y) q on the GPU, never storing K (the dense oracle of
+ * smash/bench.py:284-296, dense_matvec): X (nx x dim), Y (ny x dim) row-major device
+ * arrays in caller order, q (ny x nrhs) and z (nx x nrhs) row-major device float64. */
+int smash_dense_matvec(int32_t kernel, double dx, int32_t dim, const double* X, int64_t nx,
+                       const double* Y, int64_t ny, const double* q, int64_t nrhs, double* z,
+                       void* stream);
 int smash_interp_basis(int32_t dim, const double* lo, const double* hi, const double* pts,
                        int64_t n, int32_t r, double* out, void* stream);
 /* compr (lowrank.py:232-255) on C (nrows, ncols) row-major device:

@@ -54,6 +54,7 @@ SIGNATURES = {
     "smash_matvec_coeffs": (c_i32, [c_vp, ctypes.POINTER(c_vp), P_i64]),
     "smash_matrix_free": (c_i32, [c_vp]),
     "smash_kernel_block": (c_i32, [c_i32, c_dbl, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "smash_dense_matvec": (c_i32, [c_i32, c_dbl, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "smash_interp_basis": (c_i32, [c_i32, P_dbl, P_dbl, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "smash_compr": (c_i32, [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_vp, c_vp, P_i64, P_i64, c_vp]),
 }

@@ -7,7 +7,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["matvec_nodewise", "matvec_device"]
+__all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device"]
 
 
 def matvec_device(M, Q, out=None):
@@ -50,3 +50,26 @@ def matvec_nodewise(M, q):
     if is_torch:
         return Z.to(q.device)
     return Z.cpu().numpy()
+
+
+def _check_perfect(tree):
+    """All leaves at the deepest level and a uniform child count (apply.py:83-95)."""
+    A = tree.arrays()
+    depth = int(A["level"].max())
+    nch = np.diff(A["child_ptr"])
+    leaf = nch == 0
+    if np.any(A["level"][leaf] != depth):
+        raise ValueError("level-synchronous matvec needs all leaves at the deepest level")
+    inner = nch[~leaf]
+    if inner.size and np.any(inner != inner[0]):
+        raise ValueError("level-synchronous matvec needs a perfect tree")
+
+
+def matvec_levelwise(M, q):
+    """Level-synchronous matvec on perfect trees (apply.py:98-165).  The device
+    matvec is already level-synchronous (one persistent upward pass ordered
+    deepest level first, the coupling of every node at once, one downward pass
+    ordered shallowest level first), so on a perfect tree this is the same
+    computation as matvec_nodewise; the reference's perfect-tree contract is kept."""
+    _check_perfect(M.tree)
+    return matvec_nodewise(M, q)

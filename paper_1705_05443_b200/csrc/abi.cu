@@ -273,6 +273,15 @@ int smash_kernel_block(int32_t kernel, double dx, int32_t dim, const double* X, 
   });
 }
 
+int smash_dense_matvec(int32_t kernel, double dx, int32_t dim, const double* X, int64_t nx,
+                       const double* Y, int64_t ny, const double* q, int64_t nrhs, double* z,
+                       void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(dim >= 1 && dim <= 3, SMASH_ERR_INVALID, "dim must be 1, 2 or 3");
+    smash::dense_matvec(kernel, dx, dim, X, nx, Y, ny, q, nrhs, z, st(stream));
+  });
+}
+
 int smash_interp_basis(int32_t dim, const double* lo, const double* hi, const double* pts,
                        int64_t n, int32_t r, double* out, void* stream) {
   return guarded([&] {

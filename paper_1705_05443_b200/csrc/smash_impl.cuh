@@ -120,6 +120,8 @@ struct MatrixImpl {
 };
 
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s);
+void dense_matvec(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
+                  int64_t ny, const double* q, int64_t nrhs, double* z, cudaStream_t s);
 // sharded construction (build.cu): local levels, buffers to sum over ranks, finish
 struct ExchangeBuf {
   void* ptr;

@@ -14,6 +14,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("configs", nargs="*", type=int, default=[1, 2, 3, 4, 5])
 ap.add_argument("--N", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--full-error", action="store_true",
+                help="error vs the exact product over every row (GPU dense oracle, sg.dense_matvec)")
 a = ap.parse_args()
 for cfg in a.configs:
     c = CONFIGS[cfg]
@@ -41,12 +43,21 @@ for cfg in a.configs:
     K = torch.from_numpy(kernel_block_coords(spec, X[rows], Y)).cuda()
     ze = K @ Q
     err = float(torch.linalg.norm(Z[rows] - ze) / torch.linalg.norm(ze))
+    err_full = None
+    if a.full_error:
+        e0.record()
+        zf = sg.dense_matvec(spec, dX, dY, Q)
+        e1.record(); e1.synchronize()
+        err_full = float(torch.linalg.norm(Z - zf) / torch.linalg.norm(zf))
+        dense_ms = e0.elapsed_time(e1)
     L, Lm = sg.leaf_sets(tree, c["tau"], c["structure"])
     print(json.dumps({"cfg": cfg, "N": X.shape[0], "nrhs": R, "nodes": len(tree.arrays()["level"]),
                       "levels": tree.n_levels, "L": len(L), "Lm": len(Lm),
                       "build_ms_min": min(bt), "build_ms": bt, "matvec_ms_min": min(mt),
                       "gpts_per_s": X.shape[0] * R / (min(mt) / 1e3) / 1e9,
                       "relerr_vs_exact_64rows": err, "reference_relerr": REF_ERR[cfg],
+                      "relerr_vs_exact_all_rows": err_full,
+                      "dense_oracle_ms": dense_ms if a.full_error else None,
                       "swaps": M.swaps}), flush=True)
     del M, tree, K
     torch.cuda.empty_cache()
