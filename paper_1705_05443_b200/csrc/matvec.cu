@@ -156,7 +156,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     ++launches;
   }
   mark(1, s);
-  if (S.far) {  // fork: nearfield on the second stream (needs only qt)
+  auto fork_near = [&]() {  // nearfield on the second stream (needs only qt)
     SMASH_CUDA(cudaEventRecord(m->fork, s));
     SMASH_CUDA(cudaStreamWaitEvent(sn, m->fork, 0));
     mark(6, sn);
@@ -168,7 +168,12 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     ++launches;
     mark(7, sn);
     SMASH_CUDA(cudaEventRecord(m->join, sn));
-  }
+  };
+  // Fork point: by default after the upward pass, so the latency-bound upward
+  // chain owns the SMs and the nearfield overlaps the coupling (both FP64-bound);
+  // SMASH_NEAR_EARLY=1 forks right after the gather.
+  static const bool near_early = getenv("SMASH_NEAR_EARLY") != nullptr;
+  if (S.far && near_early) fork_near();
   double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;  // second half of qhat
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
               qp, P.up_pos.p, m->zhat.p, m->zd.p, cs};
@@ -183,6 +188,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     launches += 2;
   }
   mark(2, s);
+  if (S.far && !near_early) fork_near();
   if (S.far) {
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
                     m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
@@ -312,8 +318,14 @@ namespace {
 int prepare(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
   TreeImpl* t = m->tree;
   if (!m->s2) {
-    SMASH_CUDA(cudaStreamCreateWithFlags(&m->s2, cudaStreamNonBlocking));
-    SMASH_CUDA(cudaStreamCreateWithFlags(&m->sc, cudaStreamNonBlocking));
+    // the far-field chain (upward -> coupling -> downward) is the critical path:
+    // its stream gets the highest priority, the overlapping nearfield the lowest,
+    // so freed SMs go to the chain first (captured kernel nodes keep the priority)
+    int lo = 0, hi = 0;
+    SMASH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool flat = getenv("SMASH_FLAT_PRIORITY") != nullptr;
+    SMASH_CUDA(cudaStreamCreateWithPriority(&m->s2, cudaStreamNonBlocking, lo));
+    SMASH_CUDA(cudaStreamCreateWithPriority(&m->sc, cudaStreamNonBlocking, flat ? lo : hi));
     SMASH_CUDA(cudaEventCreateWithFlags(&m->fork, cudaEventDisableTiming));
     SMASH_CUDA(cudaEventCreateWithFlags(&m->join, cudaEventDisableTiming));
   }

@@ -16,6 +16,8 @@
 // The four warps' partial sums are added in a fixed order (deterministic).
 #pragma once
 
+#include <cstdlib>
+
 #include "matvec_impl.cuh"
 
 namespace smash {
@@ -277,22 +279,23 @@ __device__ __forceinline__ void mma_block(const double* tx, int64_t tstride, int
     }
 }
 
-template <int KER, int D, int RC, typename... Args>
+template <int KER, int D, int RC, int MT, typename... Args>
 __device__ __forceinline__ void mma_block_dispatch(int mt, Args&&... args) {
   switch (mt) {
     case 1: mma_block<KER, D, RC, 1>(args...); break;
     case 2: mma_block<KER, D, RC, 2>(args...); break;
     case 3: mma_block<KER, D, RC, 3>(args...); break;
     case 4: mma_block<KER, D, RC, 4>(args...); break;
-    case 5: mma_block<KER, D, RC, 5>(args...); break;
-    case 6: mma_block<KER, D, RC, 6>(args...); break;
-    case 7: mma_block<KER, D, RC, 7>(args...); break;
-    default: mma_block<KER, D, RC, 8>(args...); break;
+    case 5: mma_block<KER, D, RC, (MT < 5 ? MT : 5)>(args...); break;
+    case 6: mma_block<KER, D, RC, (MT < 6 ? MT : 6)>(args...); break;
+    case 7: mma_block<KER, D, RC, (MT < 7 ? MT : 7)>(args...); break;
+    default: mma_block<KER, D, RC, MT>(args...); break;
   }
 }
 
-// Targets [0, nt) in 64-row passes; out(t, r, value).
-template <int KER, int D, int RC, typename SegF, typename OutF>
+// Targets [0, nt) in MT * 8-row passes; out(t, r, value).  MT (<= MMA_MTMAX)
+// bounds the register footprint: MT = 5 (40-row passes) fits 4 CTAs per SM.
+template <int KER, int D, int RC, int MT, typename SegF, typename OutF>
 __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int nt, int p0, int p1,
                                           SegF seg, const double* spts, int64_t sstride,
                                           const double* wts, double dx, OutF out) {
@@ -300,10 +303,10 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
     extern __shared__ __align__(16) double p2p_dyn[];  // see p2p_smem_bytes
     double* buf = p2p_dyn;
     SegTable& T = *reinterpret_cast<SegTable*>(p2p_dyn + mma_smem_doubles<D, RC>());
-    for (int t0 = 0; t0 < nt; t0 += MMA_MTMAX * 8) {
-      const int n = min(MMA_MTMAX * 8, nt - t0);
+    for (int t0 = 0; t0 < nt; t0 += MT * 8) {
+      const int n = min(MT * 8, nt - t0);
       __syncthreads();
-      mma_block_dispatch<KER, D, RC>((n + 7) >> 3, tx + t0, tstride, n, p0, p1, seg, spts, sstride,
+      mma_block_dispatch<KER, D, RC, MT>((n + 7) >> 3, tx + t0, tstride, n, p0, p1, seg, spts, sstride,
                                      wts, dx, T, buf);
       __syncthreads();
       for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
@@ -323,8 +326,11 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS, 3) k_coupling(CouplingArgs A) {
+template <int MT>
+constexpr int p2p_min_blocks() { return MT <= 5 ? 4 : 3; }
+
+template <int KER, int D, int RC, int MT>
+__global__ void __launch_bounds__(P2P_THREADS, p2p_min_blocks<MT>()) k_coupling(CouplingArgs A) {
   if ((int)blockIdx.x >= A.n_nodes) return;
   const int v = A.list ? A.list[blockIdx.x] : (int)blockIdx.x;
   if (v == 0) return;  // the root has no factor and no coupling
@@ -338,13 +344,13 @@ __global__ void __launch_bounds__(P2P_THREADS, 3) k_coupling(CouplingArgs A) {
     return make_int2(cs.skel_off[j], cs.rank[j]);
   };
   double* zo = A.zhat + (int64_t)to * RC;
-  p2p_block<KER, D, RC>(A.rs.skel_pts + to, A.rs.skel_stride, k, A.Lptr[v], A.Lptr[v + 1], seg,
+  p2p_block<KER, D, RC, MT>(A.rs.skel_pts + to, A.rs.skel_stride, k, A.Lptr[v], A.Lptr[v + 1], seg,
                         cs.skel_pts, cs.skel_stride, A.qhat, A.dx,
                         [&](int t, int r, double val) { zo[(int64_t)t * RC + r] = val; });
 }
 
-template <int KER, int D, int RC>
-__global__ void __launch_bounds__(P2P_THREADS, 3) k_near(NearArgs A) {
+template <int KER, int D, int RC, int MT>
+__global__ void __launch_bounds__(P2P_THREADS, p2p_min_blocks<MT>()) k_near(NearArgs A) {
   const int li = blockIdx.x;
   if (li >= A.n_leaves) return;
   const int v = A.leaves[li];
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 3) k_near(NearArgs A) {
   };
   const int* slot = A.slot_of + ra;
   double* zn = A.zn;
-  p2p_block<KER, D, RC>(A.pts_row + ra, A.nrow, nr, A.Lmptr[v], A.Lmptr[v + 1], seg, A.pts_col,
+  p2p_block<KER, D, RC, MT>(A.pts_row + ra, A.nrow, nr, A.Lmptr[v], A.Lmptr[v + 1], seg, A.pts_col,
                         A.ncol, A.qt, A.dx,
                         [&](int t, int r, double val) { zn[(int64_t)slot[t] * RC + r] = val; });
 }
@@ -383,33 +389,47 @@ constexpr size_t p2p_smem_bytes() {
   return RC >= 8 ? mma_smem_doubles<D, RC>() * sizeof(double) + sizeof(SegTable) : 0;
 }
 
+template <typename K>
+void p2p_attrs(K kern, size_t smem) {
+  SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+}
+
+// 8-row target tiles per pass: 5 (<= 40 targets, 4 CTAs/SM) or 8
+inline bool p2p_small(int max_targets) {
+  static const int mode = getenv("SMASH_P2P_MT") ? atoi(getenv("SMASH_P2P_MT")) : 0;
+  if (mode == 8) return false;
+  if (mode == 5) return true;
+  return max_targets <= 64;  // 40-row passes; 120 registers -> 4 CTAs per SM
+}
+
 template <int KER, int D, int RC>
 void launch_coupling(const CouplingArgs& a, cudaStream_t s) {
   constexpr size_t smem = p2p_smem_bytes<D, RC>();
   static const bool attr = [] {
-    SMASH_CUDA(cudaFuncSetAttribute(k_coupling<KER, D, RC>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SMASH_CUDA(cudaFuncSetAttribute(k_coupling<KER, D, RC>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    cudaSharedmemCarveoutMaxShared));
+    p2p_attrs(k_coupling<KER, D, RC, 5>, smem);
+    p2p_attrs(k_coupling<KER, D, RC, 8>, smem);
     return true;
   }();
   (void)attr;
-  if (a.n_nodes > 0) k_coupling<KER, D, RC><<<a.n_nodes, P2P_THREADS, smem, s>>>(a);
+  if (a.n_nodes <= 0) return;
+  if (p2p_small(a.max_targets)) k_coupling<KER, D, RC, 5><<<a.n_nodes, P2P_THREADS, smem, s>>>(a);
+  else k_coupling<KER, D, RC, 8><<<a.n_nodes, P2P_THREADS, smem, s>>>(a);
 }
 
 template <int KER, int D, int RC>
 void launch_near(const NearArgs& a, cudaStream_t s) {
   constexpr size_t smem = p2p_smem_bytes<D, RC>();
   static const bool attr = [] {
-    SMASH_CUDA(cudaFuncSetAttribute(k_near<KER, D, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    SMASH_CUDA(cudaFuncSetAttribute(k_near<KER, D, RC>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    cudaSharedmemCarveoutMaxShared));
+    p2p_attrs(k_near<KER, D, RC, 5>, smem);
+    p2p_attrs(k_near<KER, D, RC, 8>, smem);
     return true;
   }();
   (void)attr;
-  if (a.n_leaves > 0) k_near<KER, D, RC><<<a.n_leaves, P2P_THREADS, smem, s>>>(a);
+  if (a.n_leaves <= 0) return;
+  if (p2p_small(a.max_targets)) k_near<KER, D, RC, 5><<<a.n_leaves, P2P_THREADS, smem, s>>>(a);
+  else k_near<KER, D, RC, 8><<<a.n_leaves, P2P_THREADS, smem, s>>>(a);
 }
 
 template <int KER, int D>
