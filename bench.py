@@ -285,24 +285,41 @@ def run_ours(args):
         t_mv = float(t[0])
     value = args.steps * M.n_row * R / t_mv / 1e9
 
-    # ---- e2e through the public API with pinned host buffers
-    q_pin = torch.from_numpy(q).pin_memory()
+    # ---- e2e through the public API with pinned host buffers: every step copies its
+    # right-hand sides host->device and its result device->host (inside the timed
+    # region); MatvecStream overlaps those copies of neighbouring steps with the
+    # compute (copy engines), as a serving loop would
+    q_pin = [torch.from_numpy(q).pin_memory(), torch.from_numpy(q.copy()).pin_memory()]
+    z_pin = [torch.empty((M.n_row, R), dtype=torch.float64).pin_memory() for _ in range(2)]
     X_host = X
     e2e_mv = []
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        e0.record()
-        if ws > 1:
-            zg = sm(q_pin.to(dev, non_blocking=True), gather_output=True)
+    if ws > 1:
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            e0.record()
+            zg = sm(q_pin[0].to(dev, non_blocking=True), gather_output=True)
             z = torch.empty(zg.shape, dtype=torch.float64, pin_memory=True)
             z.copy_(zg, non_blocking=True)
             torch.cuda.current_stream().synchronize()
-        else:
-            z = sg.matvec_nodewise(M, q_pin)
-        e1.record()
-        e1.synchronize()
-        if i >= args.warmup:
-            e2e_mv.append(e0.elapsed_time(e1))
+            e1.record()
+            e1.synchronize()
+            if i >= args.warmup:
+                e2e_mv.append(e0.elapsed_time(e1))
+        t_e2e = float(np.mean(e2e_mv)) / 1e3
+    else:
+        pipe = sg.MatvecStream(M, R, depth=2)
+        for i in range(args.warmup):
+            pipe.submit(q_pin[i % 2], z_pin[i % 2])
+        pipe.synchronize()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(pipe.s_in)
+        for i in range(args.steps):  # L2 flushed before every timed product, as for `value`
+            pipe.submit(q_pin[i % 2], z_pin[i % 2], before=flush.zero_)
+        s1.record(pipe.s_out)
+        s1.synchronize()
+        t_e2e = s0.elapsed_time(s1) / 1e3 / args.steps
+        z = z_pin[(args.steps - 1) % 2]
     e2e_build = []
     for i in range(args.warmup + args.steps):
         e0.record()
@@ -313,7 +330,6 @@ def run_ours(args):
         e1.synchronize()
         if i >= args.warmup:
             e2e_build.append(e0.elapsed_time(e1))
-    t_e2e = float(np.mean(e2e_mv)) / 1e3
     if ws > 1:
         t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -420,6 +436,8 @@ def run_ours(args):
             "build_roofline": build_roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gpoints/s", "h2d_bytes_per_step": int(q.nbytes),
+                    "mode": "MatvecStream: pinned host Q/Z per step, copies overlapped with the compute "
+                            "of neighbouring steps (2 buffer pairs), L2 flushed before each product" if ws == 1 else "synchronous per step",
                     "d2h_bytes_per_step": int(M.n_row * R * 8),
                     "build_s": statistics.median(e2e_build) / 1e3,
                     "build_h2d_bytes": int(X.nbytes)},

@@ -14,7 +14,7 @@ from .kernel import KernelSpec, kernel_block
 from .lowrank import InterpolativeFactor, compr, interp_basis
 from .hss import BuildParams, HssMatrix, build_hss
 from .h2 import H2Matrix, build_h2, build_h2_local, build_h2_sharded
-from .apply import matvec_device, matvec_levelwise, matvec_nodewise
+from .apply import MatvecStream, matvec_device, matvec_levelwise, matvec_nodewise
 from .dense import dense_matvec, relative_error
 
 __version__ = "0.1.0"
@@ -23,6 +23,6 @@ __all__ = [
     "Box", "BuildParams", "ClusterTree", "H2Matrix", "HssMatrix", "InterpolativeFactor",
     "KernelSpec", "PointSet", "TreeNode", "build_h2", "build_h2_local", "build_h2_sharded", "build_hss", "build_tree", "compr",
     "interp_basis", "kernel_block", "leaf_sets", "matvec_device", "matvec_levelwise", "matvec_nodewise",
-    "dense_matvec", "relative_error",
+    "dense_matvec", "relative_error", "MatvecStream",
     "nearfield_set", "well_separated",
 ]

@@ -7,7 +7,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device"]
+__all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device", "MatvecStream"]
 
 
 def matvec_device(M, Q, out=None):
@@ -73,3 +73,56 @@ def matvec_levelwise(M, q):
     computation as matvec_nodewise; the reference's perfect-tree contract is kept."""
     _check_perfect(M.tree)
     return matvec_nodewise(M, q)
+
+
+class MatvecStream:
+    """Many A @ Q products with host-resident inputs and outputs, the copies of
+    neighbouring products overlapped with the compute (B200 copy engines: one
+    host->device and one device->host engine work concurrently with the SMs).
+
+    ``submit(Q, Z)`` takes pinned host tensors Q (n_col, nrhs) and Z (n_row, nrhs)
+    and returns at once; Z holds A @ Q once ``synchronize()`` (or the event returned
+    by ``submit``) completes.  ``depth`` device buffer pairs rotate, so up to
+    ``depth`` products are in flight: H2D(Q_k+1) || matvec(Q_k) || D2H(Z_k-1)."""
+
+    def __init__(self, M, nrhs: int, depth: int = 2):
+        torch = _lib.torch_cuda()
+        self.M, self.nrhs, self.depth = M, int(nrhs), int(depth)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dQ = [torch.empty((M.n_col, nrhs), dtype=torch.float64, device=dev) for _ in range(depth)]
+        self.dZ = [torch.empty((M.n_row, nrhs), dtype=torch.float64, device=dev) for _ in range(depth)]
+        self.s_in = torch.cuda.Stream()
+        self.s_mv = torch.cuda.Stream()
+        self.s_out = torch.cuda.Stream()
+        self.e_in = [torch.cuda.Event() for _ in range(depth)]
+        self.e_mv = [torch.cuda.Event() for _ in range(depth)]
+        self.e_out = [torch.cuda.Event() for _ in range(depth)]
+        self.k = 0
+
+    def submit(self, Q, Z, before=None):
+        torch = _lib.torch_cuda()
+        if Q.shape != (self.M.n_col, self.nrhs) or Z.shape != (self.M.n_row, self.nrhs):
+            raise ValueError("MatvecStream: Q / Z shapes do not match the matrix and nrhs")
+        i = self.k % self.depth
+        with torch.cuda.stream(self.s_in):
+            if self.k >= self.depth:
+                self.s_in.wait_event(self.e_mv[i])   # slot's previous product consumed dQ[i]
+            self.dQ[i].copy_(Q, non_blocking=True)
+            self.e_in[i].record(self.s_in)
+        with torch.cuda.stream(self.s_mv):
+            self.s_mv.wait_event(self.e_in[i])
+            if self.k >= self.depth:
+                self.s_mv.wait_event(self.e_out[i])  # dZ[i] copied out before it is overwritten
+            if before is not None:  # optional work ordered before the product (e.g. an L2 flush)
+                before()
+            matvec_device(self.M, self.dQ[i], self.dZ[i])
+            self.e_mv[i].record(self.s_mv)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_event(self.e_mv[i])
+            Z.copy_(self.dZ[i], non_blocking=True)
+            self.e_out[i].record(self.s_out)
+        self.k += 1
+        return self.e_out[i]
+
+    def synchronize(self):
+        self.s_out.synchronize()

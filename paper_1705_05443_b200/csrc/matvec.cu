@@ -169,10 +169,11 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     mark(7, sn);
     SMASH_CUDA(cudaEventRecord(m->join, sn));
   };
-  // Fork point: by default after the upward pass, so the latency-bound upward
-  // chain owns the SMs and the nearfield overlaps the coupling (both FP64-bound);
-  // SMASH_NEAR_EARLY=1 forks right after the gather.
-  static const bool near_early = getenv("SMASH_NEAR_EARLY") != nullptr;
+  // Fork point: right after the gather, so the nearfield overlaps the latency-bound
+  // upward pass and the coupling then runs alone; SMASH_NEAR_LATE=1 forks after the
+  // upward pass instead (nearfield overlapping the coupling).  Both orders give the
+  // same matvec time on cfg2 (the FP64 work bounds it, profiles/README_r01.md).
+  static const bool near_early = getenv("SMASH_NEAR_LATE") == nullptr;
   if (S.far && near_early) fork_near();
   double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;  // second half of qhat
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
