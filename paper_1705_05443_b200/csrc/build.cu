@@ -389,18 +389,9 @@ struct SideBuild {
   }
 
   void launch_level(CompressArgs& A, int cnt) {
-    size_t smem_full = compress_smem_bytes(A.nmax, A.mmax, true);
-    size_t smem;
     int grid;
-    if ((int)smem_full <= smem_limit) {
-      A.smem_panel = 1;
-      smem = smem_full;
-      int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, (228 * 1024) / (smem + 1024)));
-      grid = std::min(cnt, nsm * per_sm);
-    } else {
-      A.smem_panel = 0;
-      smem = compress_smem_bytes(A.nmax, A.mmax, false);
-      grid = std::min(cnt, nsm * 2);
+    size_t smem = plan_compress_launch(A, cnt, smem_limit, nsm, &grid);
+    if (A.panel_cap < (int64_t)A.nmax * A.mmax) {  // some nodes may need the global workspace
       size_t need = (size_t)grid * A.mmax * A.nmax;
       if (gws.n < need) gws.alloc(need, s);
       A.gws = gws.p;
@@ -468,23 +459,7 @@ struct SideBuild {
     A.err = err.p; A.swaps = swaps.p;
     A.nmax = std::max(nmax, 1);
     A.mmax = r + max_keep;
-    size_t smem_full = compress_smem_bytes(A.nmax, A.mmax, true);
-    size_t smem;
-    int grid;
-    if ((int)smem_full <= smem_limit) {
-      A.smem_panel = 1;
-      smem = smem_full;
-      int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, (228 * 1024) / (smem + 1024)));
-      grid = std::min(cnt, nsm * per_sm);
-    } else {
-      A.smem_panel = 0;
-      smem = compress_smem_bytes(A.nmax, A.mmax, false);
-      grid = std::min(cnt, nsm * 2);
-      size_t need = (size_t)grid * A.mmax * A.nmax;
-      if (gws.n < need) gws.alloc(need, s);
-      A.gws = gws.p;
-    }
-    launch_compress(A, grid, smem, s);
+    launch_level(A, cnt);
 
     // ---- compact this level's skeletons
     DBuf<int> rc, ro;
@@ -861,8 +836,9 @@ void compr_single(const double* C, int64_t nrows, int64_t ncols, double s_bound,
   A.nmax = ni; A.mmax = (int)ncols;
   size_t smem = compress_smem_bytes(A.nmax, A.mmax, true);
   DBuf<double> gws;
+  A.panel_cap = (int64_t)A.nmax * A.mmax;
   if ((int)smem > max_sm_smem()) {
-    A.smem_panel = 0;
+    A.panel_cap = 0;
     smem = compress_smem_bytes(A.nmax, A.mmax, false);
     gws.alloc((size_t)A.nmax * A.mmax, s);
     A.gws = gws.p;

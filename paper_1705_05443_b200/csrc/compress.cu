@@ -141,10 +141,177 @@ __device__ void build_panel(const CompressArgs& A, int v, int n, int mrows, doub
   }
 }
 
-template <int D, bool SM>
-__global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
+// Compress one node whose panel lives at P (shared memory when SMP, else this
+// CTA's slice of the global workspace): panel, dlaqp2, rank, swap loop, outputs.
+template <int D, bool SMP, int CH>
+__device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, int v, int n,
+                                              int mrows, const NodeSrc& src,
+                                              double* __restrict__ P) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  build_panel<D>(A, v, n, mrows, P, nullptr, src, S.nodes);
+  const int ld = n;
+  const int m = mrows;
+  const int kmax = min(m, n);
+  // ---- dgeqp3 / dlaqp2.  Two barriers per pivot step: (1) the argmax partials
+  // of the norms just downdated, (2) the pivot swap + reflector, both done by
+  // warp 0; the trailing update and norm downdate then run over all threads,
+  // which also fold the next step's argmax candidates.
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int j = tid; j < n; j += NT) {
+    double nr = __dsqrt_rn(col_sumsq<CH>(P, ld, j, 0, m));
+    S.vn1[j] = nr;
+    S.vn2[j] = nr;
+    S.jpvt[j] = j;
+    if (nr > bv) { bv = nr; bi = j; }
+  }
+  for (int i = 0; i < kmax; ++i) {
+    const int pvt = block_argmax_1bar(bv, bi, S);
+    if (tid < 32) {
+      if (pvt != i) {
+        for (int row = tid; row < m; row += 32) {
+          double t = P[row * ld + pvt];
+          P[row * ld + pvt] = P[row * ld + i];
+          P[row * ld + i] = t;
+        }
+        if (tid == 0) {
+          int it = S.jpvt[pvt]; S.jpvt[pvt] = S.jpvt[i]; S.jpvt[i] = it;
+          S.vn1[pvt] = S.vn1[i];
+          S.vn2[pvt] = S.vn2[i];
+        }
+        __syncwarp();
+      }
+      householder(P, ld, m, i, S);
+    }
+    __syncthreads();
+    const double tau = S.misc[0];
+    bv = -1.0;
+    bi = 0x7fffffff;
+    for (int j = i + 1 + tid; j < n; j += NT) {
+      if (tau != 0.0) apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
+      double v1 = S.vn1[j];
+      if (v1 != 0.0) {
+        const double rv1 = 1.0 / v1;
+        double q = fabs(P[i * ld + j]) * rv1;
+        double temp = fmax(1.0 - q * q, 0.0);
+        double q2 = v1 / S.vn2[j];
+        double temp2 = temp * (q2 * q2);
+        if (temp2 <= TOL3Z) {
+          double nv = i + 1 < m ? __dsqrt_rn(col_sumsq<CH>(P, ld, j, i + 1, m)) : 0.0;
+          S.vn1[j] = nv;
+          S.vn2[j] = nv;
+          v1 = nv;
+        } else {
+          v1 = __dmul_rn(v1, __dsqrt_rn(temp));
+          S.vn1[j] = v1;
+        }
+      }
+      if (v1 > bv) { bv = v1; bi = j; }
+    }
+  }
+  __syncthreads();
+  // ---- numerical rank (count semantics, lowrank.py:163-167)
+  if (tid == 0) {
+    int k = 0;
+    double r0 = fabs(S.rdiag[0]);
+    if (r0 != 0.0) {
+      double thr = __dmul_rn(A.rtol, r0);
+      for (int i = 0; i < kmax; ++i) k += fabs(S.rdiag[i]) > thr ? 1 : 0;
+    }
+    S.imisc[0] = min(k, kmax);
+  }
+  __syncthreads();
+  const int k = S.imisc[0];
+  // ---- bounded-entry swap loop (lowrank.py:191-202)
+  int swaps = 0;
+  while (k > 0 && k < n) {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    const int nk = n - k;
+    for (int j = k + tid; j < n; j += NT) {
+      // W = R11^-1 R12 by back substitution, left-looking: row a accumulates
+      // the terms of rows k-1 .. a+1 in that order -- the same FMA sequence as
+      // the column-sweep (dtrsv) form, with chunked independent loads (the
+      // solved x_c of this column and row a of R11, shared by all threads).
+      for (int a = k - 1; a >= 0; --a) {
+        double acc = P[a * ld + j];
+        constexpr int CH = 8;
+        for (int c0 = k - 1; c0 > a; c0 -= CH) {
+          double xs[CH], rs[CH];
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const bool ok = c0 - c > a;
+            xs[c] = ok ? P[(c0 - c) * ld + j] : 0.0;
+            rs[c] = ok ? P[a * ld + (c0 - c)] : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (c0 - c > a) acc = __fma_rn(-xs[c], rs[c], acc);
+        }
+        const double x = __ddiv_rn(acc, P[a * ld + a]);
+        P[a * ld + j] = x;
+        argmax_combine(bv, bi, fabs(x), a * nk + (j - k));
+      }
+    }
+    block_argmax(bv, bi, S);
+    if (!(bv > A.s_bound)) break;
+    if (swaps >= MAX_SWAPS) {
+      if (tid == 0) atomicOr(A.err, DEV_SWAP_CAP);
+      break;
+    }
+    if (tid == 0) {
+      int a = bi / nk, jj = bi % nk;
+      int t = S.jpvt[a]; S.jpvt[a] = S.jpvt[k + jj]; S.jpvt[k + jj] = t;
+    }
+    __syncthreads();
+    ++swaps;
+    build_panel<D>(A, v, n, mrows, P, S.jpvt, src, S.nodes);
+    __syncthreads();
+    for (int i = 0; i < k; ++i) {  // unpivoted QR (dgeqr2); rows < k of R suffice
+      householder(P, ld, m, i, S);
+      __syncthreads();
+      const double tau = S.misc[0];
+      if (tau != 0.0)
+        for (int j = i + 1 + tid; j < n; j += NT) apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // ---- outputs
+  if (tid == 0) {
+    A.rank[v] = k;
+    if (swaps) atomicAdd(A.swaps, (unsigned long long)swaps);
+  }
+  const int64_t io = A.ib_off[v];
+  for (int c = tid; c < n; c += NT) A.perm[io + c] = S.jpvt[c];
+  if (k > 0 && k < n) {
+    double* G = A.G + A.g_off[v];
+    const int nk = n - k;
+    for (int e = tid; e < nk * k; e += NT) {
+      int b = e / k, a = e % k;
+      G[e] = P[a * ld + k + b];
+    }
+  }
+  if (A.tmp_lab) {
+    const int64_t lo = io - A.ib_level_base;
+    for (int a = tid; a < k; a += NT) {
+      int pc = S.jpvt[a];
+      A.tmp_lab[lo + a] = src.lab ? src.lab[pc] : src.lab0 + pc;
+      for (int d = 0; d < D; ++d)
+        A.tmp_pts[(size_t)d * A.tmp_stride + lo + a] = src.base[(size_t)d * src.stride + pc];
+    }
+  }
+  __syncthreads();
+}
+
+// MODE: 0 = panel in the global workspace, 1 = shared memory, 2 = per node
+// (hybrid).  The global-only variant uses deeper load chunks (more registers,
+// fewer CTAs per SM); the shared variants are sized for >= 4 CTAs per SM.
+template <int D, int MODE>
+__global__ void __launch_bounds__(COMPRESS_THREADS, MODE == 0 ? 2 : 4) k_compress(CompressArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared S;
+  double* spanel;
   {
     double* d = reinterpret_cast<double*>(smem_raw);
     S.vn1 = d; d += A.nmax;
@@ -158,15 +325,14 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
     S.redi = ip; ip += 32;
     S.imisc = ip; ip += 8;
     S.jpvt = ip; ip += A.nmax + (A.nmax & 1);
-    // SM: the panel lives in shared memory (the compiler then emits LDS/STS with
-    // 32-bit addresses); otherwise in this CTA's slice of the global workspace
-    S.panel = SM ? reinterpret_cast<double*>(ip) : A.gws + (size_t)blockIdx.x * A.mmax * A.nmax;
+    spanel = reinterpret_cast<double*>(ip);
+    S.panel = nullptr;
   }
+  double* gpanel = A.gws ? A.gws + (size_t)blockIdx.x * A.mmax * A.nmax : nullptr;
   const int tid = threadIdx.x, NT = blockDim.x;
   for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
     const int n = A.nib[v];
     const int mrows = A.Cexp ? A.C_cols : A.r + (A.keep ? A.keep[v] : 0);
-    double* P = S.panel;
     const NodeSrc src = A.Cexp ? NodeSrc{nullptr, 0, nullptr, 0} : node_src(A, v);
     if (n == 0) {
       if (tid == 0) A.rank[v] = 0;
@@ -204,140 +370,12 @@ __global__ void __launch_bounds__(COMPRESS_THREADS) k_compress(CompressArgs A) {
       }
       __syncthreads();
     }
-    build_panel<D>(A, v, n, mrows, P, nullptr, src, S.nodes);
-    const int ld = n;
-    const int m = mrows;
-    const int kmax = min(m, n);
-    // ---- dgeqp3 / dlaqp2
-    for (int j = tid; j < n; j += NT) {
-      double nr = __dsqrt_rn(col_sumsq(P, ld, j, 0, m));
-      S.vn1[j] = nr;
-      S.vn2[j] = nr;
-      S.jpvt[j] = j;
-    }
-    __syncthreads();
-    for (int i = 0; i < kmax; ++i) {
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int j = i + tid; j < n; j += NT)
-        if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
-      block_argmax(bv, bi, S);
-      const int pvt = bi;
-      if (pvt != i) {
-        for (int row = tid; row < m; row += NT) {
-          double t = P[row * ld + pvt];
-          P[row * ld + pvt] = P[row * ld + i];
-          P[row * ld + i] = t;
-        }
-        if (tid == 0) {
-          int it = S.jpvt[pvt]; S.jpvt[pvt] = S.jpvt[i]; S.jpvt[i] = it;
-          S.vn1[pvt] = S.vn1[i];
-          S.vn2[pvt] = S.vn2[i];
-        }
-      }
-      __syncthreads();
-      householder(P, ld, m, i, S);
-      __syncthreads();
-      const double tau = S.misc[0];
-      for (int j = i + 1 + tid; j < n; j += NT) {
-        if (tau != 0.0) apply_reflector(P, ld, m, i, j, tau, S.vh);
-        double v1 = S.vn1[j];
-        if (v1 != 0.0) {
-          const double rv1 = 1.0 / v1;
-          double q = fabs(P[i * ld + j]) * rv1;
-          double temp = fmax(1.0 - q * q, 0.0);
-          double q2 = v1 / S.vn2[j];
-          double temp2 = temp * (q2 * q2);
-          if (temp2 <= TOL3Z) {
-            double nv = i + 1 < m ? __dsqrt_rn(col_sumsq(P, ld, j, i + 1, m)) : 0.0;
-            S.vn1[j] = nv;
-            S.vn2[j] = nv;
-          } else {
-            S.vn1[j] = __dmul_rn(v1, __dsqrt_rn(temp));
-          }
-        }
-      }
-      __syncthreads();
-    }
-    // ---- numerical rank (count semantics, lowrank.py:163-167)
-    if (tid == 0) {
-      int k = 0;
-      double r0 = fabs(S.rdiag[0]);
-      if (r0 != 0.0) {
-        double thr = __dmul_rn(A.rtol, r0);
-        for (int i = 0; i < kmax; ++i) k += fabs(S.rdiag[i]) > thr ? 1 : 0;
-      }
-      S.imisc[0] = min(k, kmax);
-    }
-    __syncthreads();
-    const int k = S.imisc[0];
-    // ---- bounded-entry swap loop (lowrank.py:191-202)
-    int swaps = 0;
-    while (k > 0 && k < n) {
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      const int nk = n - k;
-      for (int j = k + tid; j < n; j += NT) {
-        for (int a = k - 1; a >= 0; --a) {
-          double x = __ddiv_rn(P[a * ld + j], P[a * ld + a]);
-          P[a * ld + j] = x;
-          for (int b = 0; b < a; ++b)
-            P[b * ld + j] = __fma_rn(-x, P[b * ld + a], P[b * ld + j]);
-        }
-        for (int a = 0; a < k; ++a) {
-          double ax = fabs(P[a * ld + j]);
-          argmax_combine(bv, bi, ax, a * nk + (j - k));
-        }
-      }
-      block_argmax(bv, bi, S);
-      if (!(bv > A.s_bound)) break;
-      if (swaps >= MAX_SWAPS) {
-        if (tid == 0) atomicOr(A.err, DEV_SWAP_CAP);
-        break;
-      }
-      if (tid == 0) {
-        int a = bi / nk, jj = bi % nk;
-        int t = S.jpvt[a]; S.jpvt[a] = S.jpvt[k + jj]; S.jpvt[k + jj] = t;
-      }
-      __syncthreads();
-      ++swaps;
-      build_panel<D>(A, v, n, mrows, P, S.jpvt, src, S.nodes);
-      __syncthreads();
-      for (int i = 0; i < k; ++i) {  // unpivoted QR (dgeqr2); rows < k of R suffice
-        householder(P, ld, m, i, S);
-        __syncthreads();
-        const double tau = S.misc[0];
-        if (tau != 0.0)
-          for (int j = i + 1 + tid; j < n; j += NT) apply_reflector(P, ld, m, i, j, tau, S.vh);
-        __syncthreads();
-      }
-    }
-    __syncthreads();
-    // ---- outputs
-    if (tid == 0) {
-      A.rank[v] = k;
-      if (swaps) atomicAdd(A.swaps, (unsigned long long)swaps);
-    }
-    const int64_t io = A.ib_off[v];
-    for (int c = tid; c < n; c += NT) A.perm[io + c] = S.jpvt[c];
-    if (k > 0 && k < n) {
-      double* G = A.G + A.g_off[v];
-      const int nk = n - k;
-      for (int e = tid; e < nk * k; e += NT) {
-        int b = e / k, a = e % k;
-        G[e] = P[a * ld + k + b];
-      }
-    }
-    if (A.tmp_lab) {
-      const int64_t lo = io - A.ib_level_base;
-      for (int a = tid; a < k; a += NT) {
-        int pc = S.jpvt[a];
-        A.tmp_lab[lo + a] = src.lab ? src.lab[pc] : src.lab0 + pc;
-        for (int d = 0; d < D; ++d)
-          A.tmp_pts[(size_t)d * A.tmp_stride + lo + a] = src.base[(size_t)d * src.stride + pc];
-      }
-    }
-    __syncthreads();
+    // panel in shared memory when it fits the launch's capacity (hybrid levels:
+    // the few oversized nodes use the CTA's global/L2 workspace slice)
+    if (MODE == 1 || (MODE == 2 && (int64_t)n * mrows <= A.panel_cap))
+      compress_node<D, true, 8>(A, S, v, n, mrows, src, spanel);
+    else
+      compress_node<D, false, MODE == 0 ? 32 : 8>(A, S, v, n, mrows, src, gpanel);
   }
 }
 
@@ -385,20 +423,53 @@ size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem) {
   return b;
 }
 
+size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, int* grid) {
+  constexpr size_t SM_BYTES = 228 * 1024, CTA_RESERVED = 1024;
+  const size_t fixed = compress_smem_bytes(A.nmax, A.mmax, false);
+  const size_t full = compress_smem_bytes(A.nmax, A.mmax, true);
+  static const int gper = getenv("SMASH_GWS_PER_SM") ? atoi(getenv("SMASH_GWS_PER_SM")) : 2;
+  if ((full <= SM_BYTES / 2 - CTA_RESERVED || cnt <= nsm) && (int)full <= smem_limit) {
+    // every node fits (>= 2 CTAs per SM, or a level with at most one node per SM)
+    A.panel_cap = (int64_t)A.nmax * A.mmax;
+    int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, SM_BYTES / (full + CTA_RESERVED)));
+    *grid = std::min(cnt, nsm * per_sm);
+    return full;
+  }
+  // Capacity bounds are loose (|ibar| <= sum_c min(r, |ibar_c|)): when half the
+  // capacity fits two CTAs per SM, size the shared panel for that and let the
+  // rare larger nodes fall back to the global workspace.
+  const size_t half = compress_smem_bytes((A.nmax + 1) / 2, A.mmax, true);
+  if (half <= SM_BYTES / 2 - CTA_RESERVED) {
+    const size_t smem = std::min<size_t>(SM_BYTES / 2 - CTA_RESERVED, (size_t)smem_limit);
+    A.panel_cap = (int64_t)((smem - fixed) / 8);
+    *grid = std::min(cnt, nsm * 2);
+    return smem;
+  }
+  if ((int)full <= smem_limit && full > SM_BYTES / 2) {
+    A.panel_cap = (int64_t)A.nmax * A.mmax;
+    *grid = std::min(cnt, nsm);
+    return full;
+  }
+  A.panel_cap = 0;
+  *grid = std::min(cnt, nsm * gper);
+  return fixed;
+}
+
 void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s) {
   auto go = [&](auto kern) {
     SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, COMPRESS_THREADS, smem, s>>>(a);
   };
-  if (a.smem_panel) {
-    if (a.dim == 1) go(k_compress<1, true>);
-    else if (a.dim == 2) go(k_compress<2, true>);
-    else go(k_compress<3, true>);
-  } else {
-    if (a.dim == 1) go(k_compress<1, false>);
-    else if (a.dim == 2) go(k_compress<2, false>);
-    else go(k_compress<3, false>);
-  }
+  const int mode = a.panel_cap >= (int64_t)a.nmax * a.mmax ? 1 : a.panel_cap == 0 ? 0 : 2;
+  auto by_dim = [&](auto m) {
+    constexpr int M = decltype(m)::value;
+    if (a.dim == 1) go(k_compress<1, M>);
+    else if (a.dim == 2) go(k_compress<2, M>);
+    else go(k_compress<3, M>);
+  };
+  if (mode == 0) by_dim(std::integral_constant<int, 0>{});
+  else if (mode == 1) by_dim(std::integral_constant<int, 1>{});
+  else by_dim(std::integral_constant<int, 2>{});
   SMASH_CUDA(cudaGetLastError());
 }
 

@@ -59,14 +59,17 @@ struct CompressArgs {
   unsigned long long* swaps = nullptr;
   // panel storage
   int nmax = 0, mmax = 0;
-  int smem_panel = 1;
-  double* gws = nullptr;  // global workspace, per block mmax * nmax
+  int64_t panel_cap = 0;   // nodes with |ibar| * rows <= panel_cap keep the panel in shared memory
+  double* gws = nullptr;   // global workspace, per block mmax * nmax (the other nodes)
   // single-call mode: C given explicitly (nrows x ncols row-major) instead of a basis
   const double* Cexp = nullptr;
   int C_cols = 0;
 };
 
 size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
+// Launch plan of a level: sets A.panel_cap, returns the dynamic shared memory
+// per CTA and the grid (persistent CTAs over the level's cnt nodes).
+size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, int* grid);
 void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s);
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
                          int r, const double* pts_soa, int64_t n, double* out, int* err,

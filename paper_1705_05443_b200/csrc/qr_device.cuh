@@ -54,11 +54,40 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, Shared& S) {
   i = S.redi[0];
 }
 
-__device__ __forceinline__ double col_sumsq(const double* P, int ld, int j, int r0, int r1) {
+// Sum of squares of column j over rows [r0, r1), sequential in row order.  The
+// loads of a chunk are issued before its FMAs so a global/L2-resident panel
+// keeps CH requests in flight (the accumulation order is unchanged).
+template <int CH = 8>
+// Block-wide argmax with a single barrier: each warp reduces with shuffles and
+// publishes one partial; after the barrier every thread reduces the partials
+// itself (the (max value, smallest index) rule makes the order irrelevant).
+// The caller must separate two calls by another barrier (partials are reused).
+__device__ __forceinline__ int block_argmax_1bar(double v, int i, Shared& S) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int off = 16; off; off >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    argmax_combine(v, i, ov, oi);
+  }
+  if (lane == 0) { S.redv[wid] = v; S.redi[wid] = i; }
+  __syncthreads();
+  v = S.redv[0];
+  i = S.redi[0];
+  for (int w = 1; w < nw; ++w) argmax_combine(v, i, S.redv[w], S.redi[w]);
+  return i;
+}
+
+template <int CH = 8>
+__device__ __forceinline__ double col_sumsq(const double* __restrict__ P, int ld, int j, int r0,
+                                            int r1) {
   double s = 0.0;
-  for (int row = r0; row < r1; ++row) {
-    double x = P[row * ld + j];
-    s = __fma_rn(x, x, s);
+  for (int row = r0; row < r1; row += CH) {
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = row + c < r1 ? P[(row + c) * ld + j] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (row + c < r1) s = __fma_rn(x[c], x[c], s);
   }
   return s;
 }
@@ -103,16 +132,31 @@ __device__ __forceinline__ void householder(double* P, int ld, int m, int i, Sha
 }
 
 // Apply H_i^T = I - tau v v^T (v_i = 1) to column j > i (dlarf: w = C^T v; C -= tau v w^T).
-__device__ __forceinline__ void apply_reflector(double* P, int ld, int m, int i, int j, double tau,
-                                                const double* vh) {
+// Chunked like col_sumsq: each chunk's loads are independent, the FMA order is
+// the sequential row order.
+template <int CH = 8>
+__device__ __forceinline__ void apply_reflector(double* __restrict__ P, int ld, int m, int i, int j,
+                                                double tau, const double* __restrict__ vh) {
   double w = P[i * ld + j];
-  for (int row = i + 1; row < m; ++row) w = __fma_rn(vh[row], P[row * ld + j], w);
+  for (int row = i + 1; row < m; row += CH) {
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = row + c < m ? P[(row + c) * ld + j] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (row + c < m) w = __fma_rn(vh[row + c], x[c], w);
+  }
   double t = -__dmul_rn(tau, w);
   P[i * ld + j] = __dadd_rn(P[i * ld + j], t);
-  for (int row = i + 1; row < m; ++row)
-    P[row * ld + j] = __fma_rn(t, vh[row], P[row * ld + j]);
+  for (int row = i + 1; row < m; row += CH) {
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = row + c < m ? P[(row + c) * ld + j] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (row + c < m) P[(row + c) * ld + j] = __fma_rn(t, vh[row + c], x[c]);
+  }
 }
-
 
 }  // namespace qr
 }  // namespace smash
