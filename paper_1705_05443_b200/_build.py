@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "--extended-lambda", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-I" + os.path.join(REPO, "include")] + (
-             ["-DSMASH_XFER_TRACE"] if TRACE else [])
+             ["-DSMASH_XFER_TRACE", "-DSMASH_COMPRESS_PROF"] if TRACE else [])
 
 
 def _sources():

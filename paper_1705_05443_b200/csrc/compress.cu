@@ -148,7 +148,14 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
                                               int mrows, const NodeSrc& src,
                                               double* __restrict__ P) {
   const int tid = threadIdx.x, NT = blockDim.x;
+#ifdef SMASH_COMPRESS_PROF
+  long long t0 = clock64();
+#define PROF_MARK(k) if (tid == 0) { long long t1 = clock64(); atomicAdd(A.prof + (k), (unsigned long long)(t1 - t0)); t0 = t1; }
+#else
+#define PROF_MARK(k)
+#endif
   build_panel<D>(A, v, n, mrows, P, nullptr, src, S.nodes);
+  PROF_MARK(0)
   const int ld = n;
   const int m = mrows;
   const int kmax = min(m, n);
@@ -210,6 +217,7 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
     }
   }
   __syncthreads();
+  PROF_MARK(1)
   // ---- numerical rank (count semantics, lowrank.py:163-167)
   if (tid == 0) {
     int k = 0;
@@ -277,6 +285,7 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
     }
   }
   __syncthreads();
+  PROF_MARK(2)
   // ---- outputs
   if (tid == 0) {
     A.rank[v] = k;
@@ -455,7 +464,18 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
   return fixed;
 }
 
-void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s) {
+#ifdef SMASH_COMPRESS_PROF
+__device__ unsigned long long g_compress_prof[4];
+#endif
+
+void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s) {
+  CompressArgs a = a_in;
+#ifdef SMASH_COMPRESS_PROF
+  void* pp = nullptr;
+  SMASH_CUDA(cudaGetSymbolAddress(&pp, g_compress_prof));
+  SMASH_CUDA(cudaMemsetAsync(pp, 0, sizeof(g_compress_prof), s));
+  a.prof = reinterpret_cast<unsigned long long*>(pp);
+#endif
   auto go = [&](auto kern) {
     SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, COMPRESS_THREADS, smem, s>>>(a);
@@ -471,6 +491,13 @@ void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t 
   else if (mode == 1) by_dim(std::integral_constant<int, 1>{});
   else by_dim(std::integral_constant<int, 2>{});
   SMASH_CUDA(cudaGetLastError());
+#ifdef SMASH_COMPRESS_PROF
+  unsigned long long h[4];
+  SMASH_CUDA(cudaMemcpyAsync(h, pp, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SMASH_CUDA(cudaStreamSynchronize(s));
+  fprintf(stderr, "compress nodes %d mode %d grid %d: Mcycles panel %.2f qr %.2f rank+solve+swaps %.2f\n",
+          a.le - a.lb, mode, grid, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6);
+#endif
 }
 
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
