@@ -121,6 +121,18 @@ int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_
 int smash_matrix_exchange_buffers(smash_matrix_t m, int64_t capacity, int64_t* n, void** ptrs,
                                   int64_t* counts, int32_t* dtypes);
 int smash_matrix_build_finish(smash_matrix_t m, void* stream);
+/* Matrix from saved factors (container load; replaces the factor part of
+ * smash/container.py:load_matrix, container.py:135-211).  HOST arrays per side k < nsides,
+ * postorder-indexed exactly as smash_matrix_export writes them (rank[n_nodes],
+ * perm_ptr/skel_ptr/g_ptr[n_nodes+1], perm, skel, G); nsides = 1 when the points are shared
+ * and colfac == rowfac.  Sizes are validated against the tree (|ibar| of a leaf = its points,
+ * of an internal node = the sum of its children's ranks); pair lists are rebuilt from the
+ * tree and tau.  The matrix is then used exactly like a built one. */
+int smash_matrix_import(smash_tree_t t, const smash_build_params* p, int32_t nsides,
+                        const int64_t* const* rank, const int64_t* const* perm_ptr,
+                        const int64_t* const* perm, const int64_t* const* skel_ptr,
+                        const int64_t* const* skel, const int64_t* const* g_ptr,
+                        const double* const* G, void* stream, smash_matrix_t* out);
 /* side: 0 = row factors (rowfac), 1 = column factors (colfac).  Host outputs:
  * n_factors (nodes with a factor = non-root), total |ibar|, total skeleton, total G entries. */
 int smash_matrix_sizes(smash_matrix_t m, int32_t side, int64_t* has_total, int64_t* ibar_total,

@@ -16,6 +16,7 @@ from .hss import BuildParams, HssMatrix, build_hss
 from .h2 import H2Matrix, build_h2, build_h2_local, build_h2_sharded
 from .apply import MatvecStream, matvec_device, matvec_levelwise, matvec_nodewise
 from .dense import dense_matvec, relative_error
+from .container import load_matrix, save_matrix
 
 __version__ = "0.1.0"
 
@@ -24,5 +25,5 @@ __all__ = [
     "KernelSpec", "PointSet", "TreeNode", "build_h2", "build_h2_local", "build_h2_sharded", "build_hss", "build_tree", "compr",
     "interp_basis", "kernel_block", "leaf_sets", "matvec_device", "matvec_levelwise", "matvec_nodewise",
     "dense_matvec", "relative_error", "MatvecStream",
-    "nearfield_set", "well_separated",
+    "nearfield_set", "well_separated", "save_matrix", "load_matrix",
 ]

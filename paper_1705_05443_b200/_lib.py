@@ -42,6 +42,8 @@ SIGNATURES = {
     "smash_matrix_build": (c_i32, [c_vp, ctypes.POINTER(BuildParamsC), c_vp, ctypes.POINTER(c_vp)]),
     "smash_matrix_build_local": (c_i32, [c_vp, ctypes.POINTER(BuildParamsC), c_i32, c_i32, c_i32,
                                          c_vp, ctypes.POINTER(c_vp)]),
+    "smash_matrix_import": (c_i32, [c_vp, ctypes.POINTER(BuildParamsC), c_i32] + [c_vp] * 7 +
+                            [c_vp, ctypes.POINTER(c_vp)]),
     "smash_matrix_exchange_buffers": (c_i32, [c_vp, c_i64, P_i64, c_vp, c_vp, c_vp]),
     "smash_matrix_build_finish": (c_i32, [c_vp, c_vp]),
     "smash_matrix_sizes": (c_i32, [c_vp, c_i32, P_i64, P_i64, P_i64, P_i64]),

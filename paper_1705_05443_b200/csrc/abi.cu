@@ -136,6 +136,26 @@ int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream
   });
 }
 
+int smash_matrix_import(smash_tree_t t, const smash_build_params* p, int32_t nsides,
+                        const int64_t* const* rank, const int64_t* const* perm_ptr,
+                        const int64_t* const* perm, const int64_t* const* skel_ptr,
+                        const int64_t* const* skel, const int64_t* const* g_ptr,
+                        const double* const* G, void* stream, smash_matrix_t* out) {
+  return guarded([&] {
+    SMASH_CHECK(t && t->impl && p && out && rank && perm_ptr && perm && skel_ptr && skel && g_ptr &&
+                G, SMASH_ERR_INVALID, "null argument");
+    SMASH_CHECK(nsides == 1 || nsides == 2, SMASH_ERR_INVALID, "nsides must be 1 or 2");
+    smash::ImportSide sd[2];
+    for (int k = 0; k < nsides; ++k) {
+      SMASH_CHECK(rank[k] && perm_ptr[k] && skel_ptr[k] && g_ptr[k], SMASH_ERR_INVALID,
+                  "null factor array");
+      sd[k] = smash::ImportSide{rank[k], perm_ptr[k], perm[k], skel_ptr[k], skel[k], g_ptr[k], G[k]};
+    }
+    smash::MatrixImpl* m = smash::matrix_import(t->impl, *p, sd, nsides, st(stream));
+    *out = new smash_matrix_s{m};
+  });
+}
+
 int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_t rank,
                              int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out) {
   return guarded([&] {

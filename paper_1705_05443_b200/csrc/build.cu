@@ -770,6 +770,118 @@ void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t
 }
 
 // ---------------------------------------------------------------------------
+// Import of saved factors (container load, smash/container.py:135-211): the
+// inverse of matrix_export.  Factors arrive postorder-indexed on the host; they
+// are laid out like a level-synchronous build (levels L..2, BFS order within a
+// level) so a parent's ibar is its children's consecutive compact skeletons.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_gather_skel_pts(int64_t n, int dim, const int* lab, const double* P, int64_t Pn,
+                                  double* out, int64_t stride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < dim; ++d) out[(size_t)d * stride + i] = P[(size_t)d * Pn + lab[i]];
+}
+
+void import_side(TreeImpl* t, int side, const ImportSide& in, SideFactors& F, cudaStream_t s) {
+  const int n = t->n_nodes, L = t->n_levels;
+  std::vector<int> post(n), nch(n), cf(n), a(n), b(n);
+  const bool col = side == 1 && !t->shared;
+  d2h(post.data(), t->post.p, n, s);
+  d2h(nch.data(), t->nchild.p, n, s);
+  d2h(cf.data(), t->child_first.p, n, s);
+  d2h(a.data(), col ? t->col_a.p : t->row_a.p, n, s);
+  d2h(b.data(), col ? t->col_b.p : t->row_b.p, n, s);
+  sync(s);
+  std::vector<int> nib(n, 0), rk(n, 0), skoff(n, 0);
+  std::vector<int64_t> iboff(n, 0), goff(n, 0);
+  std::vector<int> perm, skel;
+  std::vector<double> G;
+  F.level_skel_begin.assign(L + 2, 0);
+  int64_t ib = 0, g = 0, sk = 0;
+  for (int l = L; l >= 2; --l) {
+    F.level_skel_begin[l] = sk;
+    for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
+      const int pi = post[v];
+      const int64_t p0 = in.perm_ptr[pi], p1 = in.perm_ptr[pi + 1];
+      const int64_t s0 = in.skel_ptr[pi], s1 = in.skel_ptr[pi + 1];
+      const int64_t g0 = in.g_ptr[pi], g1 = in.g_ptr[pi + 1];
+      const int64_t ni = p1 - p0, k = in.rank[pi];
+      int64_t want = 0;
+      if (nch[v] == 0) want = b[v] - a[v];
+      else for (int c = 0; c < nch[v]; ++c) want += rk[cf[v] + c];
+      SMASH_CHECK(ni == want, SMASH_ERR_INVALID,
+                  "imported factor: |ibar| of node " + std::to_string(pi) + " is " +
+                      std::to_string(ni) + ", the tree implies " + std::to_string(want));
+      SMASH_CHECK(k >= 0 && k <= ni && s1 - s0 == k && g1 - g0 == (ni - k) * k, SMASH_ERR_INVALID,
+                  "imported factor: inconsistent rank / skeleton / G sizes at node " + std::to_string(pi));
+      nib[v] = (int)ni; rk[v] = (int)k;
+      iboff[v] = ib; goff[v] = g; skoff[v] = (int)sk;
+      for (int64_t e = p0; e < p1; ++e) {
+        SMASH_CHECK(in.perm[e] >= 0 && in.perm[e] < ni, SMASH_ERR_INVALID,
+                    "imported factor: permutation entry out of range at node " + std::to_string(pi));
+        perm.push_back((int)in.perm[e]);
+      }
+      const int64_t npts = col ? t->ny : t->nx;
+      for (int64_t e = s0; e < s1; ++e) {
+        SMASH_CHECK(in.skel[e] >= 0 && in.skel[e] < npts, SMASH_ERR_INVALID,
+                    "imported factor: skeleton label out of range at node " + std::to_string(pi));
+        skel.push_back((int)in.skel[e]);
+      }
+      G.insert(G.end(), in.G + g0, in.G + g1);
+      ib += ni; g += (ni - k) * k; sk += k;
+    }
+  }
+  F.level_skel_begin[1] = sk;
+  F.nib.alloc(n, s); F.rank.alloc(n, s); F.ib_off.alloc(n, s); F.g_off.alloc(n, s);
+  F.skel_off.alloc(n, s);
+  h2d(F.nib.p, nib.data(), n, s); h2d(F.rank.p, rk.data(), n, s);
+  h2d(F.ib_off.p, iboff.data(), n, s); h2d(F.g_off.p, goff.data(), n, s);
+  h2d(F.skel_off.p, skoff.data(), n, s);
+  F.perm.alloc(std::max<int64_t>(ib, 1), s);
+  F.G.alloc(std::max<int64_t>(g, 1), s);
+  F.skel.alloc(std::max<int64_t>(sk, 1), s);
+  F.skel_stride = std::max<int64_t>(sk, 1);
+  F.skel_pts.alloc((size_t)F.skel_stride * t->dim, s);
+  if (ib) h2d(F.perm.p, perm.data(), ib, s);
+  if (g) h2d(F.G.p, G.data(), g, s);
+  if (sk) {
+    h2d(F.skel.p, skel.data(), sk, s);
+    k_gather_skel_pts<<<std::min<int64_t>(cdiv(sk, 256), 4096), 256, 0, s>>>(
+        sk, t->dim, F.skel.p, col ? t->pts_col.p : t->pts_row.p, col ? t->ny : t->nx,
+        F.skel_pts.p, F.skel_stride);
+  }
+  F.ib_total = ib; F.g_total = g; F.skel_total = sk; F.swaps = 0;
+  sync(s);  // the host staging vectors go out of scope
+  SMASH_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+MatrixImpl* matrix_import(TreeImpl* t, const smash_build_params& p, const ImportSide* sides,
+                          int nsides, cudaStream_t s) {
+  SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
+              "unknown kernel kind");
+  SMASH_CHECK(p.structure == SMASH_STRUCT_H2 || p.structure == SMASH_STRUCT_HSS,
+              SMASH_ERR_INVALID, "structure must be 'hss' or 'h2'");
+  SMASH_CHECK(nsides == 1 || nsides == 2, SMASH_ERR_INVALID, "one (shared) or two factor sides");
+  SMASH_CHECK(nsides == 2 || t->shared, SMASH_ERR_INVALID,
+              "distinct row/column points need both factor sides");
+  init_pool();
+  std::unique_ptr<MatrixImpl> M(new MatrixImpl());
+  M->tree = t;
+  M->p = p;
+  M->pl = get_pairs(t, p.tau, p.structure, s);
+  import_side(t, 0, sides[0], M->rowf, s);
+  if (nsides == 2) {
+    import_side(t, 1, sides[1], M->colf_own, s);
+    M->colf = &M->colf_own;
+  } else {
+    M->colf = &M->rowf;
+  }
+  return M.release();
+}
+
+// ---------------------------------------------------------------------------
 // single-call primitives
 // ---------------------------------------------------------------------------
 void interp_basis_single(int dim, const double* lo, const double* hi, const double* pts, int64_t n,

@@ -130,6 +130,18 @@ struct ExchangeBuf {
 };
 MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int rank, int world,
                                int cut_level, cudaStream_t s);
+// saved factors of one side, postorder-indexed host arrays (smash_matrix_import)
+struct ImportSide {
+  const int64_t* rank;
+  const int64_t* perm_ptr;
+  const int64_t* perm;
+  const int64_t* skel_ptr;
+  const int64_t* skel;
+  const int64_t* g_ptr;
+  const double* G;
+};
+MatrixImpl* matrix_import(TreeImpl* t, const smash_build_params& p, const ImportSide* sides,
+                          int nsides, cudaStream_t s);
 void matrix_exchange_buffers(MatrixImpl* m, std::vector<ExchangeBuf>& out);
 void matrix_build_finish(MatrixImpl* m, cudaStream_t s);
 void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t* perm_ptr,
