@@ -339,12 +339,20 @@ __global__ void __launch_bounds__(COMPRESS_THREADS, MODE == 0 ? 2 : 4) k_compres
   }
   double* gpanel = A.gws ? A.gws + (size_t)blockIdx.x * A.mmax * A.nmax : nullptr;
   const int tid = threadIdx.x, NT = blockDim.x;
-  for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
+  // dynamic node assignment: a CTA takes the next unclaimed node when it is done
+  // (node costs vary with |ibar|, rank and swap iterations)
+  for (int v = A.lb + blockIdx.x; v < A.le;) {
     const int n = A.nib[v];
     const int mrows = A.Cexp ? A.C_cols : A.r + (A.keep ? A.keep[v] : 0);
     const NodeSrc src = A.Cexp ? NodeSrc{nullptr, 0, nullptr, 0} : node_src(A, v);
-    if (n == 0) {
-      if (tid == 0) A.rank[v] = 0;
+    if (n == 0) {  // (uniform branch) everyone has read v before it is overwritten
+      __syncthreads();
+      if (tid == 0) {
+        A.rank[v] = 0;
+        S.imisc[4] = A.lb + (int)gridDim.x + atomicAdd(A.next, 1);
+      }
+      __syncthreads();
+      v = S.imisc[4];
       continue;
     }
     // ---- padded box + Chebyshev nodes (hss.py:39-45, lowrank.py:103-105,127-134)
@@ -385,6 +393,9 @@ __global__ void __launch_bounds__(COMPRESS_THREADS, MODE == 0 ? 2 : 4) k_compres
       compress_node<D, true, 8>(A, S, v, n, mrows, src, spanel);
     else
       compress_node<D, false, MODE == 0 ? 32 : 8>(A, S, v, n, mrows, src, gpanel);
+    if (tid == 0) S.imisc[4] = A.lb + (int)gridDim.x + atomicAdd(A.next, 1);
+    __syncthreads();
+    v = S.imisc[4];
   }
 }
 
@@ -436,7 +447,7 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
   constexpr size_t SM_BYTES = 228 * 1024, CTA_RESERVED = 1024;
   const size_t fixed = compress_smem_bytes(A.nmax, A.mmax, false);
   const size_t full = compress_smem_bytes(A.nmax, A.mmax, true);
-  static const int gper = getenv("SMASH_GWS_PER_SM") ? atoi(getenv("SMASH_GWS_PER_SM")) : 2;
+  static const int gper = getenv("SMASH_GWS_PER_SM") ? atoi(getenv("SMASH_GWS_PER_SM")) : 4;
   if ((full <= SM_BYTES / 2 - CTA_RESERVED || cnt <= nsm) && (int)full <= smem_limit) {
     // every node fits (>= 2 CTAs per SM, or a level with at most one node per SM)
     A.panel_cap = (int64_t)A.nmax * A.mmax;
@@ -467,9 +478,16 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
 #ifdef SMASH_COMPRESS_PROF
 __device__ unsigned long long g_compress_prof[4];
 #endif
+__device__ int g_compress_next;  // dynamic node counter (reset before every launch)
 
 void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s) {
   CompressArgs a = a_in;
+  {
+    void* nx = nullptr;
+    SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));
+    SMASH_CUDA(cudaMemsetAsync(nx, 0, sizeof(int), s));
+    a.next = reinterpret_cast<int*>(nx);
+  }
 #ifdef SMASH_COMPRESS_PROF
   void* pp = nullptr;
   SMASH_CUDA(cudaGetSymbolAddress(&pp, g_compress_prof));

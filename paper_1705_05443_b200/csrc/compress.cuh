@@ -64,7 +64,8 @@ struct CompressArgs {
   // single-call mode: C given explicitly (nrows x ncols row-major) instead of a basis
   const double* Cexp = nullptr;
   int C_cols = 0;
-  unsigned long long* prof = nullptr;  // SMASH_COMPRESS_PROF builds: clock64 per phase
+  unsigned long long* prof = nullptr;
+  int* next = nullptr;  // dynamic node counter (launch_compress)  // SMASH_COMPRESS_PROF builds: clock64 per phase
 };
 
 size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);

@@ -6,9 +6,9 @@ kernel family (the real 1-D Cauchy kernel, Chebyshev interpolation basis) and
 writes them with the reference's own ``smash.container.save_matrix``
 (container.py:58-128), next to the reference's matvec of a seeded vector:
 
-  ref_cauchy_hss.smash  -- HSS, x_i = i/n, y_j = (j + 0.5)/n (cfg-4 geometry), n = 512
-  ref_cauchy_h2.smash   -- H2 on the same points
-  ref_container.npz     -- q and z = matvec_nodewise(M, q) for both
+  container/ref_cauchy_hss.smash  -- HSS, x_i = i/n, y_j = (j + 0.5)/n (cfg-4 geometry), n = 512
+  container/ref_cauchy_h2.smash   -- H2 on the same points
+  container/ref_container.npz     -- q and z = matvec_nodewise(M, q) for both
 
 tests/test_container.py loads the files with paper_1705_05443_b200.load_matrix
 (GPU) and checks the device matvec against z; the CPU tests parse them.
@@ -39,6 +39,6 @@ for kind in ("hss", "h2"):
     build = smash.build_hss if kind == "hss" else smash.build_h2
     M = build(tree, spec, X, Y, params)
     out["z_" + kind] = smash.matvec_nodewise(M, q)
-    save_matrix(M, os.path.join(HERE, "ref_cauchy_%s.smash" % kind))
-np.savez_compressed(os.path.join(HERE, "ref_container.npz"), **out)
+    save_matrix(M, os.path.join(HERE, "container", "ref_cauchy_%s.smash" % kind))
+np.savez_compressed(os.path.join(HERE, "container", "ref_container.npz"), **out)
 print("ok", {k: v.shape for k, v in out.items()})

@@ -14,8 +14,8 @@ import pytest
 
 from conftest import GOLDEN
 
-REF_FILES = {"hss": os.path.join(GOLDEN, "ref_cauchy_hss.smash"),
-             "h2": os.path.join(GOLDEN, "ref_cauchy_h2.smash")}
+REF_FILES = {"hss": os.path.join(GOLDEN, "container", "ref_cauchy_hss.smash"),
+             "h2": os.path.join(GOLDEN, "container", "ref_cauchy_h2.smash")}
 
 
 def _container():
@@ -84,7 +84,7 @@ def sg():
 @pytest.mark.parametrize("kind", ["hss", "h2"])
 def test_load_reference_container_matvec(sg, kind):
     """A file the reference wrote runs on the device matvec with the reference's own factors."""
-    g = np.load(os.path.join(GOLDEN, "ref_container.npz"))
+    g = np.load(os.path.join(GOLDEN, "container", "ref_container.npz"))
     M = sg.load_matrix(REF_FILES[kind])
     assert M.kind == kind
     c = _container()
