@@ -148,6 +148,16 @@ int smash_matrix_export(smash_matrix_t m, int32_t side, int64_t* has, int64_t* r
 /* number of sRRQR swap-loop iterations per side (host output) */
 int smash_matrix_stats(smash_matrix_t m, int64_t* swaps_row, int64_t* swaps_col);
 
+/* ---- HSS ULV factorisation / solve: replaces smash.apply.ulv_factor / ulv_solve
+ * (smash/apply.py:168-354).  The factorisation keeps a pointer
+ * to m, which must outlive it.  b: (n_row, nrhs) row-major device, x: (n_col, nrhs)
+ * row-major device, caller order.  Status 2 for a non-HSS matrix, 3 for a singular
+ * local block or root system (message names the postorder node id, apply.py:218-223). */
+typedef struct smash_ulv_s* smash_ulv_t;
+int smash_ulv_factor(smash_matrix_t m, void* stream, smash_ulv_t* out);
+int smash_ulv_solve(smash_ulv_t f, const double* b, double* x, int64_t nrhs, void* stream);
+int smash_ulv_free(smash_ulv_t f);
+
 /* ---- matvec: replaces smash.apply.matvec_nodewise (smash/apply.py:34-80) ----
  * q: (n_col, nrhs) row-major device, z: (n_row, nrhs) row-major device; caller order. */
 int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);

@@ -14,7 +14,8 @@ from .kernel import KernelSpec, kernel_block
 from .lowrank import InterpolativeFactor, compr, interp_basis
 from .hss import BuildParams, HssMatrix, build_hss
 from .h2 import H2Matrix, build_h2, build_h2_local, build_h2_sharded
-from .apply import MatvecStream, matvec_device, matvec_levelwise, matvec_nodewise
+from .apply import (MatvecStream, UlvFactorization, matvec_device, matvec_levelwise, matvec_nodewise,
+                    ulv_factor, ulv_solve)
 from .dense import dense_matvec, relative_error
 from .container import load_matrix, save_matrix
 
@@ -26,4 +27,5 @@ __all__ = [
     "interp_basis", "kernel_block", "leaf_sets", "matvec_device", "matvec_levelwise", "matvec_nodewise",
     "dense_matvec", "relative_error", "MatvecStream",
     "nearfield_set", "well_separated", "save_matrix", "load_matrix",
+    "UlvFactorization", "ulv_factor", "ulv_solve",
 ]

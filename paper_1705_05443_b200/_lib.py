@@ -49,6 +49,9 @@ SIGNATURES = {
     "smash_matrix_sizes": (c_i32, [c_vp, c_i32, P_i64, P_i64, P_i64, P_i64]),
     "smash_matrix_export": (c_i32, [c_vp, c_i32] + [c_vp] * 8 + [c_vp]),
     "smash_matrix_stats": (c_i32, [c_vp, P_i64, P_i64]),
+    "smash_ulv_factor": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    "smash_ulv_solve": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "smash_ulv_free": (c_i32, [c_vp]),
     "smash_matvec": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "smash_matvec_profile": (c_i32, [c_vp, c_i32, P_dbl, P_i64]),
     "smash_matvec_set_partition": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
@@ -78,6 +81,10 @@ def load():
             fn.argtypes = args
         _lib = lib
     return _lib
+
+
+def last_error() -> str:
+    return load().smash_last_error().decode(errors="replace")
 
 
 def check(status: int):

@@ -7,7 +7,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device", "MatvecStream"]
+__all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device", "MatvecStream",
+           "UlvFactorization", "ulv_factor", "ulv_solve"]
 
 
 def matvec_device(M, Q, out=None):
@@ -126,3 +127,66 @@ class MatvecStream:
 
     def synchronize(self):
         self.s_out.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# ULV factorization and solve (apply.py:168-354) -- device factorisation
+# ---------------------------------------------------------------------------
+
+
+class UlvFactorization:
+    """GPU ULV factorisation of an HSS matrix (UlvFactorization, apply.py:186-196).
+    Holds the device handle and a reference to the matrix it factors."""
+
+    def __init__(self, matrix, handle):
+        self.matrix = matrix
+        self._h = handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.smash_ulv_free(h)
+            self._h = None
+
+    def solve(self, b):
+        return ulv_solve(self, b)
+
+
+def ulv_factor(M) -> UlvFactorization:
+    """Factor an HSS matrix for repeated solves (apply.py:237-288).  Raises
+    ValueError for non-HSS input and numpy.linalg.LinAlgError when a local
+    elimination block or the root system is numerically singular (the message
+    names the node)."""
+    import ctypes
+    if getattr(M, "kind", None) != "hss":
+        raise ValueError("ULV factorization expects an HSS matrix")
+    h = ctypes.c_void_p()
+    rc = _lib.load().smash_ulv_factor(M._h, _lib.stream_ptr(), ctypes.byref(h))
+    if rc == 3:
+        raise np.linalg.LinAlgError(_lib.last_error())
+    _lib.check(rc)
+    return UlvFactorization(M, h)
+
+
+def ulv_solve(F: UlvFactorization, b):
+    """Solve A x = b with a ULV factorisation (apply.py:291-348); b is (n,) or
+    (n, nrhs), numpy or torch; the result has b's rank and container."""
+    torch = _lib.torch_cuda()
+    M = F.matrix
+    is_torch = isinstance(b, torch.Tensor)
+    if not is_torch:
+        b = np.asarray(b)
+    if b.shape[0] != M.n_row:
+        raise ValueError("right-hand side length %d does not match matrix (%d)" % (b.shape[0], M.n_row))
+    single = b.ndim == 1
+    B = _lib.to_device(b)
+    if single:
+        B = B.reshape(-1, 1)
+    B = B.contiguous()
+    X = torch.empty((M.n_col, B.shape[1]), dtype=torch.float64, device=B.device)
+    _lib.check(_lib.load().smash_ulv_solve(F._h, _lib.ptr(B), _lib.ptr(X), B.shape[1], _lib.stream_ptr()))
+    if single:
+        X = X[:, 0]
+    if is_torch:
+        return X.to(b.device)
+    return X.cpu().numpy()

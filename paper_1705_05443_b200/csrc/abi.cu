@@ -15,6 +15,9 @@ struct smash_tree_s {
 struct smash_matrix_s {
   smash::MatrixImpl* impl;
 };
+struct smash_ulv_s {
+  smash::UlvImpl* impl;
+};
 
 namespace {
 
@@ -235,6 +238,31 @@ int smash_matrix_stats(smash_matrix_t m, int64_t* swaps_row, int64_t* swaps_col)
     SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
     if (swaps_row) *swaps_row = m->impl->rowf.swaps;
     if (swaps_col) *swaps_col = m->impl->colf->swaps;
+  });
+}
+
+int smash_ulv_factor(smash_matrix_t m, void* stream, smash_ulv_t* out) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl && out, SMASH_ERR_INVALID, "null argument");
+    smash::UlvImpl* f = smash::ulv_factor(m->impl, st(stream));
+    *out = new smash_ulv_s{f};
+  });
+}
+
+int smash_ulv_solve(smash_ulv_t f, const double* b, double* x, int64_t nrhs, void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(f && f->impl, SMASH_ERR_INVALID, "null factorization");
+    SMASH_CHECK(b && x, SMASH_ERR_INVALID, "null vector");
+    smash::ulv_solve(f->impl, b, x, nrhs, st(stream));
+  });
+}
+
+int smash_ulv_free(smash_ulv_t f) {
+  return guarded([&] {
+    if (f) {
+      smash::ulv_free(f->impl);
+      delete f;
+    }
   });
 }
 

@@ -155,6 +155,12 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
                   cudaStream_t s);
 void matvec_coeffs(MatrixImpl* m, double** qhat, int64_t* rows);
 
+// HSS ULV factorisation / solve (ulv.cu)
+struct UlvImpl;
+UlvImpl* ulv_factor(MatrixImpl* m, cudaStream_t s);
+void ulv_solve(UlvImpl* f, const double* b, double* x, int64_t nrhs, cudaStream_t s);
+void ulv_free(UlvImpl* f);
+
 void kernel_block(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
                   int64_t ny, double* out, cudaStream_t s);
 void interp_basis_single(int dim, const double* lo, const double* hi, const double* pts, int64_t n,

@@ -1,0 +1,788 @@
+// HSS ULV factorisation and solve on the GPU (replaces
+// smash/apply.py:168-354, _reduce_node / ulv_factor / ulv_solve).
+//
+// The reference walks the nodes in postorder; every node only needs its
+// children, so here one level of the tree is one batch: one CTA per node,
+// levels bottom-up for the factorisation and the upward solve, top-down for
+// the downward solve.  A host-side plan (sizes from the tree and the factor
+// ranks) gives every node fixed slots in a handful of flat HBM buffers:
+//
+//   D   (m_r x m_c)  the node's diagonal block; after the reduction it holds
+//                    Dtrans = (Q^T D)[:m_r-t] Qz (Dcorr | D_red) on top and the
+//                    LQ factor L plus the Qz reflectors in its last t rows
+//   U   (m_r x k_r)  the row basis; after the reduction R (upper) + Q reflectors
+//   VT  (k_c x m_c)  V^T; after the reduction Mfull = V^T Qz (Mcorr | V_red^T)
+//   CP  (m_red x k_c(sibling))  U_red B_(c,sibling), kept for the solve
+//
+// Row-basis QR = Householder on the columns of U (dlarfg convention), applied
+// to D from the left; the elimination of the t local equations is the LQ of
+// the bottom t rows of Q^T D (= QR of Bbot^T in the reference), applied to the
+// other rows of D and to V^T from the right.  Matrices are row-major; every
+// reflector application is one warp per vector with a shuffle-reduced dot.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "smash_impl.cuh"
+
+namespace smash {
+
+namespace {
+
+constexpr int ULV_THREADS = 256;
+constexpr double PIVOT_RTOL = 1e-13;  // apply.py:18
+
+struct UlvNode {
+  int mr, mc, kr, kc, t;
+  int leaf;
+  int c1, c2;        // BFS children (HSS: binary), -1 for leaves
+  int parent, pos;   // BFS parent; row offset of this node's reduced columns in the parent's x
+  int64_t oD, oU, oVT, otU, otZ, oCP;
+  int64_t ob, ox, og;  // solve workspaces (units of nrhs)
+  int row_a, col_a;    // leaf point ranges (tree order)
+  int post;
+};
+
+__device__ __forceinline__ double warp_sum(double x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// dlarfg on x[0], x[s], ..., x[(n-1)s] by one warp: x[0] <- beta, x[1:] <- v[1:],
+// returns tau (0 when nothing to annihilate).
+__device__ double warp_larfg(double* x, int64_t s, int n) {
+  const int lane = threadIdx.x & 31;
+  double ss = 0.0;
+  for (int i = 1 + lane; i < n; i += 32) {
+    double v = x[i * s];
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  const double alpha = x[0];
+  if (n <= 1 || ss == 0.0) return 0.0;
+  const double xnorm = sqrt(ss);
+  const double beta = -copysign(hypot(alpha, xnorm), alpha);
+  const double tau = (beta - alpha) / beta;
+  const double scal = 1.0 / (alpha - beta);
+  for (int i = 1 + lane; i < n; i += 32) x[i * s] *= scal;
+  __syncwarp();
+  if (lane == 0) x[0] = beta;
+  __syncwarp();
+  return tau;
+}
+
+// y <- (I - tau v v^T) y with v[0] = 1, v[1:] = vs[1:] (vs in shared memory),
+// y[i] at y[i * sy], n entries; one warp.
+__device__ __forceinline__ void warp_apply(const double* vs, int n, double tau, double* y,
+                                           int64_t sy) {
+  const int lane = threadIdx.x & 31;
+  double w = 0.0;
+  for (int i = lane; i < n; i += 32) w = fma(i == 0 ? 1.0 : vs[i], y[i * sy], w);
+  w = warp_sum(w) * tau;
+  for (int i = lane; i < n; i += 32) y[i * sy] -= w * (i == 0 ? 1.0 : vs[i]);
+  __syncwarp();
+}
+
+// expand() entry (lowrank.py:222-229): row q of P[I; G] for a node with local
+// inverse permutation inv (ibar position -> perm position), rank k.
+__device__ __forceinline__ double expand_at(const int* inv, const double* G, int k, int q, int c) {
+  const int j = inv[q];
+  return j < k ? (j == c ? 1.0 : 0.0) : G[(int64_t)(j - k) * k + c];
+}
+
+struct FacView {
+  const int* perm;
+  const double* G;
+  const int* skel;
+  const int64_t* ib_off;
+  const int64_t* g_off;
+  const int* skel_off;
+  const int* nib;
+};
+
+__device__ void load_inv(const FacView& F, int v, int* inv) {
+  const int n = F.nib[v];
+  const int* p = F.perm + F.ib_off[v];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) inv[p[j]] = j;
+}
+
+struct UlvArgs {
+  const UlvNode* nd;
+  int lb, le, root;
+  double* D;
+  double* U;
+  double* VT;
+  double* tauU;
+  double* tauZ;
+  double* CP;
+  FacView R, C;
+  const double* prow;  // tree-ordered SoA points (rows / cols)
+  const double* pcol;
+  int64_t nrow, ncol;
+  double dx;
+  int* err;  // [0] = flag, [1] = postorder node id
+};
+
+__device__ __forceinline__ void flag_singular(const UlvArgs& A, int post) {
+  if (atomicCAS(A.err, 0, 1) == 0) A.err[1] = post;
+}
+
+// ---- assembly ------------------------------------------------------------------------
+template <int KER, int DIM>
+__global__ void __launch_bounds__(ULV_THREADS) k_ulv_assemble(UlvArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int v = A.lb + blockIdx.x;
+  if (v >= A.le) return;
+  const UlvNode& N = A.nd[v];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  double* D = A.D + N.oD;
+  if (N.leaf) {
+    int* invr = reinterpret_cast<int*>(smem);
+    int* invc = invr + N.mr;
+    if (v != A.root) {
+      load_inv(A.R, v, invr);
+      load_inv(A.C, v, invc);
+    }
+    for (int e = tid; e < N.mr * N.mc; e += NT) {
+      const int r = e / N.mc, c = e % N.mc;
+      double x[DIM], y[DIM];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        x[a] = A.prow[(int64_t)a * A.nrow + N.row_a + r];
+        y[a] = A.pcol[(int64_t)a * A.ncol + N.col_a + c];
+      }
+      D[e] = kval<KER, DIM>(x, y, A.dx);
+    }
+    if (v == A.root) return;
+    __syncthreads();
+    const double* Gr = A.R.G + A.R.g_off[v];
+    const double* Gc = A.C.G + A.C.g_off[v];
+    for (int e = tid; e < N.mr * N.kr; e += NT)
+      A.U[N.oU + e] = expand_at(invr, Gr, N.kr, e / N.kr, e % N.kr);
+    for (int e = tid; e < N.kc * N.mc; e += NT) {
+      const int a = e / N.mc, c = e % N.mc;
+      A.VT[N.oVT + e] = expand_at(invc, Gc, N.kc, c, a);
+    }
+    return;
+  }
+  // internal node: children's reduced blocks (apply.py:246-266)
+  const UlvNode& N1 = A.nd[N.c1];
+  const UlvNode& N2 = A.nd[N.c2];
+  const int m1 = N1.mr - N1.t, n1 = N1.mc - N1.t, m2 = N2.mr - N2.t, n2 = N2.mc - N2.t;
+  double* B12 = reinterpret_cast<double*>(smem);  // kr1 x kc2
+  double* B21 = B12 + N1.kr * N2.kc;              // kr2 x kc1
+  int* invr = reinterpret_cast<int*>(B21 + N2.kr * N1.kc);
+  int* invc = invr + N1.kr + N2.kr;
+  // coupling blocks at the skeletons (hss.py:106-150)
+  auto skel_pt = [&](const FacView& F, const double* P, int64_t stride, int node, int a, double* x) {
+    const int lab = F.skel[F.skel_off[node] + a];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x[d] = P[(int64_t)d * stride + lab];
+  };
+  for (int e = tid; e < N1.kr * N2.kc; e += NT) {
+    double x[DIM], y[DIM];
+    skel_pt(A.R, A.prow, A.nrow, N.c1, e / N2.kc, x);
+    skel_pt(A.C, A.pcol, A.ncol, N.c2, e % N2.kc, y);
+    B12[e] = kval<KER, DIM>(x, y, A.dx);
+  }
+  for (int e = tid; e < N2.kr * N1.kc; e += NT) {
+    double x[DIM], y[DIM];
+    skel_pt(A.R, A.prow, A.nrow, N.c2, e / N1.kc, x);
+    skel_pt(A.C, A.pcol, A.ncol, N.c1, e % N1.kc, y);
+    B21[e] = kval<KER, DIM>(x, y, A.dx);
+  }
+  if (v != A.root) {
+    load_inv(A.R, v, invr);
+    load_inv(A.C, v, invc);
+  }
+  __syncthreads();
+  // U_red of a child: [R; 0] after a reduction, U itself when nothing was eliminated
+  auto ured = [&](const UlvNode& C, int r, int a) -> double {
+    const double u = A.U[C.oU + (int64_t)r * C.kr + a];
+    return C.t > 0 ? (r <= a ? u : 0.0) : u;
+  };
+  // CP = U_red B (kept for the solve), stored with the child
+  double* CP1 = A.CP + N1.oCP;
+  double* CP2 = A.CP + N2.oCP;
+  for (int e = tid; e < m1 * N2.kc; e += NT) {
+    const int r = e / N2.kc, b = e % N2.kc;
+    double s = 0.0;
+    for (int a = 0; a < N1.kr; ++a) s = fma(ured(N1, r, a), B12[a * N2.kc + b], s);
+    CP1[e] = s;
+  }
+  for (int e = tid; e < m2 * N1.kc; e += NT) {
+    const int r = e / N1.kc, b = e % N1.kc;
+    double s = 0.0;
+    for (int a = 0; a < N2.kr; ++a) s = fma(ured(N2, r, a), B21[a * N1.kc + b], s);
+    CP2[e] = s;
+  }
+  __syncthreads();
+  const double* D1 = A.D + N1.oD;
+  const double* D2 = A.D + N2.oD;
+  const double* V1 = A.VT + N1.oVT;  // V_red^T = VT[:, t:]
+  const double* V2 = A.VT + N2.oVT;
+  for (int e = tid; e < N.mr * N.mc; e += NT) {
+    const int r = e / N.mc, c = e % N.mc;
+    double val;
+    if (r < m1 && c < n1) {
+      val = D1[(int64_t)r * N1.mc + N1.t + c];
+    } else if (r >= m1 && c >= n1) {
+      val = D2[(int64_t)(r - m1) * N2.mc + N2.t + (c - n1)];
+    } else if (r < m1) {  // CP1 V2_red^T
+      double s = 0.0;
+      for (int b = 0; b < N2.kc; ++b)
+        s = fma(CP1[(int64_t)r * N2.kc + b], V2[(int64_t)b * N2.mc + N2.t + (c - n1)], s);
+      val = s;
+    } else {
+      double s = 0.0;
+      for (int b = 0; b < N1.kc; ++b)
+        s = fma(CP2[(int64_t)(r - m1) * N1.kc + b], V1[(int64_t)b * N1.mc + N1.t + c], s);
+      val = s;
+    }
+    D[e] = val;
+  }
+  if (v == A.root) return;
+  // U = [U1_red R_c1; U2_red R_c2], V^T = [W_c1^T V1_red^T, W_c2^T V2_red^T]
+  const double* Gr = A.R.G + A.R.g_off[v];
+  const double* Gc = A.C.G + A.C.g_off[v];
+  for (int e = tid; e < N.mr * N.kr; e += NT) {
+    const int r = e / N.kr, c = e % N.kr;
+    double s = 0.0;
+    if (r < m1)
+      for (int a = 0; a < N1.kr; ++a) s = fma(ured(N1, r, a), expand_at(invr, Gr, N.kr, a, c), s);
+    else
+      for (int a = 0; a < N2.kr; ++a)
+        s = fma(ured(N2, r - m1, a), expand_at(invr, Gr, N.kr, N1.kr + a, c), s);
+    A.U[N.oU + e] = s;
+  }
+  for (int e = tid; e < N.kc * N.mc; e += NT) {
+    const int a = e / N.mc, c = e % N.mc;
+    double s = 0.0;
+    if (c < n1)
+      for (int b = 0; b < N1.kc; ++b)
+        s = fma(expand_at(invc, Gc, N.kc, b, a), V1[(int64_t)b * N1.mc + N1.t + c], s);
+    else
+      for (int b = 0; b < N2.kc; ++b)
+        s = fma(expand_at(invc, Gc, N.kc, N1.kc + b, a), V2[(int64_t)b * N2.mc + N2.t + (c - n1)], s);
+    A.VT[N.oVT + e] = s;
+  }
+}
+
+// ---- reduction (_reduce_node, apply.py:196-234) -------------------------------------------
+__global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* vs = reinterpret_cast<double*>(smem);
+  __shared__ double s_tau, s_norm;
+  const int v = A.lb + blockIdx.x;
+  if (v >= A.le || v == A.root) return;
+  const UlvNode& N = A.nd[v];
+  if (N.t == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
+  double* D = A.D + N.oD;
+  double* U = A.U + N.oU;
+  double* VT = A.VT + N.oVT;
+  const int mr = N.mr, mc = N.mc, kr = N.kr, kc = N.kc, t = N.t;
+  // 1. Householder QR of U, applied to D from the left (Q^T D)
+  for (int i = 0; i < kr; ++i) {
+    if (wid == 0) {
+      double tau = warp_larfg(U + (int64_t)i * kr + i, kr, mr - i);
+      if (lane == 0) { s_tau = tau; A.tauU[N.otU + i] = tau; }
+    }
+    __syncthreads();
+    for (int r = i + 1 + tid; r < mr; r += blockDim.x) vs[r - i] = U[(int64_t)r * kr + i];
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      for (int j = wid; j < (kr - i - 1) + mc; j += NW) {
+        if (j < kr - i - 1) warp_apply(vs, mr - i, tau, U + (int64_t)i * kr + (i + 1 + j), kr);
+        else warp_apply(vs, mr - i, tau, D + (int64_t)i * mc + (j - (kr - i - 1)), mc);
+      }
+    }
+    __syncthreads();
+  }
+  // 2. LQ of Bbot = the last t rows of Q^T D (QR of Bbot^T), applied from the right
+  //    to the other rows of D (Dtrans) and to V^T (Mfull)
+  const int r0 = mr - t;
+  if (wid == 0) {  // ||Bbot||_inf before the elimination (singularity test, apply.py:218-221)
+    double mx = 0.0;
+    for (int r = 0; r < t; ++r) {
+      double s = 0.0;
+      for (int c = lane; c < mc; c += 32) s += fabs(D[(int64_t)(r0 + r) * mc + c]);
+      s = warp_sum(s);
+      mx = fmax(mx, s);
+    }
+    if (lane == 0) s_norm = mx;
+  }
+  __syncthreads();
+  for (int i = 0; i < t; ++i) {
+    double* row = D + (int64_t)(r0 + i) * mc;
+    if (wid == 0) {
+      double tau = warp_larfg(row + i, 1, mc - i);
+      if (lane == 0) { s_tau = tau; A.tauZ[N.otZ + i] = tau; }
+    }
+    __syncthreads();
+    for (int c = i + 1 + tid; c < mc; c += blockDim.x) vs[c - i] = row[c];
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      const int nrows = (t - i - 1) + r0 + kc;
+      for (int j = wid; j < nrows; j += NW) {
+        double* y;
+        if (j < t - i - 1) y = D + (int64_t)(r0 + i + 1 + j) * mc;
+        else if (j < t - i - 1 + r0) y = D + (int64_t)(j - (t - i - 1)) * mc;
+        else y = VT + (int64_t)(j - (t - i - 1) - r0) * mc;
+        warp_apply(vs, mc - i, tau, y + i, 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double dmin = INFINITY;
+    for (int i = 0; i < t; ++i) dmin = fmin(dmin, fabs(D[(int64_t)(r0 + i) * mc + i]));
+    if (dmin <= PIVOT_RTOL * fmax(s_norm, 1e-300)) flag_singular(A, N.post);
+  }
+}
+
+// ---- root LU with partial pivoting (sla.lu_factor, apply.py:270-283) -------------------------
+__global__ void __launch_bounds__(ULV_THREADS) k_ulv_root_lu(UlvArgs A, int* piv) {
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double s_norm;
+  const UlvNode& N = A.nd[A.root];
+  const int m = N.mr, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
+  double* D = A.D + N.oD;
+  if (wid == 0) {
+    double mx = 0.0;
+    for (int r = 0; r < m; ++r) {
+      double s = 0.0;
+      for (int c = lane; c < m; c += 32) s += fabs(D[(int64_t)r * m + c]);
+      mx = fmax(mx, warp_sum(s));
+    }
+    if (lane == 0) s_norm = mx;
+  }
+  for (int k = 0; k < m; ++k) {
+    // pivot: first row of max |D[r][k]|, r >= k
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = k + tid; r < m; r += blockDim.x) {
+      double a = fabs(D[(int64_t)r * m + k]);
+      if (a > bv) { bv = a; bi = r; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[wid] = bv; red_i[wid] = bi; }
+    __syncthreads();
+    bv = red_v[0]; bi = red_i[0];
+    for (int w = 1; w < NW; ++w)
+      if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bi)) { bv = red_v[w]; bi = red_i[w]; }
+    if (tid == 0) piv[k] = bi;
+    if (bi != k)
+      for (int c = tid; c < m; c += blockDim.x) {
+        double x = D[(int64_t)k * m + c];
+        D[(int64_t)k * m + c] = D[(int64_t)bi * m + c];
+        D[(int64_t)bi * m + c] = x;
+      }
+    __syncthreads();
+    const double p = D[(int64_t)k * m + k];
+    if (p != 0.0)
+      for (int r = k + 1 + tid; r < m; r += blockDim.x) D[(int64_t)r * m + k] /= p;
+    __syncthreads();
+    for (int e = tid; e < (m - k - 1) * (m - k - 1); e += blockDim.x) {
+      const int r = k + 1 + e / (m - k - 1), c = k + 1 + e % (m - k - 1);
+      D[(int64_t)r * m + c] -= D[(int64_t)r * m + k] * D[(int64_t)k * m + c];
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && m > 0) {
+    double dmin = INFINITY;
+    for (int i = 0; i < m; ++i) dmin = fmin(dmin, fabs(D[(int64_t)i * m + i]));
+    if (dmin <= PIVOT_RTOL * fmax(s_norm, 1e-300)) flag_singular(A, N.post);
+  }
+}
+
+// ---- solve ------------------------------------------------------------------------------------
+struct SolveArgs {
+  UlvArgs A;
+  const double* b;   // caller order, n_row x R
+  double* x;         // caller order, n_col x R
+  const int64_t* perm_row;  // tree position -> caller index (int64, device)
+  const int64_t* perm_col;
+  double* wb;        // per node mr x R
+  double* wx;        // per node mc x R  ([z1; xvec])
+  double* wg;        // per node kc x R
+  const int* piv;
+  int R;
+};
+
+// upward pass of one level (apply.py:300-330); the root also runs the LU solve
+__global__ void __launch_bounds__(ULV_THREADS) k_ulv_up(SolveArgs S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const UlvArgs& A = S.A;
+  const int v = A.lb + blockIdx.x;
+  if (v >= A.le) return;
+  const UlvNode& N = A.nd[v];
+  const int R = S.R, tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5,
+            NW = NT >> 5;
+  double* b = S.wb + N.ob * R;
+  double* g = S.wg + N.og * R;
+  int* invc = reinterpret_cast<int*>(smem);
+  // bcur
+  if (N.leaf) {
+    for (int e = tid; e < N.mr * R; e += NT) {
+      const int r = e / R, c = e % R;
+      b[e] = S.b[S.perm_row[N.row_a + r] * R + c];
+    }
+    for (int e = tid; e < N.kc * R; e += NT) g[e] = 0.0;
+  } else {
+    const UlvNode& N1 = A.nd[N.c1];
+    const UlvNode& N2 = A.nd[N.c2];
+    const int m1 = N1.mr - N1.t;
+    const double* b1 = S.wb + N1.ob * R;
+    const double* b2 = S.wb + N2.ob * R;
+    const double* g1 = S.wg + N1.og * R;
+    const double* g2 = S.wg + N2.og * R;
+    const double* CP1 = A.CP + N1.oCP;
+    const double* CP2 = A.CP + N2.oCP;
+    for (int e = tid; e < N.mr * R; e += NT) {
+      const int r = e / R, c = e % R;
+      double s;
+      if (r < m1) {
+        s = b1[(int64_t)r * R + c];
+        for (int q = 0; q < N2.kc; ++q) s -= CP1[(int64_t)r * N2.kc + q] * g2[(int64_t)q * R + c];
+      } else {
+        s = b2[(int64_t)(r - m1) * R + c];
+        for (int q = 0; q < N1.kc; ++q)
+          s -= CP2[(int64_t)(r - m1) * N1.kc + q] * g1[(int64_t)q * R + c];
+      }
+      b[e] = s;
+    }
+    if (v != A.root) {  // gpre = W_c1^T g1 + W_c2^T g2
+      load_inv(A.C, v, invc);
+      __syncthreads();
+      const double* Gc = A.C.G + A.C.g_off[v];
+      for (int e = tid; e < N.kc * R; e += NT) {
+        const int a = e / R, c = e % R;
+        double s = 0.0;
+        for (int q = 0; q < N1.kc; ++q) s = fma(expand_at(invc, Gc, N.kc, q, a), g1[(int64_t)q * R + c], s);
+        for (int q = 0; q < N2.kc; ++q)
+          s = fma(expand_at(invc, Gc, N.kc, N1.kc + q, a), g2[(int64_t)q * R + c], s);
+        g[e] = s;
+      }
+    }
+  }
+  __syncthreads();
+  if (v == A.root) {  // LU solve (sla.lu_solve): P, L (unit), U
+    const int m = N.mr;
+    const double* LU = A.D + N.oD;
+    double* xr = S.wx + N.ox * R;
+    for (int c = wid; c < R; c += NW) {
+      if (lane == 0) {
+        for (int k = 0; k < m; ++k) {
+          const int p = S.piv[k];
+          if (p != k) { double q = b[(int64_t)k * R + c]; b[(int64_t)k * R + c] = b[(int64_t)p * R + c]; b[(int64_t)p * R + c] = q; }
+        }
+        for (int i = 0; i < m; ++i) {
+          double s = b[(int64_t)i * R + c];
+          for (int j = 0; j < i; ++j) s -= LU[(int64_t)i * m + j] * xr[(int64_t)j * R + c];
+          xr[(int64_t)i * R + c] = s;
+        }
+        for (int i = m - 1; i >= 0; --i) {
+          double s = xr[(int64_t)i * R + c];
+          for (int j = i + 1; j < m; ++j) s -= LU[(int64_t)i * m + j] * xr[(int64_t)j * R + c];
+          xr[(int64_t)i * R + c] = s / LU[(int64_t)i * m + i];
+        }
+      }
+    }
+    if (N.leaf) {  // single-leaf tree: the root system is the whole matrix
+      __syncthreads();
+      for (int e = tid; e < N.mc * R; e += NT) {
+        const int r = e / R, c = e % R;
+        S.x[S.perm_col[N.col_a + r] * R + c] = xr[e];
+      }
+    }
+    return;
+  }
+  if (N.t == 0) return;  // bred = bcur, g = gpre
+  const double* U = A.U + N.oU;
+  const double* D = A.D + N.oD;
+  const double* VT = A.VT + N.oVT;
+  const int mr = N.mr, mc = N.mc, kr = N.kr, t = N.t, r0 = mr - t;
+  double* vs = reinterpret_cast<double*>(smem);
+  // bp = Q^T bcur
+  for (int i = 0; i < kr; ++i) {
+    for (int r = i + 1 + tid; r < mr; r += NT) vs[r - i] = U[(int64_t)r * kr + i];
+    __syncthreads();
+    const double tau = A.tauU[N.otU + i];
+    if (tau != 0.0)
+      for (int c = wid; c < R; c += NW) warp_apply(vs, mr - i, tau, b + (int64_t)i * R + c, R);
+    __syncthreads();
+  }
+  // z1 = L^-1 bp[r0:], kept in x[0:t) for the downward pass
+  double* z = S.wx + N.ox * R;
+  for (int c = wid; c < R; c += NW) {
+    if (lane == 0)
+      for (int i = 0; i < t; ++i) {
+        double s = b[(int64_t)(r0 + i) * R + c];
+        for (int j = 0; j < i; ++j) s -= D[(int64_t)(r0 + i) * mc + j] * z[(int64_t)j * R + c];
+        z[(int64_t)i * R + c] = s / D[(int64_t)(r0 + i) * mc + i];
+      }
+  }
+  __syncthreads();
+  // bred = bp[:r0] - Dcorr z1 ; g += Mcorr z1
+  for (int e = tid; e < r0 * R; e += NT) {
+    const int r = e / R, c = e % R;
+    double s = b[e];
+    for (int j = 0; j < t; ++j) s -= D[(int64_t)r * mc + j] * z[(int64_t)j * R + c];
+    b[e] = s;
+  }
+  for (int e = tid; e < N.kc * R; e += NT) {
+    const int a = e / R, c = e % R;
+    double s = g[e];
+    for (int j = 0; j < t; ++j) s = fma(VT[(int64_t)a * mc + j], z[(int64_t)j * R + c], s);
+    g[e] = s;
+  }
+}
+
+// downward pass of one level (apply.py:332-348): x_v = Qz [z1; xvec]
+__global__ void __launch_bounds__(ULV_THREADS) k_ulv_down(SolveArgs S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const UlvArgs& A = S.A;
+  const int v = A.lb + blockIdx.x;
+  if (v >= A.le || v == A.root) return;
+  const UlvNode& N = A.nd[v];
+  const UlvNode& Pn = A.nd[N.parent];
+  const int R = S.R, tid = threadIdx.x, NT = blockDim.x, wid = tid >> 5, NW = NT >> 5;
+  double* xv = S.wx + N.ox * R;
+  const double* xp = S.wx + Pn.ox * R;
+  const int n_red = N.mc - N.t;
+  for (int e = tid; e < n_red * R; e += NT) xv[(int64_t)N.t * R + e] = xp[(int64_t)N.pos * R + e];
+  __syncthreads();
+  if (N.t > 0) {
+    const double* D = A.D + N.oD;
+    double* vs = reinterpret_cast<double*>(smem);
+    const int mc = N.mc, r0 = N.mr - N.t;
+    for (int i = N.t - 1; i >= 0; --i) {
+      const double* row = D + (int64_t)(r0 + i) * mc;
+      for (int c = i + 1 + tid; c < mc; c += NT) vs[c - i] = row[c];
+      __syncthreads();
+      const double tau = A.tauZ[N.otZ + i];
+      if (tau != 0.0)
+        for (int c = wid; c < R; c += NW) warp_apply(vs, mc - i, tau, xv + (int64_t)i * R + c, R);
+      __syncthreads();
+    }
+  }
+  if (N.leaf)
+    for (int e = tid; e < N.mc * R; e += NT) {
+      const int r = e / R, c = e % R;
+      S.x[S.perm_col[N.col_a + r] * R + c] = xv[e];
+    }
+}
+
+}  // namespace
+
+struct UlvImpl {
+  MatrixImpl* M = nullptr;
+  std::vector<UlvNode> h;
+  DBuf<UlvNode> d;
+  DBuf<double> D, U, VT, tauU, tauZ, CP;
+  DBuf<int> piv, err;
+  DBuf<int64_t> perm_row, perm_col;
+  int root = 0;
+  int64_t nb = 0, nx = 0, ng = 0;
+  size_t smem_asm = 0, smem_red = 0, smem_up = 0;
+  DBuf<double> wb, wx, wg;
+  int64_t ws_nrhs = 0;
+};
+
+namespace {
+
+UlvArgs make_args(UlvImpl* F, int lb, int le) {
+  MatrixImpl* M = F->M;
+  TreeImpl* t = M->tree;
+  auto view = [](const SideFactors& S) {
+    return FacView{S.perm.p, S.G.p, S.skel.p, S.ib_off.p, S.g_off.p, S.skel_off.p, S.nib.p};
+  };
+  UlvArgs A;
+  A.nd = F->d.p; A.lb = lb; A.le = le; A.root = F->root;
+  A.D = F->D.p; A.U = F->U.p; A.VT = F->VT.p; A.tauU = F->tauU.p; A.tauZ = F->tauZ.p; A.CP = F->CP.p;
+  A.R = view(M->rowf); A.C = view(*M->colf);
+  A.prow = t->pts_row.p;
+  A.pcol = t->shared ? t->pts_row.p : t->pts_col.p;
+  A.nrow = t->nx; A.ncol = t->shared ? t->nx : t->ny;
+  A.dx = M->p.dx;
+  A.err = F->err.p;
+  return A;
+}
+
+void check_err(UlvImpl* F, cudaStream_t s) {
+  int h[2] = {0, 0};
+  d2h(h, F->err.p, 2, s);
+  sync(s);
+  SMASH_CHECK(h[0] == 0, SMASH_ERR_NUMERICAL,
+              "ULV elimination hit a singular local block at node " + std::to_string(h[1]));
+}
+
+}  // namespace
+
+UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
+  SMASH_CHECK(M->p.structure == SMASH_STRUCT_HSS, SMASH_ERR_INVALID,
+              "ULV factorization expects an HSS matrix");
+  TreeImpl* t = M->tree;
+  const int n = t->n_nodes, L = t->n_levels;
+  std::unique_ptr<UlvImpl> F(new UlvImpl());
+  F->M = M;
+  std::vector<int> nch(n), cf(n), par(n), post(n), ra(n), rb(n), ca(n), cb(n), kr(n), kc(n);
+  d2h(nch.data(), t->nchild.p, n, s);
+  d2h(cf.data(), t->child_first.p, n, s);
+  d2h(par.data(), t->parent.p, n, s);
+  d2h(post.data(), t->post.p, n, s);
+  d2h(ra.data(), t->row_a.p, n, s);
+  d2h(rb.data(), t->row_b.p, n, s);
+  d2h(ca.data(), t->shared ? t->row_a.p : t->col_a.p, n, s);
+  d2h(cb.data(), t->shared ? t->row_b.p : t->col_b.p, n, s);
+  d2h(kr.data(), M->rowf.rank.p, n, s);
+  d2h(kc.data(), M->colf->rank.p, n, s);
+  sync(s);
+  F->root = t->level_begin(1);
+  std::vector<UlvNode>& H = F->h;
+  H.assign(n, UlvNode{});
+  int64_t oD = 0, oU = 0, oVT = 0, otU = 0, otZ = 0, oCP = 0, ob = 0, ox = 0, og = 0;
+  size_t sm_asm = 16, sm_red = 16, sm_up = 16;
+  for (int l = L; l >= 1; --l) {
+    for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
+      UlvNode& N = H[v];
+      const bool root = v == F->root;
+      N.leaf = nch[v] == 0;
+      N.post = post[v];
+      N.parent = root ? -1 : par[v];
+      N.row_a = ra[v];
+      N.col_a = ca[v];
+      N.kr = root ? 0 : kr[v];
+      N.kc = root ? 0 : kc[v];
+      if (N.leaf) {
+        N.c1 = N.c2 = -1;
+        N.mr = rb[v] - ra[v];
+        N.mc = cb[v] - ca[v];
+      } else {
+        SMASH_CHECK(nch[v] == 2, SMASH_ERR_INVALID, "ULV expects a binary (HSS) tree");
+        N.c1 = cf[v]; N.c2 = cf[v] + 1;
+        const UlvNode &A1 = H[N.c1], &A2 = H[N.c2];
+        N.mr = (A1.mr - A1.t) + (A2.mr - A2.t);
+        N.mc = (A1.mc - A1.t) + (A2.mc - A2.t);
+        sm_asm = std::max(sm_asm, 8 * (size_t)(A1.kr * A2.kc + A2.kr * A1.kc) +
+                                      4 * (size_t)(A1.kr + A2.kr + A1.kc + A2.kc) + 16);
+        sm_up = std::max(sm_up, 4 * (size_t)(A1.kc + A2.kc) + 16);
+      }
+      if (N.leaf) sm_asm = std::max(sm_asm, 4 * (size_t)(N.mr + N.mc) + 16);
+      const int e = N.mr - N.kr;
+      N.t = (!root && e > 0) ? std::min(e, N.mc) : 0;
+      if (root)
+        SMASH_CHECK(N.mr == N.mc, SMASH_ERR_NUMERICAL,
+                    "ULV root system is " + std::to_string(N.mr) + "x" + std::to_string(N.mc) +
+                        ", not square");
+      N.oD = oD; oD += (int64_t)N.mr * N.mc;
+      N.oU = oU; oU += (int64_t)N.mr * N.kr;
+      N.oVT = oVT; oVT += (int64_t)N.kc * N.mc;
+      N.otU = otU; otU += N.kr;
+      N.otZ = otZ; otZ += N.t;
+      N.ob = ob; ob += N.mr;
+      N.ox = ox; ox += N.mc;
+      N.og = og; og += N.kc;
+      sm_red = std::max(sm_red, 8 * (size_t)std::max(N.mr, N.mc) + 16);
+      sm_up = std::max(sm_up, 8 * (size_t)std::max(N.mr, N.mc) + 16);
+    }
+  }
+  // CP slots (child c: m_red(c) x k_c(sibling)) and x offsets of the children
+  for (int v = 0; v < n; ++v) {
+    UlvNode& N = H[v];
+    if (N.leaf) continue;
+    UlvNode &A1 = H[N.c1], &A2 = H[N.c2];
+    A1.oCP = oCP; oCP += (int64_t)(A1.mr - A1.t) * A2.kc;
+    A2.oCP = oCP; oCP += (int64_t)(A2.mr - A2.t) * A1.kc;
+    A1.pos = 0;
+    A2.pos = A1.mc - A1.t;
+  }
+  SMASH_CHECK(sm_asm <= 200 * 1024 && sm_red <= 200 * 1024, SMASH_ERR_INVALID,
+              "ULV: node blocks too large for one CTA");
+  F->smem_asm = sm_asm; F->smem_red = sm_red; F->smem_up = sm_up;
+  F->nb = ob; F->nx = ox; F->ng = og;
+  F->d.alloc(n, s);
+  h2d(F->d.p, H.data(), n, s);
+  F->D.alloc(std::max<int64_t>(oD, 1), s);
+  F->U.alloc(std::max<int64_t>(oU, 1), s);
+  F->VT.alloc(std::max<int64_t>(oVT, 1), s);
+  F->tauU.alloc(std::max<int64_t>(otU, 1), s);
+  F->tauZ.alloc(std::max<int64_t>(otZ, 1), s);
+  F->CP.alloc(std::max<int64_t>(oCP, 1), s);
+  F->piv.alloc(std::max(H[F->root].mr, 1), s);
+  F->err.alloc(2, s);
+  F->err.zero(s);
+  F->perm_row.alloc(t->nx, s);
+  F->perm_col.alloc(t->shared ? t->nx : t->ny, s);
+  {
+    std::vector<int> pr(t->nx), pc(t->shared ? t->nx : t->ny);
+    d2h(pr.data(), t->perm_row.p, pr.size(), s);
+    d2h(pc.data(), t->shared ? t->perm_row.p : t->perm_col.p, pc.size(), s);
+    sync(s);
+    std::vector<int64_t> a(pr.begin(), pr.end()), b(pc.begin(), pc.end());
+    h2d(F->perm_row.p, a.data(), a.size(), s);
+    h2d(F->perm_col.p, b.data(), b.size(), s);
+    sync(s);
+  }
+  const int dim = t->dim;
+  for (int l = L; l >= 1; --l) {
+    const int lb = t->level_begin(l), le = t->level_end(l);
+    UlvArgs A = make_args(F.get(), lb, le);
+    dispatch_kernel_dim(M->p.kernel, dim, [&]<int KER, int DIM>() {
+      auto k = k_ulv_assemble<KER, DIM>;
+      SMASH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_asm));
+      k<<<le - lb, ULV_THREADS, sm_asm, s>>>(A);
+    });
+    SMASH_CUDA(cudaGetLastError());
+    if (l > 1) {
+      SMASH_CUDA(cudaFuncSetAttribute(k_ulv_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm_red));
+      k_ulv_reduce<<<le - lb, ULV_THREADS, sm_red, s>>>(A);
+      SMASH_CUDA(cudaGetLastError());
+    }
+  }
+  k_ulv_root_lu<<<1, ULV_THREADS, 0, s>>>(make_args(F.get(), F->root, F->root + 1), F->piv.p);
+  SMASH_CUDA(cudaGetLastError());
+  check_err(F.get(), s);
+  return F.release();
+}
+
+void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s) {
+  SMASH_CHECK(R >= 1, SMASH_ERR_INVALID, "nrhs must be positive");
+  TreeImpl* t = F->M->tree;
+  if (F->ws_nrhs < R) {
+    F->wb.alloc(std::max<int64_t>(F->nb * R, 1), s);
+    F->wx.alloc(std::max<int64_t>(F->nx * R, 1), s);
+    F->wg.alloc(std::max<int64_t>(F->ng * R, 1), s);
+    F->ws_nrhs = R;
+  }
+  SolveArgs S;
+  S.b = b; S.x = x; S.perm_row = F->perm_row.p; S.perm_col = F->perm_col.p;
+  S.wb = F->wb.p; S.wx = F->wx.p; S.wg = F->wg.p; S.piv = F->piv.p; S.R = (int)R;
+  const size_t sm = F->smem_up;
+  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  for (int l = t->n_levels; l >= 1; --l) {
+    S.A = make_args(F, t->level_begin(l), t->level_end(l));
+    k_ulv_up<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+  }
+  for (int l = 2; l <= t->n_levels; ++l) {
+    S.A = make_args(F, t->level_begin(l), t->level_end(l));
+    k_ulv_down<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+  }
+  SMASH_CUDA(cudaGetLastError());
+}
+
+void ulv_free(UlvImpl* F) { delete F; }
+
+}  // namespace smash

@@ -39,6 +39,11 @@ for kind in ("hss", "h2"):
     build = smash.build_hss if kind == "hss" else smash.build_h2
     M = build(tree, spec, X, Y, params)
     out["z_" + kind] = smash.matvec_nodewise(M, q)
+    if kind == "hss":
+        F = smash.ulv_factor(M)
+        out["x_hss"] = smash.ulv_solve(F, q)
+        out["B3"] = np.random.default_rng(45).standard_normal((n, 3))
+        out["X3_hss"] = smash.ulv_solve(F, out["B3"])
     save_matrix(M, os.path.join(HERE, "container", "ref_cauchy_%s.smash" % kind))
 np.savez_compressed(os.path.join(HERE, "container", "ref_container.npz"), **out)
 print("ok", {k: v.shape for k, v in out.items()})
