@@ -763,3 +763,139 @@ def make_config_points(cfg: int, N: int = None, seed: int = None):
         X = np.vstack([circle, centres[lab] + off])
         return X, X, rng
     raise ValueError("unknown config %r" % cfg)
+
+
+# ---------------------------------------------------------------------------
+# ULV factorisation / solve (smash/apply.py:168-354) -- checker for the GPU ULV
+# ---------------------------------------------------------------------------
+
+ULV_PIVOT_RTOL = 1e-13  # apply.py:18
+
+
+def _child_rows(M: OMatrix, fac: dict, c: int) -> np.ndarray:
+    """R(c) / W(c): rows of the parent's expand() for child c's slice (hss.py:116-136)."""
+    tr = M.tree
+    p = tr.parent[c]
+    off = 0
+    for ch in tr.children[p]:
+        k = fac[ch].rank
+        if ch == c:
+            return fac[p].expand()[off:off + k]
+        off += k
+    raise KeyError(c)
+
+
+def _ulv_reduce(D, U, V):
+    """_reduce_node (apply.py:196-234): returns (record, D_red, U_red, V_red)."""
+    import scipy.linalg as sla
+    m_r, k_r = U.shape
+    m_c = D.shape[1]
+    e = m_r - k_r
+    t = min(e, m_c) if e > 0 else 0
+    rec = {"t": t, "mc_red": m_c}
+    if t == 0:
+        return rec, D, U, V
+    Q, _ = sla.qr(U, mode="full")
+    Dp = Q.T @ D
+    Bbot = Dp[m_r - t:]
+    Qz, Rt = sla.qr(Bbot.T, mode="full")
+    Ltri = Rt[:t].T
+    dmin = np.min(np.abs(np.diag(Ltri)))
+    if dmin <= ULV_PIVOT_RTOL * max(np.linalg.norm(Bbot, np.inf), 1e-300):
+        raise np.linalg.LinAlgError("singular local block")
+    Dtrans = Dp[:m_r - t] @ Qz
+    Mfull = V.T @ Qz
+    rec.update(Q=Q, Qz=Qz, Ltri=Ltri, Dcorr=Dtrans[:, :t], Mcorr=Mfull[:, :t], mc_red=m_c - t)
+    return rec, Dtrans[:, t:], (Q.T @ U)[:m_r - t], Mfull[:, t:].T
+
+
+def ulv_factor(M: OMatrix) -> dict:
+    """ulv_factor (apply.py:237-288), postorder over the HSS tree."""
+    import scipy.linalg as sla
+    if M.kind != "hss":
+        raise ValueError("ULV factorization expects an HSS matrix")
+    tr = M.tree
+    Xr, Xc = tr.points_row, tr.points_col
+    blk = lambda rows, cols: kernel_block(M.kernel, Xr[rows], Xc[cols], M.dx)  # noqa: E731
+    F = {"nodes": {}, "M": M}
+    red = {}
+    for i in range(tr.n_nodes):
+        if tr.is_leaf(i):
+            D = blk(np.arange(tr.row_start[i], tr.row_stop[i]), np.arange(tr.col_start[i], tr.col_stop[i]))
+            U = M.rowfac[i].expand() if i != tr.root else None
+            V = M.colfac[i].expand() if i != tr.root else None
+        else:
+            c1, c2 = tr.children[i]
+            r1, r2 = red.pop(c1), red.pop(c2)
+            CP1 = r1["U"] @ blk(M.skel_row[c1], M.skel_col[c2])
+            CP2 = r2["U"] @ blk(M.skel_row[c2], M.skel_col[c1])
+            F["nodes"][c1]["CP"], F["nodes"][c2]["CP"] = CP1, CP2
+            D = np.block([[r1["D"], CP1 @ r2["V"].T], [CP2 @ r1["V"].T, r2["D"]]])
+            if i != tr.root:
+                U = np.vstack([r1["U"] @ _child_rows(M, M.rowfac, c1), r2["U"] @ _child_rows(M, M.rowfac, c2)])
+                V = np.vstack([r1["V"] @ _child_rows(M, M.colfac, c1), r2["V"] @ _child_rows(M, M.colfac, c2)])
+                F["nodes"][c1]["W"] = _child_rows(M, M.colfac, c1)
+                F["nodes"][c2]["W"] = _child_rows(M, M.colfac, c2)
+        if i == tr.root:
+            F["root"] = sla.lu_factor(D) if D.shape[0] else None
+            F["root_n"] = D.shape[0]
+        else:
+            rec, Dr, Ur, Vr = _ulv_reduce(D, U, V)
+            F["nodes"][i] = rec
+            red[i] = {"D": Dr, "U": Ur, "V": Vr}
+    return F
+
+
+def ulv_solve(F: dict, b: np.ndarray) -> np.ndarray:
+    """ulv_solve (apply.py:291-348)."""
+    import scipy.linalg as sla
+    M = F["M"]
+    tr = M.tree
+    b = np.asarray(b, dtype=np.float64)
+    single = b.ndim == 1
+    B = b[:, None] if single else b
+    bt = B[tr.perm_row]
+    nc = bt.shape[1]
+    z1s, gs, bred, xroot = {}, {}, {}, None
+    for i in range(tr.n_nodes):
+        if tr.is_leaf(i):
+            bcur, gpre = bt[tr.row_start[i]:tr.row_stop[i]], None
+        else:
+            c1, c2 = tr.children[i]
+            n1, n2 = F["nodes"][c1], F["nodes"][c2]
+            b1, b2, g1, g2 = bred.pop(c1), bred.pop(c2), gs.pop(c1), gs.pop(c2)
+            bcur = np.vstack([b1 - n1["CP"] @ g2, b2 - n2["CP"] @ g1])
+            gpre = None if i == tr.root else n1["W"].T @ g1 + n2["W"].T @ g2
+        if i == tr.root:
+            xroot = sla.lu_solve(F["root"], bcur) if F["root_n"] else np.zeros((0, nc))
+            break
+        rec = F["nodes"][i]
+        if rec["t"] > 0:
+            bp = rec["Q"].T @ bcur
+            z1 = sla.solve_triangular(rec["Ltri"], bp[-rec["t"]:], lower=True)
+            z1s[i] = z1
+            bred[i] = bp[:-rec["t"]] - rec["Dcorr"] @ z1
+            gown = rec["Mcorr"] @ z1
+        else:
+            bred[i] = bcur
+            gown = np.zeros((M.colfac[i].rank, nc))
+        gs[i] = gown if gpre is None else gpre + gown
+    xt = np.zeros((tr.perm_col.size, nc))
+
+    def descend(i, xv):
+        rec = F["nodes"].get(i)
+        if rec is not None and rec["t"] > 0:
+            xv = rec["Qz"] @ np.vstack([z1s[i], xv])
+        if tr.is_leaf(i):
+            xt[tr.col_start[i]:tr.col_stop[i]] = xv
+            return
+        pos = 0
+        for c in tr.children[i]:
+            w = F["nodes"][c]["mc_red"]
+            descend(c, xv[pos:pos + w])
+            pos += w
+
+    descend(tr.root, xroot)
+    x = np.empty_like(xt)
+    x[tr.perm_col] = xt
+    return x[:, 0] if single else x

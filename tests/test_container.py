@@ -161,3 +161,20 @@ def test_load_rejects_tampered_tree(sg, tmp_path):
     bad.write_bytes(c._MAGIC + json.dumps(header).encode() + b"\0" + head[cut + 1:])
     with pytest.raises(ValueError):
         sg.load_matrix(str(bad))
+
+
+def test_oracle_ulv_matches_reference_ulv():
+    """The oracle's ULV restatement (checker for tests/test_ulv.py and bench numbers)
+    reproduces the reference's ulv_solve on the golden geometry."""
+    from oracle import smash_oracle as orc
+    g = np.load(os.path.join(GOLDEN, "container", "ref_container.npz"))
+    n = 512
+    x = (np.arange(n) / n)[:, None]
+    y = ((np.arange(n) + 0.5) / n)[:, None]
+    tree = orc.build_tree(x, y, nu0=32, mode="binary")
+    M = orc.build_hss(tree, "cauchy", 12, 0.6, 1e-11)
+    F = orc.ulv_factor(M)
+    xs = orc.ulv_solve(F, g["q"])
+    assert np.linalg.norm(xs - g["x_hss"]) <= 1e-9 * np.linalg.norm(g["x_hss"])
+    X3 = orc.ulv_solve(F, g["B3"])
+    assert np.linalg.norm(X3 - g["X3_hss"]) <= 1e-9 * np.linalg.norm(g["X3_hss"])
