@@ -451,7 +451,12 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
   if ((full <= SM_BYTES / 2 - CTA_RESERVED || cnt <= nsm) && (int)full <= smem_limit) {
     // every node fits (>= 2 CTAs per SM, or a level with at most one node per SM)
     A.panel_cap = (int64_t)A.nmax * A.mmax;
-    int per_sm = (int)std::min<size_t>(8, std::max<size_t>(1, SM_BYTES / (full + CTA_RESERVED)));
+    // narrow panels (<= 128 columns): 128-thread CTAs, twice as many nodes in flight
+    // for the same warps per SM (64 registers per thread)
+    static const int narrow = getenv("SMASH_COMPRESS_NARROW") ? atoi(getenv("SMASH_COMPRESS_NARROW")) : 128;
+    A.threads = A.nmax <= narrow ? 128 : COMPRESS_THREADS;
+    const int cap = A.threads == 128 ? 8 : 4;
+    int per_sm = (int)std::min<size_t>(cap, std::max<size_t>(1, SM_BYTES / (full + CTA_RESERVED)));
     *grid = std::min(cnt, nsm * per_sm);
     return full;
   }
@@ -496,7 +501,7 @@ void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream
 #endif
   auto go = [&](auto kern) {
     SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, COMPRESS_THREADS, smem, s>>>(a);
+    kern<<<grid, a.threads, smem, s>>>(a);
   };
   const int mode = a.panel_cap >= (int64_t)a.nmax * a.mmax ? 1 : a.panel_cap == 0 ? 0 : 2;
   auto by_dim = [&](auto m) {

@@ -65,7 +65,8 @@ struct CompressArgs {
   const double* Cexp = nullptr;
   int C_cols = 0;
   unsigned long long* prof = nullptr;
-  int* next = nullptr;  // dynamic node counter (launch_compress)  // SMASH_COMPRESS_PROF builds: clock64 per phase
+  int* next = nullptr;  // dynamic node counter (launch_compress)
+  int threads = COMPRESS_THREADS;  // CTA size (plan_compress_launch)  // SMASH_COMPRESS_PROF builds: clock64 per phase
 };
 
 size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
