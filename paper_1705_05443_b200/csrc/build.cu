@@ -8,6 +8,8 @@
 // sets are contiguous slices.  When row and column points are shared the
 // column factors alias the row factors (bitwise identical in the reference,
 // SURVEY.md 7 / probe p12).
+#include <thread>
+#include <exception>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -501,6 +503,51 @@ struct SideBuild {
   }
 };
 
+// get_pairs on its own host thread and stream (see matrix_build)
+struct PairsJob {
+  std::thread th;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev = nullptr;
+  PairLists* out = nullptr;
+  std::exception_ptr err;
+  void start(TreeImpl* t, double tau, int structure, cudaStream_t s) {
+    int dev = 0, lo = 0, hi = 0;
+    SMASH_CUDA(cudaGetDevice(&dev));
+    SMASH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SMASH_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));
+    SMASH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SMASH_CUDA(cudaEventRecord(ev, s));  // the tree is complete on s
+    SMASH_CUDA(cudaStreamWaitEvent(s2, ev, 0));
+    th = std::thread([this, t, tau, structure, dev] {
+      try {
+        SMASH_CUDA(cudaSetDevice(dev));
+        out = get_pairs(t, tau, structure, s2);
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+  }
+  PairLists* join(cudaStream_t s) {
+    th.join();
+    if (!err) {
+      out->rehome(s);  // released on the owner's stream later
+      SMASH_CUDA(cudaEventRecord(ev, s2));
+      SMASH_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    }
+    cleanup();
+    if (err) std::rethrow_exception(err);
+    return out;
+  }
+  void cleanup() {
+    if (s2) { cudaStreamSynchronize(s2); cudaStreamDestroy(s2); s2 = nullptr; }
+    if (ev) { cudaEventDestroy(ev); ev = nullptr; }
+  }
+  ~PairsJob() {
+    if (th.joinable()) th.join();
+    cleanup();
+  }
+};
+
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s) {
   SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
               "unknown kernel kind");
@@ -516,7 +563,13 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
   std::unique_ptr<MatrixImpl> M(new MatrixImpl());
   M->tree = t;
   M->p = p;
-  M->pl = get_pairs(t, p.tau, p.structure, s);
+  const bool hss_build = p.structure == SMASH_STRUCT_HSS;
+  // H2: the pair lists (a host-synchronising frontier sweep, independent of the
+  // compression) are built by a second host thread on a high-priority stream
+  // while this thread enqueues the compression sweep; HSS needs them first (N_i).
+  PairsJob pj;
+  if (hss_build) M->pl = get_pairs(t, p.tau, p.structure, s);
+  else pj.start(t, p.tau, p.structure, s);
   HostTables H = make_tables(p.r, t->dim);
   DevTables D;
   D.upload(H, s);
@@ -545,6 +598,7 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
     rowb.level(l, near);
     if (colb) colb->level(l, near);
   }
+  if (!hss_build) M->pl = pj.join(s);
   rowb.finish();
   if (colb) colb->finish();
   sync(s);

@@ -22,6 +22,10 @@ struct PairLists {
   DBuf<int> L_i, L_j, Lm_i, Lm_j;
   DBuf<int> L_ptr, Lm_ptr;  // CSR by target BFS id, size n_nodes + 1
   int64_t nL = 0, nLm = 0;
+  // buffers built on an auxiliary stream are released on the owner's stream
+  void rehome(cudaStream_t s) {
+    L_i.st = s; L_j.st = s; Lm_i.st = s; Lm_j.st = s; L_ptr.st = s; Lm_ptr.st = s;
+  }
 };
 
 struct NearSets {
