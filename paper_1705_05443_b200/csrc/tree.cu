@@ -279,22 +279,22 @@ __global__ void k_leaf_starts(int n, const int* nchild, const int* item_a, int* 
 }
 
 __global__ void k_perm_keys(int64_t ntot, int64_t nx, const int* sorted_item, const int* xpref,
-                            const int* lord, uint64_t* kx, uint64_t* ky) {
+                            const int* lord, int ibits, uint64_t* kx, uint64_t* ky) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ntot) return;
   int it = sorted_item[i];
-  uint64_t hi = (uint64_t)lord[i] << 32;
+  uint64_t hi = (uint64_t)lord[i] << ibits;
   if (it < nx)
     kx[xpref[i]] = hi | (uint64_t)it;
   else
     ky[i - xpref[i]] = hi | (uint64_t)(it - nx);
 }
 
-__global__ void k_perm_gather(int64_t n, int dim, const uint64_t* k, const double* P, int* perm,
-                              double* pts_soa) {
+__global__ void k_perm_gather(int64_t n, int dim, const uint64_t* k, int ibits, const double* P,
+                              int* perm, double* pts_soa) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
-  int idx = (int)(k[p] & 0xffffffffULL);
+  int idx = (int)(k[p] & ((1ULL << ibits) - 1ULL));
   perm[p] = idx;
   for (int a = 0; a < dim; ++a) pts_soa[(size_t)a * n + p] = P[(size_t)idx * dim + a];
 }
@@ -302,6 +302,14 @@ __global__ void k_perm_gather(int64_t n, int dim, const uint64_t* k, const doubl
 __global__ void k_iota(int* x, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) x[i] = (int)i;
+}
+
+// any neighbours (in high-word order) with equal high but different low words?
+__global__ void k_hi_ties(const uint64_t* hi_sorted, const int* item, const uint64_t* lo, int64_t n,
+                          int* flag) {
+  for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (hi_sorted[i] == hi_sorted[i - 1] && lo[item[i]] != lo[item[i - 1]]) *flag = 1;
 }
 
 __global__ void k_gather_u64(const uint64_t* src, const int* idx, uint64_t* dst, int64_t n) {
@@ -376,18 +384,44 @@ TreeImpl* tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, i
   }
   k_iota<<<cdiv(ntot, 256), 256, 0, s>>>(item.p, ntot);
   DBuf<char> tmp;
-  // pass 1: by low word
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, klo.p, klo2.p, item.p, item2.p, (int)ntot, 0, 64, s);
-  }, tmp, s);
-  // pass 2: by high word (stable)
-  k_gather_u64<<<cdiv(ntot, 256), 256, 0, s>>>(khi.p, item2.p, khi2.p, ntot);
-  cub_call([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, khi2.p, khi.p, item2.p, item.p, (int)ntot, 0, 64, s);
-  }, tmp, s);
-  // (SortPairs leaves its inputs intact: klo still holds the original low words)
-  k_gather_u64<<<cdiv(ntot, 256), 256, 0, s>>>(klo.p, item.p, klo2.p, ntot);
-  std::swap(klo, klo2);
+  // Stable sort by the 128-bit key.  First by the high word alone: unless two
+  // points agree on the whole high word (the first 64 bisection bits) but not on
+  // the low word, that order is already the full-key order (ties keep the
+  // original index order either way), and half the radix passes are saved.
+  bool need_low = false;
+  {
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, khi.p, khi2.p, item.p, item2.p, (int)ntot, 0, 64, s);
+    }, tmp, s);
+    DBuf<int> tie;
+    tie.alloc(1, s);
+    tie.zero(s);
+    k_hi_ties<<<std::min<int64_t>(cdiv(ntot, 256), 4096), 256, 0, s>>>(khi2.p, item2.p, klo.p, ntot,
+                                                                       tie.p);
+    int h = 0;
+    d2h(&h, tie.p, 1, s);
+    sync(s);
+    need_low = h != 0;
+  }
+  if (!need_low) {
+    std::swap(khi, khi2);
+    std::swap(item, item2);
+    k_gather_u64<<<cdiv(ntot, 256), 256, 0, s>>>(klo.p, item.p, klo2.p, ntot);
+    std::swap(klo, klo2);
+  } else {
+    // LSD over the two words: low word, then high word (stable)
+    k_iota<<<cdiv(ntot, 256), 256, 0, s>>>(item.p, ntot);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, klo.p, klo2.p, item.p, item2.p, (int)ntot, 0, 64, s);
+    }, tmp, s);
+    k_gather_u64<<<cdiv(ntot, 256), 256, 0, s>>>(khi.p, item2.p, khi2.p, ntot);
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, khi2.p, khi.p, item2.p, item.p, (int)ntot, 0, 64, s);
+    }, tmp, s);
+    // (SortPairs leaves its inputs intact: klo still holds the original low words)
+    k_gather_u64<<<cdiv(ntot, 256), 256, 0, s>>>(klo.p, item.p, klo2.p, ntot);
+    std::swap(klo, klo2);
+  }
   khi2.release(); klo2.release(); item2.release();
 
   // ---- x-item prefix counts over sorted positions
@@ -482,21 +516,25 @@ TreeImpl* tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, i
   DBuf<uint64_t> kx, ky, kx2, ky2;
   kx.alloc(nx, s); kx2.alloc(nx, s);
   if (nyy) { ky.alloc(nyy, s); ky2.alloc(nyy, s); }
-  k_perm_keys<<<cdiv(ntot, 256), 256, 0, s>>>(ntot, nx, item.p, xpref.p, lord.p, kx.p, ky.p);
-  int end_bit = 64;
+  // (leaf order, original index) keys with only the bits they need: leaf ranks
+  // are < n_nodes, indices < max(nx, ny)
+  auto nbits = [](int64_t v) { int b = 1; while ((1LL << b) <= v) ++b; return b; };
+  const int ibits = nbits(std::max<int64_t>(nx, ny));
+  const int end_bit = std::min(64, ibits + nbits(n + 1));
+  k_perm_keys<<<cdiv(ntot, 256), 256, 0, s>>>(ntot, nx, item.p, xpref.p, lord.p, ibits, kx.p, ky.p);
   cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortKeys(t, b, kx.p, kx2.p, (int)nx, 0, end_bit, s);
   }, tmp, s);
   T->perm_row.alloc(nx, s);
   T->pts_row.alloc((size_t)nx * dim, s);
-  k_perm_gather<<<cdiv(nx, 256), 256, 0, s>>>(nx, dim, kx2.p, X, T->perm_row.p, T->pts_row.p);
+  k_perm_gather<<<cdiv(nx, 256), 256, 0, s>>>(nx, dim, kx2.p, ibits, X, T->perm_row.p, T->pts_row.p);
   if (nyy) {
     cub_call([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, ky.p, ky2.p, (int)nyy, 0, end_bit, s);
     }, tmp, s);
     T->perm_col.alloc(nyy, s);
     T->pts_col.alloc((size_t)nyy * dim, s);
-    k_perm_gather<<<cdiv(nyy, 256), 256, 0, s>>>(nyy, dim, ky2.p, Y, T->perm_col.p, T->pts_col.p);
+    k_perm_gather<<<cdiv(nyy, 256), 256, 0, s>>>(nyy, dim, ky2.p, ibits, Y, T->perm_col.p, T->pts_col.p);
   }
   // leaf count
   {

@@ -226,3 +226,20 @@ def test_sharded_stages_single_process(smash_gpu, golden, name, world):
     assert rel <= 1e-12, rel
     _MATS.pop(name, None)
     _TREES.pop(name, None)
+
+
+@pytest.mark.parametrize("mode", ["2d", "binary"])
+def test_tree_bitexact_sub_2e21_cluster(smash_gpu, mode):
+    """A 3-D cluster 1e-9 wide needs bisection digits past the first 21 per axis (the
+    high key word), so the device tree sort must order by the low key word too; the
+    tree must still equal the oracle's (the reference recursion, cluster.py:263-353)."""
+    from oracle import smash_oracle as orc
+    rng = np.random.default_rng(21)
+    X = np.vstack([rng.random((300, 3)), 0.37 + 1e-9 * rng.random((200, 3))])
+    ot = orc.build_tree(X, nu0=16, mode=mode)
+    tree = smash_gpu.build_tree(smash_gpu.PointSet(X), nu0=16, mode=mode)
+    A = tree.arrays()
+    assert np.array_equal(A["perm_row"], ot.perm_row)
+    assert np.array_equal(A["level"], ot.level) and np.array_equal(A["parent"], ot.parent)
+    assert np.array_equal(A["lo"], ot.lo) and np.array_equal(A["hi"], ot.hi)
+    assert np.array_equal(A["row_start"], ot.row_start) and np.array_equal(A["row_stop"], ot.row_stop)
