@@ -9,6 +9,8 @@
 // column factors alias the row factors (bitwise identical in the reference,
 // SURVEY.md 7 / probe p12).
 #include <thread>
+#include <chrono>
+#include <cstdio>
 #include <exception>
 #include <cub/cub.cuh>
 
@@ -410,6 +412,12 @@ struct SideBuild {
     const int dim = t->dim, r = M->p.r;
     const bool hss = M->p.structure == SMASH_STRUCT_HSS;
     const int lb = t->level_begin(l), le = t->level_end(l), cnt = le - lb;
+    static const bool timing = getenv("SMASH_BUILD_TIMING") != nullptr;
+    auto now = [&] {
+      if (timing) sync(s);
+      return std::chrono::steady_clock::now();
+    };
+    auto t0 = now();
     DBuf<int64_t> ibc, gc, ibo, go;
     ibc.alloc(cnt + 1, s); gc.alloc(cnt + 1, s); ibo.alloc(cnt + 1, s); go.alloc(cnt + 1, s);
     SMASH_CUDA(cudaMemsetAsync(ibc.p + cnt, 0, 8, s));
@@ -439,7 +447,9 @@ struct SideBuild {
 
     // ---- HSS nearfield SVD (hss.py:279-299)
     int max_keep = 0;
+    auto t1 = now();
     if (hss) max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s);
+    auto t2 = now();
 
     DBuf<int> tmp_lab;
     DBuf<double> tmp_pts;
@@ -462,6 +472,12 @@ struct SideBuild {
     A.nmax = std::max(nmax, 1);
     A.mmax = r + max_keep;
     launch_level(A, cnt);
+    auto t3 = now();
+    if (timing)
+      fprintf(stderr, "level %d side %d cnt %d: sizes %.3f ms svd %.3f ms compress %.3f ms\n", l, side,
+              cnt, std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(t2 - t1).count(),
+              std::chrono::duration<double, std::milli>(t3 - t2).count());
 
     // ---- compact this level's skeletons
     DBuf<int> rc, ro;
