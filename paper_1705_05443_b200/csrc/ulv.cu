@@ -21,6 +21,7 @@
 // reflector application is one warp per vector with a shuffle-reduced dot.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -123,6 +124,8 @@ struct UlvArgs {
   int64_t nrow, ncol;
   double dx;
   int* err;  // [0] = flag, [1] = postorder node id
+  int vs_cap;         // reflector buffer (doubles) at the start of k_ulv_reduce's shared memory
+  int64_t stage_cap;  // nodes with |D| + |U| + |V^T| <= stage_cap are reduced in shared memory
 };
 
 __device__ __forceinline__ void flag_singular(const UlvArgs& A, int post) {
@@ -280,10 +283,24 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
   const UlvNode& N = A.nd[v];
   if (N.t == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
-  double* D = A.D + N.oD;
-  double* U = A.U + N.oU;
-  double* VT = A.VT + N.oVT;
   const int mr = N.mr, mc = N.mc, kr = N.kr, kc = N.kc, t = N.t;
+  // Stage D, U and V^T in shared memory when they fit (all reflector traffic then
+  // stays on chip; the row-major layouts and leading dimensions are unchanged).
+  const int64_t nD = (int64_t)mr * mc, nU = (int64_t)mr * kr, nV = (int64_t)kc * mc;
+  const bool stage = nD + nU + nV <= A.stage_cap;
+  double* Dg = A.D + N.oD;
+  double* Ug = A.U + N.oU;
+  double* Vg = A.VT + N.oVT;
+  double* sb = vs + A.vs_cap;
+  double* D = stage ? sb : Dg;
+  double* U = stage ? sb + nD : Ug;
+  double* VT = stage ? sb + nD + nU : Vg;
+  if (stage) {
+    for (int64_t e = tid; e < nD; e += blockDim.x) D[e] = Dg[e];
+    for (int64_t e = tid; e < nU; e += blockDim.x) U[e] = Ug[e];
+    for (int64_t e = tid; e < nV; e += blockDim.x) VT[e] = Vg[e];
+    __syncthreads();
+  }
   // 1. Householder QR of U, applied to D from the left (Q^T D)
   for (int i = 0; i < kr; ++i) {
     if (wid == 0) {
@@ -342,6 +359,12 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     double dmin = INFINITY;
     for (int i = 0; i < t; ++i) dmin = fmin(dmin, fabs(D[(int64_t)(r0 + i) * mc + i]));
     if (dmin <= PIVOT_RTOL * fmax(s_norm, 1e-300)) flag_singular(A, N.post);
+  }
+  if (stage) {
+    __syncthreads();
+    for (int64_t e = tid; e < nD; e += blockDim.x) Dg[e] = D[e];
+    for (int64_t e = tid; e < nU; e += blockDim.x) Ug[e] = U[e];
+    for (int64_t e = tid; e < nV; e += blockDim.x) Vg[e] = VT[e];
   }
 }
 
@@ -594,6 +617,7 @@ struct UlvImpl {
   DBuf<int64_t> perm_row, perm_col;
   int root = 0;
   int64_t nb = 0, nx = 0, ng = 0;
+  int vs_cap = 1;
   size_t smem_asm = 0, smem_red = 0, smem_up = 0;
   DBuf<double> wb, wx, wg;
   int64_t ws_nrhs = 0;
@@ -616,6 +640,8 @@ UlvArgs make_args(UlvImpl* F, int lb, int le) {
   A.nrow = t->nx; A.ncol = t->shared ? t->nx : t->ny;
   A.dx = M->p.dx;
   A.err = F->err.p;
+  A.vs_cap = F->vs_cap;
+  A.stage_cap = 0;
   return A;
 }
 
@@ -653,6 +679,8 @@ UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
   H.assign(n, UlvNode{});
   int64_t oD = 0, oU = 0, oVT = 0, otU = 0, otZ = 0, oCP = 0, ob = 0, ox = 0, og = 0;
   size_t sm_asm = 16, sm_red = 16, sm_up = 16;
+  int vs_cap = 1;
+  std::vector<int64_t> lvl_need(L + 2, 0);  // per level: largest staged reduction (doubles)
   for (int l = L; l >= 1; --l) {
     for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
       UlvNode& N = H[v];
@@ -694,6 +722,10 @@ UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
       N.ox = ox; ox += N.mc;
       N.og = og; og += N.kc;
       sm_red = std::max(sm_red, 8 * (size_t)std::max(N.mr, N.mc) + 16);
+      vs_cap = std::max(vs_cap, std::max(N.mr, N.mc));
+      if (!root && N.t > 0)
+        lvl_need[l] = std::max<int64_t>(lvl_need[l], (int64_t)N.mr * N.mc + (int64_t)N.mr * N.kr +
+                                                         (int64_t)N.kc * N.mc);
       sm_up = std::max(sm_up, 8 * (size_t)std::max(N.mr, N.mc) + 16);
     }
   }
@@ -709,6 +741,13 @@ UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
   }
   SMASH_CHECK(sm_asm <= 200 * 1024 && sm_red <= 200 * 1024, SMASH_ERR_INVALID,
               "ULV: node blocks too large for one CTA");
+  // reduce: reflector buffer + staging area, capped at 48 KB so that >= 4 CTAs
+  // share an SM (measured: cfg 1's nodes gain 1.5x in shared memory, while
+  // cfg 4's 128 x 128 leaves run faster from L2 with 8 CTAs per SM than
+  // staged with 1 CTA per SM)
+  vs_cap = (vs_cap + 1) & ~1;
+  F->vs_cap = vs_cap;
+  sm_red = 8 * (size_t)vs_cap + 64;  // unstaged levels
   F->smem_asm = sm_asm; F->smem_red = sm_red; F->smem_up = sm_up;
   F->nb = ob; F->nx = ox; F->ng = og;
   F->d.alloc(n, s);
@@ -745,9 +784,14 @@ UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
     });
     SMASH_CUDA(cudaGetLastError());
     if (l > 1) {
+      // a level is staged in shared memory when its largest node fits 48 KB (>= 4 CTAs/SM)
+      static const bool no_stage = getenv("SMASH_ULV_NOSTAGE") != nullptr;
+      const int64_t cap = (48 * 1024 - 8 * (int64_t)F->vs_cap - 64) / 8;
+      A.stage_cap = (!no_stage && lvl_need[l] <= cap) ? lvl_need[l] : 0;
+      const size_t sm = sm_red + 8 * (size_t)A.stage_cap;
       SMASH_CUDA(cudaFuncSetAttribute(k_ulv_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm_red));
-      k_ulv_reduce<<<le - lb, ULV_THREADS, sm_red, s>>>(A);
+                                      (int)std::max<size_t>(sm, 48 * 1024)));
+      k_ulv_reduce<<<le - lb, ULV_THREADS, sm, s>>>(A);
       SMASH_CUDA(cudaGetLastError());
     }
   }
