@@ -546,14 +546,21 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_up(SolveArgs S) {
     __syncthreads();
   }
   // z1 = L^-1 bp[r0:], kept in x[0:t) for the downward pass
+  // (right-looking forward substitution, one warp per right-hand side: lane 0
+  // finishes z_i, the warp subtracts its column of L from the rows below)
   double* z = S.wx + N.ox * R;
   for (int c = wid; c < R; c += NW) {
-    if (lane == 0)
-      for (int i = 0; i < t; ++i) {
-        double s = b[(int64_t)(r0 + i) * R + c];
-        for (int j = 0; j < i; ++j) s -= D[(int64_t)(r0 + i) * mc + j] * z[(int64_t)j * R + c];
-        z[(int64_t)i * R + c] = s / D[(int64_t)(r0 + i) * mc + i];
+    for (int i = 0; i < t; ++i) {
+      double zi = 0.0;
+      if (lane == 0) {
+        zi = b[(int64_t)(r0 + i) * R + c] / D[(int64_t)(r0 + i) * mc + i];
+        z[(int64_t)i * R + c] = zi;
       }
+      zi = __shfl_sync(0xffffffffu, zi, 0);
+      for (int j = i + 1 + lane; j < t; j += 32)
+        b[(int64_t)(r0 + j) * R + c] -= D[(int64_t)(r0 + j) * mc + i] * zi;
+      __syncwarp();
+    }
   }
   __syncthreads();
   // bred = bp[:r0] - Dcorr z1 ; g += Mcorr z1
@@ -816,13 +823,35 @@ void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s
   const size_t sm = F->smem_up;
   SMASH_CUDA(cudaFuncSetAttribute(k_ulv_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   SMASH_CUDA(cudaFuncSetAttribute(k_ulv_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  static const bool timing = getenv("SMASH_ULV_TIMING") != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+  }
+  auto tick = [&](const char* what, int l) {
+    if (!timing) return;
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fprintf(stderr, "ulv_solve %s level %d: %.3f ms\n", what, l, ms);
+    cudaEventRecord(e0, s);
+  };
+  if (timing) cudaEventRecord(e0, s);
   for (int l = t->n_levels; l >= 1; --l) {
     S.A = make_args(F, t->level_begin(l), t->level_end(l));
     k_ulv_up<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+    tick("up", l);
   }
   for (int l = 2; l <= t->n_levels; ++l) {
     S.A = make_args(F, t->level_begin(l), t->level_end(l));
     k_ulv_down<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+    tick("down", l);
+  }
+  if (timing) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   }
   SMASH_CUDA(cudaGetLastError());
 }
