@@ -454,7 +454,7 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
     // narrow panels (<= 128 columns): 128-thread CTAs, twice as many nodes in flight
     // for the same warps per SM (64 registers per thread)
     static const int narrow = getenv("SMASH_COMPRESS_NARROW") ? atoi(getenv("SMASH_COMPRESS_NARROW")) : 128;
-    static const int tiny = getenv("SMASH_COMPRESS_TINY") ? atoi(getenv("SMASH_COMPRESS_TINY")) : 0;
+    static const int tiny = getenv("SMASH_COMPRESS_TINY") ? atoi(getenv("SMASH_COMPRESS_TINY")) : 64;
     static const int tiny_t = getenv("SMASH_COMPRESS_TINY_T") ? atoi(getenv("SMASH_COMPRESS_TINY_T")) : 32;
     A.threads = A.nmax <= tiny ? tiny_t : A.nmax <= narrow ? 128 : COMPRESS_THREADS;
     const int cap = std::min(32, 1024 / A.threads);  // 64 registers per thread: <= 1024 threads per SM
