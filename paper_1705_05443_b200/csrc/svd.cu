@@ -563,7 +563,8 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   int dev = 0, nsm = 0;
   SMASH_CUDA(cudaGetDevice(&dev));
   SMASH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::min(cnt, nsm * 2);
+  static const int svd_per_sm = getenv("SMASH_SVD_PER_SM") ? atoi(getenv("SMASH_SVD_PER_SM")) : 2;
+  const int grid = std::min(cnt, nsm * svd_per_sm);
   DBuf<double> gws;
   gws.alloc((size_t)grid * A.gws_stride, s);
   A.gws = gws.p;
