@@ -274,7 +274,9 @@ struct SideBuild {
     F->skel.alloc(skel_cap, s);
     F->skel_pts.alloc((size_t)skel_cap * dim, s);
     F->perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
-    F->G.alloc(std::max<int64_t>(Pn * 8, 1024), s);
+    // HSS (level-synchronous path): room for ~ (n_leaf - k) k G entries per leaf point
+    // up front, so the leaf level does not reallocate + copy (grow() stays the fallback)
+    F->G.alloc(std::max<int64_t>(Pn * (hss ? 32 : 8), 1024), s);
     F->level_skel_begin.assign(t->n_levels + 2, 0);
     err.alloc(1, s); err.zero(s);
     swaps.alloc(1, s); swaps.zero(s);
