@@ -173,7 +173,13 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
     if (nr > bv) { bv = nr; bi = j; }
   }
   for (int i = 0; i < kmax; ++i) {
+#ifdef SMASH_COMPRESS_PROF
+    long long q0 = clock64();
+#endif
     const int pvt = block_argmax_1bar(bv, bi, S);
+#ifdef SMASH_COMPRESS_PROF
+    long long q1 = clock64();
+#endif
     if (tid < 32) {
       if (pvt != i) {
         for (int row = tid; row < m; row += 32) {
@@ -191,17 +197,22 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
       householder(P, ld, m, i, S);
     }
     __syncthreads();
+#ifdef SMASH_COMPRESS_PROF
+    long long q2 = clock64();
+#endif
     const double tau = S.misc[0];
     bv = -1.0;
     bi = 0x7fffffff;
     for (int j = i + 1 + tid; j < n; j += NT) {
-      if (tau != 0.0) apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
+      // the norm-downdate divisions do not depend on the reflector: issue them
+      // first so their latency hides under the dot-product chain
       double v1 = S.vn1[j];
+      const double rv1 = 1.0 / v1;
+      const double q2 = v1 / S.vn2[j];
+      if (tau != 0.0) apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
       if (v1 != 0.0) {
-        const double rv1 = 1.0 / v1;
         double q = fabs(P[i * ld + j]) * rv1;
         double temp = fmax(1.0 - q * q, 0.0);
-        double q2 = v1 / S.vn2[j];
         double temp2 = temp * (q2 * q2);
         if (temp2 <= TOL3Z) {
           double nv = i + 1 < m ? __dsqrt_rn(col_sumsq<CH>(P, ld, j, i + 1, m)) : 0.0;
@@ -215,6 +226,15 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
       }
       if (v1 > bv) { bv = v1; bi = j; }
     }
+#ifdef SMASH_COMPRESS_PROF
+    if (tid == 0) {
+      long long q3 = clock64();
+      atomicAdd(A.prof + 3, (unsigned long long)(q1 - q0));
+      atomicAdd(A.prof + 4, (unsigned long long)(q2 - q1));
+      atomicAdd(A.prof + 5, (unsigned long long)(q3 - q2));
+      atomicAdd(A.prof + 6, 1ULL);
+    }
+#endif
   }
   __syncthreads();
   PROF_MARK(1)
@@ -483,7 +503,7 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
 }
 
 #ifdef SMASH_COMPRESS_PROF
-__device__ unsigned long long g_compress_prof[4];
+__device__ unsigned long long g_compress_prof[8];
 #endif
 __device__ int g_compress_next;  // dynamic node counter (reset before every launch)
 
@@ -517,11 +537,14 @@ void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream
   else by_dim(std::integral_constant<int, 2>{});
   SMASH_CUDA(cudaGetLastError());
 #ifdef SMASH_COMPRESS_PROF
-  unsigned long long h[4];
+  unsigned long long h[8];
   SMASH_CUDA(cudaMemcpyAsync(h, pp, sizeof(h), cudaMemcpyDeviceToHost, s));
   SMASH_CUDA(cudaStreamSynchronize(s));
-  fprintf(stderr, "compress nodes %d mode %d grid %d: Mcycles panel %.2f qr %.2f rank+solve+swaps %.2f\n",
-          a.le - a.lb, mode, grid, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6);
+  fprintf(stderr, "compress nodes %d mode %d grid %d: Mcycles panel %.2f qr %.2f rank+solve+swaps %.2f"
+          " | per step: argmax+wait %.0f, swap+reflector %.0f, update+downdate %.0f cycles\n",
+          a.le - a.lb, mode, grid, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6,
+          h[6] ? (double)h[3] / h[6] : 0.0, h[6] ? (double)h[4] / h[6] : 0.0,
+          h[6] ? (double)h[5] / h[6] : 0.0);
 #endif
 }
 
