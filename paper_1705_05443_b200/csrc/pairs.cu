@@ -95,14 +95,16 @@ __global__ void k_emit(int64_t n, const int* fi, const int* fj, const int* cls,
   }
 }
 
-__global__ void k_pair_keys(int64_t n, const int* a, const int* b, uint64_t* k) {
+// (target, source) keys packed with only the bits node ids need (nb = bits(n_nodes)),
+// so the radix sort runs ceil(2 nb / 8) passes instead of 8
+__global__ void k_pair_keys(int64_t n, const int* a, const int* b, int nb, uint64_t* k) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < n) k[t] = ((uint64_t)(uint32_t)a[t] << 32) | (uint32_t)b[t];
+  if (t < n) k[t] = ((uint64_t)(uint32_t)a[t] << nb) | (uint32_t)b[t];
 }
 
-__global__ void k_pair_split(int64_t n, const uint64_t* k, int* a, int* b) {
+__global__ void k_pair_split(int64_t n, const uint64_t* k, int nb, int* a, int* b) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t < n) { a[t] = (int)(k[t] >> 32); b[t] = (int)(k[t] & 0xffffffffULL); }
+  if (t < n) { a[t] = (int)(k[t] >> nb); b[t] = (int)(k[t] & ((1ULL << nb) - 1ULL)); }
 }
 
 // CSR pointer by target: ptr[v] = first pair with target >= v
@@ -148,15 +150,18 @@ __global__ void k_hss_counts(int n, const int* nchild, int64_t* cL, int64_t* cLm
 // ordering but kept in BFS ids for the matvec.  BFS order within a level equals
 // postorder order, but across levels it does not; the CSR is by BFS target and
 // the source order inside a row is irrelevant for the sums.
-void sort_pairs(int64_t n, DBuf<int>& a, DBuf<int>& b, DBuf<char>& tmp, cudaStream_t s) {
+void sort_pairs(int64_t n, int n_nodes, DBuf<int>& a, DBuf<int>& b, DBuf<char>& tmp,
+                cudaStream_t s) {
   if (!n) return;
+  int nb = 1;
+  while ((1LL << nb) <= (int64_t)n_nodes) ++nb;
   DBuf<uint64_t> k, k2;
   k.alloc(n, s); k2.alloc(n, s);
-  k_pair_keys<<<cdiv(n, 256), 256, 0, s>>>(n, a.p, b.p, k.p);
+  k_pair_keys<<<cdiv(n, 256), 256, 0, s>>>(n, a.p, b.p, nb, k.p);
   cub_call([&](void* t, size_t& bytes) {
-    return cub::DeviceRadixSort::SortKeys(t, bytes, k.p, k2.p, (int)n, 0, 64, s);
+    return cub::DeviceRadixSort::SortKeys(t, bytes, k.p, k2.p, (int)n, 0, 2 * nb, s);
   }, tmp, s);
-  k_pair_split<<<cdiv(n, 256), 256, 0, s>>>(n, k2.p, a.p, b.p);
+  k_pair_split<<<cdiv(n, 256), 256, 0, s>>>(n, k2.p, nb, a.p, b.p);
 }
 
 }  // namespace
@@ -256,8 +261,8 @@ PairLists* get_pairs(TreeImpl* t, double tau, int structure, cudaStream_t s) {
     P->L_i = std::move(Li); P->L_j = std::move(Lj);
     P->Lm_i = std::move(Lmi); P->Lm_j = std::move(Lmj);
   }
-  sort_pairs(P->nL, P->L_i, P->L_j, tmp, s);
-  sort_pairs(P->nLm, P->Lm_i, P->Lm_j, tmp, s);
+  sort_pairs(P->nL, n, P->L_i, P->L_j, tmp, s);
+  sort_pairs(P->nLm, n, P->Lm_i, P->Lm_j, tmp, s);
   P->L_ptr.alloc(n + 1, s);
   P->Lm_ptr.alloc(n + 1, s);
   k_csr_ptr<<<cdiv(n + 1, 128), 128, 0, s>>>(n, P->nL, P->L_i.p, P->L_ptr.p);
