@@ -158,9 +158,17 @@ struct ExpandArgs {
   int* err;
 };
 
-__global__ void k_expand(int lb, int le, ExpandArgs A) {
-  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= le) return;
+// Level bounds come from the device (dlev[l] = first node of level l+1 in 0-based
+// level index), so several levels are enqueued between host round trips; threads
+// past the level's end clear their nkids slot (the scan runs over a fixed size).
+__global__ void k_expand(const int* dlev, int l, int nk_size, ExpandArgs A) {
+  const int lb = dlev[l], le = dlev[l + 1];
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t0 >= le - lb) {
+    if (t0 < nk_size) A.nkids[t0] = 0;
+    return;
+  }
+  int v = lb + t0;
   int a = A.item_a[v], b = A.item_b[v], t = A.tdep[v];
   int cx = A.xpref[b] - A.xpref[a];
   int cy = A.shared ? cx : (b - a) - cx;
@@ -208,11 +216,19 @@ __global__ void k_expand(int lb, int le, ExpandArgs A) {
   A.nkids[v - lb] = nk;
 }
 
-__global__ void k_link(int lb, int le, const int* nkids, const int* off, const int* bounds,
-                       const int* tsplit, int* child_first, int* nchild, int* item_a, int* item_b,
-                       int* tdep, int* lev, int* parent) {
-  int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= le) return;
+__global__ void k_link(int* dlev, int l, int cap, const int* nkids, const int* off,
+                       const int* bounds, const int* tsplit, int* child_first, int* nchild,
+                       int* item_a, int* item_b, int* tdep, int* lev, int* parent, int* err) {
+  const int lb = dlev[l], le = dlev[l + 1];
+  const int cnt = le - lb;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t0 == 0) {  // end of the next level
+    const int total = cnt > 0 ? off[cnt - 1] + nkids[cnt - 1] : 0;
+    if (le + total > cap) atomicOr(err, DEV_CAPACITY);
+    dlev[l + 2] = le + (le + total > cap ? 0 : total);
+  }
+  if (t0 >= cnt || le + off[cnt - 1] + nkids[cnt - 1] > cap) return;
+  int v = lb + t0;
   int nk = nkids[v - lb];
   int base = le + off[v - lb];
   child_first[v] = nk ? base : -1;
@@ -453,31 +469,47 @@ TreeImpl* tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, i
   }
   ExpandArgs A{khi.p, klo.p, xpref.p, shared ? 1 : 0, nu0, mode, dim, w, ndig, rb,
                item_a.p, item_b.p, tdep.p, tsplit.p, T->lo.p, T->hi.p, nk.p, bounds.p, err.p};
-  T->level_ptr = {0, 1};
-  int lb = 0, le = 1;
-  while (true) {
-    int cnt = le - lb;
-    k_expand<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, A);
-    cub_call([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, nk.p, off.p, cnt, s);
-    }, tmp, s);
-    k_link<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, nk.p, off.p, bounds.p, tsplit.p,
-                                           T->child_first.p, T->nchild.p, item_a.p, item_b.p,
-                                           tdep.p, T->lev.p, T->parent.p);
-    int h[3];
-    d2h(&h[0], off.p + cnt - 1, 1, s);
-    d2h(&h[1], nk.p + cnt - 1, 1, s);
-    d2h(&h[2], err.p, 1, s);
-    sync(s);
-    SMASH_CHECK(h[2] == 0, SMASH_ERR_NUMERICAL,
-                "box subdivision failed to separate points (coincident points)");
-    int total = h[0] + h[1];
-    if (total == 0) break;
-    SMASH_CHECK(le + total <= cap, SMASH_ERR_CUDA, "node capacity exceeded");
-    lb = le;
-    le = le + total;
-    T->level_ptr.push_back(le);
+  // Breadth-first expansion, LEVELS_PER_SYNC levels enqueued per host round trip
+  // (level bounds live on the device; a finished tree leaves empty levels that
+  // the kernels skip).  Node count per level <= points, so grids and the scan
+  // are sized by ntot.
+  constexpr int LEVELS_PER_SYNC = 4;
+  constexpr int MAX_LEVELS = 4 * KEY_BITS + 8;
+  DBuf<int> dlev;
+  dlev.alloc(MAX_LEVELS + 2, s);
+  {
+    int h01[2] = {0, 1};
+    h2d(dlev.p, h01, 2, s);
   }
+  const int nk_size = (int)std::min<int64_t>(ntot, cap);
+  const unsigned lgrid = cdiv(nk_size, 128);
+  T->level_ptr = {0, 1};
+  int l = 0;
+  std::vector<int> hl(MAX_LEVELS + 2, 0);
+  while (true) {
+    SMASH_CHECK(l + LEVELS_PER_SYNC <= MAX_LEVELS, SMASH_ERR_NUMERICAL,
+                "box subdivision failed to separate points (tree too deep)");
+    for (int q = 0; q < LEVELS_PER_SYNC; ++q, ++l) {
+      k_expand<<<lgrid, 128, 0, s>>>(dlev.p, l, nk_size, A);
+      cub_call([&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, nk.p, off.p, nk_size, s);
+      }, tmp, s);
+      k_link<<<lgrid, 128, 0, s>>>(dlev.p, l, cap, nk.p, off.p, bounds.p, tsplit.p,
+                                   T->child_first.p, T->nchild.p, item_a.p, item_b.p, tdep.p,
+                                   T->lev.p, T->parent.p, err.p);
+    }
+    int herr = 0;
+    d2h(hl.data(), dlev.p, l + 2, s);
+    d2h(&herr, err.p, 1, s);
+    sync(s);
+    SMASH_CHECK((herr & DEV_CAPACITY) == 0, SMASH_ERR_CUDA, "node capacity exceeded");
+    SMASH_CHECK(herr == 0, SMASH_ERR_NUMERICAL,
+                "box subdivision failed to separate points (coincident points)");
+    if (hl[l + 1] == hl[l]) break;  // the last enqueued level produced no children
+  }
+  // level_ptr = the distinct, increasing prefix of hl
+  for (int q = 2; q <= l + 1 && hl[q] > hl[q - 1]; ++q) T->level_ptr.push_back(hl[q]);
+  const int le = T->level_ptr.back();
   T->n_nodes = le;
   T->n_levels = (int)T->level_ptr.size() - 1;
   const int n = T->n_nodes;
