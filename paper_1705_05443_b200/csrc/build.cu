@@ -259,32 +259,35 @@ struct SideBuild {
     F->nib.alloc(n, s); F->rank.alloc(n, s); F->ib_off.alloc(n, s); F->g_off.alloc(n, s);
     F->skel_off.alloc(n, s);
     F->rank.zero(s); F->nib.zero(s); F->ib_off.zero(s); F->g_off.zero(s); F->skel_off.zero(s);
-    // skeleton capacity: k_v <= min(rows, |points below v|); HSS rows r + keep are bounded by |ibar|
-    DBuf<int64_t> kb, kbs;
-    kb.alloc(n + 1, s);
-    kb.zero(s);
-    kbs.alloc(1, s);
-    k_skel_bound<<<cdiv(n, 128), 128, 0, s>>>(n, 0, pt_a, pt_b, hss ? (1 << 30) : r, kb.p);
-    cub_call([&](void* tp, size_t& b) { return cub::DeviceReduce::Sum(tp, b, kb.p, kbs.p, n, s); },
-             tmp, s);
-    d2h(&skel_cap, kbs.p, 1, s);
-    sync(s);
+    async = !hss && getenv("SMASH_BUILD_SYNC") == nullptr;
+    if (async) {
+      plan_bounds();  // host-side capacities (one round trip), skeleton capacity included
+    } else {
+      // skeleton capacity: k_v <= min(rows, |points below v|); HSS rows r + keep are bounded by |ibar|
+      DBuf<int64_t> kb, kbs;
+      kb.alloc(n + 1, s);
+      kb.zero(s);
+      kbs.alloc(1, s);
+      k_skel_bound<<<cdiv(n, 128), 128, 0, s>>>(n, 0, pt_a, pt_b, hss ? (1 << 30) : r, kb.p);
+      cub_call([&](void* tp, size_t& b) { return cub::DeviceReduce::Sum(tp, b, kb.p, kbs.p, n, s); },
+               tmp, s);
+      d2h(&skel_cap, kbs.p, 1, s);
+      sync(s);
+      F->perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
+      // HSS (level-synchronous path): room for ~ (n_leaf - k) k G entries per leaf point
+      // up front, so the leaf level does not reallocate + copy (grow() stays the fallback)
+      F->G.alloc(std::max<int64_t>(Pn * (hss ? 32 : 8), 1024), s);
+    }
     skel_cap = std::max<int64_t>(skel_cap, 1);
     F->skel_stride = skel_cap;
     F->skel.alloc(skel_cap, s);
     F->skel_pts.alloc((size_t)skel_cap * dim, s);
-    F->perm.alloc(std::max<int64_t>(Pn * 2, 1024), s);
-    // HSS (level-synchronous path): room for ~ (n_leaf - k) k G entries per leaf point
-    // up front, so the leaf level does not reallocate + copy (grow() stays the fallback)
-    F->G.alloc(std::max<int64_t>(Pn * (hss ? 32 : 8), 1024), s);
     F->level_skel_begin.assign(t->n_levels + 2, 0);
     err.alloc(1, s); err.zero(s);
     swaps.alloc(1, s); swaps.zero(s);
     dmax.alloc(1, s);
     smem_limit = max_sm_smem();
     nsm = num_sms();
-    async = !hss && getenv("SMASH_BUILD_SYNC") == nullptr;
-    if (async) plan_bounds();
   }
 
   void plan_bounds() {
@@ -296,6 +299,9 @@ struct SideBuild {
     d2h(a.data(), pt_a, n, s);
     d2h(b.data(), pt_b, n, s);
     sync(s);
+    // skeleton capacity (k_skel_bound): sum over non-root nodes of min(r, |points below|)
+    skel_cap = 0;
+    for (int v = 1; v < n; ++v) skel_cap += std::min<int64_t>(b[v] - a[v], r);
     std::vector<int64_t> bib(n, 0), bk(n, 0);
     for (int v = n - 1; v >= 0; --v) {  // BFS ids: children after their parent
       int64_t ib = 0;
