@@ -38,7 +38,7 @@ struct TreeImpl {
   int dim = 0, mode = 0, nu0 = 0;
   bool shared = false;  // points_col is points_row
   int64_t nx = 0, ny = 0;
-  int n_nodes = 0, n_levels = 0, n_leaves = 0;
+  int n_nodes = 0, n_levels = 0;
   std::vector<int> level_ptr;  // host: level l (1-based) = [level_ptr[l-1], level_ptr[l])
   double root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
 

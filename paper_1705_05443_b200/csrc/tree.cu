@@ -568,13 +568,7 @@ TreeImpl* tree_build(const double* X, int64_t nx, const double* Y, int64_t ny, i
     T->pts_col.alloc((size_t)nyy * dim, s);
     k_perm_gather<<<cdiv(nyy, 256), 256, 0, s>>>(nyy, dim, ky2.p, ibits, Y, T->perm_col.p, T->pts_col.p);
   }
-  // leaf count
-  {
-    int h = 0;
-    d2h(&h, lord.p + ntot - 1, 1, s);
-    sync(s);
-    T->n_leaves = h;
-  }
+  // (no trailing host round trip: everything after the tree is stream-ordered)
   SMASH_CUDA(cudaGetLastError());
   return T.release();
 }
