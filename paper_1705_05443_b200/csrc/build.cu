@@ -9,6 +9,9 @@
 // column factors alias the row factors (bitwise identical in the reference,
 // SURVEY.md 7 / probe p12).
 #include <thread>
+#include <functional>
+#include <condition_variable>
+#include <mutex>
 #include <chrono>
 #include <cstdio>
 #include <exception>
@@ -528,47 +531,96 @@ struct SideBuild {
 };
 
 // get_pairs on its own host thread and stream (see matrix_build)
-struct PairsJob {
-  std::thread th;
+// A persistent helper thread per device with its own high-priority stream: runs
+// get_pairs while the calling thread enqueues the compression sweep (matrix_build).
+// Created on first use and kept for the life of the process (no per-build thread
+// or stream creation on the build's critical path).
+struct PairsWorker {
+  std::mutex job_mu;  // one job at a time per device
+  std::mutex mu;
+  std::condition_variable cv;
+  std::function<void()> task;
+  bool has = false, done = true;
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev = nullptr;
-  PairLists* out = nullptr;
-  std::exception_ptr err;
-  void start(TreeImpl* t, double tau, int structure, cudaStream_t s) {
-    int dev = 0, lo = 0, hi = 0;
-    SMASH_CUDA(cudaGetDevice(&dev));
+  explicit PairsWorker(int dev) {
+    int lo = 0, hi = 0;
     SMASH_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SMASH_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi));
     SMASH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    SMASH_CUDA(cudaEventRecord(ev, s));  // the tree is complete on s
-    SMASH_CUDA(cudaStreamWaitEvent(s2, ev, 0));
-    th = std::thread([this, t, tau, structure, dev] {
+    std::thread([this, dev] {
+      cudaSetDevice(dev);
+      std::unique_lock<std::mutex> lk(mu);
+      for (;;) {
+        cv.wait(lk, [this] { return has; });
+        has = false;
+        auto f = std::move(task);
+        lk.unlock();
+        f();
+        lk.lock();
+        done = true;
+        cv.notify_all();
+      }
+    }).detach();
+  }
+  static PairsWorker& get(int dev) {
+    static std::mutex reg_mu;
+    static PairsWorker* w[64] = {};
+    std::lock_guard<std::mutex> g(reg_mu);
+    SMASH_CHECK(dev >= 0 && dev < 64, SMASH_ERR_INVALID, "device index out of range");
+    if (!w[dev]) w[dev] = new PairsWorker(dev);
+    return *w[dev];
+  }
+  void submit(std::function<void()> f) {
+    std::lock_guard<std::mutex> lk(mu);
+    task = std::move(f);
+    has = true;
+    done = false;
+    cv.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return done; });
+  }
+};
+
+// get_pairs on the device's helper thread and stream (see matrix_build)
+struct PairsJob {
+  PairsWorker* w = nullptr;
+  std::unique_lock<std::mutex> hold;
+  PairLists* out = nullptr;
+  std::exception_ptr err;
+  bool pending = false;
+  void start(TreeImpl* t, double tau, int structure, cudaStream_t s) {
+    int dev = 0;
+    SMASH_CUDA(cudaGetDevice(&dev));
+    w = &PairsWorker::get(dev);
+    hold = std::unique_lock<std::mutex>(w->job_mu);
+    SMASH_CUDA(cudaEventRecord(w->ev, s));  // the tree is complete on s
+    SMASH_CUDA(cudaStreamWaitEvent(w->s2, w->ev, 0));
+    cudaStream_t s2 = w->s2;
+    w->submit([this, t, tau, structure, s2] {
       try {
-        SMASH_CUDA(cudaSetDevice(dev));
         out = get_pairs(t, tau, structure, s2);
       } catch (...) {
         err = std::current_exception();
       }
     });
+    pending = true;
   }
   PairLists* join(cudaStream_t s) {
-    th.join();
+    w->wait();
+    pending = false;
     if (!err) {
       out->rehome(s);  // released on the owner's stream later
-      SMASH_CUDA(cudaEventRecord(ev, s2));
-      SMASH_CUDA(cudaStreamWaitEvent(s, ev, 0));
+      SMASH_CUDA(cudaEventRecord(w->ev, w->s2));
+      SMASH_CUDA(cudaStreamWaitEvent(s, w->ev, 0));
     }
-    cleanup();
     if (err) std::rethrow_exception(err);
     return out;
   }
-  void cleanup() {
-    if (s2) { cudaStreamSynchronize(s2); cudaStreamDestroy(s2); s2 = nullptr; }
-    if (ev) { cudaEventDestroy(ev); ev = nullptr; }
-  }
   ~PairsJob() {
-    if (th.joinable()) th.join();
-    cleanup();
+    if (pending && w) w->wait();
   }
 };
 
