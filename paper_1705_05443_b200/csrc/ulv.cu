@@ -33,6 +33,7 @@ namespace smash {
 namespace {
 
 constexpr int ULV_THREADS = 256;
+constexpr int ULV_PF = 8;  // reflector entries per lane held in registers (rows up to 256)
 constexpr double PIVOT_RTOL = 1e-13;  // apply.py:18
 
 struct UlvNode {
@@ -440,6 +441,8 @@ struct SolveArgs {
   double* wg;        // per node kc x R
   const int* piv;
   int R;
+  int stage;         // this level's per-node vectors fit shared memory (after the vs buffer)
+  int vs_cap;        // doubles reserved for the reflector buffer at the start of shared memory
 };
 
 // upward pass of one level (apply.py:300-330); the root also runs the LU solve
@@ -536,6 +539,95 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_up(SolveArgs S) {
   const double* VT = A.VT + N.oVT;
   const int mr = N.mr, mc = N.mc, kr = N.kr, t = N.t, r0 = mr - t;
   double* vs = reinterpret_cast<double*>(smem);
+  if (S.stage) {
+    // the node's right-hand sides and z1 in shared memory: Q^T b, the forward
+    // substitution (left-looking, coalesced rows of L) and the corrections run
+    // on chip; bred, z1 and g go back to HBM for the parent / the downward pass
+    double* sb = vs + S.vs_cap;
+    double* sz = sb + (int64_t)mr * R;
+    for (int e = tid; e < mr * R; e += NT) sb[e] = b[e];
+    double* su = sz + (int64_t)t * R;  // U (reflectors below the diagonal), coalesced copy
+    for (int e = tid; e < mr * kr; e += NT) su[e] = U[e];
+    __syncthreads();
+    if (mr <= 32 * ULV_PF) {
+      // Q^T b with each warp's column in registers (entry j = lane + 32k) and the
+      // next reflector (column i+1 of U below the diagonal) prefetched
+      for (int c = wid; c < R; c += NW) {
+        double yr[ULV_PF], cur[ULV_PF], nxt[ULV_PF];
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) {
+          const int j = lane + 32 * k;
+          yr[k] = j < mr ? sb[(int64_t)j * R + c] : 0.0;
+        }
+        auto load_col = [&](int ii, double* dst) {
+#pragma unroll
+          for (int k = 0; k < ULV_PF; ++k) {
+            const int j = lane + 32 * k;
+            dst[k] = j < mr ? (j > ii ? su[j * kr + ii] : (j == ii ? 1.0 : 0.0)) : 0.0;
+          }
+        };
+        load_col(0, cur);
+        double tau = A.tauU[N.otU];
+        for (int i = 0; i < kr; ++i) {
+          double tau_n = 0.0;
+          if (i + 1 < kr) {
+            load_col(i + 1, nxt);
+            tau_n = A.tauU[N.otU + i + 1];
+          }
+          double w = 0.0;
+#pragma unroll
+          for (int k = 0; k < ULV_PF; ++k) w = fma(cur[k], yr[k], w);
+          w = warp_sum(w) * tau;
+#pragma unroll
+          for (int k = 0; k < ULV_PF; ++k) yr[k] = fma(-w, cur[k], yr[k]);
+#pragma unroll
+          for (int k = 0; k < ULV_PF; ++k) cur[k] = nxt[k];
+          tau = tau_n;
+        }
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) {
+          const int j = lane + 32 * k;
+          if (j < mr) sb[(int64_t)j * R + c] = yr[k];
+        }
+      }
+      __syncthreads();
+    } else {
+      for (int i = 0; i < kr; ++i) {
+        for (int r = i + 1 + tid; r < mr; r += NT) vs[r - i] = U[(int64_t)r * kr + i];
+        __syncthreads();
+        const double tau = A.tauU[N.otU + i];
+        if (tau != 0.0)
+          for (int c = wid; c < R; c += NW) warp_apply(vs, mr - i, tau, sb + (int64_t)i * R + c, R);
+        __syncthreads();
+      }
+    }
+    for (int c = wid; c < R; c += NW) {
+      for (int i = 0; i < t; ++i) {
+        const double* Li = D + (int64_t)(r0 + i) * mc;
+        double acc = 0.0;
+        for (int j = lane; j < i; j += 32) acc = fma(Li[j], sz[(int64_t)j * R + c], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) sz[(int64_t)i * R + c] = (sb[(int64_t)(r0 + i) * R + c] - acc) / Li[i];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    double* z = S.wx + N.ox * R;
+    for (int e = tid; e < t * R; e += NT) z[e] = sz[e];
+    for (int e = tid; e < r0 * R; e += NT) {
+      const int r = e / R, c = e % R;
+      double sacc = sb[e];
+      for (int j = 0; j < t; ++j) sacc -= D[(int64_t)r * mc + j] * sz[(int64_t)j * R + c];
+      b[e] = sacc;
+    }
+    for (int e = tid; e < N.kc * R; e += NT) {
+      const int a = e / R, c = e % R;
+      double sacc = g[e];
+      for (int j = 0; j < t; ++j) sacc = fma(VT[(int64_t)a * mc + j], sz[(int64_t)j * R + c], sacc);
+      g[e] = sacc;
+    }
+    return;
+  }
   // bp = Q^T bcur
   for (int i = 0; i < kr; ++i) {
     for (int r = i + 1 + tid; r < mr; r += NT) vs[r - i] = U[(int64_t)r * kr + i];
@@ -587,12 +679,64 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_down(SolveArgs S) {
   const UlvNode& N = A.nd[v];
   const UlvNode& Pn = A.nd[N.parent];
   const int R = S.R, tid = threadIdx.x, NT = blockDim.x, wid = tid >> 5, NW = NT >> 5;
-  double* xv = S.wx + N.ox * R;
+  double* xg = S.wx + N.ox * R;
   const double* xp = S.wx + Pn.ox * R;
   const int n_red = N.mc - N.t;
+  // [z1; xvec] assembled in shared memory when the level fits (else in place in HBM)
+  double* xv = S.stage ? reinterpret_cast<double*>(smem) + S.vs_cap : xg;
+  if (S.stage)
+    for (int e = tid; e < N.t * R; e += NT) xv[e] = xg[e];
   for (int e = tid; e < n_red * R; e += NT) xv[(int64_t)N.t * R + e] = xp[(int64_t)N.pos * R + e];
   __syncthreads();
-  if (N.t > 0) {
+  if (N.t > 0 && N.mc <= 32 * ULV_PF) {
+    // Each warp applies the reflectors to its own right-hand-side columns with
+    // the column held in registers (entry j = lane + 32k in yr[k]) and no block
+    // barriers; reflector i-1's row (and tau) are prefetched while reflector i is
+    // applied.  The row's entry at the diagonal is replaced by the implicit 1.
+    const double* D = A.D + N.oD;
+    const int mc = N.mc, r0 = N.mr - N.t, lane = tid & 31;
+    for (int c = wid; c < R; c += NW) {
+      double yr[ULV_PF], cur[ULV_PF], nxt[ULV_PF];
+#pragma unroll
+      for (int k = 0; k < ULV_PF; ++k) {
+        const int j = lane + 32 * k;
+        yr[k] = j < mc ? xv[(int64_t)j * R + c] : 0.0;
+      }
+      auto load_row = [&](int ii, double* dst) {
+        const double* row = D + (int64_t)(r0 + ii) * mc;
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) {
+          const int j = lane + 32 * k;
+          dst[k] = j < mc ? (j > ii ? row[j] : (j == ii ? 1.0 : 0.0)) : 0.0;
+        }
+      };
+      int i = N.t - 1;
+      load_row(i, cur);
+      double tau = A.tauZ[N.otZ + i];
+      for (; i >= 0; --i) {
+        double tau_n = 0.0;
+        if (i > 0) {
+          load_row(i - 1, nxt);
+          tau_n = A.tauZ[N.otZ + i - 1];
+        }
+        double w = 0.0;
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) w = fma(cur[k], yr[k], w);
+        w = warp_sum(w) * tau;
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) yr[k] = fma(-w, cur[k], yr[k]);
+#pragma unroll
+        for (int k = 0; k < ULV_PF; ++k) cur[k] = nxt[k];
+        tau = tau_n;
+      }
+#pragma unroll
+      for (int k = 0; k < ULV_PF; ++k) {
+        const int j = lane + 32 * k;
+        if (j < mc) xv[(int64_t)j * R + c] = yr[k];
+      }
+    }
+    __syncthreads();
+  } else if (N.t > 0) {
     const double* D = A.D + N.oD;
     double* vs = reinterpret_cast<double*>(smem);
     const int mc = N.mc, r0 = N.mr - N.t;
@@ -606,11 +750,15 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_down(SolveArgs S) {
       __syncthreads();
     }
   }
-  if (N.leaf)
+  if (N.leaf) {
     for (int e = tid; e < N.mc * R; e += NT) {
       const int r = e / R, c = e % R;
       S.x[S.perm_col[N.col_a + r] * R + c] = xv[e];
     }
+  } else if (S.stage) {
+    __syncthreads();
+    for (int e = tid; e < N.mc * R; e += NT) xg[e] = xv[e];
+  }
 }
 
 }  // namespace
@@ -821,8 +969,27 @@ void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s
   S.b = b; S.x = x; S.perm_row = F->perm_row.p; S.perm_col = F->perm_col.p;
   S.wb = F->wb.p; S.wx = F->wx.p; S.wg = F->wg.p; S.piv = F->piv.p; S.R = (int)R;
   const size_t sm = F->smem_up;
-  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  // per level: stage the nodes' vectors in shared memory when they fit 64 KB
+  static const bool no_stage = getenv("SMASH_ULV_NOSTAGE") != nullptr;
+  const int L = t->n_levels;
+  std::vector<int> vcap(L + 2, 1);
+  std::vector<int64_t> need_up(L + 2, 0), need_dn(L + 2, 0);
+  for (int l = 1; l <= L; ++l)
+    for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
+      const UlvNode& N = F->h[v];
+      vcap[l] = std::max(vcap[l], (std::max(N.mr, N.mc) + 1) & ~1);
+      need_up[l] = std::max<int64_t>(need_up[l], (int64_t)(N.mr + N.t) * R + (int64_t)N.mr * N.kr);
+      need_dn[l] = std::max<int64_t>(need_dn[l], (int64_t)N.mc * R);
+    }
+  auto lvl_smem = [&](int l, int64_t need, int* stage) {
+    const size_t want = 8 * ((size_t)vcap[l] + (size_t)need) + 64;
+    *stage = !no_stage && want <= 64 * 1024;
+    return *stage ? std::max(sm, want) : sm;
+  };
+  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_up, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(sm, 64 * 1024 + 64)));
+  SMASH_CUDA(cudaFuncSetAttribute(k_ulv_down, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(sm, 64 * 1024 + 64)));
   static const bool timing = getenv("SMASH_ULV_TIMING") != nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timing) {
@@ -841,12 +1008,16 @@ void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s
   if (timing) cudaEventRecord(e0, s);
   for (int l = t->n_levels; l >= 1; --l) {
     S.A = make_args(F, t->level_begin(l), t->level_end(l));
-    k_ulv_up<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+    S.vs_cap = vcap[l];
+    const size_t smu = lvl_smem(l, need_up[l], &S.stage);
+    k_ulv_up<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, smu, s>>>(S);
     tick("up", l);
   }
   for (int l = 2; l <= t->n_levels; ++l) {
     S.A = make_args(F, t->level_begin(l), t->level_end(l));
-    k_ulv_down<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, sm, s>>>(S);
+    S.vs_cap = vcap[l];
+    const size_t smd = lvl_smem(l, need_dn[l], &S.stage);
+    k_ulv_down<<<t->level_end(l) - t->level_begin(l), ULV_THREADS, smd, s>>>(S);
     tick("down", l);
   }
   if (timing) {
