@@ -275,6 +275,52 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_assemble(UlvArgs A) {
 }
 
 // ---- reduction (_reduce_node, apply.py:196-234) -------------------------------------------
+// Apply reflectors 0..nref-1, in order, to one vector y (n <= 32*ULV_PF entries,
+// y[j] at y[j*sy]) held by one warp in registers: reflector i is
+// v_i[j] = 1 (j == i), vat(i, j) (j > i), 0 (j < i), with tau taus[i]; the next
+// reflector is prefetched while the current one is applied.
+template <class VF>
+__device__ __forceinline__ void warp_apply_all(double* y, int64_t sy, int n, int nref,
+                                               const double* taus, VF vat) {
+  const int lane = threadIdx.x & 31;
+  double yr[ULV_PF], cur[ULV_PF], nxt[ULV_PF];
+#pragma unroll
+  for (int k = 0; k < ULV_PF; ++k) {
+    const int j = lane + 32 * k;
+    yr[k] = j < n ? y[j * sy] : 0.0;
+  }
+  auto load = [&](int i, double* dst) {
+#pragma unroll
+    for (int k = 0; k < ULV_PF; ++k) {
+      const int j = lane + 32 * k;
+      dst[k] = j < n ? (j > i ? vat(i, j) : (j == i ? 1.0 : 0.0)) : 0.0;
+    }
+  };
+  load(0, cur);
+  double tau = taus[0];
+  for (int i = 0; i < nref; ++i) {
+    double tau_n = 0.0;
+    if (i + 1 < nref) {
+      load(i + 1, nxt);
+      tau_n = taus[i + 1];
+    }
+    double w = 0.0;
+#pragma unroll
+    for (int k = 0; k < ULV_PF; ++k) w = fma(cur[k], yr[k], w);
+    w = warp_sum(w) * tau;
+#pragma unroll
+    for (int k = 0; k < ULV_PF; ++k) yr[k] = fma(-w, cur[k], yr[k]);
+#pragma unroll
+    for (int k = 0; k < ULV_PF; ++k) cur[k] = nxt[k];
+    tau = tau_n;
+  }
+#pragma unroll
+  for (int k = 0; k < ULV_PF; ++k) {
+    const int j = lane + 32 * k;
+    if (j < n) y[j * sy] = yr[k];
+  }
+}
+
 __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* vs = reinterpret_cast<double*>(smem);
@@ -302,6 +348,9 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     for (int64_t e = tid; e < nV; e += blockDim.x) VT[e] = Vg[e];
     __syncthreads();
   }
+  // register-resident application of whole reflector sequences (rows / columns up
+  // to 32*ULV_PF entries); otherwise every reflector is applied as it is formed
+  const bool fast = mr <= 32 * ULV_PF && mc <= 32 * ULV_PF;
   // 1. Householder QR of U, applied to D from the left (Q^T D)
   for (int i = 0; i < kr; ++i) {
     if (wid == 0) {
@@ -313,11 +362,26 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     __syncthreads();
     const double tau = s_tau;
     if (tau != 0.0) {
-      for (int j = wid; j < (kr - i - 1) + mc; j += NW) {
-        if (j < kr - i - 1) warp_apply(vs, mr - i, tau, U + (int64_t)i * kr + (i + 1 + j), kr);
-        else warp_apply(vs, mr - i, tau, D + (int64_t)i * mc + (j - (kr - i - 1)), mc);
+      if (fast) {  // U's own columns now, D's columns after the factorisation
+        for (int j = wid; j < kr - i - 1; j += NW)
+          warp_apply(vs, mr - i, tau, U + (int64_t)i * kr + (i + 1 + j), kr);
+      } else {
+        for (int j = wid; j < (kr - i - 1) + mc; j += NW) {
+          if (j < kr - i - 1) warp_apply(vs, mr - i, tau, U + (int64_t)i * kr + (i + 1 + j), kr);
+          else warp_apply(vs, mr - i, tau, D + (int64_t)i * mc + (j - (kr - i - 1)), mc);
+        }
       }
     }
+    __syncthreads();
+  }
+  if (fast && kr > 0) {
+    // Q^T D: one warp per column of D, the column in registers, all kr reflectors
+    const double* taus = A.tauU + N.otU;
+    const double* Uc = U;
+    const int ldu = kr;
+    for (int c = wid; c < mc; c += NW)
+      warp_apply_all(D + c, mc, mr, kr, taus,
+                     [Uc, ldu](int i, int j) { return Uc[(int64_t)j * ldu + i]; });
     __syncthreads();
   }
   // 2. LQ of Bbot = the last t rows of Q^T D (QR of Bbot^T), applied from the right
@@ -345,7 +409,7 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     __syncthreads();
     const double tau = s_tau;
     if (tau != 0.0) {
-      const int nrows = (t - i - 1) + r0 + kc;
+      const int nrows = fast ? (t - i - 1) : (t - i - 1) + r0 + kc;
       for (int j = wid; j < nrows; j += NW) {
         double* y;
         if (j < t - i - 1) y = D + (int64_t)(r0 + i + 1 + j) * mc;
@@ -353,6 +417,19 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
         else y = VT + (int64_t)(j - (t - i - 1) - r0) * mc;
         warp_apply(vs, mc - i, tau, y + i, 1);
       }
+    }
+    __syncthreads();
+  }
+  if (fast) {
+    // Dtrans = Dtop Qz and Mfull = V^T Qz: one warp per row, the row in registers,
+    // all t reflectors (stored in the LQ rows of D)
+    const double* taus = A.tauZ + N.otZ;
+    const double* Lz = D + (int64_t)r0 * mc;
+    const int ldz = mc;
+    auto vat = [Lz, ldz](int i, int j) { return Lz[(int64_t)i * ldz + j]; };
+    for (int j = wid; j < r0 + kc; j += NW) {
+      double* y = j < r0 ? D + (int64_t)j * mc : VT + (int64_t)(j - r0) * mc;
+      warp_apply_all(y, 1, mc, t, taus, vat);
     }
     __syncthreads();
   }
