@@ -279,19 +279,19 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_assemble(UlvArgs A) {
 // y[j] at y[j*sy]) held by one warp in registers: reflector i is
 // v_i[j] = 1 (j == i), vat(i, j) (j > i), 0 (j < i), with tau taus[i]; the next
 // reflector is prefetched while the current one is applied.
-template <class VF>
+template <int PF, class VF>
 __device__ __forceinline__ void warp_apply_all(double* y, int64_t sy, int n, int nref,
                                                const double* taus, VF vat) {
   const int lane = threadIdx.x & 31;
-  double yr[ULV_PF], cur[ULV_PF], nxt[ULV_PF];
+  double yr[PF], cur[PF], nxt[PF];
 #pragma unroll
-  for (int k = 0; k < ULV_PF; ++k) {
+  for (int k = 0; k < PF; ++k) {
     const int j = lane + 32 * k;
     yr[k] = j < n ? y[j * sy] : 0.0;
   }
   auto load = [&](int i, double* dst) {
 #pragma unroll
-    for (int k = 0; k < ULV_PF; ++k) {
+    for (int k = 0; k < PF; ++k) {
       const int j = lane + 32 * k;
       dst[k] = j < n ? (j > i ? vat(i, j) : (j == i ? 1.0 : 0.0)) : 0.0;
     }
@@ -306,16 +306,16 @@ __device__ __forceinline__ void warp_apply_all(double* y, int64_t sy, int n, int
     }
     double w = 0.0;
 #pragma unroll
-    for (int k = 0; k < ULV_PF; ++k) w = fma(cur[k], yr[k], w);
+    for (int k = 0; k < PF; ++k) w = fma(cur[k], yr[k], w);
     w = warp_sum(w) * tau;
 #pragma unroll
-    for (int k = 0; k < ULV_PF; ++k) yr[k] = fma(-w, cur[k], yr[k]);
+    for (int k = 0; k < PF; ++k) yr[k] = fma(-w, cur[k], yr[k]);
 #pragma unroll
-    for (int k = 0; k < ULV_PF; ++k) cur[k] = nxt[k];
+    for (int k = 0; k < PF; ++k) cur[k] = nxt[k];
     tau = tau_n;
   }
 #pragma unroll
-  for (int k = 0; k < ULV_PF; ++k) {
+  for (int k = 0; k < PF; ++k) {
     const int j = lane + 32 * k;
     if (j < n) y[j * sy] = yr[k];
   }
@@ -379,9 +379,11 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     const double* taus = A.tauU + N.otU;
     const double* Uc = U;
     const int ldu = kr;
-    for (int c = wid; c < mc; c += NW)
-      warp_apply_all(D + c, mc, mr, kr, taus,
-                     [Uc, ldu](int i, int j) { return Uc[(int64_t)j * ldu + i]; });
+    auto uat = [Uc, ldu](int i, int j) { return Uc[j * ldu + i]; };
+    for (int c = wid; c < mc; c += NW) {
+      if (mr <= 128) warp_apply_all<4>(D + c, mc, mr, kr, taus, uat);
+      else warp_apply_all<ULV_PF>(D + c, mc, mr, kr, taus, uat);
+    }
     __syncthreads();
   }
   // 2. LQ of Bbot = the last t rows of Q^T D (QR of Bbot^T), applied from the right
@@ -426,10 +428,11 @@ __global__ void __launch_bounds__(ULV_THREADS) k_ulv_reduce(UlvArgs A) {
     const double* taus = A.tauZ + N.otZ;
     const double* Lz = D + (int64_t)r0 * mc;
     const int ldz = mc;
-    auto vat = [Lz, ldz](int i, int j) { return Lz[(int64_t)i * ldz + j]; };
+    auto vat = [Lz, ldz](int i, int j) { return Lz[i * ldz + j]; };
     for (int j = wid; j < r0 + kc; j += NW) {
       double* y = j < r0 ? D + (int64_t)j * mc : VT + (int64_t)(j - r0) * mc;
-      warp_apply_all(y, 1, mc, t, taus, vat);
+      if (mc <= 128) warp_apply_all<4>(y, 1, mc, t, taus, vat);
+      else warp_apply_all<ULV_PF>(y, 1, mc, t, taus, vat);
     }
     __syncthreads();
   }
