@@ -17,7 +17,12 @@
 //     (lowrank.py:244-255).
 // Thread-per-column mapping keeps every column's dot products and norms in a
 // fixed sequential order; the row-major panel makes those accesses
-// bank-conflict free.
+// bank-conflict free.  Launch shape (plan_compress_launch): CTAs claim nodes
+// from an atomic counter; the panel lives in shared memory when the level's
+// capacity bound fits (1-warp CTAs for <= 64 columns, 128 threads for <= 128,
+// else 256), per node in shared memory or the CTA's global slice on hybrid
+// levels, and in the global/L2 slice (32-deep independent loads) when no
+// shared panel fits.
 #include "compress.cuh"
 #include "qr_device.cuh"
 
