@@ -121,3 +121,25 @@ def test_singular_block_reported_with_node_id(sg):
                      sg.BuildParams(r=10, tau=0.6, basis="interp", rtol=1e-8, eps_svd=1e-9))
     with pytest.raises(np.linalg.LinAlgError, match="node"):
         sg.ulv_factor(M)
+
+
+def test_adaptive_tree_and_many_rhs(sg):
+    """Leaves on several levels (clustered 1-D points) and more right-hand sides than
+    warps per CTA (R = 20: shared-memory staging off for the leaf level, on above)."""
+    from oracle import smash_oracle as orc
+    rng = np.random.default_rng(13)
+    x = np.sort(np.concatenate([rng.random(600), 0.31 + 1e-3 * rng.random(900)]))[:, None]
+    tree = sg.build_tree(sg.PointSet(x), nu0=64, mode="binary", tau=0.6)
+    depths = {tree.nodes[i].level for i in tree.leaves()}
+    assert len(depths) > 1
+    M = sg.build_hss(tree, sg.KernelSpec("log", dx=0.0), None, None,
+                     sg.BuildParams(r=12, tau=0.6, basis="interp", rtol=1e-10, eps_svd=1e-11))
+    A = orc.kernel_block("log", x, x, 0.0)
+    B = rng.standard_normal((x.shape[0], 20))
+    F = sg.ulv_factor(M)
+    X = sg.ulv_solve(F, B)
+    r = sg.matvec_nodewise(M, X) - B
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(B)
+    Xd = np.linalg.solve(A, B)
+    assert np.linalg.norm(X - Xd) <= 1e-6 * np.linalg.norm(Xd)
+    np.testing.assert_allclose(sg.ulv_solve(F, B[:, 3]), X[:, 3], rtol=1e-11, atol=1e-11 * np.abs(X).max())
