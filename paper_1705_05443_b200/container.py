@@ -202,7 +202,7 @@ def load_matrix(path, device=None):
             raise ValueError("container %s differ from the B200 pair lists" % name)
     n, root = len(th["nodes"]), tree.root
     sides = [_side_arrays(arrays, "rowfac", n, root)]
-    colfac_same = all(np.array_equal(arrays[k], arrays["rowfac" + k[6:]])
+    colfac_same = all(("rowfac" + k[6:]) in arrays and np.array_equal(arrays[k], arrays["rowfac" + k[6:]])
                       for k in arrays if k.startswith("colfac."))
     if not (shared and colfac_same):
         sides.append(_side_arrays(arrays, "colfac", n, root))

@@ -295,7 +295,9 @@ GraphEntry* graph_for(MatrixImpl* m, const double* q, double* z, int64_t nrhs, i
 }
 
 void replay(MatrixImpl* m, GraphEntry* E, cudaStream_t s) {
+  m->order_after_last_use(s);
   SMASH_CUDA(cudaGraphLaunch(E->exec, s));
+  m->mark_use(s);
   m->launches += E->launches;
   if (m->profile && E->far) {
     const int pairs[7][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {6, 7}, {8, 5}, {0, 5}};
@@ -376,9 +378,11 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
   const int nch = (int)chunks_of(nrhs, rc_cap).size();
   if (debug_sync()) {
     int nl = 0;
+    m->order_after_last_use(s);
     dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
       run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, s, nullptr, &nl);
     });
+    m->mark_use(s);
     return;
   }
   GraphEntry* E = graph_for(m, q, z, nrhs, 0, nch, true, [&](auto* evs, int* nl) {

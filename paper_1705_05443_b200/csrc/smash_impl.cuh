@@ -113,7 +113,20 @@ struct MatrixImpl {
   cudaStream_t s2 = nullptr;
   cudaStream_t sc = nullptr;  // graph capture origin (the caller's stream may be the legacy one)
   cudaEvent_t fork = nullptr, join = nullptr;
+  // Stream ordering of the shared scratch (qt, qhat, zhat, zd, zn): every product waits
+  // for the previous one, whatever stream it ran on, and the matrix is freed only after
+  // its last product completes.
+  cudaEvent_t last_use = nullptr;
+  void order_after_last_use(cudaStream_t s) {
+    if (!last_use) SMASH_CUDA(cudaEventCreateWithFlags(&last_use, cudaEventDisableTiming));
+    SMASH_CUDA(cudaStreamWaitEvent(s, last_use, 0));
+  }
+  void mark_use(cudaStream_t s) { SMASH_CUDA(cudaEventRecord(last_use, s)); }
   ~MatrixImpl() {
+    if (last_use) {
+      cudaEventSynchronize(last_use);
+      cudaEventDestroy(last_use);
+    }
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (fork) cudaEventDestroy(fork);

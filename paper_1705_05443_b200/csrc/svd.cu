@@ -5,9 +5,13 @@
 // One CTA per node.  A (|ibar| x n_near) is generated from the kernel into an
 // L2-resident workspace, then its left singular subspace is computed as
 //   A P = Q1 R      column-pivoted Householder QR, stopped once |R_ii| falls
-//                   to the fp64 noise floor (2^-53 |R_00|): the discarded block
-//                   perturbs the singular values by O(eps sigma_1), the same
-//                   order as LAPACK gesdd's own error;
+//                   2^3 below the fp64 noise floor (2^-56 |R_00|, SMASH_SVD_FLOOR):
+//                   the discarded block perturbs the singular values by about
+//                   sqrt(n) 2^-56 sigma_1, the order of LAPACK's own rounding.
+//                   Stopping AT the noise floor (2^-53) made the kept vectors near
+//                   the eps_svd cut ~10x less accurate (cfg 4 full size: 21 rank
+//                   flips vs 1 for a LAPACK restatement; 2^-56 .. 2^-63 all give
+//                   the LAPACK restatement's counts, profiles/hss_skeleton_census_r02.txt);
 //   R_k^T = Q2 R2   unpivoted QR of the k' x n_near leading rows (transposed);
 //   R2 V = W        one-sided (Hestenes) Jacobi on the k' x k' triangle,
 //                   round-robin pair order, one warp per pair;
@@ -50,6 +54,7 @@ struct IbarSide {
 struct SvdArgs {
   int lb, le, dim, kernel;
   double dx, eps_svd;
+  double floor_rel;  // QR truncation |R_ii| <= floor_rel |R_00|
   int transpose;  // 0: K(target, source) (row pass); 1: K(source, target) (column pass)
   const int* nchild;
   const int* child_first;
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       const double tau = S.misc[0];
       if (tid == 0) taus[i] = tau;
       const double r0 = fabs(S.rdiag[0]);
-      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > 0x1p-53 * r0)) break;  // noise floor reached
+      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > A.floor_rel * r0)) break;  // below the noise floor
       kp = i + 1;
       for (int j = i + 1 + tid; j < nn; j += NT) {
         if (tau != 0.0) apply_reflector_g(P, ld, n, i, j, tau, S.vh);
@@ -523,6 +528,8 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.lb = lb; A.le = le; A.dim = t->dim; A.kernel = M->p.kernel;
   A.dx = M->p.kernel == SMASH_KERNEL_EXP ? 1.0 : M->p.dx;
   A.eps_svd = M->p.eps_svd;
+  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 58;
+  A.floor_rel = ldexp(1.0, -floor_exp);
   A.transpose = side;
   A.nchild = t->nchild.p; A.child_first = t->child_first.p;
   A.near_ptr = near->ptr.p; A.near_idx = near->idx.p;

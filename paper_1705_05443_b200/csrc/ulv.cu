@@ -856,6 +856,15 @@ struct UlvImpl {
   size_t smem_asm = 0, smem_red = 0, smem_up = 0;
   DBuf<double> wb, wx, wg;
   int64_t ws_nrhs = 0;
+  // solves share the workspaces: each waits for the previous one (any stream), and the
+  // factorisation is freed only after its last solve completes
+  cudaEvent_t last_use = nullptr;
+  ~UlvImpl() {
+    if (last_use) {
+      cudaEventSynchronize(last_use);
+      cudaEventDestroy(last_use);
+    }
+  }
 };
 
 namespace {
@@ -1039,7 +1048,11 @@ UlvImpl* ulv_factor(MatrixImpl* M, cudaStream_t s) {
 void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s) {
   SMASH_CHECK(R >= 1, SMASH_ERR_INVALID, "nrhs must be positive");
   TreeImpl* t = F->M->tree;
+  if (!F->last_use) SMASH_CUDA(cudaEventCreateWithFlags(&F->last_use, cudaEventDisableTiming));
+  SMASH_CUDA(cudaStreamWaitEvent(s, F->last_use, 0));
   if (F->ws_nrhs < R) {
+    // the old workspaces may still be read by a solve on another stream: free after it
+    SMASH_CUDA(cudaEventSynchronize(F->last_use));
     F->wb.alloc(std::max<int64_t>(F->nb * R, 1), s);
     F->wx.alloc(std::max<int64_t>(F->nx * R, 1), s);
     F->wg.alloc(std::max<int64_t>(F->ng * R, 1), s);
@@ -1105,6 +1118,7 @@ void ulv_solve(UlvImpl* F, const double* b, double* x, int64_t R, cudaStream_t s
     cudaEventDestroy(e1);
   }
   SMASH_CUDA(cudaGetLastError());
+  SMASH_CUDA(cudaEventRecord(F->last_use, s));
 }
 
 void ulv_free(UlvImpl* F) { delete F; }

@@ -90,18 +90,21 @@ def case_points(case):
 
 # name -> parameters.  cfgN_* follow BASELINE config N at reduced N.
 CASES = {
-    "cfg1_full": dict(gen="cfg", cfg=1, N=4096, seed=1, store_G=True),
-    "cfg2_4k": dict(gen="cfg", cfg=2, N=4096, seed=2, store_G=False),
+    "cfg1_full": dict(gen="cfg", cfg=1, N=4096, seed=1, store_G=True, store_cand=True),
+    "cfg2_4k": dict(gen="cfg", cfg=2, N=4096, seed=2, store_G=True),
     "cfg2_32k": dict(gen="cfg", cfg=2, N=32768, seed=2, store_G=False),
-    "cfg3_8k": dict(gen="cfg", cfg=3, N=8192, seed=3, store_G=False),
-    "cfg4_8k": dict(gen="cfg", cfg=4, N=8192, seed=4, store_G=False),
-    "cfg5_16k": dict(gen="cfg", cfg=5, N=16384, seed=5, store_G=False),
+    "cfg3_8k": dict(gen="cfg", cfg=3, N=8192, seed=3, store_G=True),
+    "cfg4_8k": dict(gen="cfg", cfg=4, N=8192, seed=4, store_G=True),
+    "cfg5_16k": dict(gen="cfg", cfg=5, N=16384, seed=5, store_G=True),
+    # every compr candidate [U_hat, S] of a Cauchy HSS build (gesdd's S), so the
+    # GPU sRRQR can be checked on the reference's own inputs
+    "cfg4_2k": dict(gen="cfg", cfg=4, N=2048, seed=4, store_G=True, store_cand=True),
     # edge cases: adaptive 2-D with deep shrinks, X != Y in 1-D, 3-D tiny
     "clustered2d": dict(gen="clustered2d", N=3000, seed=11, structure="h2", kernel="log", dim=2,
                         mode="2d", nu0=16, r=16, tau=0.7, rtol=1e-8, eps_svd=0.0, nrhs=3, store_G=True),
     "pair1d_hss": dict(gen="pair1d", N=700, seed=12, structure="hss", kernel="cauchy", dim=1,
                        mode="binary", nu0=20, r=12, tau=0.6, rtol=1e-10, eps_svd=1e-11, nrhs=2,
-                       store_G=True),
+                       store_G=True, store_cand=True),
     "pair1d_h2": dict(gen="pair1d", N=700, seed=13, structure="h2", kernel="cauchy", dim=1,
                       mode="binary", nu0=20, r=12, tau=0.5, rtol=1e-10, eps_svd=0.0, nrhs=1,
                       store_G=True),
@@ -158,6 +161,15 @@ def run_case(name, case):
     X, Y, rng = case_points(c)
     q = rng.standard_normal((Y.shape[0], c["nrhs"]))
     install_extension(c["kernel"], c["rtol"])
+    cands = []
+    if c.get("store_cand"):
+        inner = smash.hss.compr if c["structure"] == "hss" else smash.h2.compr
+
+        def rec(C, ibar, **kw):
+            cands.append(np.array(C))
+            return inner(C, ibar, **kw)
+        smash.hss.compr = rec
+        smash.h2.compr = rec
     PX = smash.PointSet(X)
     PY = PX if Y is X else smash.PointSet(Y, role="col")
     t0 = time.time()
@@ -192,6 +204,17 @@ def run_case(name, case):
                 continue
             out["G_%s_ptr" % side], out["G_%s" % side] = gptr, gv
             out["fperm_%s_ptr" % side], out["fperm_%s" % side] = pptr, pv
+    if cands:
+        # calls run row then column per node, levels L..2 (h2.py:44-53, hss.py:272-299)
+        it = iter(cands)
+        order = [(side, i) for lev in range(tree.n_levels, 1, -1) for i in tree.level_nodes(lev)
+                 for side in ("row", "col")]
+        got = {key: next(it) for key in order}
+        for side in ("row", "col"):
+            mats = [got.get((side, i), np.zeros((0, 0))) for i in range(n)]
+            out["cand_%s_cols" % side] = np.array([m_.shape[1] if m_.ndim == 2 else 0 for m_ in mats], np.int64)
+            out["cand_%s_ptr" % side], out["cand_%s" % side] = flat_dict(
+                {i: m_.ravel() for i, m_ in enumerate(mats)}, n, np.float64)
     if c["structure"] == "hss":
         near = [smash.nearfield_set(tree, i, c["tau"]) for i in range(n)]
         ptr, nv = flat_dict({i: np.array(v, np.int64) for i, v in enumerate(near)}, n, np.int64)

@@ -9,6 +9,7 @@ error against the exact product no worse than 1.1x the reference's + 1e-12.
 import numpy as np
 import pytest
 
+import parity
 from conftest import golden_names, unflatten
 
 pytestmark = pytest.mark.gpu
@@ -96,48 +97,92 @@ def test_skeletons_bitexact(smash_gpu, golden, name):
             if not np.array_equal(fac[i].skel, ref):
                 mism.append((side, i, fac[i].skel.size, ref.size))
     m = g["meta"]
+    print("%s: %d factors, %d ordered-skeleton mismatches %s" % (name, total, len(mism), mism[:6]))
     if m["structure"] == "hss" and m["kernel"] == "cauchy":
-        # The HSS candidate adds the trailing kept left singular vectors of the
-        # nearfield block (hss.py:286-287); for the antisymmetric Cauchy kernel
-        # those are determined only to ~eps*sigma_1/gap (~1e-5) in ANY fp64 SVD,
-        # so near-tied pivots follow LAPACK gesdd's rounding.  Ranks must agree
-        # everywhere, ordered skeletons on >= 80% of nodes (matvec parity is
-        # checked separately at 1e-10).
+        # The HSS candidate [U_hat, S] carries the kept left singular vectors of the
+        # nearfield block (hss.py:286-287) unscaled; those near the eps_svd cut are fixed
+        # only to ~eps*sigma_1/gap by ANY fp64 SVD, so near-tied pivots follow the SVD's
+        # rounding.  The GPU sRRQR is bit-exact on the reference's own candidates
+        # (test_hss_compr_on_reference_candidates); here ranks must agree everywhere and
+        # the order mismatches stay within those of the reference's own algorithm run
+        # with another backward-stable SVD (tests/golden/hss_svd_sensitivity.py), +10% + 2.
+        sens = parity.hss_sensitivity(name)
         assert all(kg == kr for _, _, kg, kr in mism), mism[:10]
-        assert len(mism) <= 0.2 * total, (len(mism), total, mism[:10])
+        bar = int(1.1 * sens["order_mismatch"]) + 2 if sens else 0
+        assert len(mism) <= bar, (len(mism), bar, mism[:10])
     else:
         assert not mism, "skeleton mismatches (side, node, k_gpu, k_ref): %s" % mism[:10]
 
 
 @pytest.mark.parametrize("name", CASES)
 def test_transfer_G(smash_gpu, golden, name):
-    _h2_or_skip(golden, name)
+    """Transfer matrices by SURVEY 8(c) rule 3 (tests/parity.py) on every fixture that
+    stores the reference's G, H^2 and HSS.  Nodes whose ordered skeleton differs from
+    the reference (HSS-Cauchy only, see test_skeletons_bitexact) cannot be compared by
+    label; for them the GPU factor must interpolate the reference's own compr input
+    within 10x of the worse of the reference's own factor and the reference algorithm run
+    with another backward-stable SVD (tests/golden/hss_svd_sensitivity.py)."""
     g = golden(name)
     if "G_row" not in g:
-        pytest.skip("fixture stores no G")
-    if g["meta"]["structure"] == "hss":
-        # HSS panels carry the nearfield SVD's trailing singular vectors, which any
-        # fp64 SVD determines only to ~eps*sigma_1/gap; G = (R11^-1 R12)^T inherits
-        # that (and kappa(R11)), so entrywise G parity is not a well-posed check.
-        # HSS transfer parity is enforced through the matvec (<= 1e-10 vs the
-        # reference) and the exact-product error in test_matvec_vs_reference.
-        pytest.skip("HSS G checked through the matvec")
+        pytest.skip("fixture stores no G (cfg2_32k: the full-size cfg2 digest samples G)")
     M = gpu_matrix(smash_gpu, golden, name)
-    for i, f in M.rowfac.items():
-        Gr = unflatten(g["G_row_ptr"], g["G_row"], i)
-        pr = unflatten(g["fperm_row_ptr"], g["fperm_row"], i)
-        k = f.rank
-        if (g["meta"]["structure"] == "hss" and g["meta"]["kernel"] == "cauchy"
-                and not np.array_equal(pr[:k], f.perm[:k])):
-            continue  # pivot follows gesdd rounding (see test_skeletons_bitexact)
-        Xg = f.expand()
-        Xr = np.zeros_like(Xg)
-        Xr[pr[:k]] = np.eye(k)
-        if k < pr.size:
-            Xr[pr[k:]] = Gr.reshape(pr.size - k, k)
-        # conditioning-aware rule (SURVEY.md 8(c) rule 3), first clause
-        err = np.linalg.norm(Xg - Xr) / max(np.linalg.norm(Xr), 1e-300)
-        assert err <= 1e-8, (i, err)
+    bad, clause2, clause3, skipped, e1max = [], 0, 0, 0, 0.0
+    for side, fac in (("row", M.rowfac), ("col", M.colfac)):
+        for i, f in fac.items():
+            pr, Gr = parity.ref_factor(g, side, i)
+            k = f.rank
+            Xg = f.expand()
+            Xr = parity.expand(pr, Gr, k)
+            C = parity.ref_candidate(g, side, i)
+            if not np.array_equal(pr[:k], f.perm[:k]):
+                skipped += 1
+                if C is not None:
+                    ref_res = np.linalg.norm(C - Xr @ C[pr[:k]]) / np.linalg.norm(C)
+                    gpu_res = np.linalg.norm(C - Xg @ C[f.perm[:k]]) / np.linalg.norm(C)
+                    sens = parity.hss_sensitivity(name) or {}
+                    bar = max(10 * ref_res + 1e-13, 10 * sens.get("mismatched_residual_max", 0.0))
+                    assert gpu_res <= bar, (side, i, gpu_res, ref_res, bar)
+                continue
+            ok, clause, e1, e2, kappa = parity.rule3(Xg, Xr, C, pr[:k])
+            clause2 += clause == 2
+            if not ok and g["meta"]["structure"] == "hss" and parity.hss_g_ok(name, e1):
+                ok, clause = True, 3
+                clause3 += 1
+                e1max = max(e1max, e1)
+            if not ok:
+                bad.append((side, i, e1, e2, kappa))
+    assert not bad, "rule 3 failures (side, node, e1, e2, kappa): %s" % bad[:10]
+    print("%s: %d nodes by clause 2, %d by the HSS SVD-sensitivity clause (max e1 %.2e), "
+          "%d label-mismatched nodes checked by residual" % (name, clause2, clause3, e1max, skipped))
+
+
+@pytest.mark.parametrize("name", ["cfg4_2k", "pair1d_hss", "cfg1_full"])
+def test_hss_compr_on_reference_candidates(smash_gpu, golden, name):
+    """The GPU sRRQR on the reference's OWN compr inputs [U_hat, S] (S from the
+    reference's gesdd, recorded by make_golden.py): ordered skeletons bit-exact and G by
+    rule 3 on every node.  This isolates the sRRQR from the SVD -- any HSS skeleton
+    difference of the full GPU build comes from the batched SVD's rounding."""
+    g = golden(name)
+    m = g["meta"]
+    n = len(g["level"])
+    checked = 0
+    for side in ("row", "col"):
+        for i in range(n):
+            if not g["has_%s" % side][i]:
+                continue
+            C = parity.ref_candidate(g, side, i)
+            ref = unflatten(g["skel_%s_ptr" % side], g["skel_%s" % side], i)
+            ibar = parity.ref_ibar(g, side, i)
+            if C is None:
+                assert ref.size == 0
+                continue
+            f = smash_gpu.compr(C, ibar, s=2.0, rtol=m["rtol"])
+            assert np.array_equal(f.skel, ref), (side, i, f.skel[:8], ref[:8])
+            pr, Gr = parity.ref_factor(g, side, i)
+            ok, clause, e1, e2, kappa = parity.rule3(f.expand(), parity.expand(pr, Gr, f.rank), C, pr[:f.rank])
+            assert ok, (side, i, e1, e2, kappa)
+            checked += 1
+    assert checked > 0
 
 
 @pytest.mark.parametrize("name", CASES)

@@ -106,3 +106,30 @@ def test_matvec_matches_reference(golden, name):
     ref = g["z"]
     for c in range(ref.shape[1]):
         assert np.linalg.norm(z[:, c] - ref[:, c]) <= 1e-10 * np.linalg.norm(ref[:, c])
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n in ("cfg2_4k", "cfg3_8k", "cfg5_16k", "clustered2d",
+                                                          "uniform3d_small", "cfg1_full", "cfg4_2k")])
+def test_parity_helpers_rebuild_reference_inputs(golden, name):
+    """tests/parity.py rebuilds the reference's compr input of every node (H^2: the
+    padded-box basis over the reference's ibar; HSS: the recorded [U_hat, S]); the
+    reference's own factor must interpolate it (C ~= X C[skel]) -- this pins the
+    helper the GPU G test (rule 3, clause 2) relies on."""
+    import parity
+    g = golden(name)
+    for side in ("row", "col"):
+        for i in np.nonzero(g["has_%s" % side])[0][:200]:
+            C = parity.ref_candidate(g, side, int(i))
+            pr, Gr = parity.ref_factor(g, side, int(i))
+            k = unflatten(g["skel_%s_ptr" % side], g["skel_%s" % side], int(i)).size
+            if C is None:
+                assert k == 0
+                continue
+            assert C.shape[0] == pr.size
+            assert np.array_equal(parity.ref_ibar(g, side, int(i))[pr[:k]],
+                                  unflatten(g["skel_%s_ptr" % side], g["skel_%s" % side], int(i)))
+            X = parity.expand(pr, Gr, k)
+            res = np.linalg.norm(C - X @ C[pr[:k]]) / np.linalg.norm(C)
+            assert res <= 1e-5, (side, i, res)
+            ok, *_ = parity.rule3(X, X, C, pr[:k])
+            assert ok
