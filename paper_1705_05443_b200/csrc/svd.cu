@@ -528,7 +528,7 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.lb = lb; A.le = le; A.dim = t->dim; A.kernel = M->p.kernel;
   A.dx = M->p.kernel == SMASH_KERNEL_EXP ? 1.0 : M->p.dx;
   A.eps_svd = M->p.eps_svd;
-  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 58;
+  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 56;
   A.floor_rel = ldexp(1.0, -floor_exp);
   A.transpose = side;
   A.nchild = t->nchild.p; A.child_first = t->child_first.p;
