@@ -161,6 +161,10 @@ int smash_ulv_free(smash_ulv_t f);
 /* ---- matvec: replaces smash.apply.matvec_nodewise (smash/apply.py:34-80) ----
  * q: (n_col, nrhs) row-major device, z: (n_row, nrhs) row-major device; caller order. */
 int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
+/* ---- level-synchronous matvec: replaces smash.apply.matvec_levelwise (smash/apply.py:98-165)
+ * on perfect trees (status 2 otherwise, apply.py:83-95).  One launch per tree level for the
+ * transfer passes, per-level coefficient blocks, the upward sum taken child by child. */
+int smash_matvec_levelwise(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
 /* Matvec phase timing (CUDA events on the launch streams; synchronises each matvec while on).
  * Returns the accumulated per-phase milliseconds since the last reset into phase_ms[7] =
  * [gather, upward, coupling, downward, nearfield (concurrent stream), leaf far-field, whole

@@ -22,7 +22,7 @@ __all__ = [
     "OTree", "OMatrix", "norm_rows", "box_center", "box_radius", "separated",
     "build_tree", "leaf_sets", "nearfield_sets", "cheb_nodes", "lagrange_cols",
     "interp_basis", "srrqr", "compr", "truncated_svd", "kernel_block",
-    "build_h2", "build_hss", "matvec", "dense_matvec", "Factor",
+    "build_h2", "build_hss", "matvec", "matvec_levelwise", "dense_matvec", "Factor",
     "make_config_points", "CONFIGS",
 ]
 
@@ -696,6 +696,67 @@ def matvec(M: OMatrix, q: np.ndarray, cache: dict = None) -> np.ndarray:
         blk = block(("NF", i, j), lambda: kernel_block(
             M.kernel, Xr[tr.row_start[i]:tr.row_stop[i]], Xc[tr.col_start[j]:tr.col_stop[j]], M.dx))
         zt[tr.row_start[i]:tr.row_stop[i]] += blk @ qt[tr.col_start[j]:tr.col_stop[j]]
+    z = np.empty_like(zt)
+    z[tr.perm_row] = zt
+    return z[:, 0] if single else z
+
+
+def _check_perfect(tr):
+    """All leaves on the deepest level and one child count (apply.py:83-95)."""
+    width = None
+    for i in range(tr.n_nodes):
+        if tr.is_leaf(i):
+            if tr.level[i] != tr.n_levels:
+                raise ValueError("level-synchronous matvec needs all leaves at the deepest level")
+        else:
+            if width is None:
+                width = len(tr.children[i])
+            elif len(tr.children[i]) != width:
+                raise ValueError("level-synchronous matvec needs a perfect tree")
+
+
+def matvec_levelwise(M: OMatrix, q: np.ndarray) -> np.ndarray:
+    """Level-synchronous matvec on perfect trees (apply.py:98-165): per-level
+    coefficient blocks; a parent's coefficients are the sum over its children of
+    W(c)^T qbuf[c] (one product per child); couplings, then the downward sweep
+    zbuf[c] += R(c) zbuf[p] and the leaf far field, then the nearfield."""
+    tr = M.tree
+    _check_perfect(tr)
+    q = np.asarray(q, dtype=np.float64)
+    single = q.ndim == 1
+    Q = q[:, None] if single else q
+    if Q.shape[0] != tr.perm_col.size:
+        raise ValueError("vector length %d does not match matrix (%d)" % (Q.shape[0], tr.perm_col.size))
+    qt = Q[tr.perm_col]
+    nr = Q.shape[1]
+    Xr, Xc = tr.points_row, tr.points_col
+    qbuf = {}
+    for lev in range(tr.n_levels, 1, -1):
+        for i in tr.level_nodes(lev):
+            if tr.is_leaf(i):
+                qbuf[i] = M.colfac[i].expand().T @ qt[tr.col_start[i]:tr.col_stop[i]]
+            else:
+                e = None
+                for c in tr.children[i]:
+                    term = _child_rows(M, M.colfac, c).T @ qbuf[c]
+                    e = term if e is None else e + term
+                qbuf[i] = e
+    zbuf = {i: np.zeros((M.rowfac[i].rank, nr)) for lev in range(2, tr.n_levels + 1)
+            for i in tr.level_nodes(lev)}
+    for i, j in M.pairs_L:
+        zbuf[i] += kernel_block(M.kernel, Xr[M.skel_row[i]], Xc[M.skel_col[j]], M.dx) @ qbuf[j]
+    zt = np.zeros((tr.perm_row.size, nr))
+    for lev in range(2, tr.n_levels + 1):
+        for i in tr.level_nodes(lev):
+            if tr.is_leaf(i):
+                zt[tr.row_start[i]:tr.row_stop[i]] += M.rowfac[i].expand() @ zbuf[i]
+            else:
+                for c in tr.children[i]:
+                    zbuf[c] += _child_rows(M, M.rowfac, c) @ zbuf[i]
+    for i, j in M.pairs_Lm:
+        zt[tr.row_start[i]:tr.row_stop[i]] += kernel_block(
+            M.kernel, Xr[tr.row_start[i]:tr.row_stop[i]], Xc[tr.col_start[j]:tr.col_stop[j]], M.dx) \
+            @ qt[tr.col_start[j]:tr.col_stop[j]]
     z = np.empty_like(zt)
     z[tr.perm_row] = zt
     return z[:, 0] if single else z

@@ -53,27 +53,32 @@ def matvec_nodewise(M, q):
     return Z.cpu().numpy()
 
 
-def _check_perfect(tree):
-    """All leaves at the deepest level and a uniform child count (apply.py:83-95)."""
-    A = tree.arrays()
-    depth = int(A["level"].max())
-    nch = np.diff(A["child_ptr"])
-    leaf = nch == 0
-    if np.any(A["level"][leaf] != depth):
-        raise ValueError("level-synchronous matvec needs all leaves at the deepest level")
-    inner = nch[~leaf]
-    if inner.size and np.any(inner != inner[0]):
-        raise ValueError("level-synchronous matvec needs a perfect tree")
-
-
 def matvec_levelwise(M, q):
-    """Level-synchronous matvec on perfect trees (apply.py:98-165).  The device
-    matvec is already level-synchronous (one persistent upward pass ordered
-    deepest level first, the coupling of every node at once, one downward pass
-    ordered shallowest level first), so on a perfect tree this is the same
-    computation as matvec_nodewise; the reference's perfect-tree contract is kept."""
-    _check_perfect(M.tree)
-    return matvec_nodewise(M, q)
+    """Level-synchronous matvec on perfect trees (apply.py:98-165): one device
+    launch per tree level for each transfer pass, per-level coefficient blocks
+    and the upward sum taken child by child (csrc/matvec_level.cu); ValueError
+    unless every leaf is on the deepest level and every internal node has the
+    same number of children (apply.py:83-95).  Same conventions as
+    matvec_nodewise."""
+    torch = _lib.torch_cuda()
+    is_torch = isinstance(q, torch.Tensor)
+    if not is_torch:
+        q = np.asarray(q)
+    if q.shape[0] != M.n_col:
+        raise ValueError("vector length %d does not match matrix (%d)" % (q.shape[0], M.n_col))
+    single = q.ndim == 1
+    Q = _lib.to_device(q)
+    if single:
+        Q = Q.reshape(-1, 1)
+    Q = Q.contiguous()
+    Z = torch.empty((M.n_row, Q.shape[1]), dtype=torch.float64, device=Q.device)
+    _lib.check(_lib.load().smash_matvec_levelwise(M._h, _lib.ptr(Q), _lib.ptr(Z), Q.shape[1],
+                                                  _lib.stream_ptr()))
+    if single:
+        Z = Z[:, 0]
+    if is_torch:
+        return Z.to(q.device)
+    return Z.cpu().numpy()
 
 
 class MatvecStream:

@@ -274,6 +274,15 @@ int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, voi
   });
 }
 
+int smash_matvec_levelwise(smash_matrix_t m, const double* q, double* z, int64_t nrhs,
+                           void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl, SMASH_ERR_INVALID, "null matrix");
+    SMASH_CHECK(q && z, SMASH_ERR_INVALID, "null vector");
+    smash::matvec_levelwise(m->impl, q, z, nrhs, st(stream));
+  });
+}
+
 int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64_t n_own,
                                const int64_t* top_nodes, int64_t n_top, void* stream) {
   return guarded([&] {

@@ -394,6 +394,88 @@ void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_
   SMASH_CUDA(cudaGetLastError());
 }
 
+// Level-synchronous matvec on perfect trees (smash/apply.py:83-165): gather, the
+// leaves' upward projections, one upward launch per level (deepest first), the
+// coupling of every node, one downward launch per level (shallowest first), the
+// nearfield and the leaf far field + combine.  No dataflow flags, no graph: each
+// level's coefficient block is complete before the next level starts.
+namespace {
+template <int KER, int D, int RC>
+void run_chunk_level(MatrixImpl* m, MatvecPlan& P, const double* q, double* z, int64_t nrhs,
+                     int64_t c0, cudaStream_t s) {
+  TreeImpl* t = m->tree;
+  const SideFactors& R = m->rowf;
+  const SideFactors& C = *m->colf;
+  const Side rs = side_of(R), cs = side_of(C);
+  const int* perm_col = t->shared ? t->perm_row.p : t->perm_col.p;
+  const double* pts_col = t->shared ? t->pts_row.p : t->pts_col.p;
+  const int* col_a = t->shared ? t->row_a.p : t->col_a.p;
+  const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
+  launch_gather<RC>(q, nrhs, perm_col, t->ny, c0, m->qt.p, s);
+  double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;
+  XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
+              qp, P.up_pos.p, m->zhat.p, m->zd.p, cs};
+  launch_up_leaves<RC>(up, P.leaves.p, P.n_leaves, s);
+  for (int l = t->n_levels - 1; l >= 2; --l)
+    launch_level_up(cs, t->nchild.p, t->child_first.p, t->level_begin(l), t->level_end(l),
+                    m->qhat.p, RC, s);
+  CouplingArgs ca{t->n_nodes, nullptr, rs, cs, m->pl->L_ptr.p, m->pl->L_j.p, m->qhat.p,
+                  m->zhat.p, m->p.dx, P.max_rank};
+  launch_coupling<KER, D, RC>(ca, s);
+  for (int l = 2; l <= t->n_levels - 1; ++l)
+    launch_level_down(rs, t->nchild.p, t->child_first.p, t->parent.p, t->level_begin(l),
+                      t->level_end(l), m->zhat.p, m->zd.p, RC, P.max_rank, s);
+  NearArgs na{P.leaves.p, P.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
+              pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, P.slot_of.p, m->zn.p,
+              m->p.dx, t->nu0};
+  launch_near<KER, D, RC>(na, s);
+  XferArgs down{t->nchild.p, t->child_first.p, t->parent.p, t->row_a.p, t->row_b.p, m->qt.p,
+                m->qhat.p, qp, P.up_pos.p, m->zhat.p, m->zd.p, rs};
+  launch_down_leaves<RC>(down, P.leaves.p, P.n_leaves, P.zrow.p, m->zn.p, z, nrhs, c0, s);
+  SMASH_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+void matvec_levelwise(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s) {
+  SMASH_CHECK(nrhs >= 1, SMASH_ERR_INVALID, "nrhs must be positive");
+  TreeImpl* t = m->tree;
+  const int n = t->n_nodes;
+  {  // apply.py:83-95: all leaves on the deepest level, one child count
+    std::vector<int> nchild(n);
+    d2h(nchild.data(), t->nchild.p, n, s);
+    sync(s);
+    int width = -1;
+    for (int l = 1; l <= t->n_levels; ++l)
+      for (int v = t->level_begin(l); v < t->level_end(l); ++v) {
+        if (nchild[v] == 0) {
+          SMASH_CHECK(l == t->n_levels, SMASH_ERR_INVALID,
+                      "level-synchronous matvec needs all leaves at the deepest level");
+        } else {
+          SMASH_CHECK(width < 0 || nchild[v] == width, SMASH_ERR_INVALID,
+                      "level-synchronous matvec needs a perfect tree");
+          width = nchild[v];
+        }
+      }
+  }
+  MatvecPlan* P = plan_of(m, s);
+  const int rc_cap = prepare(m, P, s);
+  SMASH_CHECK(P->max_nib <= level_max_nib(), SMASH_ERR_INVALID,
+              "intermediate sets too large for the level-synchronous matvec");
+  m->order_after_last_use(s);
+  int64_t c0 = 0;
+  for (int c : chunks_of(nrhs, rc_cap)) {
+    dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
+      if (c == 16) run_chunk_level<KER, D, 16>(m, *P, q, z, nrhs, c0, s);
+      else if (c == 8) run_chunk_level<KER, D, 8>(m, *P, q, z, nrhs, c0, s);
+      else if (c == 4) run_chunk_level<KER, D, 4>(m, *P, q, z, nrhs, c0, s);
+      else if (c == 2) run_chunk_level<KER, D, 2>(m, *P, q, z, nrhs, c0, s);
+      else run_chunk_level<KER, D, 1>(m, *P, q, z, nrhs, c0, s);
+    });
+    c0 += c;
+  }
+  m->mark_use(s);
+}
+
 void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
                           const int64_t* top_post, int64_t n_top, cudaStream_t s) {
   TreeImpl* t = m->tree;

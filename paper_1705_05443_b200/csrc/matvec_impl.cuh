@@ -131,6 +131,13 @@ void launch_up_leaves(const XferArgs& a, const int* leaves, int n, cudaStream_t 
 template <int RC>
 void launch_down_leaves(const XferArgs& a, const int* leaves, int n, const int* zrow,
                         const double* zn, double* z, int64_t ldz, int64_t c0, cudaStream_t s);
+// level-synchronous transfer passes (matvec_level.cu): one launch per level
+void launch_level_up(const Side& cs, const int* nchild, const int* child_first, int lb, int le,
+                     double* qhat, int rc, cudaStream_t s);
+void launch_level_down(const Side& rs, const int* nchild, const int* child_first, const int* parent,
+                       int lb, int le, const double* zhat, double* zd, int rc, int max_rank,
+                       cudaStream_t s);
+int level_max_nib();
 void launch_leaf_slots(const Side& rs, const int* leaves, int n, const int* row_a, const int* row_b,
                        const int* perm_row, int* slot_of, int* zrow, cudaStream_t s);
 

@@ -165,6 +165,7 @@ void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t
                    int64_t* perm, int64_t* skel_ptr, int64_t* skel, int64_t* g_ptr, double* G,
                    cudaStream_t s);
 void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
+void matvec_levelwise(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
 void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launches);
 void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
                           const int64_t* top_post, int64_t n_top, cudaStream_t s);

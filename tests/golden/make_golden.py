@@ -184,6 +184,10 @@ def run_case(name, case):
     z = smash.matvec_nodewise(M, q)
     n = len(tree.nodes)
     out = dict(X=X, Y=Y, q=q, z=z, t_build=t_build)
+    try:  # the reference's level-synchronous matvec where the tree is perfect (apply.py:98-165)
+        out["z_levelwise"] = smash.matvec_levelwise(M, q)
+    except ValueError:
+        pass
     out.update(tree_arrays(tree))
     L = np.array(M.pairs_L, np.int64).reshape(-1, 2)
     Lm = np.array(M.pairs_Lm, np.int64).reshape(-1, 2)
