@@ -165,6 +165,15 @@ int smash_matvec(smash_matrix_t m, const double* q, double* z, int64_t nrhs, voi
  * on perfect trees (status 2 otherwise, apply.py:83-95).  One launch per tree level for the
  * transfer passes, per-level coefficient blocks, the upward sum taken child by child. */
 int smash_matvec_levelwise(smash_matrix_t m, const double* q, double* z, int64_t nrhs, void* stream);
+/* ---- HSS algebra: the product of diag_scale / hss_add / cauchy_like_hss results
+ * (smash/hss.py:317-400), S = sum_t diag(dl_t) A_t diag(dr_t) on one cluster tree.
+ * bases: HOST array of n_terms built matrices (repeats allowed: terms sharing a base are
+ * applied in one multi-column product); dl: (n_terms, n_row), dr: (n_terms, n_col) row-major
+ * device scalings in caller order; q (n_col, nrhs) -> z (n_row, nrhs).  levelwise = 1 applies
+ * the bases with smash_matvec_levelwise (perfect trees), 0 with smash_matvec. */
+int smash_sum_matvec(int32_t n_terms, const smash_matrix_t* bases, const double* dl,
+                     const double* dr, const double* q, double* z, int64_t nrhs, int32_t levelwise,
+                     void* stream);
 /* Matvec phase timing (CUDA events on the launch streams; synchronises each matvec while on).
  * Returns the accumulated per-phase milliseconds since the last reset into phase_ms[7] =
  * [gather, upward, coupling, downward, nearfield (concurrent stream), leaf far-field, whole

@@ -18,6 +18,7 @@ from .apply import (MatvecStream, UlvFactorization, matvec_device, matvec_levelw
                     ulv_factor, ulv_solve)
 from .dense import dense_matvec, relative_error
 from .container import load_matrix, save_matrix
+from .algebra import ScaledSumHss, cauchy_like_hss, diag_scale, hss_add
 
 __version__ = "0.1.0"
 
@@ -28,4 +29,5 @@ __all__ = [
     "dense_matvec", "relative_error", "MatvecStream",
     "nearfield_set", "well_separated", "save_matrix", "load_matrix",
     "UlvFactorization", "ulv_factor", "ulv_solve",
+    "ScaledSumHss", "cauchy_like_hss", "diag_scale", "hss_add",
 ]

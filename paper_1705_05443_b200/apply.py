@@ -14,6 +14,8 @@ __all__ = ["matvec_nodewise", "matvec_levelwise", "matvec_device", "MatvecStream
 def matvec_device(M, Q, out=None):
     """A @ Q for a CUDA float64 tensor Q of shape (n_col, nrhs); returns (n_row, nrhs)."""
     torch = _lib.torch_cuda()
+    if hasattr(M, "terms"):  # algebra result (algebra.py): sum of scaled device matrices
+        return M.matvec_device(Q, out)
     if Q.dim() != 2 or Q.shape[0] != M.n_col:
         raise ValueError("vector length %d does not match matrix (%d)" % (Q.shape[0], M.n_col))
     Q = Q.contiguous()
@@ -71,9 +73,12 @@ def matvec_levelwise(M, q):
     if single:
         Q = Q.reshape(-1, 1)
     Q = Q.contiguous()
-    Z = torch.empty((M.n_row, Q.shape[1]), dtype=torch.float64, device=Q.device)
-    _lib.check(_lib.load().smash_matvec_levelwise(M._h, _lib.ptr(Q), _lib.ptr(Z), Q.shape[1],
-                                                  _lib.stream_ptr()))
+    if hasattr(M, "terms"):  # algebra result: every base through the level-wise product
+        Z = M.matvec_device(Q, levelwise=True)
+    else:
+        Z = torch.empty((M.n_row, Q.shape[1]), dtype=torch.float64, device=Q.device)
+        _lib.check(_lib.load().smash_matvec_levelwise(M._h, _lib.ptr(Q), _lib.ptr(Z), Q.shape[1],
+                                                      _lib.stream_ptr()))
     if single:
         Z = Z[:, 0]
     if is_torch:
@@ -165,6 +170,10 @@ def ulv_factor(M) -> UlvFactorization:
     import ctypes
     if getattr(M, "kind", None) != "hss":
         raise ValueError("ULV factorization expects an HSS matrix")
+    if hasattr(M, "terms"):
+        raise NotImplementedError("the device ULV factors built (interpolative) HSS matrices; "
+                                  "algebra results (hss_add / diag_scale / cauchy_like_hss) "
+                                  "are applied with matvec_nodewise only")
     h = ctypes.c_void_p()
     rc = _lib.load().smash_ulv_factor(M._h, _lib.stream_ptr(), ctypes.byref(h))
     if rc == 3:

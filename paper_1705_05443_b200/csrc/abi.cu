@@ -283,6 +283,21 @@ int smash_matvec_levelwise(smash_matrix_t m, const double* q, double* z, int64_t
   });
 }
 
+int smash_sum_matvec(int32_t n_terms, const smash_matrix_t* bases, const double* dl,
+                     const double* dr, const double* q, double* z, int64_t nrhs,
+                     int32_t levelwise, void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(n_terms >= 1 && bases, SMASH_ERR_INVALID, "no terms");
+    SMASH_CHECK(dl && dr && q && z, SMASH_ERR_INVALID, "null vector");
+    std::vector<smash::MatrixImpl*> b(n_terms);
+    for (int t = 0; t < n_terms; ++t) {
+      SMASH_CHECK(bases[t] && bases[t]->impl, SMASH_ERR_INVALID, "null matrix");
+      b[t] = bases[t]->impl;
+    }
+    smash::sum_matvec(n_terms, b.data(), dl, dr, q, z, nrhs, levelwise, st(stream));
+  });
+}
+
 int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64_t n_own,
                                const int64_t* top_nodes, int64_t n_top, void* stream) {
   return guarded([&] {

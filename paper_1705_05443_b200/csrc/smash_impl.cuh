@@ -166,6 +166,8 @@ void matrix_export(MatrixImpl* m, int side, int64_t* has, int64_t* rank, int64_t
                    cudaStream_t s);
 void matvec(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
 void matvec_levelwise(MatrixImpl* m, const double* q, double* z, int64_t nrhs, cudaStream_t s);
+void sum_matvec(int T, MatrixImpl* const* bases, const double* dl, const double* dr,
+                const double* q, double* z, int64_t nrhs, int levelwise, cudaStream_t s);
 void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launches);
 void matvec_set_partition(MatrixImpl* m, const int64_t* own_post, int64_t n_own,
                           const int64_t* top_post, int64_t n_top, cudaStream_t s);
