@@ -54,7 +54,7 @@ struct IbarSide {
 struct SvdArgs {
   int lb, le, dim, kernel;
   double dx, eps_svd;
-  double floor_rel;  // QR truncation |R_ii| <= floor_rel |R_00|
+  double floor_rel, floor_leaf;  // QR truncation |R_ii| <= floor |R_00| (internal / leaf nodes)
   int transpose;  // 0: K(target, source) (row pass); 1: K(source, target) (column pass)
   const int* nchild;
   const int* child_first;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       const double tau = S.misc[0];
       if (tid == 0) taus[i] = tau;
       const double r0 = fabs(S.rdiag[0]);
-      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > A.floor_rel * r0)) break;  // below the noise floor
+      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > (A.nchild[v] ? A.floor_rel : A.floor_leaf) * r0)) break;
       kp = i + 1;
       for (int j = i + 1 + tid; j < nn; j += NT) {
         if (tau != 0.0) apply_reflector_g(P, ld, n, i, j, tau, S.vh);
@@ -528,8 +528,10 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.lb = lb; A.le = le; A.dim = t->dim; A.kernel = M->p.kernel;
   A.dx = M->p.kernel == SMASH_KERNEL_EXP ? 1.0 : M->p.dx;
   A.eps_svd = M->p.eps_svd;
-  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 56;
+  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 60;
+  static const int floor_leaf = getenv("SMASH_SVD_FLOOR_LEAF") ? atoi(getenv("SMASH_SVD_FLOOR_LEAF")) : 56;
   A.floor_rel = ldexp(1.0, -floor_exp);
+  A.floor_leaf = ldexp(1.0, -floor_leaf);
   A.transpose = side;
   A.nchild = t->nchild.p; A.child_first = t->child_first.p;
   A.near_ptr = near->ptr.p; A.near_idx = near->idx.p;

@@ -76,21 +76,26 @@ def small(name):
     order = rank = total = 0
     e1, res = [], []
     for side, fac in (("row", M.rowfac), ("col", M.colfac)):
+        skels = M.skel_row if side == "row" else M.skel_col
         for i, f in fac.items():
             ref = g["skel_%s" % side][g["skel_%s_ptr" % side][i]:g["skel_%s_ptr" % side][i + 1]]
             total += 1
+            ib_r, ib_a = parity.ref_ibar(g, side, i), orc._ibar(M.tree, i, skels, side)
             if f.skel.size != ref.size:
                 rank += 1
-            elif not np.array_equal(f.skel, ref):
-                order += 1
+                continue
+            X = parity.align_rows(f.expand(), ib_a, ib_r)
+            if X is None or not np.array_equal(f.skel, ref):
+                order += int(not np.array_equal(f.skel, ref))
                 C = parity.ref_candidate(g, side, i)
-                if C is not None:
+                if C is not None and X is not None:
                     # how well the alternative factor interpolates the reference's own candidate
-                    res.append(np.linalg.norm(C - f.expand() @ C[f.perm[:f.rank]]) / np.linalg.norm(C))
+                    C_a = parity.align_rows(C, ib_r, ib_a)
+                    res.append(np.linalg.norm(C_a - f.expand() @ C_a[f.perm[:f.rank]]) / np.linalg.norm(C))
             elif "G_row" in g:
                 pr, Gr = parity.ref_factor(g, side, i)
                 Xr = parity.expand(pr, Gr, f.rank)
-                e1.append(np.linalg.norm(f.expand() - Xr) / max(np.linalg.norm(Xr), 1e-300))
+                e1.append(np.linalg.norm(X - Xr) / max(np.linalg.norm(Xr), 1e-300))
     z = orc.matvec(M, g["q"])
     dz = max(np.linalg.norm(z[:, c] - g["z"][:, c]) / np.linalg.norm(g["z"][:, c]) for c in range(z.shape[1]))
     rows, ze = g["exact_rows"], g["z_exact_rows"]
@@ -120,21 +125,25 @@ def full4():
     e1, res = [], []
     for side, fac in (("row", M.rowfac), ("col", M.colfac)):
         ids = g["gs_%s_nodes" % side]
+        skels = M.skel_row if side == "row" else M.skel_col
         for t, i in enumerate(ids):
             sl = lambda key: g["gs_%s_%s" % (side, key)][g["gs_%s_%s_ptr" % (side, key)][t]:
                                                          g["gs_%s_%s_ptr" % (side, key)][t + 1]]
             f = fac[int(i)]
-            pr, Gr = sl("perm").astype(np.int64), sl("G")
+            pr, Gr, ibar = sl("perm").astype(np.int64), sl("G"), sl("ibar").astype(np.int64)
             ncol = int(g["gs_%s_cand_cols" % side][t])
             k = int(g["rank_" + side][i])
             if f.rank != k:
                 continue
+            ib_a = orc._ibar(M.tree, int(i), skels, side)
             Xr = parity.expand(pr, Gr, k)
-            if np.array_equal(f.perm[:k], pr[:k]):
-                e1.append(np.linalg.norm(f.expand() - Xr) / max(np.linalg.norm(Xr), 1e-300))
-            elif ncol:
+            X = parity.align_rows(f.expand(), ib_a, ibar)
+            if X is not None and np.array_equal(f.skel, ibar[pr[:k]]):
+                e1.append(np.linalg.norm(X - Xr) / max(np.linalg.norm(Xr), 1e-300))
+            elif X is not None and ncol:
                 C = sl("cand").reshape(-1, ncol)
-                res.append(np.linalg.norm(C - f.expand() @ C[f.perm[:k]]) / np.linalg.norm(C))
+                C_a = parity.align_rows(C, ibar, ib_a)
+                res.append(np.linalg.norm(C_a - f.expand() @ C_a[f.perm[:k]]) / np.linalg.norm(C))
     z = orc.matvec(M, q)
     rows, er = g["z_rows"].astype(np.int64), g["exact_rows"].astype(np.int64)
     dz = max(np.linalg.norm(z[rows, c] - g["z_at_rows"][:, c]) / np.linalg.norm(g["z_at_rows"][:, c])

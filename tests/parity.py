@@ -111,3 +111,29 @@ def hss_g_ok(name, e1):
     algorithm shows under another backward-stable SVD (hss_svd_sensitivity.json)."""
     s = hss_sensitivity(name)
     return s is not None and e1 <= 2 * max(s["G_e1_max"], 1e-10)
+
+
+def align_rows(X, ibar_from, ibar_to):
+    """X's rows (labelled by ibar_from) reordered into ibar_to's label order, or None
+    when the two ibar label sets differ (G rows are compared by label, SURVEY 8(c) rule 3:
+    a child whose ordered skeleton differs reorders its parent's ibar)."""
+    ibar_from = np.asarray(ibar_from)
+    ibar_to = np.asarray(ibar_to)
+    if ibar_from.size != ibar_to.size:
+        return None
+    o_from, o_to = np.argsort(ibar_from, kind="stable"), np.argsort(ibar_to, kind="stable")
+    if not np.array_equal(ibar_from[o_from], ibar_to[o_to]):
+        return None
+    idx = np.empty(ibar_to.size, np.int64)
+    idx[o_to] = o_from  # row of ibar_from carrying the label of ibar_to[r]
+    return X[idx]
+
+
+def gpu_ibar(M, side, i):
+    """ibar of node i in the GPU build: leaf range, else the children's GPU skeletons."""
+    tr = M.tree
+    kids = tr.nodes[i].children
+    if not kids:
+        return np.asarray(tr.row_range(i) if side == "row" else tr.col_range(i), np.int64)
+    fac = M.rowfac if side == "row" else M.colfac
+    return np.concatenate([np.asarray(fac[c].skel, np.int64) for c in kids])

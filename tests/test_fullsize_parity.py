@@ -146,19 +146,27 @@ def test_full_transfer_G(sg, cfg):
                 continue  # counted by test_full_skeletons (HSS-Cauchy rank cut)
             perm = E["perm"][E["perm_ptr"][i]:E["perm_ptr"][i + 1]]
             Gg = E["G"][E["g_ptr"][i]:E["g_ptr"][i + 1]]
-            Xg, Xr = parity.expand(perm, Gg, k), parity.expand(pr, Gr, k)
+            kids = A["child_idx"][A["child_ptr"][i]:A["child_ptr"][i + 1]]
+            if kids.size:
+                ib_g = np.concatenate([E["skel"][E["skel_ptr"][c]:E["skel_ptr"][c + 1]] for c in kids])
+            else:
+                a0, a1 = (A["row_start"][i], A["row_stop"][i]) if side == "row" else (A["col_start"][i], A["col_stop"][i])
+                ib_g = np.arange(a0, a1)
+            Xr = parity.expand(pr, Gr, k)
+            Xg = parity.align_rows(parity.expand(perm, Gg, k), ib_g, ibar)  # rows by label
             if ("gs_%s_cand" % src) in g:
                 ncol = int(g["gs_%s_cand_cols" % src][t])
                 C = sl("cand").reshape(-1, ncol) if ncol else None
             else:
                 lo, hi = orc.pad_box(A["lo"][i], A["hi"][i], pad)
                 C = orc.interp_basis(lo, hi, pts[ibar], c["r"])
-            if not np.array_equal(perm[:k], pr[:k]):
+            if Xg is None or not np.array_equal(ib_g[perm[:k]], ibar[pr[:k]]):
                 n_label += 1
                 assert c["structure"] == "hss", (side, i)
-                if C is not None:
+                if C is not None and Xg is not None:
+                    C_g = parity.align_rows(C, ibar, ib_g)
                     rr = np.linalg.norm(C - Xr @ C[pr[:k]]) / np.linalg.norm(C)
-                    rg = np.linalg.norm(C - Xg @ C[perm[:k]]) / np.linalg.norm(C)
+                    rg = np.linalg.norm(C_g - parity.expand(perm, Gg, k) @ C_g[perm[:k]]) / np.linalg.norm(C)
                     bar = max(10 * rr + 1e-13, 10 * parity.hss_sensitivity("full4")["mismatched_residual_max"])
                     assert rg <= bar, (side, i, rg, rr, bar)
                 continue
