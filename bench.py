@@ -511,11 +511,17 @@ def run_ours(args):
         zd = out.cpu().numpy()
         assert np.array_equal(zd, z.numpy()), "device and e2e results differ"
         parity = golden_parity(cfg, N, R, zd)
-    else:  # sharded (full, gathered) vs the single-GPU matvec
-        zf = sg.matvec_device(M, dQ).cpu().numpy()
+    else:  # sharded (full, gathered) vs a single-GPU build + matvec on this rank
+        tree1 = sg.build_tree(sg.PointSet(dX), nu0=c["nu0"], mode=c["mode"], tau=c["tau"])
+        R1 = builder(tree1, spec, None, None, params)
+        zf = sg.matvec_device(R1, dQ).cpu().numpy()
+        del R1
         rel = np.linalg.norm(z.numpy() - zf) / np.linalg.norm(zf)
         assert rel <= 1e-12, "sharded matvec differs from the single-GPU one: %g" % rel
-        parity = {"sharded_vs_single_gpu_rel": float(rel)}
+        parity = {"sharded_vs_single_gpu_rel": float(rel),
+                  "halo_bytes_per_matvec": int(sm.halo_bytes(R)),
+                  "all_gather_bytes_per_matvec": int(sm.half * R * 8 * (ws - 1))}
+        parity.update(golden_parity(cfg, N, R, z.numpy()) or {})
 
     # ---- rooflines: dominant FP64 kernel, transfer passes (HBM), construction
     W = work_counts(sg, M, c, R, owned, top)
@@ -584,7 +590,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
             "config": workload_config(cfg, N, R),
             "build_s": b_s,
-            "build_mode": "sharded (cut-level exchange)" if ws > 1 else "single",
+            "build_mode": "sharded: work-balanced cut, skeleton exchange, factors kept on their owner"
+                          if ws > 1 else "single",
             "phase_ms": {"gather": phase[0], "upward": phase[1], "coupling": ms_coup, "downward": phase[3],
                          "nearfield_concurrent": ms_near, "leaf_farfield": phase[5],
                          "matvec_profiled": phase[6],

@@ -118,6 +118,19 @@ int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream
  * on every rank.  The result equals smash_matrix_build's bit for bit. */
 int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_t rank,
                              int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out);
+/* As smash_matrix_build_local, with cut_weight (HOST float64[number of cut-level nodes],
+ * left to right; NULL = subtree point counts) balancing the contiguous cut-level ranges,
+ * and replicate = 0 to keep the factors sharded: perm and G are then NOT in the exchange list,
+ * so every rank ends with the factors of its own subtrees and of the levels above the cut
+ * only (enough for the sharded matvec over the same partition, smash_matrix_shard_owner). */
+int smash_matrix_build_local_w(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                               int32_t world, int32_t cut_level, const double* cut_weight,
+                               int32_t replicate, void* stream, smash_matrix_t* out);
+/* cut level a sharded build over world ranks uses (cut_level < 2: the default rule); host out */
+int smash_matrix_shard_cut(smash_tree_t t, int32_t world, int32_t cut_level, int32_t* cut);
+/* owning rank of every node of a sharded build (HOST int64[n_nodes], postorder; -1 above the
+ * cut: replicated on every rank) */
+int smash_matrix_shard_owner(smash_matrix_t m, int64_t* owner_post);
 int smash_matrix_exchange_buffers(smash_matrix_t m, int64_t capacity, int64_t* n, void** ptrs,
                                   int64_t* counts, int32_t* dtypes);
 int smash_matrix_build_finish(smash_matrix_t m, void* stream);
@@ -193,6 +206,12 @@ int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64
                                const int64_t* top_nodes, int64_t n_top, void* stream);
 int smash_matvec_stage(smash_matrix_t m, int32_t stage, const double* q, double* z, int64_t nrhs,
                        void* stream);
+/* layout of that buffer (HOST outputs): row_off_post[n_nodes] = first row of each node's
+ * skeleton coefficients (postorder; -1 for the root / rank-0 nodes), up_pos[half_rows] = row in
+ * the second half (coefficients in the parent's ibar order, minus half_rows) of every
+ * coefficient row (-1 below the root) or NULL, half_rows = rows of each half */
+int smash_matvec_coeff_layout(smash_matrix_t m, int64_t* row_off_post, int64_t* up_pos,
+                              int64_t* half_rows, void* stream);
 /* device pointer of the coefficient buffer exchanged between stages: rows x nrhs doubles */
 int smash_matvec_coeffs(smash_matrix_t m, double** qhat, int64_t* rows);
 int smash_matrix_free(smash_matrix_t m);

@@ -54,6 +54,10 @@ SIGNATURES = {
     "smash_ulv_free": (c_i32, [c_vp]),
     "smash_matvec": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "smash_matvec_levelwise": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "smash_matrix_build_local_w": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp, c_vp]),
+    "smash_matrix_shard_cut": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
+    "smash_matrix_shard_owner": (c_i32, [c_vp, c_vp]),
+    "smash_matvec_coeff_layout": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "smash_sum_matvec": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "smash_matvec_profile": (c_i32, [c_vp, c_i32, P_dbl, P_i64]),
     "smash_matvec_set_partition": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),

@@ -16,6 +16,9 @@ def matvec_device(M, Q, out=None):
     torch = _lib.torch_cuda()
     if hasattr(M, "terms"):  # algebra result (algebra.py): sum of scaled device matrices
         return M.matvec_device(Q, out)
+    if getattr(M, "sharded_factors", False):
+        raise ValueError("this rank holds only its share of the factors (build_h2_sharded with "
+                         "replicate_factors=False): apply it with shard.ShardedMatvec")
     if Q.dim() != 2 or Q.shape[0] != M.n_col:
         raise ValueError("vector length %d does not match matrix (%d)" % (Q.shape[0], M.n_col))
     Q = Q.contiguous()

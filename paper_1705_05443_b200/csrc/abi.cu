@@ -163,8 +163,54 @@ int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_
                              int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out) {
   return guarded([&] {
     SMASH_CHECK(t && t->impl && p && out, SMASH_ERR_INVALID, "null argument");
-    smash::MatrixImpl* m = smash::matrix_build_local(t->impl, *p, rank, world, cut_level, st(stream));
+    smash::MatrixImpl* m = smash::matrix_build_local(t->impl, *p, rank, world, cut_level, nullptr, 1,
+                                                     st(stream));
     *out = new smash_matrix_s{m};
+  });
+}
+
+int smash_matrix_build_local_w(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                               int32_t world, int32_t cut_level, const double* cut_weight,
+                               int32_t replicate, void* stream, smash_matrix_t* out) {
+  return guarded([&] {
+    SMASH_CHECK(t && t->impl && p && out, SMASH_ERR_INVALID, "null argument");
+    smash::MatrixImpl* m = smash::matrix_build_local(t->impl, *p, rank, world, cut_level, cut_weight,
+                                                     replicate, st(stream));
+    *out = new smash_matrix_s{m};
+  });
+}
+
+int smash_matrix_shard_cut(smash_tree_t t, int32_t world, int32_t cut_level, int32_t* cut) {
+  return guarded([&] {
+    SMASH_CHECK(t && t->impl && cut && world >= 1, SMASH_ERR_INVALID, "bad argument");
+    const smash::TreeImpl* ti = t->impl;
+    const int L = ti->n_levels;
+    int c = L;
+    for (int l = 2; l <= L; ++l)
+      if (ti->level_end(l) - ti->level_begin(l) >= 8 * world) { c = l; break; }
+    if (cut_level >= 2 && cut_level <= L) c = cut_level;
+    *cut = c;
+  });
+}
+
+int smash_matrix_shard_owner(smash_matrix_t m, int64_t* owner_post) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl && owner_post, SMASH_ERR_INVALID, "null argument");
+    const smash::MatrixImpl* mi = m->impl;
+    SMASH_CHECK(!mi->shard_owner.empty(), SMASH_ERR_INVALID, "matrix was not built sharded");
+    const smash::TreeImpl* ti = mi->tree;
+    std::vector<int> post(ti->n_nodes);
+    smash::d2h(post.data(), ti->post.p, ti->n_nodes, ti->stream);
+    smash::sync(ti->stream);
+    for (int v = 0; v < ti->n_nodes; ++v) owner_post[post[v]] = mi->shard_owner[v];
+  });
+}
+
+int smash_matvec_coeff_layout(smash_matrix_t m, int64_t* row_off_post, int64_t* up_pos,
+                              int64_t* half_rows, void* stream) {
+  return guarded([&] {
+    SMASH_CHECK(m && m->impl && row_off_post && half_rows, SMASH_ERR_INVALID, "null argument");
+    smash::matvec_coeff_layout(m->impl, row_off_post, up_pos, half_rows, st(stream));
   });
 }
 

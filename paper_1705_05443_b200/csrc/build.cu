@@ -695,6 +695,7 @@ struct ShardState {
   DevTables D;
   std::unique_ptr<SideBuild> rowb;
   int cut = 0, rank = 0, world = 1;
+  bool replicate = true;            // exchange perm and G too (every rank holds the full matrix)
   std::vector<int> own_lb, own_le;  // per level l (>= cut): owned BFS range
   DBuf<int> tmp_lab;                // ordered skeleton labels of levels L..cut (perm layout)
   DBuf<double> tmp_pts;             // [dim][tmp_len]
@@ -704,7 +705,8 @@ struct ShardState {
 };
 
 MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int rank, int world,
-                               int cut_level, cudaStream_t s) {
+                               int cut_level, const double* cut_weight, int replicate,
+                               cudaStream_t s) {
   SMASH_CHECK(p.structure == SMASH_STRUCT_H2, SMASH_ERR_INVALID,
               "sharded construction supports the H2 structure");
   SMASH_CHECK(world >= 1 && rank >= 0 && rank < world, SMASH_ERR_INVALID, "bad rank / world size");
@@ -738,7 +740,9 @@ MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int ran
   st->cut = cut;
   st->rank = rank;
   st->world = world;
-  // balance contiguous cut-level ranges by subtree point counts
+  st->replicate = replicate != 0;
+  // balance contiguous cut-level ranges by the caller's per-node weights (left to right,
+  // e.g. the subtrees' coupling + nearfield work), else by subtree point counts
   const int n = t->n_nodes;
   std::vector<int> ra(n), rb(n), par(n);
   d2h(ra.data(), t->row_a.p, n, s);
@@ -747,13 +751,14 @@ MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int ran
   sync(s);
   const int cb = t->level_begin(cut), ce = t->level_end(cut);
   std::vector<int> owner(n, -1);
-  int64_t total = 0;
-  for (int v = cb; v < ce; ++v) total += rb[v] - ra[v];
-  int64_t acc = 0;
+  auto weight = [&](int v) { return cut_weight ? cut_weight[v - cb] : (double)(rb[v] - ra[v]); };
+  double total = 0;
+  for (int v = cb; v < ce; ++v) total += weight(v);
+  double acc = 0;
   for (int v = cb; v < ce; ++v) {
-    const double mid = acc + 0.5 * (rb[v] - ra[v]);
-    owner[v] = std::min(world - 1, (int)(mid * world / std::max<int64_t>(total, 1)));
-    acc += rb[v] - ra[v];
+    const double mid = acc + 0.5 * weight(v);
+    owner[v] = std::min(world - 1, (int)(mid * world / std::max(total, 1e-300)));
+    acc += weight(v);
   }
   st->own_lb.assign(L + 2, 0);
   st->own_le.assign(L + 2, 0);
@@ -766,6 +771,7 @@ MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int ran
     st->own_lb[l] = lo < 0 ? 0 : lo;
     st->own_le[l] = lo < 0 ? 0 : hi;
   }
+  M->shard_owner = owner;  // BFS: rank owning the subtree, -1 above the cut (replicated)
   // exchanged buffers: zero them (owned slots are written, the rest stays 0)
   st->perm_len = std::max<int64_t>(B.lvl_ib_base[cut] + B.lvl_ib_b[cut], 1);
   st->g_len = std::max<int64_t>(M->rowf.g_total, 1);  // whole G (top levels are zero too)
@@ -803,10 +809,10 @@ void matrix_exchange_buffers(MatrixImpl* m, std::vector<ExchangeBuf>& out) {
   out.clear();
   out.push_back({m->rowf.rank.p, (int64_t)n, 0});
   out.push_back({m->rowf.nib.p, (int64_t)n, 0});
-  out.push_back({m->rowf.perm.p, st->perm_len, 0});
+  if (st->replicate) out.push_back({m->rowf.perm.p, st->perm_len, 0});
   out.push_back({st->tmp_lab.p, st->tmp_len, 0});
   out.push_back({st->err32.p, 1, 0});
-  out.push_back({m->rowf.G.p, st->g_len, 1});
+  if (st->replicate) out.push_back({m->rowf.G.p, st->g_len, 1});
   out.push_back({st->tmp_pts.p, st->tmp_len * m->tree->dim, 1});
   out.push_back({st->swaps64.p, 1, 2});
 }

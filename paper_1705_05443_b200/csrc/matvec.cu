@@ -568,6 +568,25 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
   SMASH_CUDA(cudaGetLastError());
 }
 
+void matvec_coeff_layout(MatrixImpl* m, int64_t* row_off_post, int64_t* up_pos, int64_t* half_rows,
+                         cudaStream_t s) {
+  TreeImpl* t = m->tree;
+  MatvecPlan* P = plan_of(m, s);
+  const int n = t->n_nodes;
+  const SideFactors& C = *m->colf;
+  std::vector<int> post(n), off(n), rk(n);
+  d2h(post.data(), t->post.p, n, s);
+  d2h(off.data(), C.skel_off.p, n, s);
+  d2h(rk.data(), C.rank.p, n, s);
+  std::vector<int> up(std::max<int64_t>(C.skel_total, 1));
+  d2h(up.data(), P->up_pos.p, up.size(), s);
+  sync(s);
+  for (int v = 0; v < n; ++v) row_off_post[post[v]] = (v == 0 || rk[v] == 0) ? -1 : off[v];
+  if (up_pos)
+    for (int64_t x = 0; x < C.skel_total; ++x) up_pos[x] = up[x];
+  *half_rows = std::max<int64_t>(C.skel_total, 1);
+}
+
 void matvec_coeffs(MatrixImpl* m, double** qhat, int64_t* rows) {
   *qhat = m->qhat.p;  // qhat | qp (both exchanged between the stages)
   *rows = 2 * std::max<int64_t>(m->colf->skel_total, 1);

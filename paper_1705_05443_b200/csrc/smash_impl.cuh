@@ -117,6 +117,8 @@ struct MatrixImpl {
   // for the previous one, whatever stream it ran on, and the matrix is freed only after
   // its last product completes.
   cudaEvent_t last_use = nullptr;
+  // sharded build: owning rank of every node (BFS), -1 above the cut level; empty otherwise
+  std::vector<int> shard_owner;
   void order_after_last_use(cudaStream_t s) {
     if (!last_use) SMASH_CUDA(cudaEventCreateWithFlags(&last_use, cudaEventDisableTiming));
     SMASH_CUDA(cudaStreamWaitEvent(s, last_use, 0));
@@ -146,7 +148,10 @@ struct ExchangeBuf {
   int dtype;  // 0 int32, 1 float64, 2 int64
 };
 MatrixImpl* matrix_build_local(TreeImpl* t, const smash_build_params& p, int rank, int world,
-                               int cut_level, cudaStream_t s);
+                               int cut_level, const double* cut_weight, int replicate,
+                               cudaStream_t s);
+void matvec_coeff_layout(MatrixImpl* m, int64_t* row_off_post, int64_t* up_pos, int64_t* half_rows,
+                         cudaStream_t s);
 // saved factors of one side, postorder-indexed host arrays (smash_matrix_import)
 struct ImportSide {
   const int64_t* rank;

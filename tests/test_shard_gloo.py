@@ -1,11 +1,13 @@
 """Multi-rank host logic of the sharded matvec (paper_1705_05443_b200/shard.py),
 run with torch.distributed gloo, world_size 2 and 3, on CPU.
 
-Each rank executes the same staged algorithm the GPU path runs (partition ->
-local upward of owned subtrees -> all-reduce of the coefficients -> top upward,
-coupling / downward for owned + top targets, nearfield + far field for owned
-leaves -> all-reduce of z), with numpy on the oracle's factors, and the result
-must equal the single-process oracle matvec."""
+Each rank executes the same staged algorithm the GPU path runs (work-balanced cut
+partition -> local upward of owned subtrees -> halo all-to-all of exactly the
+coefficient rows halo_rows() lists -> top upward, coupling / downward for owned +
+top targets, nearfield + far field for owned leaves -> all-reduce of z), with numpy
+on the oracle's factors; the result must equal the single-process oracle matvec.
+Coefficients that are neither owned, replicated nor received stay NaN, so a missing
+halo row cannot go unnoticed."""
 
 import os
 import socket
@@ -18,7 +20,7 @@ import torch.multiprocessing as mp
 
 from conftest import load_golden
 from oracle import smash_oracle as orc
-from paper_1705_05443_b200.shard import partition
+from paper_1705_05443_b200.shard import cut_partition, halo_rows, own_top_leaves, partition, subtree_work
 
 
 def tree_arrays(t):
@@ -28,21 +30,23 @@ def tree_arrays(t):
         cp[i + 1] = cp[i] + len(c)
     ci = np.array([c for ch in t.children for c in ch], np.int64)
     return dict(child_ptr=cp, child_idx=ci, row_start=t.row_start, row_stop=t.row_stop,
-                level=t.level)
+                col_start=t.col_start, col_stop=t.col_stop, level=t.level, parent=t.parent)
 
 
-def staged_matvec(M, q, owned, top):
-    """One rank's stages (numpy mirror of smash_matvec_stage 1/2)."""
+def staged_matvec(M, q, owner, rank, world):
+    """One rank's stages (numpy mirror of smash_matvec_stage 1 / halo / 2)."""
     tr = M.tree
     n = tr.n_nodes
     root = tr.root
+    owned = np.nonzero(owner == rank)[0]
+    top = np.nonzero(owner < 0)[0]
     qt = q[tr.perm_col]
     R = q.shape[1]
-    kcol = {v: M.colfac[v].rank for v in M.colfac}
+    kcol = np.array([M.colfac[v].rank if v in M.colfac else 0 for v in range(n)], np.int64)
     off = np.zeros(n + 1, np.int64)
-    for v in range(n):
-        off[v + 1] = off[v] + kcol.get(v, 0)
-    buf = np.zeros((off[-1], R))
+    off[1:] = np.cumsum(kcol)
+    row_off = np.where(kcol > 0, off[:-1], -1)
+    buf = np.full((off[-1], R), np.nan)
 
     def up(v):
         if tr.is_leaf(v):
@@ -53,9 +57,14 @@ def staged_matvec(M, q, owned, top):
 
     for v in sorted((v for v in owned if v != root), key=lambda v: -tr.level[v]):
         up(v)
-    t = torch.from_numpy(buf)
-    dist.all_reduce(t)  # disjoint supports: the all-gather of the coefficients
-    buf = t.numpy()
+    rows, _ = halo_rows(owner, tr.parent, M.pairs_L, row_off, kcol, world)
+    send = torch.from_numpy(np.ascontiguousarray(
+        np.concatenate([buf[rows[rank][s_]] for s_ in range(world)]).reshape(-1)))
+    recv_rows = np.concatenate([rows[s_][rank] for s_ in range(world)])
+    recv = torch.empty(recv_rows.size * R, dtype=torch.float64)
+    dist.all_to_all_single(recv, send, [rows[s_][rank].size * R for s_ in range(world)],
+                           [rows[rank][s_].size * R for s_ in range(world)])
+    buf[recv_rows] = recv.numpy().reshape(-1, R)
     for v in sorted((v for v in top if v != root), key=lambda v: -tr.level[v]):
         up(v)
     targets = set(int(v) for v in owned) | set(int(v) for v in top)
@@ -101,12 +110,18 @@ def _worker(rank, world, port, name, ret):
         tree = orc.build_tree(g["X"], None, nu0=m["nu0"], mode=m["mode"])
         M = orc.build_h2(tree, m["kernel"], m["r"], m["tau"], rtol=m["rtol"],
                          dx=None if m["kernel"] == "exp" else 0.0, symmetric=True)
-        owned, top, frontier = partition(tree_arrays(tree), world)
-        z = staged_matvec(M, g["q"], owned[rank], top)
+        A = tree_arrays(tree)
+        L, Lm = np.asarray(M.pairs_L), np.asarray(M.pairs_Lm)
+        w = subtree_work(A, L, Lm, m["r"])
+        cut = next((l for l in range(2, tree.n_levels + 1) if np.sum(A["level"] == l) >= 8 * world),
+                   tree.n_levels)
+        owner, cut_nodes = cut_partition(A, world, cut, w[A["level"] == cut])
+        owner = own_top_leaves(A, owner, world, w)
+        z = staged_matvec(M, g["q"], owner, rank, world)
         if rank == 0:
             zr = orc.matvec(M, g["q"])
             ret.put((float(np.linalg.norm(z - zr) / np.linalg.norm(zr)),
-                     [int(o.size) for o in owned], len(frontier)))
+                     [int(np.sum(owner == r)) for r in range(world)], len(cut_nodes)))
     finally:
         dist.destroy_process_group()
 
@@ -134,6 +149,30 @@ def test_sharded_matvec_gloo(name, world):
     rel, sizes, nf = ret.get(timeout=10)
     assert rel <= 1e-13, rel
     assert all(s > 0 for s in sizes) and nf >= 8 * world
+
+
+def test_cut_partition_balances_work():
+    """Work-balanced cut partition (the rule smash_matrix_build_local_w applies): every
+    node owned once or replicated, owned subtrees contiguous, and the ranks' matvec work
+    within the granularity of one cut-level subtree of each other."""
+    g = load_golden("cfg5_16k")
+    m = g["meta"]
+    tree = orc.build_tree(g["X"], None, nu0=m["nu0"], mode=m["mode"])
+    A = tree_arrays(tree)
+    OM = orc.build_h2(tree, m["kernel"], m["r"], m["tau"], rtol=m["rtol"], dx=0.0, symmetric=True)
+    w = subtree_work(A, np.asarray(OM.pairs_L), np.asarray(OM.pairs_Lm), m["r"])
+    for world in (2, 4, 8):
+        cut = next(l for l in range(2, tree.n_levels + 1) if np.sum(A["level"] == l) >= 8 * world)
+        owner, cut_nodes = cut_partition(A, world, cut, w[A["level"] == cut])
+        for v in range(tree.n_nodes):  # subtrees inherit their cut node's owner
+            if owner[v] >= 0 and tree.level[v] > cut:
+                assert owner[v] == owner[tree.parent[v]]
+        per = np.array([w[cut_nodes][owner[cut_nodes] == r].sum() for r in range(world)])
+        assert per.min() > 0
+        assert per.max() - per.min() <= 2 * w[cut_nodes].max() + 1e-9
+        o2 = own_top_leaves(A, owner, world, w)
+        leaves = np.array([tree.is_leaf(v) for v in range(tree.n_nodes)])
+        assert np.all(o2[leaves] >= 0)
 
 
 def test_partition_covers_every_node_once():

@@ -78,7 +78,7 @@ def _worker(rank, world, port, cfg, N, out):
     torch.cuda.set_device(0)
     import paper_1705_05443_b200 as sg
     tree, spec, params, q = _case(sg, cfg, N)
-    M = sg.build_h2_sharded(tree, spec, None, None, params)
+    M = sg.build_h2_sharded(tree, spec, None, None, params, replicate_factors=True)
     R = sg.build_h2(tree, spec, None, None, params)
     ok = True
     try:
@@ -104,3 +104,67 @@ def test_sharded_two_processes_gloo(sg):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def _worker_sharded(rank, world, port, cfg, N, out):
+    """Sharded factors (replicate_factors=False) + ShardedMatvec with the halo all-to-all:
+    the owned + top factors equal the single-GPU build's bit for bit, and the gathered
+    product equals the single-GPU matvec."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1705_05443_b200 as sg
+    from paper_1705_05443_b200.shard import ShardedMatvec
+    tree, spec, params, q = _case(sg, cfg, N)
+    M = sg.build_h2_sharded(tree, spec, None, None, params)
+    R = sg.build_h2(tree, spec, None, None, params)
+    res = {}
+    try:
+        sm = ShardedMatvec(M)
+        mine = set(int(v) for v in np.nonzero((M.shard_owner == rank) | (M.shard_owner < 0))[0])
+        ok = True
+        for side in (0, 1):
+            a, b = M.export_side(side), R.export_side(side)
+            for v in mine:
+                if not a["has"][v]:
+                    continue
+                for key, ptr in (("perm", "perm_ptr"), ("G", "g_ptr"), ("skel", "skel_ptr")):
+                    ok &= bool(np.array_equal(a[key][a[ptr][v]:a[ptr][v + 1]], b[key][b[ptr][v]:b[ptr][v + 1]]))
+        Q = torch.from_numpy(q).cuda()
+        z = sm(Q, gather_output=True).cpu().numpy()
+        zr = sg.matvec_nodewise(R, q)
+        rel = float(np.linalg.norm(z - zr) / np.linalg.norm(zr))
+        try:
+            sg.matvec_nodewise(M, q)
+            guarded = False
+        except ValueError:
+            guarded = True
+        res = dict(ok=ok, rel=rel, guarded=guarded, halo=sm.halo_rows_total,
+                   rows=int(sm.half))
+    except Exception as e:  # report instead of hanging the other rank
+        res = dict(err=repr(e))
+    out.put((rank, res))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,N,world", [(2, 1 << 14, 2), (5, 1 << 15, 2), (3, 1 << 13, 3)])
+def test_sharded_factors_and_matvec_processes_gloo(sg, cfg, N, world):
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, world, port, cfg, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert "err" not in res[r], res[r]
+        assert res[r]["ok"] and res[r]["guarded"], res[r]
+        assert res[r]["rel"] <= 1e-13, res[r]
+        assert res[r]["halo"] < 2 * res[r]["rows"]  # the halo is not an all-gather
