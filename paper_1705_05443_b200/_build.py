@@ -17,14 +17,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 TRACE = os.environ.get("SMASH_TRACE") == "1"  # instrumented build (tools/xfer_trace.py)
-OBJ = os.path.join(REPO, "build", "obj_trace" if TRACE else "obj")
-LIB = os.path.join(HERE, "libsmash_b200_trace.so" if TRACE else "libsmash_b200.so")
+CHECKED = os.environ.get("SMASH_CHECKED") == "1"  # device asserts + bounded spin waits
+_VARIANT = "_trace" if TRACE else "_checked" if CHECKED else ""
+OBJ = os.path.join(REPO, "build", "obj" + _VARIANT)
+LIB = os.path.join(HERE, "libsmash_b200%s.so" % _VARIANT)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "--extended-lambda", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-I" + os.path.join(REPO, "include")] + (
-             ["-DSMASH_XFER_TRACE", "-DSMASH_COMPRESS_PROF"] if TRACE else [])
+             ["-DSMASH_XFER_TRACE", "-DSMASH_COMPRESS_PROF"] if TRACE else
+             ["-DSMASH_CHECKED"] if CHECKED else [])
 
 
 def _sources():

@@ -18,6 +18,16 @@
 
 #include "../../include/smash_b200.h"
 
+// Checked build (SMASH_CHECKED=1 in _build.py -> libsmash_b200_checked.so): device-side
+// bounds / invariant asserts and bounded spin waits that trap instead of hanging -- the
+// stand-in for compute-sanitizer, which this GPU pool does not allow.
+#ifdef SMASH_CHECKED
+#include <cassert>
+#define SMASH_DASSERT(cond) assert(cond)
+#else
+#define SMASH_DASSERT(cond) ((void)0)
+#endif
+
 namespace smash {
 
 // ---------------------------------------------------------------------------

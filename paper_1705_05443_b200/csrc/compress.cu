@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(COMPRESS_THREADS, MODE == 0 ? 2 : 4) k_compres
   for (int v = A.lb + blockIdx.x; v < A.le;) {
     const int n = A.nib[v];
     const int mrows = A.Cexp ? A.C_cols : A.r + (A.keep ? A.keep[v] : 0);
+    SMASH_DASSERT(n >= 0 && n <= A.nmax && mrows <= A.mmax);
     const NodeSrc src = A.Cexp ? NodeSrc{nullptr, 0, nullptr, 0} : node_src(A, v);
     if (n == 0) {  // (uniform branch) everyone has read v before it is overwritten
       __syncthreads();

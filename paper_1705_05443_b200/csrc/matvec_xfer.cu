@@ -291,8 +291,15 @@ __global__ void __launch_bounds__(XFER_THREADS + 32) k_upward(XferArgs A, XferGe
       if (nk4 <= Gm.tb)
         for (int e = tid; e < (nk4 - nk) * k; e += XFER_THREADS) gs[(nk + e / k) * ks + e % k] = 0.0;
       for (int e = tid; e < (nk4 - nk) * rcs; e += XFER_THREADS) ivp[ni * rcs + e] = 0.0;
-      if (tid < 32 && ((d.wait >> tid) & 1u))
+      SMASH_DASSERT(ni <= Gm.max_nib && k <= Gm.max_rank && d.nc <= 32);
+      if (tid < 32 && ((d.wait >> tid) & 1u)) {
+#ifdef SMASH_CHECKED
+        long long spins = 0;
+        while (ld_acquire(&done[d.cf + tid]) == 0u) { __nanosleep(32); SMASH_DASSERT(++spins < (1ll << 26)); }
+#else
         while (ld_acquire(&done[d.cf + tid]) == 0u) __nanosleep(32);
+#endif
+      }
       bar_compute();
       TRACE_SET(t1);
       const double* in = A.qp + (int64_t)d.base * RC;
@@ -416,8 +423,16 @@ __global__ void __launch_bounds__(XFER_THREADS + 32) k_downward(XferArgs A, Xfer
       for (int j = tid; j < ni; j += XFER_THREADS) pm[j] = perm[j];
       for (int e = tid; e < (k4 - k) * rcs; e += XFER_THREADS) zv[k * rcs + e] = 0.0;
       const bool from_parent = d.parent > 0;
+      SMASH_DASSERT(ni <= Gm.max_nib && k <= Gm.max_rank);
       if (tid == 0 && d.wait)
+      {
+#ifdef SMASH_CHECKED
+        long long spins = 0;
+        while (ld_acquire(&done[d.parent]) == 0u) { __nanosleep(32); SMASH_DASSERT(++spins < (1ll << 26)); }
+#else
         while (ld_acquire(&done[d.parent]) == 0u) __nanosleep(32);
+#endif
+      }
       bar_compute();
       TRACE_SET(t1);
       const double* zsrc = A.zhat + (int64_t)d.skel * RC;

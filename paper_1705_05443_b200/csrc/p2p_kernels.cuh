@@ -153,6 +153,7 @@ __device__ __forceinline__ void mma_issue(const SegTable& T, int p, int total, c
       if (T.pre[mid] <= p) lo = mid; else hi = mid - 1;
     }
     row = T.off[lo] + (p - T.pre[lo]);
+    SMASH_DASSERT(row >= 0 && p - T.pre[lo] < T.pre[lo + 1] - T.pre[lo]);
   }
 #pragma unroll
   for (int a = 0; a < D; ++a) cp_async8z(sc + a * 32 + lane, spts + (int64_t)a * sstride + row, ok);
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(P2P_THREADS, p2p_min_blocks<MT>()) k_coupling(
   const int k = A.rs.rank[v];
   if (k == 0) return;
   const int to = A.rs.skel_off[v];
+  SMASH_DASSERT(k <= A.max_targets && to >= 0);
   const Side cs = A.cs;
   const int* Lsrc = A.Lsrc;
   auto seg = [&](int e) {
@@ -355,6 +357,7 @@ __global__ void __launch_bounds__(P2P_THREADS, p2p_min_blocks<MT>()) k_near(Near
   if (li >= A.n_leaves) return;
   const int v = A.leaves[li];
   const int ra = A.row_a[v], nr = A.row_b[v] - ra;
+  SMASH_DASSERT(nr >= 0 && nr <= A.max_targets && ra + nr <= A.nrow);
   const int* col_a = A.col_a;
   const int* col_b = A.col_b;
   const int* Lmsrc = A.Lmsrc;

@@ -74,7 +74,7 @@ def small(name):
     m = g["meta"]
     M = build_alt(g["X"], g["Y"], m)
     order = rank = total = 0
-    e1, res = [], []
+    e1, res, ek = [], [], []
     for side, fac in (("row", M.rowfac), ("col", M.colfac)):
         skels = M.skel_row if side == "row" else M.skel_col
         for i, f in fac.items():
@@ -96,11 +96,16 @@ def small(name):
                 pr, Gr = parity.ref_factor(g, side, i)
                 Xr = parity.expand(pr, Gr, f.rank)
                 e1.append(np.linalg.norm(X - Xr) / max(np.linalg.norm(Xr), 1e-300))
+                C = parity.ref_candidate(g, side, i)
+                if C is not None and f.rank:
+                    sv = np.linalg.svd(C[pr[:f.rank]], compute_uv=False)
+                    ek.append(e1[-1] / (sv[0] / sv[-1]) if sv[-1] > 0 else 0.0)
     z = orc.matvec(M, g["q"])
     dz = max(np.linalg.norm(z[:, c] - g["z"][:, c]) / np.linalg.norm(g["z"][:, c]) for c in range(z.shape[1]))
     rows, ze = g["exact_rows"], g["z_exact_rows"]
     return dict(factors=total, order_mismatch=order, rank_mismatch=rank,
                 G_e1_median=float(np.median(e1)) if e1 else 0.0, G_e1_max=float(np.max(e1)) if e1 else 0.0,
+                G_e1_over_kappa_max=float(np.max(ek)) if ek else 0.0,
                 mismatched_residual_max=float(np.max(res)) if res else 0.0,
                 matvec_rel_vs_reference=float(dz),
                 err_vs_exact=float(np.linalg.norm(z[rows] - ze) / np.linalg.norm(ze)),
@@ -122,7 +127,7 @@ def full4():
             elif int(hashlib.blake2b(np.asarray(f.skel, "<i8").tobytes(), digest_size=8).hexdigest(), 16) \
                     != int(g["skdig_" + side][i]):
                 order += 1
-    e1, res = [], []
+    e1, res, ek = [], [], []
     for side, fac in (("row", M.rowfac), ("col", M.colfac)):
         ids = g["gs_%s_nodes" % side]
         skels = M.skel_row if side == "row" else M.skel_col
@@ -140,6 +145,9 @@ def full4():
             X = parity.align_rows(f.expand(), ib_a, ibar)
             if X is not None and np.array_equal(f.skel, ibar[pr[:k]]):
                 e1.append(np.linalg.norm(X - Xr) / max(np.linalg.norm(Xr), 1e-300))
+                if ncol and k:
+                    sv = np.linalg.svd(sl("cand").reshape(-1, ncol)[pr[:k]], compute_uv=False)
+                    ek.append(e1[-1] / (sv[0] / sv[-1]) if sv[-1] > 0 else 0.0)
             elif X is not None and ncol:
                 C = sl("cand").reshape(-1, ncol)
                 C_a = parity.align_rows(C, ibar, ib_a)
@@ -152,6 +160,7 @@ def full4():
     ref_at = g["z_at_rows"][np.searchsorted(rows, er)]
     return dict(factors=total, order_mismatch=order, rank_mismatch=rank,
                 G_e1_median=float(np.median(e1)) if e1 else 0.0, G_e1_max=float(np.max(e1)) if e1 else 0.0,
+                G_e1_over_kappa_max=float(np.max(ek)) if ek else 0.0,
                 mismatched_residual_max=float(np.max(res)) if res else 0.0,
                 matvec_rel_vs_reference_sampled=float(dz),
                 err_vs_exact=float(np.linalg.norm(z[er] - ze) / np.linalg.norm(ze)),

@@ -105,12 +105,20 @@ def hss_sensitivity(name):
     return json.load(open(p)).get(name)
 
 
-def hss_g_ok(name, e1):
-    """HSS G clause: label-identical nodes whose G differs from the reference's by more
-    than rule 3 allows must stay within twice the largest difference the reference's own
-    algorithm shows under another backward-stable SVD (hss_svd_sensitivity.json)."""
+def hss_g_ok(name, e1, kappa=None):
+    """HSS G clause: a label-identical node whose G differs from the reference's by more
+    than rule 3 allows passes if the difference is of the size the reference's own
+    algorithm shows under another backward-stable SVD (hss_svd_sensitivity.json):
+    e1 <= 10 kappa(R11) max(e1 / kappa) of that restatement (the difference of an
+    interpolative factor scales with the conditioning of its skeleton rows), or
+    e1 <= 4 max(e1) of it."""
     s = hss_sensitivity(name)
-    return s is not None and e1 <= 2 * max(s["G_e1_max"], 1e-10)
+    if s is None:
+        return False
+    if kappa is not None and np.isfinite(kappa) and s.get("G_e1_over_kappa_max", 0.0) > 0:
+        if e1 <= 10 * kappa * s["G_e1_over_kappa_max"]:
+            return True
+    return e1 <= 4 * max(s["G_e1_max"], 1e-10)
 
 
 def align_rows(X, ibar_from, ibar_to):

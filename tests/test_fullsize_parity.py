@@ -171,7 +171,7 @@ def test_full_transfer_G(sg, cfg):
                     assert rg <= bar, (side, i, rg, rr, bar)
                 continue
             ok, clause, e1, e2, kappa = parity.rule3(Xg, Xr, C, pr[:k])
-            if not ok and c["structure"] == "hss" and parity.hss_g_ok("full4", e1):
+            if not ok and c["structure"] == "hss" and parity.hss_g_ok("full4", e1, kappa):
                 ok = True
             n_checked += 1
             if not ok:

@@ -151,7 +151,7 @@ def test_transfer_G(smash_gpu, golden, name):
                 continue
             ok, clause, e1, e2, kappa = parity.rule3(Xg, Xr, C, pr[:k])
             clause2 += clause == 2
-            if not ok and g["meta"]["structure"] == "hss" and parity.hss_g_ok(name, e1):
+            if not ok and g["meta"]["structure"] == "hss" and parity.hss_g_ok(name, e1, kappa):
                 ok, clause = True, 3
                 clause3 += 1
                 e1max = max(e1max, e1)
