@@ -53,7 +53,8 @@ FP64_PEAK_TFLOPS = 34.1
 C_K = {"inv_r": 14.0, "log": 51.0, "exp": 52.0, "cauchy": 11.0}
 L2_FLUSH_BYTES = 256 << 20
 # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full, profiles/coupling_r01.txt)
-NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6}
+NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6,
+               (5, 16, "k_coupling"): 1.030274e9 + 0.454930e9}  # profiles/matvec_cfg5_r02.txt
 
 
 def parse():
@@ -328,18 +329,22 @@ def time_config(sg, torch, cfg, R, N, steps, warmup, flush, dev):
         e1.record()
         e1.synchronize()
         mv_ms.append(e0.elapsed_time(e1))
-    # profiled pass (phase events on the launch streams; synchronises each product)
+    # profiled passes (phase events on the launch streams; synchronise each product):
+    # as timed (nearfield concurrent), and serialised (isolated per-phase kernel times)
     lib = _lib.load()
-    lib.smash_matvec_profile(M._h, 1, None, None)
-    for _ in range(steps):
-        flush.zero_()
-        sg.matvec_device(M, dQ)
-    torch.cuda.synchronize()
-    phase = (ctypes.c_double * 7)()
-    launches = ctypes.c_int64()
-    lib.smash_matvec_profile(M._h, 0, phase, ctypes.byref(launches))
+    res = []
+    for mode in (1, 2):
+        lib.smash_matvec_profile(M._h, mode, None, None)
+        for _ in range(steps):
+            flush.zero_()
+            sg.matvec_device(M, dQ)
+        torch.cuda.synchronize()
+        phase = (ctypes.c_double * 7)()
+        launches = ctypes.c_int64()
+        lib.smash_matvec_profile(M._h, 0, phase, ctypes.byref(launches))
+        res.append(([phase[i] / steps for i in range(7)], launches.value / steps))
     return dict(M=M, X=X, Y=Y, q=q, dQ=dQ, out=out, build_ms=build_ms, mv_ms=mv_ms,
-                phase=[phase[i] / steps for i in range(7)], launches_per_product=launches.value / steps,
+                phase=res[0][0], phase_serial=res[1][0], launches_per_product=res[0][1],
                 spec=spec, params=params, builder=builder, c=c)
 
 
@@ -392,6 +397,7 @@ def run_ours(args):
         M, X, Y, q, dQ, out = T["M"], T["X"], T["Y"], T["q"], T["dQ"], T["out"]
         spec, params, builder = T["spec"], T["params"], T["builder"]
         build_ms, mv_ms, phase = T["build_ms"], T["mv_ms"], T["phase"]
+        phase_serial = T["phase_serial"]
         launches_per_product = T["launches_per_product"]
         t_mv = sum(mv_ms) / 1e3
         owned = top = None
@@ -453,6 +459,7 @@ def run_ours(args):
         lc = ctypes.c_int64()
         lib.smash_matvec_profile(M._h, 0, ph, ctypes.byref(lc))
         phase = [ph[i] / args.steps for i in range(7)]
+        phase_serial = phase
         launches_per_product = lc.value / args.steps
     value = args.steps * M.n_row * R / t_mv / 1e9
 
@@ -526,7 +533,7 @@ def run_ours(args):
     # ---- rooflines: dominant FP64 kernel, transfer passes (HBM), construction
     W = work_counts(sg, M, c, R, owned, top)
     per_int = C_K[c["kernel"]] + 2 * R
-    ms_coup, ms_near = phase[2], phase[4]
+    ms_coup, ms_near = phase_serial[2], phase_serial[4]  # isolated kernel times
     if ms_coup >= ms_near:
         dom, flops, ms = "k_coupling", W["I_coup"] * per_int, ms_coup
     else:
@@ -542,15 +549,15 @@ def run_ours(args):
                 "c_K": C_K[c["kernel"]], "interactions_coupling": W["I_coup"], "interactions_near": W["I_near"],
                 "matvec_total_frac": total_flops / (t_mv / args.steps) / 1e12 / FP64_PEAK_TFLOPS,
                 "scope": "rank 0's share" if ws > 1 else "whole matvec"}
-    xfer_ms = phase[1] + phase[3] + phase[5]
+    xfer_ms = phase_serial[1] + phase_serial[3] + phase_serial[5]
     transfer_roofline = {"bound": "hbm", "kernels": "k_up_leaves + k_upward + k_downward + k_down_leaves",
                          "bytes": W["xfer_bytes"], "ms": xfer_ms,
                          "achieved": W["xfer_bytes"] / (xfer_ms / 1e3) / 1e9 if xfer_ms > 0 else None,
                          "peak": hbm, "unit": "GB/s", "peak_source": hbm_src,
                          "frac": W["xfer_bytes"] / (xfer_ms / 1e3) / 1e9 / hbm if xfer_ms > 0 else None,
-                         "note": "algorithmic bytes (G of both sides once, coefficient slices, perms, "
-                                 "tree-order vectors) over the profiled upward + downward + leaf far-field "
-                                 "phase times"}
+                         "note": "algorithmic bytes (G once per pass, coefficient slices, perms, "
+                                 "tree-order vectors) over the upward + downward + leaf far-field phase "
+                                 "times of the serialised profiling pass (no nearfield overlap)"}
     b_s = statistics.median(build_ms) / 1e3
     build_roofline = {"bound": "fp64", "flops": W["build_flops"], "achieved": W["build_flops"] / b_s / 1e12,
                       "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -592,11 +599,17 @@ def run_ours(args):
             "build_s": b_s,
             "build_mode": "sharded: work-balanced cut, skeleton exchange, factors kept on their owner"
                           if ws > 1 else "single",
-            "phase_ms": {"gather": phase[0], "upward": phase[1], "coupling": ms_coup, "downward": phase[3],
-                         "nearfield_concurrent": ms_near, "leaf_farfield": phase[5],
+            "phase_ms": {"gather": phase[0], "upward": phase[1], "coupling": phase[2], "downward": phase[3],
+                         "nearfield_concurrent": phase[4], "leaf_farfield": phase[5],
                          "matvec_profiled": phase[6],
                          "note": "separate profiled pass (per-phase events, host-synchronised); "
                                  "the timed loop runs unprofiled"},
+            "phase_ms_serial": {"gather": phase_serial[0], "upward": phase_serial[1],
+                                "coupling": phase_serial[2], "downward": phase_serial[3],
+                                "nearfield": phase_serial[4], "leaf_farfield": phase_serial[5],
+                                "matvec": phase_serial[6],
+                                "note": "profiled pass with the nearfield on the main stream: isolated "
+                                        "kernel times (roofline denominators)"},
             "roofline": roofline,
             "transfer_roofline": transfer_roofline,
             "build_roofline": build_roofline,

@@ -191,7 +191,8 @@ int smash_sum_matvec(int32_t n_terms, const smash_matrix_t* bases, const double*
  * Returns the accumulated per-phase milliseconds since the last reset into phase_ms[7] =
  * [gather, upward, coupling, downward, nearfield (concurrent stream), leaf far-field, whole
  * matvec] and the number of kernel launches; then
- * enable = 1 turns profiling on and resets, 0 turns it off and resets, -1 leaves it as is. */
+ * enable = 1 turns profiling on and resets, 2 likewise with the nearfield serialised on the main
+ * stream (isolated per-phase kernel times), 0 turns it off and resets, -1 leaves it as is. */
 int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int64_t* launches);
 /* ---- sharded matvec (one rank of a multi-GPU job; NCCL is driven by the caller) ----
  * Partition: own_nodes = the postorder ids of this rank's subtrees (frontier nodes and all

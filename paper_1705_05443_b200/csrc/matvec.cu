@@ -139,7 +139,8 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   const double* pts_col = t->shared ? t->pts_row.p : t->pts_col.p;
   const int* col_a = t->shared ? t->row_a.p : t->col_a.p;
   const int* col_b = t->shared ? t->row_b.p : t->col_b.p;
-  static const bool serial = getenv("SMASH_MATVEC_SERIAL") != nullptr || debug_sync();
+  static const bool serial_env = getenv("SMASH_MATVEC_SERIAL") != nullptr || debug_sync();
+  const bool serial = serial_env || m->serial_phases;
   cudaStream_t sn = serial ? s : m->s2;
   auto mark = [&](int i, cudaStream_t st) {  // external record: a timing node in the graph
     if (ev) SMASH_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
@@ -173,7 +174,9 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   // upward pass and the coupling then runs alone; SMASH_NEAR_LATE=1 forks after the
   // upward pass instead (nearfield overlapping the coupling).  Both orders give the
   // same matvec time on cfg2 (the FP64 work bounds it, profiles/README_r01.md).
-  static const bool near_early = getenv("SMASH_NEAR_LATE") == nullptr;
+  static const bool near_early_env = getenv("SMASH_NEAR_LATE") == nullptr;
+  // serialised profiling: the nearfield runs alone after the downward pass
+  const bool near_early = near_early_env && !m->serial_phases;
   if (S.far && near_early) fork_near();
   double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;  // second half of qhat
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
@@ -189,7 +192,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     launches += 2;
   }
   mark(2, s);
-  if (S.far && !near_early) fork_near();
+  if (S.far && !near_early && !m->serial_phases) fork_near();
   if (S.far) {
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
                     m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
@@ -205,6 +208,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
       launches += 2;
     }
     mark(4, s);
+    if (m->serial_phases) fork_near();
     SMASH_CUDA(cudaStreamWaitEvent(s, m->join, 0));
     mark(8, s);
     launch_down_leaves<RC>(down, S.leaves, S.n_leaves, P.zrow.p, m->zn.p, z, nrhs, c0, s);
@@ -252,6 +256,7 @@ struct GraphEntry {
   double* z = nullptr;
   int64_t nrhs = 0;
   int stage = 0;
+  bool serial = false;  // captured with the nearfield on the main stream (phase profiling)
   cudaGraphExec_t exec = nullptr;
   std::vector<std::array<cudaEvent_t, 9>> ev;
   bool far = true;
@@ -271,9 +276,10 @@ GraphEntry* graph_for(MatrixImpl* m, const double* q, double* z, int64_t nrhs, i
   cudaStream_t s = m->sc;  // captured work is recorded on the capture stream
   auto& L = g_graphs[m];
   for (auto& e : L)
-    if (e->q == q && e->z == z && e->nrhs == nrhs && e->stage == stage) return e.get();
+    if (e->q == q && e->z == z && e->nrhs == nrhs && e->stage == stage && e->serial == m->serial_phases)
+      return e.get();
   std::unique_ptr<GraphEntry> E(new GraphEntry());
-  E->q = q; E->z = z; E->nrhs = nrhs; E->stage = stage; E->far = far;
+  E->q = q; E->z = z; E->nrhs = nrhs; E->stage = stage; E->far = far; E->serial = m->serial_phases;
   E->ev.resize(n_chunks);
   for (auto& a : E->ev)
     for (auto& e : a) SMASH_CUDA(cudaEventCreate(&e));
@@ -606,6 +612,7 @@ void matvec_profile(MatrixImpl* m, int enable, double* phase_ms, int64_t* launch
     if (enable && !m->ev[0])
       for (auto& e : m->ev) SMASH_CUDA(cudaEventCreate(&e));
     m->profile = enable != 0;
+    m->serial_phases = enable == 2;  // phases one after another (isolated kernel times)
     for (double& x : m->phase_ms) x = 0;
     m->launches = 0;
   }

@@ -106,6 +106,7 @@ struct MatrixImpl {
   int64_t ws_nrhs = 0;
   // optional per-phase timing of the matvec (CUDA events on the launch streams)
   bool profile = false;
+  bool serial_phases = false;  // profiling mode 2: nearfield on the main stream
   cudaEvent_t ev[9] = {};
   double phase_ms[7] = {0, 0, 0, 0, 0, 0, 0};  // gather, up, coupling, down, near, leaf-add, total
   int64_t launches = 0;
