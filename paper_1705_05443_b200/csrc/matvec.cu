@@ -24,7 +24,68 @@ using namespace mv;
 
 namespace {
 
-struct MatvecPlan : XferPlan {};
+struct MatvecPlan : XferPlan {
+  // symmetric coupling (shared points, symmetric kernel): upper pair list, pair buffer
+  bool sym = false;
+  DBuf<int> Uptr, Usrc, tptr, te;
+  DBuf<int64_t> pbuf;
+  DBuf<double> symbuf;  // pair rows x 16
+};
+
+// Shared points and a symmetric kernel: the coupling can evaluate each block once
+// (SymCoupling, matvec_impl.cuh) -- opt-in with SMASH_COUPLING_SYM=1.  Measured at cfg 5
+// (profiles/coupling_sym_r02.txt): 12.1 ms + 1.1 ms pass 2 vs 13.2 ms for the two-sided
+// kernel -- half the kernel evaluations, but 218 registers (half the occupancy), a
+// 6.2 GB pair buffer written and re-read, and read-modify-write across target passes.
+void plan_sym(MatrixImpl* m, MatvecPlan* P, cudaStream_t s) {
+  static const bool on = getenv("SMASH_COUPLING_SYM") && getenv("SMASH_COUPLING_SYM")[0] == '1';
+  if (!on || m->colf != &m->rowf || m->p.kernel == SMASH_KERNEL_CAUCHY) return;
+  TreeImpl* t = m->tree;
+  const int n = t->n_nodes;
+  std::vector<int> ptr(n + 1), rk(n);
+  d2h(ptr.data(), m->pl->L_ptr.p, n + 1, s);
+  d2h(rk.data(), m->rowf.rank.p, n, s);
+  sync(s);
+  std::vector<int> src(ptr[n]);
+  d2h(src.data(), m->pl->L_j.p, src.size(), s);
+  sync(s);
+  std::vector<int> up(n + 1, 0), us;
+  std::vector<int64_t> pb;
+  int64_t rows = 0;
+  us.reserve(src.size() / 2 + 1);
+  for (int v = 0; v < n; ++v) {
+    up[v] = (int)us.size();
+    for (int e = ptr[v]; e < ptr[v + 1]; ++e) {
+      const int j = src[e];
+      SMASH_CHECK(j != v, SMASH_ERR_CUDA, "coupling pair with itself");
+      if (j > v) {
+        us.push_back(j);
+        pb.push_back(rows);
+        rows += rk[j];
+      }
+    }
+  }
+  up[n] = (int)us.size();
+  // source-major index of the upper pairs: for every j the pairs (i, j), i ascending
+  std::vector<int> tp(n + 1, 0), tcount(n, 0);
+  for (int j : us) ++tcount[j];
+  for (int j = 0; j < n; ++j) tp[j + 1] = tp[j] + tcount[j];
+  std::vector<int> te(us.size()), fill(tp.begin(), tp.end() - 1);
+  for (int v = 0; v < n; ++v)
+    for (int e = up[v]; e < up[v + 1]; ++e) te[fill[us[e]]++] = e;
+  auto put = [&](auto& d, const auto& h) {
+    d.alloc(std::max<size_t>(h.size(), 1), s);
+    h2d(d.p, h.data(), h.size(), s);
+  };
+  put(P->Uptr, up);
+  put(P->Usrc, us);
+  put(P->pbuf, pb);
+  put(P->tptr, tp);
+  put(P->te, te);
+  P->symbuf.alloc(std::max<int64_t>(rows, 1) * 16, s);
+  sync(s);
+  P->sym = true;
+}
 
 std::map<const MatrixImpl*, std::unique_ptr<MatvecPlan>> g_plans;
 
@@ -95,6 +156,7 @@ MatvecPlan* plan_of(MatrixImpl* m, cudaStream_t s) {
   P->done.zero(s);
   P->counters.alloc(2, s);
   sync(s);
+  plan_sym(m, P.get(), s);
   MatvecPlan* out = P.get();
   g_plans[m] = std::move(P);
   return out;
@@ -196,7 +258,17 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   if (S.far) {
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
                     m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
-    launch_coupling<KER, D, RC>(ca, s);
+    if constexpr (RC == 8 || RC == 16) {
+      if (P.sym && S.coup == nullptr) {  // whole-tree product: each block evaluated once
+        SymCoupling y{P.Uptr.p, P.Usrc.p, P.pbuf.p, P.symbuf.p, P.tptr.p, P.te.p};
+        launch_coupling_sym<KER, D, RC>(ca, y, s);
+        ++launches;
+      } else {
+        launch_coupling<KER, D, RC>(ca, s);
+      }
+    } else {
+      launch_coupling<KER, D, RC>(ca, s);
+    }
     check_phase("coupling", s);
     ++launches;
     mark(3, s);

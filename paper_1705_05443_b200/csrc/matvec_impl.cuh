@@ -44,6 +44,20 @@ struct CouplingArgs {
   int max_targets;  // largest target set (skeleton rank) -> CTA size of the DMMA path
 };
 
+// symmetric coupling (X = Y, K(x, y) = K(y, x)): every coupling block is evaluated once.
+// Pass 1 runs over the upper pair list U(v) = {j in L(v) : j > v}: zhat[v] = sum_{j in U(v)}
+// B_vj qhat_j, and for each pair its transposed product B_vj^T qhat_v goes to the pair's
+// rows of `buf` (pbuf[e] = first row of upper pair e).  Pass 2 adds, per target j, the rows
+// of the pairs (i, j), i < j, listed by the source-major index (tptr / te), in order.
+struct SymCoupling {
+  const int* Uptr;   // CSR by target over the upper pairs
+  const int* Usrc;
+  const int64_t* pbuf;
+  double* buf;
+  const int* tptr;   // per target j: upper pairs (i, j) with i < j, sorted by i
+  const int* te;
+};
+
 // nearfield: zn[p] = sum_{j in Lm(v)} K(x_p, y_s) qt_s for the rows p of every listed leaf v
 struct NearArgs {
   const int* leaves;
@@ -69,6 +83,9 @@ template <int KER, int D, int RC>
 void launch_coupling(const CouplingArgs& a, cudaStream_t s);
 template <int KER, int D, int RC>
 void launch_near(const NearArgs& a, cudaStream_t s);
+// symmetric coupling (RC = 8 / 16): pass 1 + pass 2
+template <int KER, int D, int RC>
+void launch_coupling_sym(const CouplingArgs& a, const SymCoupling& y, cudaStream_t s);
 template <int KER, int D>
 void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx, double* out,
                   cudaStream_t s);

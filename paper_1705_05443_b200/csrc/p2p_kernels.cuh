@@ -372,6 +372,287 @@ __global__ void __launch_bounds__(P2P_THREADS, p2p_min_blocks<MT>()) k_near(Near
                         [&](int t, int r, double val) { zn[(int64_t)slot[t] * RC + r] = val; });
 }
 
+// ---------------------------------------------------------------------------
+// symmetric coupling (SymCoupling, matvec_impl.cuh): each block K(S_v, S_j), j > v, is
+// generated once and contracted both ways.  Per 8-source block (two 4-source DMMA
+// steps) the lanes hold A[t][s] for target t = 8m + g, source s = 4h + q; the transposed
+// fragment A^T (8 sources x 4 targets) is gathered with two shuffles per K chunk and
+// contracted with the target's own coefficients (B operand), giving B_vj^T qhat_v for the
+// 8 sources, which go to the pair buffer rows (added over the target passes).
+// ---------------------------------------------------------------------------
+struct SegTableSym {
+  int pre[MMA_SEG_CAP + 1];
+  int off[MMA_SEG_CAP];
+  int64_t boff[MMA_SEG_CAP];  // pair buffer row of the segment's first source
+  int n;
+};
+
+template <int D, int RC>
+constexpr int mma_stage_doubles_sym() { return 2 * (32 * D + 32 * mma_wstride<RC>() + 32); }
+
+template <int D, int RC>
+constexpr int mma_smem_doubles_sym() {
+  return P2P_WARPS * MMA_MTMAX * 8 * RC > P2P_WARPS * mma_stage_doubles_sym<D, RC>()
+             ? P2P_WARPS * MMA_MTMAX * 8 * RC
+             : P2P_WARPS * mma_stage_doubles_sym<D, RC>();
+}
+
+template <int D, int RC>
+__device__ __forceinline__ void mma_issue_sym(const SegTableSym& T, int p, int total,
+                                              const double* spts, int64_t sstride,
+                                              const double* wts, double* sc, double* sw,
+                                              long long* sb) {
+  const int lane = threadIdx.x & 31;
+  const bool ok = p < total;
+  int row = 0;
+  long long brow = -1;
+  if (ok) {
+    int lo = 0, hi = T.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (T.pre[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    row = T.off[lo] + (p - T.pre[lo]);
+    brow = T.boff[lo] + (p - T.pre[lo]);
+  }
+  sb[lane] = brow;  // plain store: read after this chunk's wait + __syncwarp
+#pragma unroll
+  for (int a = 0; a < D; ++a) cp_async8z(sc + a * 32 + lane, spts + (int64_t)a * sstride + row, ok);
+  double* dw = sw + lane * mma_wstride<RC>();
+  const double* w = wts + (int64_t)row * RC;
+#pragma unroll
+  for (int u = 0; u < RC / 2; ++u) cp_async16z(dw + 2 * u, w + 2 * u, ok);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int KER, int D, int RC, int MTX>
+__device__ __forceinline__ void mma_warp_stream_sym(const SegTableSym& T, const double* spts,
+                                                    int64_t sstride, const double* wts,
+                                                    const double (&xt)[MTX][D],
+                                                    const bool (&tv)[MTX],
+                                                    const double (&bq)[MTX][2][RC / 8], double dx,
+                                                    double* stage, double* buf, bool first_pass,
+                                                    double (&c)[MTX][RC / 8][2]) {
+  constexpr int NT = RC / 8;
+  constexpr int WS = mma_wstride<RC>();
+  constexpr int BUF = 32 * D + 32 * WS + 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int total = T.pre[T.n];
+  const int nch = (total + 31) >> 5;
+  const int per = (nch + P2P_WARPS - 1) / P2P_WARPS;
+  const int c0 = wid * per, c1 = min(nch, c0 + per);
+  auto bufs = [&](int k) { return stage + (k & 1) * BUF; };
+  if (c0 < c1) {
+    double* sc = bufs(0);
+    mma_issue_sym<D, RC>(T, c0 * 32 + lane, total, spts, sstride, wts, sc, sc + 32 * D,
+                         reinterpret_cast<long long*>(sc + 32 * D + 32 * WS));
+  }
+  for (int ch = c0; ch < c1; ++ch) {
+    double* sc = bufs(ch - c0);
+    double* sw = sc + 32 * D;
+    const long long* sb = reinterpret_cast<const long long*>(sw + 32 * WS);
+    if (ch + 1 < c1) {
+      double* nc = bufs(ch + 1 - c0);
+      mma_issue_sym<D, RC>(T, (ch + 1) * 32 + lane, total, spts, sstride, wts, nc, nc + 32 * D,
+                           reinterpret_cast<long long*>(nc + 32 * D + 32 * WS));
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const int cnt = min(32, total - ch * 32);
+    for (int kk = 0; kk < cnt; kk += 8) {
+      double av[2][MTX];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int si = kk + 4 * h + q;
+        const bool sv = si < cnt;
+        double ys[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) ys[a] = sc[a * 32 + (si & 31)];
+        double b[NT];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) b[n] = sw[(si & 31) * WS + n * 8 + g];
+#pragma unroll
+        for (int m = 0; m < MTX; ++m) {
+          const double kv = kval<KER, D>(xt[m], ys, dx);
+          av[h][m] = (sv && tv[m]) ? kv : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < MTX; ++m)
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma_8x8x4(c[m][n][0], c[m][n][1], av[h][m], b[n]);
+      }
+      // transposed: D[s][r] = sum_t A[t][s] qhat_v[t][r] for the 8 sources kk..kk+7
+      double dacc[NT][2];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dacc[n][0] = dacc[n][1] = 0.0;
+#pragma unroll
+      for (int m = 0; m < MTX; ++m)
+#pragma unroll
+        for (int ck = 0; ck < 2; ++ck) {
+          const int src = (4 * ck + q) * 4 + (g & 3);  // lane holding A[4ck + q][g]
+          const double x0 = __shfl_sync(0xffffffffu, av[0][m], src);
+          const double x1 = __shfl_sync(0xffffffffu, av[1][m], src);
+          const double at = g < 4 ? x0 : x1;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma_8x8x4(dacc[n][0], dacc[n][1], at, bq[m][ck][n]);
+        }
+      const int si = kk + g;  // this lane's source row of D
+      if (si < cnt) {
+        const long long br = sb[si];
+        double* o = buf + br * RC;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int r = n * 8 + 2 * q;
+          if (first_pass) {
+            o[r] = dacc[n][0];
+            o[r + 1] = dacc[n][1];
+          } else {
+            o[r] += dacc[n][0];
+            o[r + 1] += dacc[n][1];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int KER, int D, int RC, int MTX, typename SegF>
+__device__ __forceinline__ void mma_block_sym(const double* tx, int64_t tstride, int nt, int p0,
+                                              int p1, SegF seg, const double* spts,
+                                              int64_t sstride, const double* wts,
+                                              const double* qv, double* pbuf_base,
+                                              const int64_t* pbuf, double dx, bool first_pass,
+                                              SegTableSym& T, double* buf) {
+  constexpr int NT = RC / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double xt[MTX][D];
+  bool tv[MTX];
+  double bq[MTX][2][NT];
+#pragma unroll
+  for (int m = 0; m < MTX; ++m) {
+    const int t = m * 8 + g;
+    tv[m] = t < nt;
+#pragma unroll
+    for (int a = 0; a < D; ++a) xt[m][a] = tv[m] ? tx[(int64_t)a * tstride + t] : 0.0;
+#pragma unroll
+    for (int ck = 0; ck < 2; ++ck) {
+      const int tk = m * 8 + 4 * ck + q;  // B operand row k = target, column n = rhs
+#pragma unroll
+      for (int n = 0; n < NT; ++n) bq[m][ck][n] = tk < nt ? qv[(int64_t)tk * RC + n * 8 + g] : 0.0;
+    }
+  }
+  double c[MTX][NT][2];
+#pragma unroll
+  for (int m = 0; m < MTX; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) c[m][n][0] = c[m][n][1] = 0.0;
+  for (int e0 = p0; e0 < p1; e0 += MMA_SEG_CAP) {
+    const int ns = min(MMA_SEG_CAP, p1 - e0);
+    __syncthreads();
+    if (threadIdx.x == 0) T.n = ns;
+    for (int e = threadIdx.x; e < ns; e += blockDim.x) {
+      const int2 oc = seg(e0 + e);
+      T.off[e] = oc.x;
+      T.pre[e + 1] = oc.y;
+      T.boff[e] = pbuf[e0 + e];
+    }
+    __syncthreads();
+    if (wid == 0) {
+      int carry = 0;
+      for (int b0 = 0; b0 < ns; b0 += 32) {
+        int x = b0 + lane < ns ? T.pre[b0 + lane + 1] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (b0 + lane < ns) T.pre[b0 + lane + 1] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) T.pre[0] = 0;
+    }
+    __syncthreads();
+    mma_warp_stream_sym<KER, D, RC, MTX>(T, spts, sstride, wts, xt, tv, bq, dx,
+                                         buf + wid * mma_stage_doubles_sym<D, RC>(), pbuf_base,
+                                         first_pass, c);
+  }
+  __syncthreads();
+  double* rw = buf + wid * (MMA_MTMAX * 8 * RC);
+#pragma unroll
+  for (int m = 0; m < MTX; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int t = m * 8 + g, r = n * 8 + 2 * q;
+      rw[t * RC + r] = c[m][n][0];
+      rw[t * RC + r + 1] = c[m][n][1];
+    }
+}
+
+template <int KER, int D, int RC, int MT>
+__global__ void __launch_bounds__(P2P_THREADS, 2) k_coupling_sym(CouplingArgs A, SymCoupling Y) {
+  if ((int)blockIdx.x >= A.n_nodes) return;
+  const int v = (int)blockIdx.x;
+  if (v == 0) return;
+  const int k = A.rs.rank[v];
+  if (k == 0) return;
+  const int to = A.rs.skel_off[v];
+  SMASH_DASSERT(k <= A.max_targets && to >= 0);
+  const Side cs = A.cs;
+  const int* Usrc = Y.Usrc;
+  auto seg = [&](int e) {
+    const int j = Usrc[e];
+    return make_int2(cs.skel_off[j], cs.rank[j]);
+  };
+  double* zo = A.zhat + (int64_t)to * RC;
+  const double* qv = A.qhat + (int64_t)cs.skel_off[v] * RC;
+  extern __shared__ __align__(16) double p2p_dyn[];
+  double* buf = p2p_dyn;
+  SegTableSym& T = *reinterpret_cast<SegTableSym*>(p2p_dyn + mma_smem_doubles_sym<D, RC>());
+  const int p0 = Y.Uptr[v], p1 = Y.Uptr[v + 1];
+  for (int t0 = 0; t0 < k; t0 += MT * 8) {
+    const int n = min(MT * 8, k - t0);
+    __syncthreads();
+    const double* tx = A.rs.skel_pts + to + t0;
+    const int64_t ts = A.rs.skel_stride;
+    const bool first = t0 == 0;
+    switch ((n + 7) >> 3) {
+      case 1: mma_block_sym<KER, D, RC, 1>(tx, ts, n, p0, p1, seg, cs.skel_pts, cs.skel_stride, A.qhat, qv + (int64_t)t0 * RC, Y.buf, Y.pbuf, A.dx, first, T, buf); break;
+      case 2: mma_block_sym<KER, D, RC, 2>(tx, ts, n, p0, p1, seg, cs.skel_pts, cs.skel_stride, A.qhat, qv + (int64_t)t0 * RC, Y.buf, Y.pbuf, A.dx, first, T, buf); break;
+      case 3: mma_block_sym<KER, D, RC, 3>(tx, ts, n, p0, p1, seg, cs.skel_pts, cs.skel_stride, A.qhat, qv + (int64_t)t0 * RC, Y.buf, Y.pbuf, A.dx, first, T, buf); break;
+      default: mma_block_sym<KER, D, RC, MT>(tx, ts, n, p0, p1, seg, cs.skel_pts, cs.skel_stride, A.qhat, qv + (int64_t)t0 * RC, Y.buf, Y.pbuf, A.dx, first, T, buf); break;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
+      double sm = 0.0;
+      if (p1 > p0) {
+        sm = buf[e];
+        for (int w = 1; w < P2P_WARPS; ++w) sm += buf[w * (MMA_MTMAX * 8 * RC) + e];
+      }
+      zo[(int64_t)t0 * RC + e] = sm;
+    }
+  }
+}
+
+// pass 2: zhat[j] += sum over the upper pairs (i, j), i < j (ascending i), of their rows
+template <int RC>
+__global__ void __launch_bounds__(128) k_coupling_tsum(CouplingArgs A, SymCoupling Y) {
+  const int j = (int)blockIdx.x;
+  if (j == 0 || j >= A.n_nodes) return;
+  const int k = A.cs.rank[j];
+  const int e0 = Y.tptr[j], e1 = Y.tptr[j + 1];
+  if (k == 0 || e0 == e1) return;
+  double* zo = A.zhat + (int64_t)A.rs.skel_off[j] * RC;
+  for (int x = threadIdx.x; x < k * RC; x += blockDim.x) {
+    double acc = zo[x];
+    for (int e = e0; e < e1; ++e) acc += Y.buf[Y.pbuf[Y.te[e]] * RC + x];
+    zo[x] = acc;
+  }
+}
+
 template <int KER, int D>
 __global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny, double dx,
                         double* out) {
@@ -422,6 +703,23 @@ void launch_coupling(const CouplingArgs& a, cudaStream_t s) {
 }
 
 template <int KER, int D, int RC>
+void launch_coupling_sym(const CouplingArgs& a, const SymCoupling& y, cudaStream_t s) {
+  if constexpr (RC == 8 || RC == 16) {
+    constexpr size_t smem = mma_smem_doubles_sym<D, RC>() * sizeof(double) + sizeof(SegTableSym);
+    static const bool attr = [] {
+      p2p_attrs(k_coupling_sym<KER, D, RC, 4>, smem);
+      return true;
+    }();
+    (void)attr;
+    if (a.n_nodes <= 0) return;
+    k_coupling_sym<KER, D, RC, 4><<<a.n_nodes, P2P_THREADS, smem, s>>>(a, y);
+    k_coupling_tsum<RC><<<a.n_nodes, 128, 0, s>>>(a, y);
+  } else {
+    throw Error(SMASH_ERR_INVALID, "symmetric coupling needs 8 or 16 right-hand-side columns");
+  }
+}
+
+template <int KER, int D, int RC>
 void launch_near(const NearArgs& a, cudaStream_t s) {
   constexpr size_t smem = p2p_smem_bytes<D, RC>();
   static const bool attr = [] {
@@ -452,6 +750,8 @@ void launch_block(const double* X, int64_t nx, const double* Y, int64_t ny, doub
   template void launch_near<KER, D, 4>(const NearArgs&, cudaStream_t);                \
   template void launch_near<KER, D, 8>(const NearArgs&, cudaStream_t);                \
   template void launch_near<KER, D, 16>(const NearArgs&, cudaStream_t);               \
+  template void launch_coupling_sym<KER, D, 8>(const CouplingArgs&, const SymCoupling&, cudaStream_t); \
+  template void launch_coupling_sym<KER, D, 16>(const CouplingArgs&, const SymCoupling&, cudaStream_t); \
   template void launch_block<KER, D>(const double*, int64_t, const double*, int64_t,  \
                                      double, double*, cudaStream_t);
 
