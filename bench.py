@@ -49,8 +49,8 @@ sys.path.insert(0, REPO)
 # MEASURED_PEAKS.json has no FP64 entry.  DFMA 34.1 TF/s (DMMA 37.1 TF/s).
 FP64_PEAK_TFLOPS = 34.1
 # DP flops per kernel evaluation c_K (DADD + DMUL + 2*DFMA of the compiled kval<> path,
-# counted by ncu on k_block -- profiles/ckernel_r01.txt); 2*nrhs flops per interaction added.
-C_K = {"inv_r": 14.0, "log": 51.0, "exp": 52.0, "cauchy": 11.0}
+# counted by ncu on k_block -- profiles/ckernel_r02.txt); 2*nrhs flops per interaction added.
+C_K = {"inv_r": 14.0, "log": 41.0, "exp": 52.0, "cauchy": 7.0}
 L2_FLUSH_BYTES = 256 << 20
 # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full, profiles/coupling_r01.txt)
 NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6,
