@@ -26,6 +26,8 @@
 // batch.  The GEMM runs on the FP64 tensor cores (mma.sync m8n8k4 DMMA) with
 // operands read from shared memory at bank-conflict-free strides (row strides
 // = 4 mod 8 doubles), one 8x8 output tile per warp and item.
+#include <cstdlib>
+
 #include "matvec_impl.cuh"
 
 namespace smash {
@@ -691,7 +693,8 @@ XferGeom xfer_geom(int max_nib, int max_rank, int max_nk, int rc) {
   G.ks = (max_rank + 3) & ~3;
   if (G.ks % 8 == 0) G.ks += 4;  // row stride = 4 (mod 8) doubles: conflict-free fragments
   G.rcs = rc < 8 ? rc : rc + 4;
-  const int cap = std::max(8, ((64 * 1024) / (G.ks * 8)) & ~7);
+  static const int kb = getenv("SMASH_XFER_GKB") ? atoi(getenv("SMASH_XFER_GKB")) : 64;
+  const int cap = std::max(8, ((kb * 1024) / (G.ks * 8)) & ~7);
   G.tb = std::min(cap, std::max(8, (max_nk + 7) & ~7));
   G.max_nib = max_nib;
   G.max_rank = max_rank;
