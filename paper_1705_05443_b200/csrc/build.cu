@@ -404,14 +404,17 @@ struct SideBuild {
   }
 
   void launch_level(CompressArgs& A, int cnt) {
-    int grid;
-    size_t smem = plan_compress_launch(A, cnt, smem_limit, nsm, &grid);
-    if (A.panel_cap < (int64_t)A.nmax * A.mmax) {  // some nodes may need the global workspace
-      size_t need = (size_t)grid * A.mmax * A.nmax;
-      if (gws.n < need) gws.alloc(need, s);
-      A.gws = gws.p;
+    CompressPass ps[3];
+    const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
+    for (int k = 0; k < np; ++k) {
+      CompressArgs& a = ps[k].a;
+      if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
+        size_t need = (size_t)ps[k].grid * a.mmax * a.nmax;
+        if (gws.n < need) gws.alloc(need, s);
+        a.gws = gws.p;
+      }
+      launch_compress(a, ps[k].grid, ps[k].smem, s);
     }
-    launch_compress(A, grid, smem, s);
   }
 
   void level(int l, NearSets* near) {

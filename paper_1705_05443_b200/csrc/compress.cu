@@ -368,6 +368,13 @@ __global__ void __launch_bounds__(COMPRESS_THREADS, MODE == 0 ? 2 : 4) k_compres
   // (node costs vary with |ibar|, rank and swap iterations)
   for (int v = A.lb + blockIdx.x; v < A.le;) {
     const int n = A.nib[v];
+    if (n <= A.n_lo || n > A.n_hi) {  // another launch of this level takes this size class
+      __syncthreads();
+      if (tid == 0) S.imisc[4] = A.lb + (int)gridDim.x + atomicAdd(A.next, 1);
+      __syncthreads();
+      v = S.imisc[4];
+      continue;
+    }
     const int mrows = A.Cexp ? A.C_cols : A.r + (A.keep ? A.keep[v] : 0);
     SMASH_DASSERT(n >= 0 && n <= A.nmax && mrows <= A.mmax);
     const NodeSrc src = A.Cexp ? NodeSrc{nullptr, 0, nullptr, 0} : node_src(A, v);
@@ -506,6 +513,34 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
   A.panel_cap = 0;
   *grid = std::min(cnt, nsm * gper);
   return fixed;
+}
+
+// Wide levels of adaptive trees mix small nodes (leaves, sparse parents) with nodes near
+// the capacity bound; one launch sized for the capacity runs the small ones in oversized
+// CTAs at low occupancy.  Such a level is split by |ibar| into size classes (<= 64,
+// <= 128, rest), each launched with its own CTA size and shared panel; the CTAs of a
+// launch skip the other classes' nodes.  Latency-bound levels (<= one node per SM) and
+// levels whose capacity is already small keep one launch.
+int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass out[3]) {
+  static const bool split = getenv("SMASH_COMPRESS_NOSPLIT") == nullptr;
+  const int bounds[3] = {64, 128, 0x7fffffff};
+  if (!split || cnt <= nsm || A0.nmax <= bounds[0]) {
+    out[0].a = A0;
+    out[0].smem = plan_compress_launch(out[0].a, cnt, smem_limit, nsm, &out[0].grid);
+    return 1;
+  }
+  int np = 0, lo = -1;
+  for (int b : bounds) {
+    if (lo >= A0.nmax) break;
+    CompressPass& P = out[np++];
+    P.a = A0;
+    P.a.n_lo = lo;
+    P.a.n_hi = b;
+    P.a.nmax = std::min(A0.nmax, b);
+    P.smem = plan_compress_launch(P.a, cnt, smem_limit, nsm, &P.grid);
+    lo = b;
+  }
+  return np;
 }
 
 #ifdef SMASH_COMPRESS_PROF

@@ -66,7 +66,8 @@ struct CompressArgs {
   int C_cols = 0;
   unsigned long long* prof = nullptr;
   int* next = nullptr;  // dynamic node counter (launch_compress)
-  int threads = COMPRESS_THREADS;  // CTA size (plan_compress_launch)  // SMASH_COMPRESS_PROF builds: clock64 per phase
+  int threads = COMPRESS_THREADS;  // CTA size (plan_compress_launch)
+  int n_lo = -1, n_hi = 0x7fffffff;  // size class of this launch: n_lo < |ibar| <= n_hi
 };
 
 size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
@@ -74,6 +75,13 @@ size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
 // per CTA and the grid (persistent CTAs over the level's cnt nodes).
 size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, int* grid);
 void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s);
+struct CompressPass {
+  CompressArgs a;
+  int grid = 0;
+  size_t smem = 0;
+};
+// Up to three size-class launches of a level (see compress.cu); returns their count.
+int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass out[3]);
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
                          int r, const double* pts_soa, int64_t n, double* out, int* err,
                          cudaStream_t s);
