@@ -171,7 +171,7 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
   double bv = -1.0;
   int bi = 0x7fffffff;
   for (int j = tid; j < n; j += NT) {
-    double nr = __dsqrt_rn(col_sumsq<CH>(P, ld, j, 0, m));
+    double nr = __dsqrt_rn(A.chains4 ? col_sumsq4<CH>(P, ld, j, 0, m) : col_sumsq<CH>(P, ld, j, 0, m));
     S.vn1[j] = nr;
     S.vn2[j] = nr;
     S.jpvt[j] = j;
@@ -214,13 +214,17 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
       double v1 = S.vn1[j];
       const double rv1 = 1.0 / v1;
       const double q2 = v1 / S.vn2[j];
-      if (tau != 0.0) apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
+      if (tau != 0.0) {
+        if (A.chains4) apply_reflector4<CH>(P, ld, m, i, j, tau, S.vh);
+        else apply_reflector<CH>(P, ld, m, i, j, tau, S.vh);
+      }
       if (v1 != 0.0) {
         double q = fabs(P[i * ld + j]) * rv1;
         double temp = fmax(1.0 - q * q, 0.0);
         double temp2 = temp * (q2 * q2);
         if (temp2 <= TOL3Z) {
-          double nv = i + 1 < m ? __dsqrt_rn(col_sumsq<CH>(P, ld, j, i + 1, m)) : 0.0;
+          double nv = i + 1 < m ? __dsqrt_rn(A.chains4 ? col_sumsq4<CH>(P, ld, j, i + 1, m)
+                                                      : col_sumsq<CH>(P, ld, j, i + 1, m)) : 0.0;
           S.vn1[j] = nv;
           S.vn2[j] = nv;
           v1 = nv;
@@ -550,6 +554,10 @@ __device__ int g_compress_next;  // dynamic node counter (reset before every lau
 
 void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s) {
   CompressArgs a = a_in;
+  // four-chain dot products by default (cfg5 build -8 %, the full-size skeleton / G parity
+  // unchanged); SMASH_QR_CHAINS=1 restores the sequential dlarf / dnrm2 order
+  static const bool chains4 = !(getenv("SMASH_QR_CHAINS") && atoi(getenv("SMASH_QR_CHAINS")) == 1);
+  a.chains4 = chains4;
   {
     void* nx = nullptr;
     SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));

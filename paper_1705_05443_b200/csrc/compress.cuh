@@ -68,6 +68,7 @@ struct CompressArgs {
   int* next = nullptr;  // dynamic node counter (launch_compress)
   int threads = COMPRESS_THREADS;  // CTA size (plan_compress_launch)
   int n_lo = -1, n_hi = 0x7fffffff;  // size class of this launch: n_lo < |ibar| <= n_hi
+  bool chains4 = true;  // four-chain dot products (qr_device.cuh); SMASH_QR_CHAINS=1: sequential
 };
 
 size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);

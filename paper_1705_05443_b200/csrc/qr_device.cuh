@@ -158,5 +158,54 @@ __device__ __forceinline__ void apply_reflector(double* __restrict__ P, int ld, 
   }
 }
 
+// Four-chain variants (the compression default; SMASH_QR_CHAINS=1 selects the sequential
+// ones above): the same sums split over four independent accumulators (rows round-robin,
+// combined (0+1)+(2+3)), a quarter of the dependent FMA latency per pivot step.  Neither
+// order is OpenBLAS's (dgemv / x87 dnrm2); the pivots and ranks are the reference's either
+// way on every fixture and full-size node (tests/test_fullsize_parity.py).
+template <int CH = 8>
+__device__ __forceinline__ double col_sumsq4(const double* __restrict__ P, int ld, int j, int r0,
+                                             int r1) {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int row = r0;
+  for (; row + 4 <= r1; row += 4) {
+    double x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = P[(row + c) * ld + j];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[c] = __fma_rn(x[c], x[c], s[c]);
+  }
+  for (int c = 0; row < r1; ++row, ++c) {
+    const double x = P[row * ld + j];
+    s[c] = __fma_rn(x, x, s[c]);
+  }
+  return __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]));
+}
+
+template <int CH = 8>
+__device__ __forceinline__ void apply_reflector4(double* __restrict__ P, int ld, int m, int i, int j,
+                                                 double tau, const double* __restrict__ vh) {
+  double w[4] = {P[i * ld + j], 0.0, 0.0, 0.0};
+  int row = i + 1;
+  for (; row + 4 <= m; row += 4) {
+    double x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = P[(row + c) * ld + j];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) w[c] = __fma_rn(vh[row + c], x[c], w[c]);
+  }
+  for (int c = 0; row < m; ++row, ++c) w[c] = __fma_rn(vh[row], P[row * ld + j], w[c]);
+  const double t = -__dmul_rn(tau, __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3])));
+  P[i * ld + j] = __dadd_rn(P[i * ld + j], t);
+  for (row = i + 1; row < m; row += CH) {
+    double x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = row + c < m ? P[(row + c) * ld + j] : 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (row + c < m) P[(row + c) * ld + j] = __fma_rn(t, vh[row + c], x[c]);
+  }
+}
+
 }  // namespace qr
 }  // namespace smash

@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     // elements per lane, 3 shuffle levels per reduction
     const int g8 = tid >> 3, gl = tid & 7, ngr = NT >> 3;
     const unsigned gm = 0xffu << (lane & ~7);
+    int sweeps_done = 0;
     for (int sweep = 0; sweep < 40; ++sweep) {
+      sweeps_done = sweep + 1;
       for (int c = g8; c < kp; c += ngr) {  // exact squared norms
         double s2 = 0.0;
         for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     if (dbg) {
       tsv[5] = clock64();
       for (int q = 0; q < 5; ++q) A.dbg[dbg_n * 8 + q] = tsv[q + 1] - tsv[q];
-      A.dbg[dbg_n * 8 + 5] = kp; A.dbg[dbg_n * 8 + 6] = keep; A.dbg[dbg_n * 8 + 7] = n * 1000 + nn;
+      A.dbg[dbg_n * 8 + 5] = kp; A.dbg[dbg_n * 8 + 6] = keep + 1000 * sweeps_done; A.dbg[dbg_n * 8 + 7] = n * 1000 + nn;
     }
     ++dbg_n;
   }
