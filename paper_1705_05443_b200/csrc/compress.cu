@@ -270,8 +270,11 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
       // the terms of rows k-1 .. a+1 in that order -- the same FMA sequence as
       // the column-sweep (dtrsv) form, with chunked independent loads (the
       // solved x_c of this column and row a of R11, shared by all threads).
+      // (With the four-chain option the terms of a row go to four accumulators by c mod 4:
+      // G = W^T is compared by SURVEY 8(c) rule 3, not bit for bit.)
       for (int a = k - 1; a >= 0; --a) {
         double acc = P[a * ld + j];
+        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
         constexpr int CH = 8;
         for (int c0 = k - 1; c0 > a; c0 -= CH) {
           double xs[CH], rs[CH];
@@ -281,10 +284,16 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
             xs[c] = ok ? P[(c0 - c) * ld + j] : 0.0;
             rs[c] = ok ? P[a * ld + (c0 - c)] : 0.0;
           }
+          if (A.chains4) {
 #pragma unroll
-          for (int c = 0; c < CH; ++c)
-            if (c0 - c > a) acc = __fma_rn(-xs[c], rs[c], acc);
+            for (int c = 0; c < CH; ++c) acc4[c & 3] = __fma_rn(-xs[c], rs[c], acc4[c & 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              if (c0 - c > a) acc = __fma_rn(-xs[c], rs[c], acc);
+          }
         }
+        if (A.chains4) acc = __dadd_rn(acc, __dadd_rn(__dadd_rn(acc4[0], acc4[1]), __dadd_rn(acc4[2], acc4[3])));
         const double x = __ddiv_rn(acc, P[a * ld + a]);
         P[a * ld + j] = x;
         argmax_combine(bv, bi, fabs(x), a * nk + (j - k));
