@@ -198,11 +198,13 @@ int smash_matvec_profile(smash_matrix_t m, int32_t enable, double* phase_ms, int
  * Partition: own_nodes = the postorder ids of this rank's subtrees (frontier nodes and all
  * their descendants), top_nodes = the ancestors of all frontier nodes (replicated work).
  * Both are HOST arrays.  Stage 1: gather q and compute the coefficients qhat of the owned
- * subtrees (all other coefficients zeroed); the caller then sums the coefficient buffer over
- * ranks (the supports are disjoint, so this all-reduce is an all-gather of the skeleton
- * coefficients).  Stage 2: top-level upward pass, coupling / downward /
- * nearfield for the owned targets; writes only the owned rows of z.  nrhs: a power of two
- * <= 16 (one chunk). */
+ * subtrees (other rows of the coefficient buffer untouched); the caller then brings in the
+ * coefficient rows stage 2 reads from other ranks (shard.halo_rows: the cut-level skeleton
+ * coefficients and the coupling sources of its targets).  Stage 2: top-level
+ * upward pass, coupling / downward / nearfield for the owned targets; writes only the owned
+ * rows of z.  Stage 3 + stage 4 split stage 2 so the nearfield can overlap the exchange:
+ * stage 3 (after stage 1, on any stream) runs the owned leaves' nearfield alone, stage 4 is
+ * stage 2 without it (ordered after stage 3 by the caller).  nrhs: a power of two <= 16. */
 int smash_matvec_set_partition(smash_matrix_t m, const int64_t* own_nodes, int64_t n_own,
                                const int64_t* top_nodes, int64_t n_top, void* stream);
 int smash_matvec_stage(smash_matrix_t m, int32_t stage, const double* q, double* z, int64_t nrhs,

@@ -174,6 +174,7 @@ struct PhaseSets {
   const int* coup = nullptr; int n_coup = -1;  // coupling targets (nullptr + -1: all nodes)
   const int* down = nullptr; int n_down = 0;   // internal downward order (shallowest first)
   const int* leaves = nullptr; int n_leaves = 0;  // nearfield / far-field + combine rows
+  int near_mode = 0;  // 0: nearfield forked here; 1: nearfield only; 2: nearfield done earlier
 };
 
 // SMASH_DEBUG_SYNC=1: eager (uncaptured) matvec with a synchronize + error
@@ -208,6 +209,14 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     if (ev) SMASH_CUDA(cudaEventRecordWithFlags(ev[i], st, cudaEventRecordExternal));
   };
   int launches = 0;
+  if (S.near_mode == 1) {  // sharded stage 3: the owned leaves' nearfield alone (needs only qt)
+    NearArgs na{S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
+                pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, P.slot_of.p, m->zn.p,
+                m->p.dx, t->nu0};
+    launch_near<KER, D, RC>(na, s);
+    *nlaunch += 1;
+    return;
+  }
   mark(0, s);
   if (S.gather) {
     launch_gather<RC>(q, nrhs, perm_col, t->ny, c0, m->qt.p, s);
@@ -239,7 +248,8 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
   static const bool near_early_env = getenv("SMASH_NEAR_LATE") == nullptr;
   // serialised profiling: the nearfield runs alone after the downward pass
   const bool near_early = near_early_env && !m->serial_phases;
-  if (S.far && near_early) fork_near();
+  const bool near_here = S.near_mode == 0;
+  if (S.far && near_here && near_early) fork_near();
   double* qp = m->qhat.p + std::max<int64_t>(C.skel_total, 1) * RC;  // second half of qhat
   XferArgs up{t->nchild.p, t->child_first.p, t->parent.p, col_a, col_b, m->qt.p, m->qhat.p,
               qp, P.up_pos.p, m->zhat.p, m->zd.p, cs};
@@ -254,7 +264,7 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     launches += 2;
   }
   mark(2, s);
-  if (S.far && !near_early && !m->serial_phases) fork_near();
+  if (S.far && near_here && !near_early && !m->serial_phases) fork_near();
   if (S.far) {
     CouplingArgs ca{S.n_coup < 0 ? t->n_nodes : S.n_coup, S.coup, rs, cs, m->pl->L_ptr.p,
                     m->pl->L_j.p, m->qhat.p, m->zhat.p, m->p.dx, P.max_rank};
@@ -280,8 +290,8 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
       launches += 2;
     }
     mark(4, s);
-    if (m->serial_phases) fork_near();
-    SMASH_CUDA(cudaStreamWaitEvent(s, m->join, 0));
+    if (near_here && m->serial_phases) fork_near();
+    if (near_here) SMASH_CUDA(cudaStreamWaitEvent(s, m->join, 0));
     mark(8, s);
     launch_down_leaves<RC>(down, S.leaves, S.n_leaves, P.zrow.p, m->zn.p, z, nrhs, c0, s);
     check_phase("downward leaves", s);
@@ -617,7 +627,7 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
                   cudaStream_t s) {
   auto it = g_shards.find(m);
   SMASH_CHECK(it != g_shards.end(), SMASH_ERR_INVALID, "no partition set (smash_matvec_set_partition)");
-  SMASH_CHECK(stage == 1 || stage == 2, SMASH_ERR_INVALID, "stage must be 1 or 2");
+  SMASH_CHECK(stage >= 1 && stage <= 4, SMASH_ERR_INVALID, "stage must be 1, 2, 3 or 4");
   TreeImpl* t = m->tree;
   MatvecPlan* P = plan_of(m, s);
   const int rc_cap = prepare(m, P, s);
@@ -625,19 +635,24 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
               "sharded matvec takes one nrhs chunk (power of two <= the chunk cap)");
   const ShardSets& H = *it->second;
   PhaseSets S;
-  if (stage == 1) {  // local upward of the owned subtrees; unowned coefficients 0
-    S.zero_qhat = true;
+  if (stage == 1) {  // local upward of the owned subtrees (other coefficients untouched)
     S.up_leaves = H.leaves.p; S.n_up_leaves = H.n_leaves;
     S.up = H.own_up.p; S.n_up = H.n_own_up; S.up_in = H.own_in.p;
     S.far = false;
-  } else {  // after the coefficient exchange: top upward, then owned far/near field
+  } else if (stage == 3) {  // the owned leaves' nearfield only (overlaps the exchange)
+    S.gather = false;
+    S.far = false;
+    S.leaves = H.leaves.p; S.n_leaves = H.n_leaves;
+    S.near_mode = 1;
+  } else {  // after the coefficient exchange: top upward, then owned far (+ near) field
     S.gather = false;
     S.up = H.top_up.p; S.n_up = H.n_top_up; S.up_in = H.top_in.p;
     S.coup = H.coup.p; S.n_coup = H.n_coup;
     S.down = H.down.p; S.n_down = H.n_down; S.down_in = H.down_in.p;
     S.leaves = H.leaves.p; S.n_leaves = H.n_leaves;
+    S.near_mode = stage == 4 ? 2 : 0;  // 4: the nearfield ran as stage 3
   }
-  GraphEntry* E = graph_for(m, q, z, nrhs, stage, 1, stage == 2, [&](auto* evs, int* nl) {
+  GraphEntry* E = graph_for(m, q, z, nrhs, stage, 1, stage == 2 || stage == 4, [&](auto* evs, int* nl) {
     dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
       run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, m->sc, evs, nl);
     });

@@ -17,7 +17,8 @@ Matvec on rank r (ShardedMatvec):
   halo     all-to-all of skeleton coefficients: every rank receives exactly the
            coefficient rows its stage 2 reads from other ranks' subtrees -- the
            coupling sources of its owned + top targets, and the cut-level nodes
-           (inputs of the replicated top upward pass) -- nothing else;
+           (inputs of the replicated top upward pass) -- nothing else; the owned
+           leaves' nearfield (stage 3, needs only q) runs on a side stream meanwhile;
   stage 2  upward pass of the top nodes, coupling / downward pass for owned + top
            targets, nearfield + leaf far field for the owned leaves: the owned rows
            of z (disjoint over ranks, no reduction);
@@ -34,7 +35,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["partition", "subtree_work", "cut_partition", "own_top_leaves", "halo_rows", "ShardedMatvec"]
+__all__ = ["partition", "subtree_work", "cut_partition", "own_top_leaves", "halo_rows", "matvec_plan",
+           "set_partition", "frontier_fixup", "ShardedMatvec"]
 
 
 def subtree_work(A: dict, L: np.ndarray, Lm: np.ndarray, r: int, ranks=None) -> np.ndarray:
@@ -183,6 +185,60 @@ class _DevBuf:
                                          "version": 3, "strides": None}
 
 
+def matvec_plan(M, world: int, per_rank: int = 8) -> dict:
+    """Host plan of a sharded matvec of M over ``world`` ranks (no communication):
+    owner per node (M.shard_owner of a sharded build, else a work-balanced frontier
+    partition; leaves above the cut handed to one rank each), the coefficient layout
+    (row_off per node, up_pos per coefficient row, half = rows per half of the buffer)
+    and the halo rows[r][s] rank r sends to rank s."""
+    from .cluster import _pairs
+    A = M.tree.arrays()
+    L, Lm = _pairs(M.tree, M.params.tau, M.kind)
+    kcol = M.export_side(1)["rank"]
+    n = len(A["level"])
+    owner = getattr(M, "shard_owner", None)
+    w = subtree_work(A, L, Lm, M.params.r, kcol)
+    if owner is None:
+        owned, _, _ = partition(A, world, per_rank, w)
+        owner = np.full(n, -1, np.int64)
+        for r_, o in enumerate(owned):
+            owner[o] = r_
+    owner = own_top_leaves(A, np.asarray(owner, np.int64), world, w)
+    lib = _lib.load()
+    row_off = np.zeros(n, np.int64)
+    half = _lib.c_i64()
+    _lib.check(lib.smash_matvec_coeff_layout(M._h, row_off.ctypes.data_as(ctypes.c_void_p), None,
+                                             ctypes.byref(half), _lib.stream_ptr()))
+    up_pos = np.zeros(half.value, np.int64)
+    _lib.check(lib.smash_matvec_coeff_layout(M._h, row_off.ctypes.data_as(ctypes.c_void_p),
+                                             up_pos.ctypes.data_as(ctypes.c_void_p),
+                                             ctypes.byref(half), _lib.stream_ptr()))
+    rows, frontier = halo_rows(owner, A["parent"], L, row_off, kcol, world)
+    return dict(owner=owner, row_off=row_off, up_pos=up_pos, half=half.value, rows=rows,
+                frontier=frontier, kcol=kcol)
+
+
+def set_partition(M, plan: dict, rank: int):
+    """Hand rank's owned / replicated node lists to the device matvec (stage kernels)."""
+    owner = plan["owner"]
+    own = np.ascontiguousarray(np.nonzero(owner == rank)[0].astype(np.int64))
+    tp = np.ascontiguousarray(np.nonzero(owner < 0)[0].astype(np.int64))
+    _lib.check(_lib.load().smash_matvec_set_partition(
+        M._h, own.ctypes.data_as(ctypes.c_void_p), own.size, tp.ctypes.data_as(ctypes.c_void_p),
+        tp.size, _lib.stream_ptr()))
+    return own, tp
+
+
+def frontier_fixup(plan: dict, rank: int):
+    """(src, dst) coefficient rows: received cut-level rows copied into the parent-ibar
+    half of the buffer, the input order of the top upward pass."""
+    owner, fr = plan["owner"], plan["frontier"]
+    m = np.zeros(plan["half"], bool)
+    m[_rows_of(fr[owner[fr] != rank], plan["row_off"], plan["kcol"])] = True
+    src = np.nonzero(m & (plan["up_pos"] >= 0))[0]
+    return src, plan["half"] + plan["up_pos"][src]
+
+
 class ShardedMatvec:
     """Rank-local sharded matvec over a process group.  M is either a matrix built by
     h2.build_h2_sharded (its partition and sharded factors are used) or a replicated
@@ -191,59 +247,26 @@ class ShardedMatvec:
     def __init__(self, M, group=None, per_rank: int = 8):
         import torch
         import torch.distributed as dist
-        from .cluster import _pairs
         self.M = M
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.backend = dist.get_backend(group)
-        A = M.tree.arrays()
-        tau = M.params.tau
-        L, Lm = _pairs(M.tree, tau, M.kind)
-        kcol = M.export_side(1)["rank"]
-        n = len(A["level"])
-        owner = getattr(M, "shard_owner", None)
-        w = subtree_work(A, L, Lm, M.params.r, kcol)
-        if owner is None:
-            owned, top, self.frontier = partition(A, self.world, per_rank, w)
-            owner = np.full(n, -1, np.int64)
-            for r_, o in enumerate(owned):
-                owner[o] = r_
-        owner = own_top_leaves(A, np.asarray(owner, np.int64), self.world, w)
-        self.owner = owner
-        self.owned = np.nonzero(owner == self.rank)[0].astype(np.int64)
-        self.top = np.nonzero(owner < 0)[0].astype(np.int64)
-        own = np.ascontiguousarray(self.owned)
-        tp = np.ascontiguousarray(self.top)
-        lib = _lib.load()
-        _lib.check(lib.smash_matvec_set_partition(
-            M._h, own.ctypes.data_as(ctypes.c_void_p), own.size, tp.ctypes.data_as(ctypes.c_void_p),
-            tp.size, _lib.stream_ptr()))
-        # coefficient layout and the halo rows
-        row_off = np.zeros(n, np.int64)
-        half = _lib.c_i64()
-        _lib.check(lib.smash_matvec_coeff_layout(M._h, row_off.ctypes.data_as(ctypes.c_void_p), None,
-                                                 ctypes.byref(half), _lib.stream_ptr()))
-        up_pos = np.zeros(half.value, np.int64)
-        _lib.check(lib.smash_matvec_coeff_layout(M._h, row_off.ctypes.data_as(ctypes.c_void_p),
-                                                 up_pos.ctypes.data_as(ctypes.c_void_p),
-                                                 ctypes.byref(half), _lib.stream_ptr()))
-        self.half = half.value
-        rows, frontier = halo_rows(owner, A["parent"], L, row_off, kcol, self.world)
-        self.frontier_nodes = frontier
+        plan = matvec_plan(M, self.world, per_rank)
+        self.owner = plan["owner"]
+        self.owned, self.top = set_partition(M, plan, self.rank)
+        self.half = plan["half"]
+        rows = plan["rows"]
+        self.frontier_nodes = plan["frontier"]
         self.send_counts = [int(rows[self.rank][s].size) for s in range(self.world)]
         self.recv_counts = [int(rows[s][self.rank].size) for s in range(self.world)]
         cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)  # noqa: E731
         dev = torch.device("cuda", torch.cuda.current_device())
         self.send_idx = torch.from_numpy(cat([rows[self.rank][s] for s in range(self.world)])).to(dev)
-        recv = cat([rows[s][self.rank] for s in range(self.world)])
-        self.recv_idx = torch.from_numpy(recv).to(dev)
-        # received cut-level rows also feed the top upward pass in parent-ibar order
-        fr = np.zeros(self.half, bool)
-        fr[_rows_of(frontier[owner[frontier] != self.rank], row_off, kcol)] = True
-        fr_rows = np.nonzero(fr & (up_pos >= 0))[0]
-        self.fr_src = torch.from_numpy(fr_rows).to(dev)
-        self.fr_dst = torch.from_numpy(self.half + up_pos[fr_rows]).to(dev)
+        self.recv_idx = torch.from_numpy(cat([rows[s][self.rank] for s in range(self.world)])).to(dev)
+        src, dst = frontier_fixup(plan, self.rank)
+        self.fr_src = torch.from_numpy(src).to(dev)
+        self.fr_dst = torch.from_numpy(dst).to(dev)
         self.halo_rows_total = int(sum(rows[r][s].size for r in range(self.world) for s in range(self.world)))
 
     def coeff_view(self, nrhs: int):
@@ -276,19 +299,32 @@ class ShardedMatvec:
         if self.fr_src.numel():
             C.index_copy_(0, self.fr_dst, C.index_select(0, self.fr_src))
 
-    def __call__(self, Q, gather_output: bool = True):
+    def __call__(self, Q, gather_output: bool = True, overlap: bool = True):
         """Q: (n_col, nrhs) CUDA float64, replicated on every rank (nrhs a power of
         two <= 16).  Returns z (n_row, nrhs): the owned rows (others 0), or the full
-        product when gather_output."""
+        product when gather_output.  overlap: the owned leaves' nearfield (stage 3, it
+        needs only q) runs on a side stream during the halo exchange."""
         import torch
         import torch.distributed as dist
         Q = Q.contiguous()
         nrhs = Q.shape[1]
         lib = _lib.load()
         z = torch.zeros((self.M.n_row, nrhs), dtype=torch.float64, device=Q.device)
+        main = torch.cuda.current_stream()
         _lib.check(lib.smash_matvec_stage(self.M._h, 1, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
-        self.exchange(nrhs)
-        _lib.check(lib.smash_matvec_stage(self.M._h, 2, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
+        if overlap:
+            if not hasattr(self, "_side"):
+                self._side = torch.cuda.Stream()
+            self._side.wait_stream(main)
+            with torch.cuda.stream(self._side):
+                _lib.check(lib.smash_matvec_stage(self.M._h, 3, _lib.ptr(Q), _lib.ptr(z), nrhs,
+                                                  _lib.stream_ptr()))
+            self.exchange(nrhs)
+            main.wait_stream(self._side)
+            _lib.check(lib.smash_matvec_stage(self.M._h, 4, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
+        else:
+            self.exchange(nrhs)
+            _lib.check(lib.smash_matvec_stage(self.M._h, 2, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
         if gather_output:
             if self.backend == "gloo":
                 zh = z.cpu()

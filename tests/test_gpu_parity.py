@@ -229,48 +229,53 @@ def test_matvec_multi_rhs_vs_oracle(smash_gpu, golden, name, nrhs):
         assert rel <= 1e-10, (c, rel)
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("name", ["cfg2_32k", "cfg5_16k", "pair1d_hss"])
-def test_sharded_stages_single_process(smash_gpu, golden, name, world):
-    """The multi-GPU stages (shard.py) emulated in one process on one GPU: one
-    matrix per virtual rank, the coefficient all-reduce and the z all-reduce done
-    with plain tensor sums (no inter-rank waiting on one device)."""
+def test_sharded_stages_single_process(smash_gpu, golden, name, world, overlap):
+    """The multi-GPU stages (shard.py) emulated in one process on one GPU: one matrix per
+    virtual rank, the halo exchange done by copying exactly the planned coefficient rows
+    between the ranks' buffers (no inter-rank waiting on one device), stage 2 or the
+    stage 3 (nearfield) + stage 4 split; the owned rows summed must equal the product."""
     import torch
     from paper_1705_05443_b200 import _lib
-    from paper_1705_05443_b200.shard import partition
+    from paper_1705_05443_b200.shard import _DevBuf, frontier_fixup, matvec_plan, set_partition
     import ctypes
     g = golden(name)
-    m = g["meta"]
     mats = []
     for r in range(world):
         _MATS.pop(name, None)
         _TREES.pop(name, None)
         mats.append(gpu_matrix(smash_gpu, golden, name))
-    owned, top, _ = partition(mats[0].tree.arrays(), world)
+    plan = matvec_plan(mats[0], world)
     lib = _lib.load()
     nrhs = 8
     Q = torch.from_numpy(np.random.default_rng(7).standard_normal((g["Y"].shape[0], nrhs))).cuda()
-    zs, coeffs = [], []
+    zs = []
     for r, M in enumerate(mats):
-        own = np.ascontiguousarray(owned[r])
-        tp = np.ascontiguousarray(top)
-        _lib.check(lib.smash_matvec_set_partition(M._h, own.ctypes.data_as(ctypes.c_void_p), own.size,
-                                                  tp.ctypes.data_as(ctypes.c_void_p), tp.size,
-                                                  _lib.stream_ptr()))
+        set_partition(M, plan, r)
         z = torch.zeros((M.n_row, nrhs), dtype=torch.float64, device="cuda")
         _lib.check(lib.smash_matvec_stage(M._h, 1, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
+        if overlap:
+            _lib.check(lib.smash_matvec_stage(M._h, 3, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
         zs.append(z)
-    from paper_1705_05443_b200.shard import _DevBuf
     views = []
     for M in mats:
         p, rows = ctypes.c_void_p(), _lib.c_i64()
         _lib.check(lib.smash_matvec_coeffs(M._h, ctypes.byref(p), ctypes.byref(rows)))
-        views.append(torch.as_tensor(_DevBuf(p.value, rows.value * nrhs), device="cuda"))
-    total = sum(v.clone() for v in views)
-    for v in views:
-        v.copy_(total)
+        views.append(torch.as_tensor(_DevBuf(p.value, rows.value * nrhs), device="cuda").view(rows.value, nrhs))
+    sent = [v.clone() for v in views]  # what each rank holds after stage 1
+    for r in range(world):
+        for s_ in range(world):
+            idx = torch.from_numpy(plan["rows"][s_][r]).cuda()
+            if idx.numel():
+                views[r].index_copy_(0, idx, sent[s_].index_select(0, idx))
+        src, dst = frontier_fixup(plan, r)
+        if src.size:
+            views[r].index_copy_(0, torch.from_numpy(dst).cuda(), views[r].index_select(0, torch.from_numpy(src).cuda()))
     for M, z in zip(mats, zs):
-        _lib.check(lib.smash_matvec_stage(M._h, 2, _lib.ptr(Q), _lib.ptr(z), nrhs, _lib.stream_ptr()))
+        _lib.check(lib.smash_matvec_stage(M._h, 4 if overlap else 2, _lib.ptr(Q), _lib.ptr(z), nrhs,
+                                          _lib.stream_ptr()))
     zsum = sum(zs).cpu().numpy()
     zref = smash_gpu.matvec_nodewise(mats[0], Q.cpu().numpy())
     rel = np.linalg.norm(zsum - zref) / np.linalg.norm(zref)
