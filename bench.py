@@ -409,11 +409,13 @@ def run_ours(args):
         dX = torch.from_numpy(X).to(dev)
         dQ = torch.from_numpy(q).to(dev)
         builder = sg.build_h2 if c["structure"] == "h2" else sg.build_hss
-        sharded_build = c["structure"] == "h2" and Y is X
+        sharded_build = c["structure"] == "hss" or Y is X
 
         def build_device():
             tree = sg.build_tree(sg.PointSet(dX), None if Y is X else sg.PointSet(torch.from_numpy(Y).to(dev)),
                                  nu0=c["nu0"], mode=c["mode"], tau=c["tau"])
+            if c["structure"] == "hss":  # level-distributed, factors replicated
+                return sg.build_hss_sharded(tree, spec, None, None, params)
             if sharded_build:
                 return sg.build_h2_sharded(tree, spec, None, None, params)
             return builder(tree, spec, None, None, params)
@@ -519,7 +521,8 @@ def run_ours(args):
         assert np.array_equal(zd, z.numpy()), "device and e2e results differ"
         parity = golden_parity(cfg, N, R, zd)
     else:  # sharded (full, gathered) vs a single-GPU build + matvec on this rank
-        tree1 = sg.build_tree(sg.PointSet(dX), nu0=c["nu0"], mode=c["mode"], tau=c["tau"])
+        tree1 = sg.build_tree(sg.PointSet(dX), None if Y is X else sg.PointSet(torch.from_numpy(Y).to(dev)),
+                              nu0=c["nu0"], mode=c["mode"], tau=c["tau"])
         R1 = builder(tree1, spec, None, None, params)
         zf = sg.matvec_device(R1, dQ).cpu().numpy()
         del R1
@@ -597,8 +600,10 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md 8(d))",
             "config": workload_config(cfg, N, R),
             "build_s": b_s,
-            "build_mode": "sharded: work-balanced cut, skeleton exchange, factors kept on their owner"
-                          if ws > 1 else "single",
+            "build_mode": ("single" if ws == 1 else
+                           "sharded (HSS): level-distributed, one exchange per level and side"
+                           if c["structure"] == "hss" else
+                           "sharded: work-balanced cut, skeleton exchange, factors kept on their owner"),
             "phase_ms": {"gather": phase[0], "upward": phase[1], "coupling": phase[2], "downward": phase[3],
                          "nearfield_concurrent": phase[4], "leaf_farfield": phase[5],
                          "matvec_profiled": phase[6],

@@ -118,6 +118,18 @@ int smash_matrix_build(smash_tree_t t, const smash_build_params* p, void* stream
  * on every rank.  The result equals smash_matrix_build's bit for bit. */
 int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_t rank,
                              int32_t world, int32_t cut_level, void* stream, smash_matrix_t* out);
+/* Level-distributed HSS construction (SURVEY.md 8(e) for configs 1 and 4; replaces the level
+ * loop of smash/hss.py:271-299 when one process per GPU builds): at every level each rank
+ * runs the nearfield SVDs and compressions of its contiguous share of the level's nodes, then
+ * calls fn(ctx, n, ptrs, counts, dtypes) -- the caller must sum each listed device buffer over
+ * the ranks in place (dtype 0 int32, 1 float64 summed as int64 bit patterns, 2 int64, 3 int32
+ * maximum; the shares are disjoint and zero elsewhere) and return 0 -- and compacts the level's
+ * skeletons.  Every rank ends with the full matrix, identical to smash_matrix_build's. */
+typedef int32_t (*smash_exchange_fn)(void* ctx, int64_t n, void** ptrs, const int64_t* counts,
+                                     const int32_t* dtypes);
+int smash_matrix_build_sharded(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                               int32_t world, smash_exchange_fn fn, void* ctx, void* stream,
+                               smash_matrix_t* out);
 /* As smash_matrix_build_local, with cut_weight (HOST float64[number of cut-level nodes],
  * left to right; NULL = subtree point counts) balancing the contiguous cut-level ranges,
  * and replicate = 0 to keep the factors sharded: perm and G are then NOT in the exchange list,

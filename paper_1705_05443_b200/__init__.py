@@ -12,7 +12,7 @@ from .cluster import (Box, ClusterTree, PointSet, TreeNode, build_tree, leaf_set
                       well_separated)
 from .kernel import KernelSpec, kernel_block
 from .lowrank import InterpolativeFactor, compr, interp_basis
-from .hss import BuildParams, HssMatrix, build_hss
+from .hss import BuildParams, HssMatrix, build_hss, build_hss_sharded
 from .h2 import H2Matrix, build_h2, build_h2_local, build_h2_sharded
 from .apply import (MatvecStream, UlvFactorization, matvec_device, matvec_levelwise, matvec_nodewise,
                     ulv_factor, ulv_solve)
@@ -24,7 +24,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Box", "BuildParams", "ClusterTree", "H2Matrix", "HssMatrix", "InterpolativeFactor",
-    "KernelSpec", "PointSet", "TreeNode", "build_h2", "build_h2_local", "build_h2_sharded", "build_hss", "build_tree", "compr",
+    "KernelSpec", "PointSet", "TreeNode", "build_h2", "build_h2_local", "build_h2_sharded", "build_hss", "build_hss_sharded", "build_tree", "compr",
     "interp_basis", "kernel_block", "leaf_sets", "matvec_device", "matvec_levelwise", "matvec_nodewise",
     "dense_matvec", "relative_error", "MatvecStream",
     "nearfield_set", "well_separated", "save_matrix", "load_matrix",

@@ -21,6 +21,11 @@ c_i32, c_i64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, cty
 P_i32, P_i64, P_dbl = ctypes.POINTER(c_i32), ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl)
 
 
+# smash_exchange_fn (include/smash_b200.h)
+EXCHANGE_FN = ctypes.CFUNCTYPE(c_i32, c_vp, c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_i64),
+                               ctypes.POINTER(c_i32))
+
+
 class BuildParamsC(ctypes.Structure):
     _fields_ = [("structure", c_i32), ("kernel", c_i32), ("dx", c_dbl), ("r", c_i32),
                 ("tau", c_dbl), ("s", c_dbl), ("rtol", c_dbl), ("eps_svd", c_dbl)]
@@ -54,6 +59,8 @@ SIGNATURES = {
     "smash_ulv_free": (c_i32, [c_vp]),
     "smash_matvec": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "smash_matvec_levelwise": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "smash_matrix_build_sharded": (c_i32, [c_vp, ctypes.POINTER(BuildParamsC), c_i32, c_i32, c_vp,
+                                           c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "smash_matrix_build_local_w": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp, c_vp]),
     "smash_matrix_shard_cut": (c_i32, [c_vp, c_i32, c_i32, c_vp]),
     "smash_matrix_shard_owner": (c_i32, [c_vp, c_vp]),

@@ -169,6 +169,16 @@ int smash_matrix_build_local(smash_tree_t t, const smash_build_params* p, int32_
   });
 }
 
+int smash_matrix_build_sharded(smash_tree_t t, const smash_build_params* p, int32_t rank,
+                               int32_t world, smash_exchange_fn fn, void* ctx, void* stream,
+                               smash_matrix_t* out) {
+  return guarded([&] {
+    SMASH_CHECK(t && t->impl && p && out, SMASH_ERR_INVALID, "null argument");
+    smash::MatrixImpl* m = smash::matrix_build_sharded(t->impl, *p, rank, world, fn, ctx, st(stream));
+    *out = new smash_matrix_s{m};
+  });
+}
+
 int smash_matrix_build_local_w(smash_tree_t t, const smash_build_params* p, int32_t rank,
                                int32_t world, int32_t cut_level, const double* cut_weight,
                                int32_t replicate, void* stream, smash_matrix_t* out) {

@@ -246,6 +246,10 @@ struct SideBuild {
   // the whole sweep is enqueued without a host round trip; the device keeps the
   // running skeleton count.  HSS needs the SVD keep counts on the host.
   bool async = false;
+  // level-distributed build (matrix_build_sharded): this rank's share of every level
+  int shard_rank = 0, shard_world = 1;
+  smash_exchange_fn xfn = nullptr;
+  void* xctx = nullptr;
   std::vector<int64_t> lvl_ib_b, lvl_g_b, lvl_ib_base;
   std::vector<int> lvl_nmax_b;
   DBuf<int> d_used;
@@ -459,16 +463,28 @@ struct SideBuild {
     k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, ibo.p, F->ib_total, F->ib_off.p);
     k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, go.p, F->g_total, F->g_off.p);
 
-    // ---- HSS nearfield SVD (hss.py:279-299)
-    int max_keep = 0;
-    auto t1 = now();
-    if (hss) max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s);
-    auto t2 = now();
-
+    // level-distributed build: this rank's contiguous share of the level's nodes; the
+    // level's outputs are zero elsewhere and summed over the ranks below
+    const bool sharded = shard_world > 1;
+    const int sub_lb = sharded ? lb + (int)((int64_t)cnt * shard_rank / shard_world) : lb;
+    const int sub_le = sharded ? lb + (int)((int64_t)cnt * (shard_rank + 1) / shard_world) : le;
     DBuf<int> tmp_lab;
     DBuf<double> tmp_pts;
     tmp_lab.alloc(std::max<int64_t>(lvl_ib, 1), s);
     tmp_pts.alloc((size_t)std::max<int64_t>(lvl_ib, 1) * dim, s);
+    if (sharded) {
+      SMASH_CUDA(cudaMemsetAsync(F->rank.p + lb, 0, 4 * (size_t)cnt, s));
+      SMASH_CUDA(cudaMemsetAsync(F->perm.p + F->ib_total, 0, 4 * (size_t)lvl_ib, s));
+      SMASH_CUDA(cudaMemsetAsync(F->G.p + F->g_total, 0, 8 * (size_t)lvl_g, s));
+      tmp_lab.zero(s);
+      tmp_pts.zero(s);
+    }
+
+    // ---- HSS nearfield SVD (hss.py:279-299)
+    int max_keep = 0;
+    auto t1 = now();
+    if (hss) max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s, sub_lb, sub_le);
+    auto t2 = now();
 
     CompressArgs A;
     A.lb = lb; A.le = le; A.dim = dim; A.r = r; A.side = side;
@@ -485,7 +501,21 @@ struct SideBuild {
     A.err = err.p; A.swaps = swaps.p;
     A.nmax = std::max(nmax, 1);
     A.mmax = r + max_keep;
-    launch_level(A, cnt);
+    if (sharded) {
+      A.lb = sub_lb;
+      A.le = sub_le;
+      if (sub_le > sub_lb) launch_level(A, sub_le - sub_lb);
+      // the cut-level exchange of this level: ranks, perm, G, ordered skeleton labels and
+      // coordinates (disjoint shares summed), error flags (maximum)
+      sync(s);
+      void* ptrs[6] = {F->rank.p + lb, F->perm.p + F->ib_total, F->G.p + F->g_total, tmp_lab.p,
+                       tmp_pts.p, err.p};
+      int64_t counts[6] = {cnt, lvl_ib, lvl_g, lvl_ib, lvl_ib * dim, 1};
+      int32_t dts[6] = {0, 0, 1, 0, 1, 3};
+      SMASH_CHECK(xfn(xctx, 6, ptrs, counts, dts) == 0, SMASH_ERR_CUDA, "sharded build exchange failed");
+    } else {
+      launch_level(A, cnt);
+    }
     auto t3 = now();
     if (timing)
       fprintf(stderr, "level %d side %d cnt %d: sizes %.3f ms svd %.3f ms compress %.3f ms\n", l, side,
@@ -517,6 +547,13 @@ struct SideBuild {
   }
 
   void finish() {
+    if (shard_world > 1) {  // the rank's pivot-swap count -> the job's
+      sync(s);
+      void* ptrs[1] = {swaps.p};
+      int64_t counts[1] = {1};
+      int32_t dts[1] = {2};
+      SMASH_CHECK(xfn(xctx, 1, ptrs, counts, dts) == 0, SMASH_ERR_CUDA, "sharded build exchange failed");
+    }
     unsigned long long hs = 0;
     int used = 0, herr = 0;
     d2h(&hs, swaps.p, 1, s);
@@ -627,7 +664,10 @@ struct PairsJob {
   }
 };
 
-MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s) {
+// The level sweep of matrix_build; with world > 1 (HSS only) every level is split over
+// the ranks and summed through fn (matrix_build_sharded).
+static MatrixImpl* build_levels(TreeImpl* t, const smash_build_params& p, cudaStream_t s, int rank,
+                                int world, smash_exchange_fn fn, void* ctx) {
   SMASH_CHECK(p.kernel >= SMASH_KERNEL_LOG && p.kernel <= SMASH_KERNEL_CAUCHY, SMASH_ERR_INVALID,
               "unknown kernel kind");
   SMASH_CHECK(p.structure == SMASH_STRUCT_H2 || p.structure == SMASH_STRUCT_HSS,
@@ -671,6 +711,8 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
     colb.reset(new SideBuild{M.get(), 1, &M->colf_own, &D, pad, s});
     colb->init();
   }
+  for (SideBuild* b : {&rowb, colb.get()})
+    if (b) { b->shard_rank = rank; b->shard_world = world; b->xfn = fn; b->xctx = ctx; }
   // row and column passes interleave per level: the HSS row pass at level l
   // reads the column side's level-(l+1) skeletons and vice versa (hss.py:274-299)
   for (int l = t->n_levels; l >= 2; --l) {
@@ -682,6 +724,19 @@ MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t 
   if (colb) colb->finish();
   sync(s);
   return M.release();
+}
+
+MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s) {
+  return build_levels(t, p, s, 0, 1, nullptr, nullptr);
+}
+
+MatrixImpl* matrix_build_sharded(TreeImpl* t, const smash_build_params& p, int rank, int world,
+                                 smash_exchange_fn fn, void* ctx, cudaStream_t s) {
+  SMASH_CHECK(p.structure == SMASH_STRUCT_HSS, SMASH_ERR_INVALID,
+              "level-distributed construction builds HSS matrices (H2: smash_matrix_build_local)");
+  SMASH_CHECK(world >= 1 && rank >= 0 && rank < world && fn, SMASH_ERR_INVALID,
+              "bad rank / world size / exchange function");
+  return build_levels(t, p, s, rank, world, fn, ctx);
 }
 
 // ---------------------------------------------------------------------------

@@ -213,7 +213,10 @@ void run_chunk(MatrixImpl* m, MatvecPlan& P, const PhaseSets& S, const double* q
     NearArgs na{S.leaves, S.n_leaves, t->row_a.p, t->row_b.p, col_a, col_b, t->pts_row.p, t->nx,
                 pts_col, t->ny, m->pl->Lm_ptr.p, m->pl->Lm_j.p, m->qt.p, P.slot_of.p, m->zn.p,
                 m->p.dx, t->nu0};
+    mark(6, s);
     launch_near<KER, D, RC>(na, s);
+    mark(7, s);
+    mark(5, s);
     *nlaunch += 1;
     return;
   }
@@ -392,6 +395,8 @@ void replay(MatrixImpl* m, GraphEntry* E, cudaStream_t s) {
     for (auto& ev : E->ev) {
       SMASH_CUDA(cudaEventSynchronize(ev[5]));
       for (int i = 0; i < 7; ++i) {
+        // sharded stages: 3 records only the nearfield, 4 everything but it
+        if ((E->stage == 4 && i == 4) || (E->stage == 3 && i != 4)) continue;
         float ms = 0;
         SMASH_CUDA(cudaEventElapsedTime(&ms, ev[pairs[i][0]], ev[pairs[i][1]]));
         m->phase_ms[i] += ms;
@@ -652,7 +657,7 @@ void matvec_stage(MatrixImpl* m, int stage, const double* q, double* z, int64_t 
     S.leaves = H.leaves.p; S.n_leaves = H.n_leaves;
     S.near_mode = stage == 4 ? 2 : 0;  // 4: the nearfield ran as stage 3
   }
-  GraphEntry* E = graph_for(m, q, z, nrhs, stage, 1, stage == 2 || stage == 4, [&](auto* evs, int* nl) {
+  GraphEntry* E = graph_for(m, q, z, nrhs, stage, 1, stage >= 2, [&](auto* evs, int* nl) {
     dispatch_kernel_dim(m->p.kernel, t->dim, [&]<int KER, int D>() {
       run_all<KER, D>(m, *P, S, q, z, nrhs, rc_cap, m->sc, evs, nl);
     });

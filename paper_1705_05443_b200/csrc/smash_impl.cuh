@@ -140,6 +140,10 @@ struct MatrixImpl {
 };
 
 MatrixImpl* matrix_build(TreeImpl* t, const smash_build_params& p, cudaStream_t s);
+// level-distributed construction: every level's nodes are split over the ranks, the
+// level's outputs summed over them through the caller's exchange (smash_exchange_fn)
+MatrixImpl* matrix_build_sharded(TreeImpl* t, const smash_build_params& p, int rank, int world,
+                                 smash_exchange_fn fn, void* ctx, cudaStream_t s);
 void dense_matvec(int kernel, double dx, int dim, const double* X, int64_t nx, const double* Y,
                   int64_t ny, const double* q, int64_t nrhs, double* z, cudaStream_t s);
 // sharded construction (build.cu): local levels, buffers to sum over ranks, finish

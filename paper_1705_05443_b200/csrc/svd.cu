@@ -516,10 +516,12 @@ IbarSide ibar_side(MatrixImpl* M, int side) {
 }  // namespace
 
 int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, SvdWorkspace& ws,
-                  cudaStream_t s) {
+                  cudaStream_t s, int sub_lb, int sub_le) {
   TreeImpl* t = M->tree;
   const int n_nodes = t->n_nodes;
   const int lb = t->level_begin(level), le = t->level_end(level), cnt = le - lb;
+  // sharded build: the SVDs of this rank's node range only (capacities stay level-wide)
+  const int run_lb = sub_lb >= 0 ? sub_lb : lb, run_le = sub_lb >= 0 ? sub_le : le;
   if (ws.keep.n < (size_t)n_nodes) {
     ws.keep.alloc(n_nodes, s);
     ws.keep.zero(s);
@@ -599,10 +601,15 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
     SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-    k_svd<KER, D><<<grid, SVD_THREADS, smem, s>>>(A);
+    SvdArgs Ar = A;
+    Ar.lb = run_lb;
+    Ar.le = run_le;
+    if (run_le > run_lb) k_svd<KER, D><<<std::min(grid, run_le - run_lb), SVD_THREADS, smem, s>>>(Ar);
   });
   SMASH_CUDA(cudaGetLastError());
-  k_max_keep<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(lb, le, ws.keep.p, dmax.p);
+  if (run_le > run_lb)
+    k_max_keep<<<std::min<unsigned>(cdiv(run_le - run_lb, 256), 64), 256, 0, s>>>(run_lb, run_le, ws.keep.p,
+                                                                                dmax.p);
   int hk = 0, he = 0;
   d2h(&hk, dmax.p, 1, s);
   d2h(&he, err.p, 1, s);

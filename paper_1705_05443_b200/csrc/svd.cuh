@@ -15,6 +15,6 @@ struct SvdWorkspace {
 // (hss.py:281-285 / 292-296), compute its truncated SVD (lowrank.py:265-276)
 // and leave S in ws.  Returns the level's maximum keep count.
 int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, SvdWorkspace& ws,
-                  cudaStream_t s);
+                  cudaStream_t s, int sub_lb = -1, int sub_le = -1);
 
 }  // namespace smash

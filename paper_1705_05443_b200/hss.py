@@ -22,7 +22,7 @@ from .cluster import ClusterTree, leaf_sets
 from .kernel import KernelSpec, kernel_block_coords
 from .lowrank import InterpolativeFactor
 
-__all__ = ["BuildParams", "HssMatrix", "build_hss", "make_matrix"]
+__all__ = ["BuildParams", "HssMatrix", "build_hss", "build_hss_sharded", "make_matrix"]
 
 
 @dataclass
@@ -227,15 +227,19 @@ class HssMatrix(_StructuredMatrix):
         return self.B(i, self.tree.sibling(i))
 
 
-def make_matrix(cls, tree: ClusterTree, kernel: KernelSpec, params: BuildParams, use_cache: bool):
-    """Run the GPU construction for ``cls.kind`` and wrap the handle."""
+def _params_c(kind: str, tree: ClusterTree, kernel: KernelSpec, params: BuildParams):
     _resolve_basis(params, kernel)
     if kernel.kind == "cauchy" and kernel.dx is None and tree.shared_points:
         raise ValueError("coincident points need a diagonal value d_x")
-    p = _lib.BuildParamsC(structure=_lib.STRUCT[cls.kind], kernel=kernel.code,
-                          dx=kernel.dx_value if kernel.dx_value == kernel.dx_value else 0.0,
-                          r=int(params.r), tau=float(params.tau), s=float(params.s),
-                          rtol=float(params.rtol), eps_svd=float(params.eps_svd))
+    return _lib.BuildParamsC(structure=_lib.STRUCT[kind], kernel=kernel.code,
+                             dx=kernel.dx_value if kernel.dx_value == kernel.dx_value else 0.0,
+                             r=int(params.r), tau=float(params.tau), s=float(params.s),
+                             rtol=float(params.rtol), eps_svd=float(params.eps_svd))
+
+
+def make_matrix(cls, tree: ClusterTree, kernel: KernelSpec, params: BuildParams, use_cache: bool):
+    """Run the GPU construction for ``cls.kind`` and wrap the handle."""
+    p = _params_c(cls.kind, tree, kernel, params)
     h = ctypes.c_void_p()
     _lib.check(_lib.load().smash_matrix_build(tree._h, ctypes.byref(p), _lib.stream_ptr(),
                                               ctypes.byref(h)))
@@ -250,3 +254,54 @@ def build_hss(tree: ClusterTree, kernel: KernelSpec, X=None, Y=None, params: Bui
     if tree.mode == "2d" and tree.dim > 1:
         raise ValueError("HSS construction needs a binary tree")
     return make_matrix(HssMatrix, tree, kernel, params, use_cache)
+
+
+def build_hss_sharded(tree: ClusterTree, kernel: KernelSpec, X=None, Y=None, params: BuildParams = None,
+                      group=None, use_cache: bool = True) -> HssMatrix:
+    """HSS construction distributed over the ranks of a torch.distributed process group
+    (SURVEY.md 8(e), configs 1 and 4).  HSS levels depend on each other through the
+    nearfield SVD (hss.py:279-299 reads the other side's level-(l+1) skeletons), so the
+    work is split level by level: every rank runs the SVDs and sRRQRs of a contiguous
+    share of the level's nodes, and one exchange per level and side sums the disjoint,
+    zero-filled ranks / perm / G / ordered skeleton labels and coordinates over the ranks
+    (float64 as int64 bit patterns: exact) before every rank compacts the level.  Every
+    rank ends with the full matrix, bit-identical to build_hss's."""
+    import torch
+    import torch.distributed as dist
+    from .h2 import _DevView
+    params = params or BuildParams()
+    if tree.mode == "2d" and tree.dim > 1:
+        raise ValueError("HSS construction needs a binary tree")
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    p = _params_c("hss", tree, kernel, params)
+    gloo = dist.get_backend(group) == "gloo"
+    failure = []
+    VIEW = {0: 0, 1: 2, 2: 2, 3: 0}  # float64 summed as its int64 bit pattern
+
+    def exchange(ctx, n, ptrs, counts, dtypes):
+        try:
+            for i in range(n):
+                dt = dtypes[i]
+                t = torch.as_tensor(_DevView(ptrs[i], counts[i], VIEW[dt]), device="cuda")
+                op = dist.ReduceOp.MAX if dt == 3 else dist.ReduceOp.SUM
+                if gloo:
+                    h = t.cpu()
+                    dist.all_reduce(h, op=op, group=group)
+                    t.copy_(h)
+                else:
+                    dist.all_reduce(t, op=op, group=group)
+            torch.cuda.current_stream().synchronize()
+            return 0
+        except BaseException as e:  # surfaced after the C call returns
+            failure.append(e)
+            return 1
+
+    fn = _lib.EXCHANGE_FN(exchange)
+    h = ctypes.c_void_p()
+    rc = _lib.load().smash_matrix_build_sharded(tree._h, ctypes.byref(p), int(rank), int(world),
+                                                ctypes.cast(fn, ctypes.c_void_p), None,
+                                                _lib.stream_ptr(), ctypes.byref(h))
+    if failure:
+        raise failure[0]
+    _lib.check(rc)
+    return HssMatrix(tree, params, kernel, h, use_cache)

@@ -168,3 +168,51 @@ def test_sharded_factors_and_matvec_processes_gloo(sg, cfg, N, world):
         assert res[r]["ok"] and res[r]["guarded"], res[r]
         assert res[r]["rel"] <= 1e-13, res[r]
         assert res[r]["halo"] < 2 * res[r]["rows"]  # the halo is not an all-gather
+
+
+def _same_hss(M, R):
+    _same(M, R)
+    assert tuple(M.swaps) == tuple(R.swaps)
+
+
+def _worker_hss(rank, world, port, cfg, N, out):
+    """Level-distributed HSS construction (build_hss_sharded): every rank compresses a
+    share of each level and the level's outputs are summed through the exchange
+    callback; every rank must hold build_hss's matrix bit for bit."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1705_05443_b200 as sg
+    res = {}
+    try:
+        tree, spec, params, q = _case(sg, cfg, N)
+        M = sg.build_hss_sharded(tree, spec, None, None, params)
+        R = sg.build_hss(tree, spec, None, None, params)
+        _same_hss(M, R)
+        res = dict(ok=bool(np.array_equal(sg.matvec_nodewise(M, q), sg.matvec_nodewise(R, q))))
+    except AssertionError as e:
+        res = dict(ok=False, why=repr(e))
+    except Exception as e:  # report instead of hanging the other rank
+        res = dict(err=repr(e))
+    out.put((rank, res))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,N,world", [(1, 1 << 14, 2), (4, 1 << 14, 2), (1, 1 << 13, 3)])
+def test_hss_sharded_processes_gloo(sg, cfg, N, world):
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_hss, args=(r, world, port, cfg, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r].get("ok"), res[r]
