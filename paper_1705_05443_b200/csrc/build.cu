@@ -46,9 +46,12 @@ void grow(DBuf<T>& b, size_t used, size_t need, cudaStream_t s) {
   b = std::move(nb);
 }
 
+// G capacity per node: |ibar| x min(|ibar|, bound) with bound = r (H2) or, for HSS,
+// r + keep_v (the compression panel's row count, known after the nearfield SVD)
 __global__ void k_level_sizes(int lb, int le, const int* nchild, const int* child_first,
                               const int* pt_a, const int* pt_b, const int* rank, int* nib,
-                              int64_t* ibcnt, int64_t* gcnt, int mrows_bound) {
+                              int64_t* ibcnt, int64_t* gcnt, int mrows_bound,
+                              const int* keep = nullptr) {
   int v = lb + blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= le) return;
   int n;
@@ -60,7 +63,7 @@ __global__ void k_level_sizes(int lb, int le, const int* nchild, const int* chil
   }
   nib[v] = n;
   ibcnt[v - lb] = n;
-  gcnt[v - lb] = (int64_t)n * min(n, mrows_bound);
+  gcnt[v - lb] = (int64_t)n * min(n, keep ? mrows_bound + keep[v] : mrows_bound);
 }
 
 __global__ void k_level_nib(int lb, int le, const int* nchild, const int* child_first,
@@ -436,13 +439,43 @@ struct SideBuild {
       return std::chrono::steady_clock::now();
     };
     auto t0 = now();
+    // level-distributed build: this rank's contiguous share of the level's nodes; the
+    // level's outputs are zero elsewhere and summed over the ranks below
+    const bool sharded = shard_world > 1;
+    const int sub_lb = sharded ? lb + (int)((int64_t)cnt * shard_rank / shard_world) : lb;
+    const int sub_le = sharded ? lb + (int)((int64_t)cnt * (shard_rank + 1) / shard_world) : le;
+
+    // ---- HSS nearfield SVD (hss.py:279-299) first: the kept count bounds the rank
+    // (the compression panel has r + keep rows) and so the G capacity
+    int max_keep = 0;
+    auto t1 = t0;
+    if (hss) {
+      k_level_nib<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a, pt_b,
+                                                  F->rank.p, F->nib.p);
+      dmax.zero(s);
+      k_max_int<<<std::min<unsigned>(cdiv(cnt, 256), 64), 256, 0, s>>>(F->nib.p + lb, cnt, dmax.p);
+      int nmax0 = 0;
+      d2h(&nmax0, dmax.p, 1, s);
+      sync(s);
+      t1 = now();
+      max_keep = hss_level_svd(M, side, l, near, nmax0, svdws, s, sub_lb, sub_le);
+      if (sharded) {  // every rank sizes the level identically
+        sync(s);
+        void* ptrs[1] = {svdws.keep.p + lb};
+        int64_t counts[1] = {cnt};
+        int32_t dts[1] = {0};
+        SMASH_CHECK(xfn(xctx, 1, ptrs, counts, dts) == 0, SMASH_ERR_CUDA, "sharded build exchange failed");
+      }
+    }
+    auto t2 = now();
+
     DBuf<int64_t> ibc, gc, ibo, go;
     ibc.alloc(cnt + 1, s); gc.alloc(cnt + 1, s); ibo.alloc(cnt + 1, s); go.alloc(cnt + 1, s);
     SMASH_CUDA(cudaMemsetAsync(ibc.p + cnt, 0, 8, s));
     SMASH_CUDA(cudaMemsetAsync(gc.p + cnt, 0, 8, s));
     k_level_sizes<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, t->nchild.p, t->child_first.p, pt_a,
-                                                 pt_b, F->rank.p, F->nib.p, ibc.p, gc.p,
-                                                 hss ? (1 << 30) : r);
+                                                 pt_b, F->rank.p, F->nib.p, ibc.p, gc.p, r,
+                                                 hss ? svdws.keep.p : nullptr);
     cub_call([&](void* tp, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(tp, b, ibc.p, ibo.p, cnt + 1, s);
     }, tmp, s);
@@ -463,11 +496,6 @@ struct SideBuild {
     k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, ibo.p, F->ib_total, F->ib_off.p);
     k_add_base<<<cdiv(cnt, 128), 128, 0, s>>>(lb, le, go.p, F->g_total, F->g_off.p);
 
-    // level-distributed build: this rank's contiguous share of the level's nodes; the
-    // level's outputs are zero elsewhere and summed over the ranks below
-    const bool sharded = shard_world > 1;
-    const int sub_lb = sharded ? lb + (int)((int64_t)cnt * shard_rank / shard_world) : lb;
-    const int sub_le = sharded ? lb + (int)((int64_t)cnt * (shard_rank + 1) / shard_world) : le;
     DBuf<int> tmp_lab;
     DBuf<double> tmp_pts;
     tmp_lab.alloc(std::max<int64_t>(lvl_ib, 1), s);
@@ -479,12 +507,6 @@ struct SideBuild {
       tmp_lab.zero(s);
       tmp_pts.zero(s);
     }
-
-    // ---- HSS nearfield SVD (hss.py:279-299)
-    int max_keep = 0;
-    auto t1 = now();
-    if (hss) max_keep = hss_level_svd(M, side, l, near, nmax, svdws, s, sub_lb, sub_le);
-    auto t2 = now();
 
     CompressArgs A;
     A.lb = lb; A.le = le; A.dim = dim; A.r = r; A.side = side;
@@ -518,7 +540,7 @@ struct SideBuild {
     }
     auto t3 = now();
     if (timing)
-      fprintf(stderr, "level %d side %d cnt %d: sizes %.3f ms svd %.3f ms compress %.3f ms\n", l, side,
+      fprintf(stderr, "level %d side %d cnt %d: nib %.3f ms svd %.3f ms sizes+compress %.3f ms\n", l, side,
               cnt, std::chrono::duration<double, std::milli>(t1 - t0).count(),
               std::chrono::duration<double, std::milli>(t2 - t1).count(),
               std::chrono::duration<double, std::milli>(t3 - t2).count());

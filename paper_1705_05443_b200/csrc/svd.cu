@@ -36,8 +36,9 @@ using namespace qr;
 
 constexpr int SVD_THREADS = 256;
 constexpr int MAX_NEAR = 64;
-constexpr int SVD_JV_MAX = 64;  // Jacobi factors in shared memory up to this rank
-constexpr int SVD_Y_MAX = 128 * 65;  // shared-memory back-transform area (doubles), >= 2 * 64 * 64
+// shared-memory area (doubles) for B = R_k^T, then J / V, then the back-transform Y
+// (96 KB: two CTAs per SM; J + V fit up to rank 78)
+constexpr int SVD_BIG = 12288;
 
 struct IbarSide {
   const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
@@ -101,55 +102,66 @@ __global__ void k_near_cols(SvdArgs A) {
   A.nn_out[v - A.lb] = nn;
 }
 
-// Reflector application / column norms on the L2-resident panel with the row
-// loads batched 16 at a time (independent L2 loads in flight instead of one
-// dependent round trip per row) and four partial sums.
-constexpr int GB = 16;
+// Column work by 8-lane groups: a column of the panel (column-major, stride 1) is
+// split over the group's lanes (rows gl, gl + 8, ...), each lane keeping up to
+// GR rows in registers between the dot product and the update; sums are
+// combined by a 3-level butterfly (identical in every lane of the group).
+constexpr int GR = 16;  // register-cached rows per lane (covers 128 rows below the pivot)
 
-__device__ __forceinline__ double col_sumsq_g(const double* P, int ld, int j, int r0, int r1) {
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
-  int row = r0;
-  for (; row + GB <= r1; row += GB) {
-    double x[GB];
-#pragma unroll
-    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
-#pragma unroll
-    for (int q = 0; q < GB; ++q) s[q & 3] = fma(x[q], x[q], s[q & 3]);
-  }
-  for (; row < r1; ++row) {
-    const double x = P[(size_t)row * ld + j];
-    s[0] = fma(x, x, s[0]);
-  }
-  return (s[0] + s[1]) + (s[2] + s[3]);
+__device__ __forceinline__ double grp_sum(double x, unsigned gm) {
+  x += __shfl_xor_sync(gm, x, 4);
+  x += __shfl_xor_sync(gm, x, 2);
+  x += __shfl_xor_sync(gm, x, 1);
+  return x;
 }
 
-__device__ __forceinline__ void apply_reflector_g(double* P, int ld, int m, int i, int j, double tau,
-                                                  const double* vh) {
-  double w[4] = {P[(size_t)i * ld + j], 0.0, 0.0, 0.0};
-  int row = i + 1;
-  for (; row + GB <= m; row += GB) {
-    double x[GB];
-#pragma unroll
-    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
-#pragma unroll
-    for (int q = 0; q < GB; ++q) w[q & 3] = fma(vh[row + q], x[q], w[q & 3]);
+__device__ __forceinline__ double grp_sumsq(const double* c, int r0, int r1, int gl, unsigned gm) {
+  double s0 = 0.0, s1 = 0.0;
+  int r = r0 + gl;
+  for (; r + 8 < r1; r += 16) {
+    const double a = c[r], b = c[r + 8];
+    s0 = fma(a, a, s0);
+    s1 = fma(b, b, s1);
   }
-  for (; row < m; ++row) w[0] = fma(vh[row], P[(size_t)row * ld + j], w[0]);
-  const double t = -tau * ((w[0] + w[1]) + (w[2] + w[3]));
-  P[(size_t)i * ld + j] += t;
-  row = i + 1;
-  for (; row + GB <= m; row += GB) {
-    double x[GB];
+  if (r < r1) s0 = fma(c[r], c[r], s0);
+  return grp_sum(s0 + s1, gm);
+}
+
+// H_i^T applied to column c (rows i..m-1; v_i = 1, v_r = vh[r] below): the
+// group's rows i+1.. are loaded once (registers), w = c_i + v^T c, c -= tau w v.
+// Returns the updated c_i in every lane; x[] keeps the updated rows (row
+// i + 1 + gl + 8q) for a following norm recomputation.
+__device__ __forceinline__ double grp_reflect(double* c, int m, int i, double tau, const double* vh,
+                                              int gl, unsigned gm, double (&x)[GR], bool store) {
+  const int rb = i + 1 + gl;
 #pragma unroll
-    for (int q = 0; q < GB; ++q) x[q] = P[(size_t)(row + q) * ld + j];
+  for (int q = 0; q < GR; ++q) x[q] = rb + 8 * q < m ? c[rb + 8 * q] : 0.0;
+  const double ci = c[i];
+  if (tau == 0.0) return ci;
+  double w0 = 0.0, w1 = 0.0;
 #pragma unroll
-    for (int q = 0; q < GB; ++q) P[(size_t)(row + q) * ld + j] = fma(t, vh[row + q], x[q]);
+  for (int q = 0; q < GR; q += 2) {
+    if (rb + 8 * q < m) w0 = fma(vh[rb + 8 * q], x[q], w0);
+    if (rb + 8 * q + 8 < m) w1 = fma(vh[rb + 8 * q + 8], x[q + 1], w1);
   }
-  for (; row < m; ++row) P[(size_t)row * ld + j] = fma(t, vh[row], P[(size_t)row * ld + j]);
+  for (int r = rb + 8 * GR; r < m; r += 8) w0 = fma(vh[r], c[r], w0);
+  const double w = ci + grp_sum(w0 + w1, gm);
+  const double t = -tau * w;
+#pragma unroll
+  for (int q = 0; q < GR; ++q) {
+    const int r = rb + 8 * q;
+    if (r < m) {
+      x[q] = fma(t, vh[r], x[q]);
+      if (store) c[r] = x[q];
+    }
+  }
+  for (int r = rb + 8 * GR; r < m; r += 8)
+    if (store) c[r] = fma(t, vh[r], c[r]);
+  return ci + t;
 }
 
 template <int KER, int D>
-__global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
+__global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared S;
   double* taus;
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
   const double** near_base;
   int64_t* near_stride;
   int* order;
-  double* jv_smem;
+  double* big;
   {
     double* d = reinterpret_cast<double*>(smem_raw);
     S.vn1 = d; d += A.nnmax;
@@ -178,10 +190,13 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     near_start = ip; ip += MAX_NEAR + 1;
     order = ip; ip += A.nmax;
     S.jpvt = ip; ip += A.nnmax;
-    jv_smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ip) + 15) & ~uintptr_t(15));
+    big = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ip) + 15) & ~uintptr_t(15));
   }
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = NT >> 5;
+  const int lane = tid & 31;
+  // 8-lane groups: one column (or Jacobi pair) per group
+  const int g8 = tid >> 3, gl = tid & 7, ngr = NT >> 3;
+  const unsigned gm = 0xffu << (lane & ~7);
   double* W = A.gws + (size_t)blockIdx.x * A.gws_stride;
   int dbg_n = 0;
   for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
@@ -210,51 +225,57 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       __syncthreads();
       continue;
     }
-    const bool dbg = A.dbg && blockIdx.x == 0 && tid == 0 && dbg_n < 4;
+    const bool dbg = A.dbg && blockIdx.x < 4 && tid == 0 && dbg_n == 0;  // first node of blocks 0-3
     long long tsv[6];
     if (dbg) tsv[0] = clock64();
-    // ---- assemble A (n x nn), row-major in W
+    // ---- assemble A (n x nn), column-major in W (one column per nearfield point)
     int64_t ts;
     const double* tb = ibar_base(A.self, A.nchild, A.child_first, v, &ts);
-    for (int e = tid; e < n * nn; e += NT) {
-      const int a = e / nn, b = e % nn;
+    const int ldp = n;
+    {
       int g = 0;
-      while (g + 1 < nnear && near_start[g + 1] <= b) ++g;
-      const int bl = b - near_start[g];
-      double x[D], y[D];
+      for (int b = tid / n, a = tid % n; b < nn;) {
+        while (g + 1 < nnear && near_start[g + 1] <= b) ++g;
+        const int bl = b - near_start[g];
+        double x[D], y[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        x[d] = tb[(int64_t)d * ts + a];
-        y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
+        for (int d = 0; d < D; ++d) {
+          x[d] = tb[(int64_t)d * ts + a];
+          y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
+        }
+        W[(size_t)b * ldp + a] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
+        a += NT;
+        while (a >= n) { a -= n; ++b; }
       }
-      W[e] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
     }
     __syncthreads();
     if (dbg) tsv[1] = clock64();
     // ---- column-pivoted QR of A, truncated at the noise floor
     double* P = W;
-    const int ld = nn;
     const int kmax = min(n, nn);
-    for (int j = tid; j < nn; j += NT) {
-      double nr = __dsqrt_rn(col_sumsq_g(P, ld, j, 0, n));
-      S.vn1[j] = nr;
-      S.vn2[j] = nr;
-      S.jpvt[j] = j;
+    for (int j = g8; j < nn; j += ngr) {
+      const double nr = __dsqrt_rn(grp_sumsq(P + (size_t)j * ldp, 0, n, gl, gm));
+      if (gl == 0) {
+        S.vn1[j] = nr;
+        S.vn2[j] = nr;
+      }
     }
     __syncthreads();
+    const double floor_v = A.nchild[v] ? A.floor_rel : A.floor_leaf;
     int kp = 0;
     for (int i = 0; i < kmax; ++i) {
       double bv = -1.0;
       int bi = 0x7fffffff;
       for (int j = i + tid; j < nn; j += NT)
         if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
-      block_argmax(bv, bi, S);
-      const int pvt = bi;
+      const int pvt = block_argmax_1bar(bv, bi, S);
       if (pvt != i) {
+        double* ci = P + (size_t)i * ldp;
+        double* cp = P + (size_t)pvt * ldp;
         for (int row = tid; row < n; row += NT) {
-          double t = P[(size_t)row * ld + pvt];
-          P[(size_t)row * ld + pvt] = P[(size_t)row * ld + i];
-          P[(size_t)row * ld + i] = t;
+          const double t = cp[row];
+          cp[row] = ci[row];
+          ci[row] = t;
         }
         if (tid == 0) {
           S.vn1[pvt] = S.vn1[i];
@@ -262,25 +283,35 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
         }
       }
       __syncthreads();
-      householder(P, ld, n, i, S);
+      householder(P + (size_t)i * ldp - i, 1, n, i, S);  // column i (stride 1)
       __syncthreads();
       const double tau = S.misc[0];
       if (tid == 0) taus[i] = tau;
       const double r0 = fabs(S.rdiag[0]);
-      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > (A.nchild[v] ? A.floor_rel : A.floor_leaf) * r0)) break;
+      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > floor_v * r0)) break;
       kp = i + 1;
-      for (int j = i + 1 + tid; j < nn; j += NT) {
-        if (tau != 0.0) apply_reflector_g(P, ld, n, i, j, tau, S.vh);
-        double v1 = S.vn1[j];
+      for (int j = i + 1 + g8; j < nn; j += ngr) {
+        double* c = P + (size_t)j * ldp;
+        double x[GR];
+        const double rij = grp_reflect(c, n, i, tau, S.vh, gl, gm, x, true);
+        if (gl == 0 && tau != 0.0) c[i] = rij;
+        // norm downdate (dlaqp2), exact recomputation when cancellation is severe
+        const double v1 = S.vn1[j];
         if (v1 != 0.0) {
-          double q = fabs(P[(size_t)i * ld + j]) / v1;
-          double temp = fmax(1.0 - q * q, 0.0);
-          double q2 = v1 / S.vn2[j];
+          const double q = fabs(rij) / v1;
+          const double temp = fmax(1.0 - q * q, 0.0);
+          const double q2 = v1 / S.vn2[j];
           if (temp * (q2 * q2) <= TOL3Z) {
-            double nv = i + 1 < n ? sqrt(col_sumsq_g(P, ld, j, i + 1, n)) : 0.0;
-            S.vn1[j] = nv;
-            S.vn2[j] = nv;
-          } else {
+            double s0 = 0.0;
+#pragma unroll
+            for (int qq = 0; qq < GR; ++qq) s0 = fma(x[qq], x[qq], s0);
+            for (int r = i + 1 + gl + 8 * GR; r < n; r += 8) s0 = fma(c[r], c[r], s0);
+            const double nv = i + 1 < n ? sqrt(grp_sum(s0, gm)) : 0.0;
+            if (gl == 0) {
+              S.vn1[j] = nv;
+              S.vn2[j] = nv;
+            }
+          } else if (gl == 0) {
             S.vn1[j] = v1 * sqrt(temp);
           }
         }
@@ -294,47 +325,62 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       continue;
     }
     if (dbg) tsv[2] = clock64();
-    // ---- B = R_k^T (nn x kp), unpivoted QR -> R2 (kp x kp)
-    double* B = W + (size_t)n * nn;
+    // ---- B = R_k^T (nn x kp, column-major), unpivoted QR -> R2 (kp x kp); B in
+    // shared memory when it fits
+    const bool bsm = (int64_t)nn * kp <= SVD_BIG;
+    double* B = bsm ? big : W + (size_t)n * nn;
+    double* T = W + (size_t)n * nn;  // global staging (free once B is in shared memory / consumed)
+    const int ldb = nn;
     for (int e = tid; e < nn * kp; e += NT) {
-      const int b = e / kp, j = e % kp;
-      B[e] = b >= j ? P[(size_t)j * ld + b] : 0.0;
+      const int j = e / nn, b = e - j * nn;
+      B[(size_t)j * ldb + b] = b >= j ? P[(size_t)b * ldp + j] : 0.0;
     }
     __syncthreads();
     for (int i = 0; i < kp; ++i) {
-      householder(B, kp, nn, i, S);
+      householder(B + (size_t)i * ldb - i, 1, nn, i, S);
       __syncthreads();
       const double tau = S.misc[0];
       if (tau != 0.0)
-        for (int j = i + 1 + tid; j < kp; j += NT) apply_reflector_g(B, kp, nn, i, j, tau, S.vh);
+        for (int j = i + 1 + g8; j < kp; j += ngr) {
+          double* c = B + (size_t)j * ldb;
+          double x[GR];
+          const double rij = grp_reflect(c, nn, i, tau, S.vh, gl, gm, x, true);
+          if (gl == 0) c[i] = rij;
+        }
       __syncthreads();
     }
-    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated.
-    // J and V live in shared memory when kp <= SVD_JV_MAX.  Column norms are kept
-    // up to date through the rotation (one dot product per pair) and refreshed
-    // exactly at every sweep.
-    double* J = kp <= SVD_JV_MAX ? jv_smem : B + (size_t)nn * kp;
+    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated;
+    // J and V in shared memory when they fit (R2 staged through global scratch when
+    // B occupies that area).  Column norms are kept up to date through the rotation
+    // (one dot product per pair) and refreshed exactly at every sweep.
+    const bool jsm = 2 * kp * kp <= SVD_BIG;
+    double* J = jsm ? big : W + (size_t)n * nn + (size_t)nn * kp;
     double* V = J + (size_t)kp * kp;
     double* nrm = sig;  // squared column norms (reuses the sigma scratch)
-    for (int e = tid; e < kp * kp; e += NT) {
-      const int c = e / kp, r = e % kp;
-      J[e] = r <= c ? B[(size_t)r * kp + c] : 0.0;
-      V[e] = r == c ? 1.0 : 0.0;
+    if (bsm && jsm) {
+      for (int e = tid; e < kp * kp; e += NT) {
+        const int c = e / kp, r = e - c * kp;
+        T[e] = r <= c ? B[(size_t)c * ldb + r] : 0.0;
+      }
+      __syncthreads();
+      for (int e = tid; e < kp * kp; e += NT) J[e] = T[e];
+    } else {
+      for (int e = tid; e < kp * kp; e += NT) {
+        const int c = e / kp, r = e - c * kp;
+        J[e] = r <= c ? B[(size_t)c * ldb + r] : 0.0;
+      }
     }
+    for (int e = tid; e < kp * kp; e += NT) V[e] = (e % (kp + 1)) == 0 ? 1.0 : 0.0;
     __syncthreads();
     const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
     if (dbg) tsv[3] = clock64();
-    // 8-lane groups: one column pair (or column) per group, kp <= 64 -> <= 8
-    // elements per lane, 3 shuffle levels per reduction
-    const int g8 = tid >> 3, gl = tid & 7, ngr = NT >> 3;
-    const unsigned gm = 0xffu << (lane & ~7);
     int sweeps_done = 0;
     for (int sweep = 0; sweep < 40; ++sweep) {
       sweeps_done = sweep + 1;
       for (int c = g8; c < kp; c += ngr) {  // exact squared norms
         double s2 = 0.0;
         for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
-        for (int off = 4; off; off >>= 1) s2 += __shfl_xor_sync(gm, s2, off);
+        s2 = grp_sum(s2, gm);
         if (gl == 0) nrm[c] = s2;
       }
       if (tid == 0) S.imisc[2] = 0;
@@ -349,12 +395,12 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
           double* jb = J + (size_t)b * kp;
           double ga = 0;
           for (int r = gl; r < kp; r += 8) ga = fma(ja[r], jb[r], ga);
-          for (int off = 4; off; off >>= 1) ga += __shfl_xor_sync(gm, ga, off);
+          ga = grp_sum(ga, gm);
           const double al = nrm[a], be = nrm[b];
-          if (fabs(ga) > 1e-15 * sqrt(al * be) && ga != 0.0) {
+          if (ga * ga > 1e-30 * (al * be) && ga != 0.0) {
             const double zeta = (be - al) / (2.0 * ga);
             const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+            const double c = rsqrt(1.0 + t * t), s = c * t;
             double* va = V + (size_t)a * kp;
             double* vb = V + (size_t)b * kp;
             for (int r = gl; r < kp; r += 8) {
@@ -369,7 +415,7 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
             if (gl == 0) {
               nrm[a] = fmax(al - t * ga, 0.0);
               nrm[b] = be + t * ga;
-              atomicAdd(&S.imisc[2], 1);
+              S.imisc[2] = 1;
             }
           }
         }
@@ -379,11 +425,16 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
       __syncthreads();
     }
     if (dbg) tsv[4] = clock64();
+    if (A.dbg && tid == 0) {  // every node: max sweeps, nodes at the sweep cap
+      atomicMax(reinterpret_cast<unsigned long long*>(A.dbg + 32), (unsigned long long)sweeps_done);
+      if (sweeps_done >= 40) atomicAdd(reinterpret_cast<unsigned long long*>(A.dbg + 33), 1ull);
+    }
     // ---- singular values, keep count, descending order
-    for (int c = tid; c < kp; c += NT) {
+    for (int c = g8; c < kp; c += ngr) {
       double s2 = 0.0;
-      for (int r = 0; r < kp; ++r) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
-      sig[c] = sqrt(s2);
+      for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
+      s2 = grp_sum(s2, gm);
+      if (gl == 0) sig[c] = sqrt(s2);
     }
     __syncthreads();
     if (tid == 0) {
@@ -412,43 +463,32 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     // the J/V area, through registers) when it fits, reflectors applied by
     // 8-lane groups per column
     double* Yg = A.sv + A.sv_off[v];
-    const bool ysm = kp <= SVD_JV_MAX && n * (keep | 1) <= SVD_Y_MAX;
-    double* Y = ysm ? jv_smem : Yg;
+    const bool ysm = n * (keep | 1) <= SVD_BIG;
+    double* Y = ysm ? big : Yg;
     const int ldy = ysm ? (keep | 1) : keep;
-    if (ysm) {
-      constexpr int STG = SVD_JV_MAX * SVD_JV_MAX / SVD_THREADS;
-      double stg[STG];
-      const int cnt = kp * keep;
-#pragma unroll
-      for (int q = 0; q < STG; ++q) {
-        const int e = tid + q * NT;
-        stg[q] = e < cnt ? V[(size_t)order[e % keep] * kp + e / keep] : 0.0;
+    {
+      // kept columns of V (descending sigma) -> T (global staging: Y may overlap V)
+      for (int e = tid; e < kp * keep; e += NT) {
+        const int a = e / keep, c = e - a * keep;
+        T[e] = V[(size_t)order[c] * kp + a];
       }
       __syncthreads();
-      for (int e = tid; e < n * ldy; e += NT) Y[e] = 0.0;
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < STG; ++q) {
-        const int e = tid + q * NT;
-        if (e < cnt) Y[(e / keep) * ldy + e % keep] = stg[q];
-      }
-    } else {
-      for (int e = tid; e < n * keep; e += NT) {
-        const int a = e / keep, c = e % keep;
-        Y[e] = a < kp ? V[(size_t)order[c] * kp + a] : 0.0;
+      for (int e = tid; e < n * ldy; e += NT) {
+        const int a = e / ldy, c = e - a * ldy;
+        Y[e] = (a < kp && c < keep) ? T[a * keep + c] : 0.0;
       }
     }
     __syncthreads();
     for (int i = kp - 1; i >= 0; --i) {
       const double tau = taus[i];
       if (tau == 0.0) continue;
-      for (int row = i + 1 + tid; row < n; row += NT) S.vh[row] = P[(size_t)row * ld + i];
+      for (int row = i + 1 + tid; row < n; row += NT) S.vh[row] = P[(size_t)i * ldp + row];
       __syncthreads();
       for (int c = g8; c < keep; c += ngr) {
         double w = 0.0;
         for (int row = i + gl; row < n; row += 8)
           w = fma(row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c], w);
-        for (int off = 4; off; off >>= 1) w += __shfl_xor_sync(gm, w, off);
+        w = grp_sum(w, gm);
         const double t = -tau * w;
         for (int row = i + gl; row < n; row += 8)
           Y[(size_t)row * ldy + c] = fma(t, row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c]);
@@ -461,8 +501,9 @@ __global__ void __launch_bounds__(SVD_THREADS) k_svd(SvdArgs A) {
     }
     if (dbg) {
       tsv[5] = clock64();
-      for (int q = 0; q < 5; ++q) A.dbg[dbg_n * 8 + q] = tsv[q + 1] - tsv[q];
-      A.dbg[dbg_n * 8 + 5] = kp; A.dbg[dbg_n * 8 + 6] = keep + 1000 * sweeps_done; A.dbg[dbg_n * 8 + 7] = n * 1000 + nn;
+      long long* o = A.dbg + blockIdx.x * 8;
+      for (int q = 0; q < 5; ++q) o[q] = tsv[q + 1] - tsv[q];
+      o[5] = kp; o[6] = keep + 1000 * sweeps_done; o[7] = n * 1000 + nn;
     }
     ++dbg_n;
   }
@@ -589,14 +630,14 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   DBuf<long long> dbgbuf;
   A.dbg = nullptr;
   if (svd_dbg) {
-    dbgbuf.alloc(32, s);
+    dbgbuf.alloc(40, s);
     dbgbuf.zero(s);
     A.dbg = dbgbuf.p;
   }
   const int mx = std::max(A.nmax, A.nnmax);
   size_t smem = 8 * ((size_t)2 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
                 4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64 + 16 +
-                8 * (size_t)SVD_Y_MAX;
+                8 * (size_t)SVD_BIG;
   SMASH_CHECK(smem <= 200 * 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
     SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -616,14 +657,14 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   sync(s);
   SMASH_CHECK(he == 0, SMASH_ERR_INVALID, "nearfield set larger than the supported cap");
   if (svd_dbg) {
-    long long h[32];
-    d2h(h, dbgbuf.p, 32, s);
+    long long h[40];
+    d2h(h, dbgbuf.p, 40, s);
     sync(s);
     fprintf(stderr, "svd level %d side %d cnt %d:", level, side, cnt);
     for (int q = 0; q < 4; ++q)
       fprintf(stderr, " [asm %lld qr %lld qr2 %lld jac %lld back %lld kp %lld keep %lld n.nn %lld]", h[q * 8], h[q * 8 + 1],
               h[q * 8 + 2], h[q * 8 + 3], h[q * 8 + 4], h[q * 8 + 5], h[q * 8 + 6], h[q * 8 + 7]);
-    fprintf(stderr, "\n");
+    fprintf(stderr, " max_sweeps %lld capped %lld\n", h[32], h[33]);
   }
   return hk;
 }
