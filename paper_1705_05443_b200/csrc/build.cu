@@ -411,7 +411,7 @@ struct SideBuild {
   }
 
   void launch_level(CompressArgs& A, int cnt) {
-    CompressPass ps[3];
+    CompressPass ps[4];
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
@@ -420,7 +420,22 @@ struct SideBuild {
         if (gws.n < need) gws.alloc(need, s);
         a.gws = gws.p;
       }
+      static const bool dbg = getenv("SMASH_COMPRESS_DBG") != nullptr;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (dbg) {
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+      }
       launch_compress(a, ps[k].grid, ps[k].smem, s);
+      if (dbg) {
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        fprintf(stderr, "compress launch: nodes %d class (%d, %d] nmax %d mmax %d threads %d grid %d smem %zu cap %lld: %.3f ms\n",
+                cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+      }
     }
   }
 
@@ -741,8 +756,15 @@ static MatrixImpl* build_levels(TreeImpl* t, const smash_build_params& p, cudaSt
     rowb.level(l, near);
     if (colb) colb->level(l, near);
   }
+  static const bool jdbg = getenv("SMASH_JOIN_DBG") != nullptr;
+  auto tj0 = std::chrono::steady_clock::now();
   if (!hss_build) M->pl = pj.join(s);
+  auto tj1 = std::chrono::steady_clock::now();
   rowb.finish();
+  if (jdbg)
+    fprintf(stderr, "build: waited %.3f ms for the pair lists after enqueueing the sweep, %.3f ms more for the sweep\n",
+            std::chrono::duration<double, std::milli>(tj1 - tj0).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj1).count());
   if (colb) colb->finish();
   sync(s);
   return M.release();

@@ -512,7 +512,11 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
   // capacity fits two CTAs per SM, size the shared panel for that and let the
   // rare larger nodes fall back to the global workspace.
   const size_t half = compress_smem_bytes((A.nmax + 1) / 2, A.mmax, true);
-  if (half <= SM_BYTES / 2 - CTA_RESERVED) {
+  // (a launch whose whole size class exceeds the two-per-SM panel skips this: one CTA per SM
+  // with the full panel in shared memory beats two CTAs on global/L2 panels)
+  const bool all_oversized = (int)full <= smem_limit &&
+      (int64_t)(A.n_lo + 1) * A.mmax > (int64_t)((SM_BYTES / 2 - CTA_RESERVED - fixed) / 8);
+  if (half <= SM_BYTES / 2 - CTA_RESERVED && !all_oversized) {
     const size_t smem = std::min<size_t>(SM_BYTES / 2 - CTA_RESERVED, (size_t)smem_limit);
     A.panel_cap = (int64_t)((smem - fixed) / 8);
     *grid = std::min(cnt, nsm * 2);
@@ -534,9 +538,21 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
 // <= 128, rest), each launched with its own CTA size and shared panel; the CTAs of a
 // launch skip the other classes' nodes.  Latency-bound levels (<= one node per SM) and
 // levels whose capacity is already small keep one launch.
-int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass out[3]) {
+int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass out[4]) {
   static const bool split = getenv("SMASH_COMPRESS_NOSPLIT") == nullptr;
-  const int bounds[3] = {64, 128, 0x7fffffff};
+  static const bool split4 = getenv("SMASH_COMPRESS_NOSPLIT4") == nullptr;
+  // fourth class: nodes too wide for two shared panels per SM but not for one
+  int b3 = 0x7fffffff;
+  {
+    constexpr size_t SM_BYTES = 228 * 1024, CTA_RESERVED = 1024;
+    const size_t lim2 = SM_BYTES / 2 - CTA_RESERVED;
+    // widest panel of mmax rows with two CTAs per SM (fixed part grows with the columns)
+    int n2 = A0.nmax;
+    while (n2 > 128 && compress_smem_bytes(n2, A0.mmax, true) > lim2) --n2;
+    if (split4 && n2 > 128 && n2 < A0.nmax && (int)compress_smem_bytes(A0.nmax, A0.mmax, true) <= smem_limit)
+      b3 = n2;
+  }
+  const int bounds[4] = {64, 128, b3, 0x7fffffff};
   if (!split || cnt <= nsm || A0.nmax <= bounds[0]) {
     out[0].a = A0;
     out[0].smem = plan_compress_launch(out[0].a, cnt, smem_limit, nsm, &out[0].grid);

@@ -81,8 +81,8 @@ struct CompressPass {
   int grid = 0;
   size_t smem = 0;
 };
-// Up to three size-class launches of a level (see compress.cu); returns their count.
-int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass out[3]);
+// Up to four size-class launches of a level (see compress.cu); returns their count.
+int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass out[4]);
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
                          int r, const double* pts_soa, int64_t n, double* out, int* err,
                          cudaStream_t s);
