@@ -415,7 +415,13 @@ struct SideBuild {
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
-      if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
+      if (ps[k].rc_nt) {  // register-column launch: R11 slices of the 64-thread CTAs
+        const size_t need = compress_rc_gws_doubles(ps[k].rc_nt, a.mmax, ps[k].grid);
+        if (need) {
+          if (gws.n < need) gws.alloc(need, s);
+          a.gws = gws.p;
+        }
+      } else if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
         size_t need = (size_t)ps[k].grid * a.mmax * a.nmax;
         if (gws.n < need) gws.alloc(need, s);
         a.gws = gws.p;
@@ -426,14 +432,23 @@ struct SideBuild {
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
       }
-      launch_compress(a, ps[k].grid, ps[k].smem, s);
+      if (ps[k].rc_nt) launch_compress_rc(a, ps[k].rc_nt, ps[k].grid, ps[k].smem, s);
+      else launch_compress(a, ps[k].grid, ps[k].smem, s);
       if (dbg) {
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
-        fprintf(stderr, "compress launch: nodes %d class (%d, %d] nmax %d mmax %d threads %d grid %d smem %zu cap %lld: %.3f ms\n",
-                cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
+        {  // nodes and columns of this size class
+          std::vector<int> hn(a.le - a.lb);
+          cudaMemcpy(hn.data(), a.nib + a.lb, sizeof(int) * hn.size(), cudaMemcpyDeviceToHost);
+          long long nn = 0, cols = 0;
+          for (int x : hn) if (x > a.n_lo && x <= a.n_hi) { ++nn; cols += x; }
+          fprintf(stderr, "  class holds %lld nodes, %lld columns (%.1f per node): %.2f us per node x CTA slot\n", nn, cols,
+                  nn ? (double)cols / nn : 0.0, nn ? ms * 1e3 * ps[k].grid / nn : 0.0);
+        }
+        fprintf(stderr, "compress launch: %s nodes %d class (%d, %d] nmax %d mmax %d threads %d grid %d smem %zu cap %lld: %.3f ms\n",
+                ps[k].rc_nt ? "rc" : "sm", cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
         cudaEventDestroy(e0); cudaEventDestroy(e1);
       }
     }

@@ -351,6 +351,8 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
   __syncthreads();
 }
 
+#include "compress_rc.cuh"
+
 // MODE: 0 = panel in the global workspace, 1 = shared memory, 2 = per node
 // (hybrid).  The global-only variant uses deeper load chunks (more registers,
 // fewer CTAs per SM); the shared variants are sized for >= 4 CTAs per SM.
@@ -538,8 +540,56 @@ size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, i
 // <= 128, rest), each launched with its own CTA size and shared panel; the CTAs of a
 // launch skip the other classes' nodes.  Latency-bound levels (<= one node per SM) and
 // levels whose capacity is already small keep one launch.
+// four-chain dot products by default (cfg5 build -8 %, the full-size skeleton / G parity
+// unchanged); SMASH_QR_CHAINS=1 restores the sequential dlarf / dnrm2 order
+static bool compress_chains4() {
+  static const bool c4 = !(getenv("SMASH_QR_CHAINS") && atoi(getenv("SMASH_QR_CHAINS")) == 1);
+  return c4;
+}
+
+// Register-column launch (compress_rc.cuh) of a size class of at most 256 columns.
+static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) {
+  constexpr size_t SM_BYTES = 228 * 1024, CTA_RESERVED = 1024;
+  const int nt = P.a.nmax <= 64 ? 64 : P.a.nmax <= 128 ? 128 : P.a.nmax <= 256 ? 256 : 0;
+  if (!nt) return false;
+  const size_t smem = compress_rc_smem_bytes(nt, P.a.mmax);
+  if ((int64_t)smem > (int64_t)smem_limit) return false;
+  const int by_regs = 65536 / (nt * 128);  // __launch_bounds__ of k_compress_rc
+  const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
+  P.grid = std::min(cnt, nsm * std::min(by_regs, by_smem));
+  P.smem = smem;
+  P.rc_nt = nt;
+  P.a.threads = nt;
+  return true;
+}
+
 int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass out[4]) {
   static const bool split = getenv("SMASH_COMPRESS_NOSPLIT") == nullptr;
+  // (read per call: tests switch between the two kernels within a process)
+  const bool rc = !(getenv("SMASH_COMPRESS_RC") && atoi(getenv("SMASH_COMPRESS_RC")) == 0) &&
+                  !A0.Cexp && compress_chains4();
+  if (rc && (!split || cnt <= nsm || A0.nmax <= 64)) {
+    out[0] = CompressPass();
+    out[0].a = A0;
+    if (plan_compress_rc(out[0], cnt, smem_limit, nsm)) return 1;
+  }
+  if (rc && split && cnt > nsm && A0.nmax > 64) {
+    const int rb[4] = {64, 128, 256, 0x7fffffff};
+    int np = 0, lo = -1;
+    for (int b : rb) {
+      if (lo >= A0.nmax) break;
+      CompressPass& P = out[np++];
+      P = CompressPass();
+      P.a = A0;
+      P.a.n_lo = lo;
+      P.a.n_hi = b;
+      P.a.nmax = std::min(A0.nmax, b);
+      if (!plan_compress_rc(P, cnt, smem_limit, nsm))
+        P.smem = plan_compress_launch(P.a, cnt, smem_limit, nsm, &P.grid);
+      lo = b;
+    }
+    return np;
+  }
   static const bool split4 = getenv("SMASH_COMPRESS_NOSPLIT4") == nullptr;
   // fourth class: nodes too wide for two shared panels per SM but not for one
   int b3 = 0x7fffffff;
@@ -554,6 +604,7 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
   }
   const int bounds[4] = {64, 128, b3, 0x7fffffff};
   if (!split || cnt <= nsm || A0.nmax <= bounds[0]) {
+    out[0] = CompressPass();
     out[0].a = A0;
     out[0].smem = plan_compress_launch(out[0].a, cnt, smem_limit, nsm, &out[0].grid);
     return 1;
@@ -562,6 +613,7 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
   for (int b : bounds) {
     if (lo >= A0.nmax) break;
     CompressPass& P = out[np++];
+    P = CompressPass();
     P.a = A0;
     P.a.n_lo = lo;
     P.a.n_hi = b;
@@ -579,10 +631,7 @@ __device__ int g_compress_next;  // dynamic node counter (reset before every lau
 
 void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s) {
   CompressArgs a = a_in;
-  // four-chain dot products by default (cfg5 build -8 %, the full-size skeleton / G parity
-  // unchanged); SMASH_QR_CHAINS=1 restores the sequential dlarf / dnrm2 order
-  static const bool chains4 = !(getenv("SMASH_QR_CHAINS") && atoi(getenv("SMASH_QR_CHAINS")) == 1);
-  a.chains4 = chains4;
+  a.chains4 = compress_chains4();
   {
     void* nx = nullptr;
     SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));
@@ -619,6 +668,49 @@ void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream
           a.le - a.lb, mode, grid, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6,
           h[6] ? (double)h[3] / h[6] : 0.0, h[6] ? (double)h[4] / h[6] : 0.0,
           h[6] ? (double)h[5] / h[6] : 0.0);
+#endif
+}
+
+size_t compress_rc_gws_doubles(int nt, int mmax, int grid) {
+  return rc_r11_global(nt) ? (size_t)grid * rc_r11_doubles(nt, mmax) : 0;
+}
+
+void launch_compress_rc(const CompressArgs& a_in, int nt, int grid, size_t smem, cudaStream_t s) {
+  CompressArgs a = a_in;
+  a.chains4 = true;
+  void* nx = nullptr;
+  SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));
+  SMASH_CUDA(cudaMemsetAsync(nx, 0, sizeof(int), s));
+  a.next = reinterpret_cast<int*>(nx);
+#ifdef SMASH_COMPRESS_PROF
+  void* pp = nullptr;
+  SMASH_CUDA(cudaGetSymbolAddress(&pp, g_compress_prof));
+  SMASH_CUDA(cudaMemsetAsync(pp, 0, sizeof(g_compress_prof), s));
+  a.prof = reinterpret_cast<unsigned long long*>(pp);
+#endif
+  auto go = [&](auto kern) {
+    SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, nt, smem, s>>>(a);
+  };
+  auto by_nt = [&](auto d) {
+    constexpr int D = decltype(d)::value;
+    if (nt == 64) go(k_compress_rc<D, 64>);
+    else if (nt == 128) go(k_compress_rc<D, 128>);
+    else go(k_compress_rc<D, 256>);
+  };
+  if (a.dim == 1) by_nt(std::integral_constant<int, 1>{});
+  else if (a.dim == 2) by_nt(std::integral_constant<int, 2>{});
+  else by_nt(std::integral_constant<int, 3>{});
+  SMASH_CUDA(cudaGetLastError());
+#ifdef SMASH_COMPRESS_PROF
+  unsigned long long h[8];
+  SMASH_CUDA(cudaMemcpyAsync(h, pp, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SMASH_CUDA(cudaStreamSynchronize(s));
+  const double st = h[7] ? (double)h[7] : 1.0;
+  fprintf(stderr, "compress_rc nodes %d nt %d grid %d: Mcycles (thread 0 of every CTA) build %.2f qr %.2f solve %.2f reqr %.2f"
+          " | per step: argmax %.0f, publish %.0f, reflector %.0f, update+downdate %.0f cycles (%llu steps)\n",
+          a.le - a.lb, nt, grid, h[0] * 1e-6, (h[1] + h[2] + h[3] + h[4]) * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
+          h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[7]);
 #endif
 }
 

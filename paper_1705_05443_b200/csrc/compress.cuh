@@ -80,7 +80,10 @@ struct CompressPass {
   CompressArgs a;
   int grid = 0;
   size_t smem = 0;
+  int rc_nt = 0;  // > 0: register-column kernel with this CTA size (launch_compress_rc)
 };
+size_t compress_rc_gws_doubles(int nt, int mmax, int grid);  // global workspace of a register-column launch
+void launch_compress_rc(const CompressArgs& a, int nt, int grid, size_t smem, cudaStream_t s);
 // Up to four size-class launches of a level (see compress.cu); returns their count.
 int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass out[4]);
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,

@@ -1,0 +1,567 @@
+// K3 + K4, register-column variant (included by compress.cu, inside its namespaces).
+//
+// Same algorithm and the same floating-point operation order as k_compress (pivots,
+// ranks, swap decisions and G are bit-identical to it), with a different home for the
+// panel: thread j owns ibar column j for the whole node.  The last RC_RR rows of the
+// column live in registers, the rows above them in shared memory (row-major, one column
+// per thread, conflict free).  Consequences:
+//  * a 64 x 256 panel needs 64 KB of shared memory instead of 128 KB: two CTAs per SM
+//    with everything on chip (k_compress ran such nodes from global/L2 panels or alone
+//    on an SM), and four times less shared-memory traffic per pivot step;
+//  * columns are never swapped physically: dlaqp2's column order is a position kept per
+//    thread (pos) and the position -> column table jpvt; the first-maximum pivot rule is
+//    evaluated on positions;
+//  * register rows are indexed statically, so every step runs over all RC_RR register
+//    rows with the reflector zero-padded above the pivot row (adds exact zeros); the
+//    four accumulation chains are assigned by row mod 4 and combined in the rotation
+//    that reproduces k_compress's (row - i - 1) mod 4 chains bit for bit;
+//  * the pivot column is published to shared memory for warp 0's dlarfg, which keeps
+//    the lane-strided norm of k_compress.
+// Used for size classes of at most 256 columns (one column per thread, CTAs of 64 / 128 /
+// 256 threads); wider panels and the single-call compr stay on k_compress.
+
+constexpr int RC_RR = 32;
+
+struct RcShared {
+  double* vh0;     // reflector, zero at rows <= i        [vhn]
+  double* vh1;     // reflector, one at row i, zero above [vhn]
+  double* colbuf;  // published pivot column              [vhn]
+  double* rdiag;   // [mmax]
+  double* nodes;   // [3][MAX_M_AXIS_1D]
+  double* redv;    // [8]
+  double* misc;    // [8]
+  double* r11;     // R11, [kcap][kld], zero outside the strict upper triangle (global slice for NT = 64)
+  double* panel;   // [srows][NT]
+  int* redi;       // [8]
+  int* imisc;      // [8]
+  int* jpvt;       // [NT]
+};
+
+__host__ __device__ inline int rc_round4(int x) { return (x + 3) & ~3; }
+inline int rc_vhn(int mmax) { return rc_round4(mmax) + RC_RR + 4; }
+inline int rc_kcap(int mmax, int nt) { return rc_round4(std::min(mmax, nt)); }
+inline int rc_kld(int mmax) { return std::max(rc_round4(mmax), RC_RR); }  // >= rbase + RC_RR of every node
+// CTAs of 64 threads (size class |ibar| <= 64, where k < |ibar| is the exception) keep R11 in a
+// global/L2 slice instead of shared memory: eight CTAs per SM instead of five
+inline bool rc_r11_global(int nt) { return nt == 64; }
+inline size_t rc_r11_doubles(int nt, int mmax) { return (size_t)rc_kcap(mmax, nt) * rc_kld(mmax); }
+inline int rc_srows(int mmax) { return std::max(0, rc_round4(mmax - RC_RR)); }
+
+size_t compress_rc_smem_bytes(int nt, int mmax) {
+  size_t d = 3 * (size_t)rc_vhn(mmax) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 8 + 8 +
+             (rc_r11_global(nt) ? 0 : rc_r11_doubles(nt, mmax)) + (size_t)rc_srows(mmax) * nt;
+  size_t i = 8 + 8 + (size_t)nt;
+  return 8 * d + 4 * i + 16;
+}
+
+// x[s], s uniform over the CTA (31 selects instead of a dynamically indexed array)
+__device__ __forceinline__ double rc_sel(const double (&x)[RC_RR], int s) {
+  double a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) a[t] = (s & 1) ? x[2 * t + 1] : x[2 * t];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) b[t] = (s & 2) ? a[2 * t + 1] : a[2 * t];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) c[t] = (s & 4) ? b[2 * t + 1] : b[2 * t];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) d[t] = (s & 8) ? c[2 * t + 1] : c[2 * t];
+  return (s & 16) ? d[1] : d[0];
+}
+
+// (max value, smallest index) over the CTA with one barrier; two calls must be separated
+// by another barrier.  Returns the value through v.
+template <int NT>
+__device__ __forceinline__ int rc_argmax(double& v, int i, RcShared& S) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int off = 16; off; off >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    argmax_combine(v, i, ov, oi);
+  }
+  if (lane == 0) { S.redv[wid] = v; S.redi[wid] = i; }
+  __syncthreads();
+  v = S.redv[0];
+  i = S.redi[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) argmax_combine(v, i, S.redv[w], S.redi[w]);
+  return i;
+}
+
+// dlarfg on the published pivot column c at step i (warp 0), as qr::householder: the
+// lane-strided sum of squares, beta / tau / scal, the scaled reflector to vh0 / vh1.
+template <int NT>
+__device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, int rbase, int m, int i,
+                                               int c, RcShared& S) {
+  const int lane = threadIdx.x;
+  auto colv = [&](int row) { return row < rbase ? Ps[row * NT + c] : S.colbuf[row]; };
+  const double alpha = colv(i);
+  double ss = 0.0;
+#pragma unroll 1
+  for (int row = i + 1 + lane; row < m; row += 32) {
+    const double x = colv(row);
+    ss = __fma_rn(x, x, ss);
+  }
+  for (int off = 16; off; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
+  const double xnorm = __dsqrt_rn(ss);
+  double tau = 0.0, diag = alpha;
+  if (m - i > 1 && xnorm != 0.0) {
+    const double beta = -copysign(dlapy2(alpha, xnorm), alpha);
+    tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+    const double scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
+#pragma unroll 1
+    for (int row = i + 1 + lane; row < m; row += 32) {
+      const double x = __dmul_rn(scal, colv(row));
+      S.vh0[row] = x;
+      S.vh1[row] = x;
+    }
+    diag = beta;
+  }
+  if (lane == 0) {
+    S.vh0[i] = 0.0;
+    S.vh1[i] = 1.0;
+    if (i > 0) S.vh1[i - 1] = 0.0;
+    S.misc[0] = tau;
+    S.rdiag[i] = diag;
+  }
+}
+
+template <int D, int NT>
+__device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int v, int n, int m,
+                                        const NodeSrc& src, int vhn, int kld) {
+  const int tid = threadIdx.x;
+  const int rbase = max(0, rc_round4(m - RC_RR));
+  double* __restrict__ Ps = S.panel;
+#ifdef SMASH_COMPRESS_PROF
+  long long pt0 = clock64();
+#define RC_MARK(k) if (tid == 0) { long long pt1 = clock64(); atomicAdd(A.prof + (k), (unsigned long long)(pt1 - pt0)); pt0 = pt1; }
+#else
+#define RC_MARK(k)
+#endif
+  const bool have = tid < n;
+  double xr[RC_RR];
+
+  // ---- own column of the panel (smash/lowrank.py:103-144; HSS rows hss.py:287)
+  auto build_col = [&]() {
+    const int r = A.r;
+    const int mt = A.tab.m;
+    double x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = src.base[(size_t)a * src.stride + tid];
+    const int kp = m - r;
+    const double* sv = kp > 0 ? A.sv + A.sv_off[v] + (size_t)tid * kp : nullptr;
+    if (D == 1) {
+      const double* nd = S.nodes;
+      bool exact = false;
+      for (int k = 0; k < mt; ++k) exact |= (__dsub_rn(x[0], nd[k]) == 0.0);
+      double Ssum = 1.0;
+      if (!exact)
+        Ssum = np_pairwise_sum(mt, [&](int k) { return __ddiv_rn(A.tab.wv[k], __dsub_rn(x[0], nd[k])); });
+      auto val = [&](int q) -> double {
+        if (q >= r) return q < m ? sv[q - r] : 0.0;
+        const double dx = __dsub_rn(x[0], nd[q]);
+        if (exact) return dx == 0.0 ? 1.0 : 0.0;
+        return __ddiv_rn(__ddiv_rn(A.tab.wv[q], dx), Ssum);
+      };
+      for (int q = 0; q < rbase; ++q) Ps[q * NT + tid] = val(q);
+#pragma unroll
+      for (int t = 0; t < RC_RR; ++t) xr[t] = val(rbase + t);
+    } else {
+      double L[D][MAX_M_AXIS_ND];
+#pragma unroll
+      for (int a = 0; a < D; ++a) lagrange_axis(x[a], S.nodes + a * MAX_M_AXIS_1D, A.tab.wv, mt, L[a]);
+      auto val = [&](int q) -> double {
+        if (q >= r) return q < m ? sv[q - r] : 0.0;
+        const int* o = A.tab.order + 3 * q;
+        double pv = __dmul_rn(L[0][o[0]], L[1][o[1]]);
+        if (D == 3) pv = __dmul_rn(pv, L[D - 1][o[2]]);
+        return pv;
+      };
+      for (int q = 0; q < rbase; ++q) Ps[q * NT + tid] = val(q);
+#pragma unroll
+      for (int t = 0; t < RC_RR; ++t) xr[t] = val(rbase + t);
+    }
+  };
+  // sum of squares of the own column over rows > i0, chains by (row - i0 - 1) mod 4
+  auto sumsq_after = [&](int i0) -> double {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int g = (i0 + 1) & ~3; g < rbase; g += 4) {
+      const double x0 = g + 0 > i0 ? Ps[(g + 0) * NT + tid] : 0.0;
+      const double x1 = g + 1 > i0 ? Ps[(g + 1) * NT + tid] : 0.0;
+      const double x2 = g + 2 > i0 ? Ps[(g + 2) * NT + tid] : 0.0;
+      const double x3 = g + 3 > i0 ? Ps[(g + 3) * NT + tid] : 0.0;
+      s0 = __fma_rn(x0, x0, s0); s1 = __fma_rn(x1, x1, s1);
+      s2 = __fma_rn(x2, x2, s2); s3 = __fma_rn(x3, x3, s3);
+    }
+#pragma unroll
+    for (int t = 0; t < RC_RR; t += 4) {
+      const double x0 = rbase + t + 0 > i0 ? xr[t + 0] : 0.0;
+      const double x1 = rbase + t + 1 > i0 ? xr[t + 1] : 0.0;
+      const double x2 = rbase + t + 2 > i0 ? xr[t + 2] : 0.0;
+      const double x3 = rbase + t + 3 > i0 ? xr[t + 3] : 0.0;
+      s0 = __fma_rn(x0, x0, s0); s1 = __fma_rn(x1, x1, s1);
+      s2 = __fma_rn(x2, x2, s2); s3 = __fma_rn(x3, x3, s3);
+    }
+    return ((i0 + 1) & 1) ? __dadd_rn(__dadd_rn(s1, s2), __dadd_rn(s3, s0))
+                          : __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
+  };
+  // own entry of row i (uniform i)
+  auto own_row = [&](int i) -> double { return i < rbase ? Ps[i * NT + tid] : rc_sel(xr, i - rbase); };
+  auto publish_col = [&]() {
+#pragma unroll
+    for (int t = 0; t < RC_RR; t += 2)
+      *reinterpret_cast<double2*>(S.colbuf + rbase + t) = make_double2(xr[t], xr[t + 1]);
+  };
+
+  for (int e = tid; e < vhn; e += NT) { S.vh0[e] = 0.0; S.vh1[e] = 0.0; S.colbuf[e] = 0.0; }
+  if (have) {
+    build_col();
+    S.jpvt[tid] = tid;
+  } else {
+#pragma unroll
+    for (int t = 0; t < RC_RR; ++t) xr[t] = 0.0;
+  }
+  int pos = have ? tid : 0x7fffffff;
+  double vn1 = 0.0, vn2 = 0.0;
+  double cv = -1.0;
+  int cp = 0x7fffffff;
+  if (have) {
+    const double nr = __dsqrt_rn(sumsq_after(-1));
+    vn1 = nr;
+    vn2 = nr;
+    if (nr > cv) { cv = nr; cp = pos; }
+  }
+  const int kmax = min(m, n);
+  RC_MARK(0)
+  // ---- dgeqp3 / dlaqp2 (three barriers per pivot step: pivot choice, published pivot
+  // column, reflector)
+  for (int i = 0; i < kmax; ++i) {
+    int pp = rc_argmax<NT>(cv, cp, S);
+    if (pp >= n) pp = i;  // (all candidates NaN)
+    RC_MARK(1)
+    const int c = S.jpvt[pp], q = S.jpvt[i];
+    if (tid == c) publish_col();
+    if (tid == q) pos = pp;
+    if (tid == c) pos = i;
+    __syncthreads();
+    RC_MARK(2)
+    if (tid < 32) {
+      if (tid == 0) { S.jpvt[pp] = q; S.jpvt[i] = c; }
+      rc_householder<NT>(Ps, rbase, m, i, c, S);
+    }
+    __syncthreads();
+    RC_MARK(3)
+    cv = -1.0;
+    cp = 0x7fffffff;
+    if (have && pos > i) {
+      const double tau = S.misc[0];
+      // the norm-downdate divisions do not depend on the reflector: issue them first
+      double v1 = vn1;
+      const double rv1 = 1.0 / v1;
+      const double q2 = v1 / vn2;
+      const double xi = own_row(i);
+      double pij = xi;
+      if (tau != 0.0) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        {
+          const int a = (i + 1) & 3;
+          s0 = a == 0 ? xi : 0.0; s1 = a == 1 ? xi : 0.0; s2 = a == 2 ? xi : 0.0; s3 = a == 3 ? xi : 0.0;
+        }
+        for (int g = (i + 1) & ~3; g < rbase; g += 4) {
+          const double2 va = *reinterpret_cast<const double2*>(S.vh0 + g);
+          const double2 vb = *reinterpret_cast<const double2*>(S.vh0 + g + 2);
+          const double x0 = Ps[(g + 0) * NT + tid], x1 = Ps[(g + 1) * NT + tid];
+          const double x2 = Ps[(g + 2) * NT + tid], x3 = Ps[(g + 3) * NT + tid];
+          s0 = __fma_rn(va.x, x0, s0); s1 = __fma_rn(va.y, x1, s1);
+          s2 = __fma_rn(vb.x, x2, s2); s3 = __fma_rn(vb.y, x3, s3);
+        }
+#pragma unroll
+        for (int t = 0; t < RC_RR; t += 4) {
+          const double2 va = *reinterpret_cast<const double2*>(S.vh0 + rbase + t);
+          const double2 vb = *reinterpret_cast<const double2*>(S.vh0 + rbase + t + 2);
+          s0 = __fma_rn(va.x, xr[t + 0], s0); s1 = __fma_rn(va.y, xr[t + 1], s1);
+          s2 = __fma_rn(vb.x, xr[t + 2], s2); s3 = __fma_rn(vb.y, xr[t + 3], s3);
+        }
+        const double w = ((i + 1) & 1) ? __dadd_rn(__dadd_rn(s1, s2), __dadd_rn(s3, s0))
+                                       : __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
+        const double tt = -__dmul_rn(tau, w);
+        pij = __dadd_rn(xi, tt);
+        for (int g = i & ~3; g < rbase; g += 4) {
+          const double2 va = *reinterpret_cast<const double2*>(S.vh1 + g);
+          const double2 vb = *reinterpret_cast<const double2*>(S.vh1 + g + 2);
+          const double x0 = Ps[(g + 0) * NT + tid], x1 = Ps[(g + 1) * NT + tid];
+          const double x2 = Ps[(g + 2) * NT + tid], x3 = Ps[(g + 3) * NT + tid];
+          Ps[(g + 0) * NT + tid] = __fma_rn(tt, va.x, x0);
+          Ps[(g + 1) * NT + tid] = __fma_rn(tt, va.y, x1);
+          Ps[(g + 2) * NT + tid] = __fma_rn(tt, vb.x, x2);
+          Ps[(g + 3) * NT + tid] = __fma_rn(tt, vb.y, x3);
+        }
+#pragma unroll
+        for (int t = 0; t < RC_RR; t += 4) {
+          const double2 va = *reinterpret_cast<const double2*>(S.vh1 + rbase + t);
+          const double2 vb = *reinterpret_cast<const double2*>(S.vh1 + rbase + t + 2);
+          xr[t + 0] = __fma_rn(tt, va.x, xr[t + 0]); xr[t + 1] = __fma_rn(tt, va.y, xr[t + 1]);
+          xr[t + 2] = __fma_rn(tt, vb.x, xr[t + 2]); xr[t + 3] = __fma_rn(tt, vb.y, xr[t + 3]);
+        }
+      }
+      if (v1 != 0.0) {
+        double q = fabs(pij) * rv1;
+        double temp = fmax(1.0 - q * q, 0.0);
+        double temp2 = temp * (q2 * q2);
+        if (temp2 <= TOL3Z) {
+          double nv = i + 1 < m ? __dsqrt_rn(sumsq_after(i)) : 0.0;
+          vn1 = nv;
+          vn2 = nv;
+          v1 = nv;
+        } else {
+          v1 = __dmul_rn(v1, __dsqrt_rn(temp));
+          vn1 = v1;
+        }
+      }
+      if (v1 > cv) { cv = v1; cp = pos; }
+    }
+    RC_MARK(4)
+#ifdef SMASH_COMPRESS_PROF
+    if (tid == 0) atomicAdd(A.prof + 7, 1ULL);
+#endif
+  }
+  __syncthreads();
+  // ---- numerical rank (count semantics, lowrank.py:163-167)
+  if (tid == 0) {
+    int k = 0;
+    double r0 = fabs(S.rdiag[0]);
+    if (r0 != 0.0) {
+      double thr = __dmul_rn(A.rtol, r0);
+      for (int i = 0; i < kmax; ++i) k += fabs(S.rdiag[i]) > thr ? 1 : 0;
+    }
+    S.imisc[0] = min(k, kmax);
+  }
+  __syncthreads();
+  const int k = S.imisc[0];
+  const int ktop = min(k, rbase);  // rows of R below it are register rows
+  // ---- bounded-entry swap loop (lowrank.py:191-202)
+  int swaps = 0;
+  while (k > 0 && k < n) {
+    const int nk = n - k;
+    // R11 -> compact [a][c] array, zero outside the strict upper triangle (so the solve's
+    // aligned groups need no bounds: out-of-range terms multiply by zero)
+    {
+      const int tot = k * kld;
+      for (int e = tid; e < tot; e += NT) S.r11[e] = 0.0;
+    }
+    __syncthreads();
+    if (have && pos < k) {
+      const int top = min(pos, rbase);
+      for (int a = 0; a < top; ++a) S.r11[a * kld + pos] = Ps[a * NT + tid];
+#pragma unroll
+      for (int t = 0; t < RC_RR; ++t)
+        if (rbase + t < pos) S.r11[(rbase + t) * kld + pos] = xr[t];
+    }
+    __syncthreads();
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    if (have && pos >= k) {
+      // W = R11^-1 R12 by back substitution on the own column, the same FMA sequence as
+      // k_compress (terms k-1 .. a+1 of row a on four chains by (k-1-c) mod 4)
+      const bool odd = (k - 1) & 1;
+      if (rbase < k) {
+#pragma unroll
+        for (int t = RC_RR - 1; t >= 0; --t) {
+          const int a = rbase + t;
+          if (a < k) {
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            const double* __restrict__ Rr = S.r11 + a * kld + rbase;
+#pragma unroll
+            for (int p2 = RC_RR / 2 - 1; 2 * p2 + 1 > t; --p2) {
+              const double2 rr = *reinterpret_cast<const double2*>(Rr + 2 * p2);
+              s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
+              if (2 * p2 > t) s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
+            }
+            const double comb = odd ? __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]))
+                                    : __dadd_rn(__dadd_rn(s[1], s[2]), __dadd_rn(s[3], s[0]));
+            const double x = __ddiv_rn(__dadd_rn(xr[t], comb), S.rdiag[a]);
+            xr[t] = x;
+            argmax_combine(bv, bi, fabs(x), a * nk + (pos - k));
+          }
+        }
+      }
+      for (int a = ktop - 1; a >= 0; --a) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* __restrict__ Ra = S.r11 + a * kld;
+        if (rbase < k) {
+#pragma unroll
+          for (int p2 = RC_RR / 2 - 1; p2 >= 0; --p2) {
+            const double2 rr = *reinterpret_cast<const double2*>(Ra + rbase + 2 * p2);
+            s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
+            s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
+          }
+        }
+        for (int g = (ktop - 1) & ~3; g + 3 > a; g -= 4) {
+          const double2 r01 = *reinterpret_cast<const double2*>(Ra + g);
+          const double2 r23 = *reinterpret_cast<const double2*>(Ra + g + 2);
+          const double x0 = Ps[(g + 0) * NT + tid], x1 = Ps[(g + 1) * NT + tid];
+          const double x2 = Ps[(g + 2) * NT + tid], x3 = Ps[(g + 3) * NT + tid];
+          s[3] = __fma_rn(-x3, r23.y, s[3]); s[2] = __fma_rn(-x2, r23.x, s[2]);
+          s[1] = __fma_rn(-x1, r01.y, s[1]); s[0] = __fma_rn(-x0, r01.x, s[0]);
+        }
+        const double comb = odd ? __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]))
+                                : __dadd_rn(__dadd_rn(s[1], s[2]), __dadd_rn(s[3], s[0]));
+        const double x = __ddiv_rn(__dadd_rn(Ps[a * NT + tid], comb), S.rdiag[a]);
+        Ps[a * NT + tid] = x;
+        argmax_combine(bv, bi, fabs(x), a * nk + (pos - k));
+      }
+    }
+    bi = rc_argmax<NT>(bv, bi, S);
+    RC_MARK(5)
+    if (!(bv > A.s_bound)) break;
+    if (swaps >= MAX_SWAPS) {
+      if (tid == 0) atomicOr(A.err, DEV_SWAP_CAP);
+      break;
+    }
+    if (tid == 0) {
+      const int a = bi / nk, jj = bi % nk;
+      const int ca = S.jpvt[a], cb = S.jpvt[k + jj];
+      S.jpvt[a] = cb;
+      S.jpvt[k + jj] = ca;
+      S.imisc[1] = ca; S.imisc[2] = cb; S.imisc[3] = a; S.imisc[5] = k + jj;
+    }
+    for (int e = tid; e < vhn; e += NT) { S.vh0[e] = 0.0; S.vh1[e] = 0.0; }
+    __syncthreads();
+    if (tid == S.imisc[1]) pos = S.imisc[5];
+    if (tid == S.imisc[2]) pos = S.imisc[3];
+    ++swaps;
+    if (have) build_col();
+    // unpivoted QR (dgeqr2) of the permuted panel; rows < k of R suffice.  Sequential
+    // dot-product order, as k_compress's refactorisation.
+    for (int i = 0; i < k; ++i) {
+      const int c = S.jpvt[i];
+      if (tid == c) publish_col();
+      __syncthreads();
+      if (tid < 32) rc_householder<NT>(Ps, rbase, m, i, c, S);
+      __syncthreads();
+      const double tau = S.misc[0];
+      if (have && pos > i && tau != 0.0) {
+        const double xi = own_row(i);
+        double w = xi;
+        for (int row = i + 1; row < rbase; ++row) w = __fma_rn(S.vh0[row], Ps[row * NT + tid], w);
+#pragma unroll
+        for (int t = 0; t < RC_RR; ++t) w = __fma_rn(S.vh0[rbase + t], xr[t], w);
+        const double tt = -__dmul_rn(tau, w);
+        for (int row = i; row < rbase; ++row)
+          Ps[row * NT + tid] = __fma_rn(tt, S.vh1[row], Ps[row * NT + tid]);
+#pragma unroll
+        for (int t = 0; t < RC_RR; ++t) xr[t] = __fma_rn(tt, S.vh1[rbase + t], xr[t]);
+      }
+    }
+    __syncthreads();
+    RC_MARK(6)
+  }
+  __syncthreads();
+  // ---- outputs
+  if (tid == 0) {
+    A.rank[v] = k;
+    if (swaps) atomicAdd(A.swaps, (unsigned long long)swaps);
+  }
+  const int64_t io = A.ib_off[v];
+  if (have) A.perm[io + tid] = S.jpvt[tid];
+  if (k > 0 && k < n && have && pos >= k) {
+    double* __restrict__ G = A.G + A.g_off[v] + (size_t)(pos - k) * k;
+    for (int a = 0; a < ktop; ++a) G[a] = Ps[a * NT + tid];
+#pragma unroll
+    for (int t = 0; t < RC_RR; ++t)
+      if (rbase + t < k) G[rbase + t] = xr[t];
+  }
+  if (A.tmp_lab) {
+    const int64_t lo = io - A.ib_level_base;
+    if (tid < k) {
+      const int pc = S.jpvt[tid];
+      A.tmp_lab[lo + tid] = src.lab ? src.lab[pc] : src.lab0 + pc;
+      for (int d = 0; d < D; ++d)
+        A.tmp_pts[(size_t)d * A.tmp_stride + lo + tid] = src.base[(size_t)d * src.stride + pc];
+    }
+  }
+  __syncthreads();
+}
+
+template <int D, int NT>
+__global__ void __launch_bounds__(NT, NT >= 256 ? 2 : NT == 128 ? 4 : 8) k_compress_rc(CompressArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int vhn = rc_round4(A.mmax) + RC_RR + 4;
+  const int kcap = rc_round4(min(A.mmax, NT));
+  const int kld = max(rc_round4(A.mmax), RC_RR);
+  const int srows = max(0, rc_round4(A.mmax - RC_RR));
+  constexpr bool R11G = NT == 64;
+  RcShared S;
+  {
+    double* d = reinterpret_cast<double*>(smem_raw);
+    S.vh0 = d; d += vhn;
+    S.vh1 = d; d += vhn;
+    S.colbuf = d; d += vhn;
+    if (R11G) S.r11 = A.gws + (size_t)blockIdx.x * kcap * kld;
+    else { S.r11 = d; d += (size_t)kcap * kld; }
+    S.panel = d; d += (size_t)srows * NT;
+    S.rdiag = d; d += rc_round4(A.mmax);
+    S.nodes = d; d += 3 * MAX_M_AXIS_1D;
+    S.redv = d; d += 8;
+    S.misc = d; d += 8;
+    int* ip = reinterpret_cast<int*>(d);
+    S.redi = ip; ip += 8;
+    S.imisc = ip; ip += 8;
+    S.jpvt = ip;
+  }
+  const int tid = threadIdx.x;
+  auto next_node = [&]() {
+    __syncthreads();
+    if (tid == 0) S.imisc[4] = A.lb + (int)gridDim.x + atomicAdd(A.next, 1);
+    __syncthreads();
+    return S.imisc[4];
+  };
+  for (int v = A.lb + blockIdx.x; v < A.le;) {
+    const int n = A.nib[v];
+    if (n <= A.n_lo || n > A.n_hi) {  // another launch of this level takes this size class
+      v = next_node();
+      continue;
+    }
+    if (n == 0) {
+      if (tid == 0) A.rank[v] = 0;
+      v = next_node();
+      continue;
+    }
+    const int m = A.r + (A.keep ? A.keep[v] : 0);
+    SMASH_DASSERT(n <= NT && m <= A.mmax);
+    const NodeSrc src = node_src(A, v);
+    // ---- padded box + Chebyshev nodes (hss.py:39-45, lowrank.py:103-105,127-134)
+    if (tid == 0) {
+      double plo[3], phi[3];
+      double scale = 1.0;
+      for (int a = 0; a < D; ++a) {
+        double lo = A.lo[(size_t)v * D + a], hi = A.hi[(size_t)v * D + a];
+        if (__dsub_rn(hi, lo) < A.pad) {
+          lo = __dsub_rn(lo, A.half_pad);
+          hi = __dadd_rn(hi, A.half_pad);
+        }
+        plo[a] = lo; phi[a] = hi;
+        scale = fmax(scale, __dsub_rn(hi, lo));
+      }
+      int bad = 0;
+      for (int a = 0; a < D; ++a)
+        if (!(__dsub_rn(phi[a], plo[a]) > __dmul_rn(1e-14, scale))) bad = 1;
+      if (bad) atomicOr(A.err, DEV_DEGENERATE_BOX);
+      for (int a = 0; a < D; ++a) { S.misc[2 + a] = plo[a]; S.misc[5 + a] = phi[a]; }
+    }
+    __syncthreads();
+    {
+      const int mt = A.tab.m;
+      for (int e = tid; e < D * mt; e += NT) {
+        int a = e / mt, k = e % mt;
+        double lo = S.misc[2 + a], hi = S.misc[5 + a];
+        double t1 = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        double t2 = __dmul_rn(0.5, __dsub_rn(hi, lo));
+        S.nodes[a * MAX_M_AXIS_1D + k] = __dadd_rn(t1, __dmul_rn(t2, A.tab.cosv[k]));
+      }
+    }
+    __syncthreads();
+    rc_node<D, NT>(A, S, v, n, m, src, vhn, kld);
+    v = next_node();
+  }
+}
