@@ -69,37 +69,51 @@ __device__ __forceinline__ double rc_sel(const double (&x)[RC_RR], int s) {
 }
 
 // (max value, smallest index) over the CTA with one barrier; two calls must be separated
-// by another barrier.  Returns the value through v.
+// by another barrier.  Candidates are non-negative doubles (norms, |W| entries) or -1 for
+// "none": their bit patterns order like unsigned integers, so each warp reduces with three
+// redux.sync operations (high word, low word among the leaders, smallest index among the
+// equals) instead of five shuffle rounds.  Returns the index, the value through v.
 template <int NT>
 __device__ __forceinline__ int rc_argmax(double& v, int i, RcShared& S) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int off = 16; off; off >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, v, off);
-    int oi = __shfl_xor_sync(0xffffffffu, i, off);
-    argmax_combine(v, i, ov, oi);
+  const bool valid = v >= 0.0;
+  const unsigned long long key = valid ? (unsigned long long)__double_as_longlong(v) : 0ULL;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const unsigned mi = __reduce_min_sync(0xffffffffu, (valid && hi == mh && lo == ml) ? (unsigned)i : 0x7fffffffu);
+  if (lane == 0) {
+    reinterpret_cast<unsigned long long*>(S.redv)[wid] = ((unsigned long long)mh << 32) | ml;
+    S.redi[wid] = (int)mi;
   }
-  if (lane == 0) { S.redv[wid] = v; S.redi[wid] = i; }
   __syncthreads();
-  v = S.redv[0];
-  i = S.redi[0];
+  unsigned long long bk = reinterpret_cast<const unsigned long long*>(S.redv)[0];
+  int bi = S.redi[0];
 #pragma unroll
-  for (int w = 1; w < NW; ++w) argmax_combine(v, i, S.redv[w], S.redi[w]);
-  return i;
+  for (int w = 1; w < NW; ++w) {
+    const unsigned long long ok = reinterpret_cast<const unsigned long long*>(S.redv)[w];
+    const int oi = S.redi[w];
+    if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+  }
+  v = bi == 0x7fffffff ? -1.0 : __longlong_as_double((long long)bk);
+  return bi;
 }
 
-// dlarfg on the published pivot column c at step i (warp 0), as qr::householder: the
-// lane-strided sum of squares, beta / tau / scal, the scaled reflector to vh0 / vh1.
+// dlarfg on the published pivot column c at step i, by one warp (the owner's), as
+// qr::householder: the lane-strided sum of squares, beta / tau / scal, the scaled
+// reflector to vh0 / vh1.
 template <int NT>
 __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, int rbase, int m, int i,
                                                int c, RcShared& S) {
-  const int lane = threadIdx.x;
-  auto colv = [&](int row) { return row < rbase ? Ps[row * NT + c] : S.colbuf[row]; };
-  const double alpha = colv(i);
+  const int lane = threadIdx.x & 31;
+  const double* __restrict__ pc = Ps + c;
+  const double* __restrict__ cb = S.colbuf;
+  const double alpha = i < rbase ? pc[i * NT] : cb[i];
   double ss = 0.0;
 #pragma unroll 1
   for (int row = i + 1 + lane; row < m; row += 32) {
-    const double x = colv(row);
+    const double x = row < rbase ? pc[row * NT] : cb[row];
     ss = __fma_rn(x, x, ss);
   }
   for (int off = 16; off; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
@@ -111,7 +125,7 @@ __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, in
     const double scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
 #pragma unroll 1
     for (int row = i + 1 + lane; row < m; row += 32) {
-      const double x = __dmul_rn(scal, colv(row));
+      const double x = __dmul_rn(scal, row < rbase ? pc[row * NT] : cb[row]);
       S.vh0[row] = x;
       S.vh1[row] = x;
     }
@@ -233,22 +247,23 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   }
   const int kmax = min(m, n);
   RC_MARK(0)
-  // ---- dgeqp3 / dlaqp2 (three barriers per pivot step: pivot choice, published pivot
-  // column, reflector)
+  // ---- dgeqp3 / dlaqp2 (two barriers per pivot step: pivot choice, reflector)
   for (int i = 0; i < kmax; ++i) {
     int pp = rc_argmax<NT>(cv, cp, S);
     if (pp >= n) pp = i;  // (all candidates NaN)
     RC_MARK(1)
-    const int c = S.jpvt[pp], q = S.jpvt[i];
-    if (tid == c) publish_col();
-    if (tid == q) pos = pp;
-    if (tid == c) pos = i;
-    __syncthreads();
-    RC_MARK(2)
-    if (tid < 32) {
-      if (tid == 0) { S.jpvt[pp] = q; S.jpvt[i] = c; }
-      rc_householder<NT>(Ps, rbase, m, i, c, S);
+    // the column at position pp becomes pivot i, the column at position i takes its place
+    // (each of the two threads records itself in the position -> column table)
+    const bool owner = have && pos == pp;
+    if (have && pos == i) { pos = pp; S.jpvt[pp] = tid; }
+    if (owner) { pos = i; S.jpvt[i] = tid; }
+    const unsigned own_mask = __ballot_sync(0xffffffffu, owner);
+    if (own_mask) {  // the owner's warp: publish the register rows, then dlarfg
+      if (owner) publish_col();
+      __syncwarp();
+      rc_householder<NT>(Ps, rbase, m, i, (tid & ~31) + (__ffs(own_mask) - 1), S);
     }
+    RC_MARK(2)
     __syncthreads();
     RC_MARK(3)
     cv = -1.0;
@@ -435,9 +450,11 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
     // dot-product order, as k_compress's refactorisation.
     for (int i = 0; i < k; ++i) {
       const int c = S.jpvt[i];
-      if (tid == c) publish_col();
-      __syncthreads();
-      if (tid < 32) rc_householder<NT>(Ps, rbase, m, i, c, S);
+      if ((tid >> 5) == (c >> 5)) {
+        if (tid == c) publish_col();
+        __syncwarp();
+        rc_householder<NT>(Ps, rbase, m, i, c, S);
+      }
       __syncthreads();
       const double tau = S.misc[0];
       if (have && pos > i && tau != 0.0) {
@@ -452,8 +469,8 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
 #pragma unroll
         for (int t = 0; t < RC_RR; ++t) xr[t] = __fma_rn(tt, S.vh1[rbase + t], xr[t]);
       }
+      __syncthreads();  // the next reflector overwrites vh0 / vh1
     }
-    __syncthreads();
     RC_MARK(6)
   }
   __syncthreads();
