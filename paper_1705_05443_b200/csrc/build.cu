@@ -411,12 +411,12 @@ struct SideBuild {
   }
 
   void launch_level(CompressArgs& A, int cnt) {
-    CompressPass ps[4];
+    CompressPass ps[MAX_COMPRESS_PASSES];
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
-      if (ps[k].rc_nt) {  // register-column launch: R11 slices of the 64-thread CTAs
-        const size_t need = compress_rc_gws_doubles(ps[k].rc_nt, a.mmax, ps[k].grid);
+      if (ps[k].rc.nt) {  // register-column launch: global R11 slices
+        const size_t need = compress_rc_gws_doubles(ps[k].rc, a.mmax, ps[k].grid);
         if (need) {
           if (gws.n < need) gws.alloc(need, s);
           a.gws = gws.p;
@@ -432,7 +432,7 @@ struct SideBuild {
         cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
       }
-      if (ps[k].rc_nt) launch_compress_rc(a, ps[k].rc_nt, ps[k].grid, ps[k].smem, s);
+      if (ps[k].rc.nt) launch_compress_rc(a, ps[k].rc, ps[k].grid, ps[k].smem, s);
       else launch_compress(a, ps[k].grid, ps[k].smem, s);
       if (dbg) {
         cudaEventRecord(e1, s);
@@ -448,7 +448,7 @@ struct SideBuild {
                   nn ? (double)cols / nn : 0.0, nn ? ms * 1e3 * ps[k].grid / nn : 0.0);
         }
         fprintf(stderr, "compress launch: %s nodes %d class (%d, %d] nmax %d mmax %d threads %d grid %d smem %zu cap %lld: %.3f ms\n",
-                ps[k].rc_nt ? "rc" : "sm", cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
+                ps[k].rc.nt ? (ps[k].rc.rr > 32 ? "rc48" : "rc") : "sm", cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
         cudaEventDestroy(e0); cudaEventDestroy(e1);
       }
     }

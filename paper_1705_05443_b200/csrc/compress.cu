@@ -23,81 +23,14 @@
 // else 256), per node in shared memory or the CTA's global slice on hybrid
 // levels, and in the global/L2 slice (32-deep independent loads) when no
 // shared panel fits.
-#include "compress.cuh"
-#include "qr_device.cuh"
+#include "compress_common.cuh"
 
 namespace smash {
 
 namespace {
 
 using namespace qr;
-
-constexpr int MAX_SWAPS = 200;                     // lowrank.py:171
-
-// numpy's pairwise summation (8 accumulators, n <= 128) over terms f(0..n-1);
-// this is the order of `terms.sum(axis=1)` in lowrank.py:116.
-template <typename F>
-__device__ __forceinline__ double np_pairwise_sum(int n, F f) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(i));
-    return r;
-  }
-  double a0 = f(0), a1 = f(1), a2 = f(2), a3 = f(3), a4 = f(4), a5 = f(5), a6 = f(6), a7 = f(7);
-  int i = 8;
-  const int lim = n - (n % 8);
-  for (; i < lim; i += 8) {
-    a0 = __dadd_rn(a0, f(i + 0)); a1 = __dadd_rn(a1, f(i + 1));
-    a2 = __dadd_rn(a2, f(i + 2)); a3 = __dadd_rn(a3, f(i + 3));
-    a4 = __dadd_rn(a4, f(i + 4)); a5 = __dadd_rn(a5, f(i + 5));
-    a6 = __dadd_rn(a6, f(i + 6)); a7 = __dadd_rn(a7, f(i + 7));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)),
-                         __dadd_rn(__dadd_rn(a4, a5), __dadd_rn(a6, a7)));
-  for (; i < n; ++i) res = __dadd_rn(res, f(i));
-  return res;
-}
-
-// Lagrange cardinal functions of one axis at x (lowrank.py:108-120), written to L[0..m).
-__device__ __forceinline__ void lagrange_axis(double x, const double* nd, const double* w, int m,
-                                              double* L) {
-  bool exact = false;
-  for (int k = 0; k < m; ++k) exact |= (__dsub_rn(x, nd[k]) == 0.0);
-  if (exact) {
-    for (int k = 0; k < m; ++k) L[k] = (__dsub_rn(x, nd[k]) == 0.0) ? 1.0 : 0.0;
-    return;
-  }
-  double S = np_pairwise_sum(m, [&](int k) { return __ddiv_rn(w[k], __dsub_rn(x, nd[k])); });
-  for (int k = 0; k < m; ++k) L[k] = __ddiv_rn(__ddiv_rn(w[k], __dsub_rn(x, nd[k])), S);
-}
-
-// ---------------------------------------------------------------------------
-// ibar point access
-// ---------------------------------------------------------------------------
-struct NodeSrc {
-  const double* base;  // coordinate SoA base for this node's ibar
-  int64_t stride;
-  const int* lab;      // labels (nullptr -> leaf: label = lab0 + c)
-  int lab0;
-};
-
-__device__ __forceinline__ NodeSrc node_src(const CompressArgs& A, int v) {
-  NodeSrc s;
-  if (A.nchild[v] == 0) {
-    int a = A.pt_a[v];
-    s.base = A.P + a;
-    s.stride = A.P_stride;
-    s.lab = nullptr;
-    s.lab0 = a;
-  } else {
-    int o = A.skel_off[A.child_first[v]];
-    s.base = A.Sk + o;
-    s.stride = A.S_stride;
-    s.lab = A.Slab + o;
-    s.lab0 = 0;
-  }
-  return s;
-}
+using namespace cmn;
 
 // Fill panel columns c in [0, n): column c is ibar point colmap[c] (or c).
 template <int D>
@@ -351,8 +284,6 @@ __device__ __forceinline__ void compress_node(const CompressArgs& A, Shared& S, 
   __syncthreads();
 }
 
-#include "compress_rc.cuh"
-
 // MODE: 0 = panel in the global workspace, 1 = shared memory, 2 = per node
 // (hybrid).  The global-only variant uses deeper load chunks (more registers,
 // fewer CTAs per SM); the shared variants are sized for >= 4 CTAs per SM.
@@ -547,23 +478,32 @@ static bool compress_chains4() {
   return c4;
 }
 
-// Register-column launch (compress_rc.cuh) of a size class of at most 256 columns.
+// Register-column launch (compress_rc.cuh) of a size class of at most 320 columns: the first
+// variant whose shared memory fits.
 static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) {
   constexpr size_t SM_BYTES = 228 * 1024, CTA_RESERVED = 1024;
-  const int nt = P.a.nmax <= 64 ? 64 : P.a.nmax <= 128 ? 128 : P.a.nmax <= 256 ? 256 : 0;
-  if (!nt) return false;
-  const size_t smem = compress_rc_smem_bytes(nt, P.a.mmax);
-  if ((int64_t)smem > (int64_t)smem_limit) return false;
-  const int by_regs = 65536 / (nt * 128);  // __launch_bounds__ of k_compress_rc
-  const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
-  P.grid = std::min(cnt, nsm * std::min(by_regs, by_smem));
-  P.smem = smem;
-  P.rc_nt = nt;
-  P.a.threads = nt;
-  return true;
+  const int nmax = P.a.nmax, mmax = P.a.mmax;
+  RcVariant cand[2];
+  int nc = 0;
+  if (nmax <= 64) cand[nc++] = {64, 32, true};
+  else if (nmax <= 128) { cand[nc++] = {128, 32, false}; cand[nc++] = {128, 32, true}; }
+  else if (nmax <= 256) { cand[nc++] = {256, 32, false}; cand[nc++] = {256, 48, true}; }
+  else if (nmax <= 320) cand[nc++] = {320, 44, true};
+  for (int c = 0; c < nc; ++c) {
+    const size_t smem = compress_rc_smem_bytes(cand[c], mmax);
+    if ((int64_t)smem > (int64_t)smem_limit) continue;
+    const int by_regs = cand[c].rr > 32 ? 1 : 65536 / (cand[c].nt * 128);  // __launch_bounds__ of k_compress_rc
+    const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
+    P.grid = std::min(cnt, nsm * std::min(by_regs, by_smem));
+    P.smem = smem;
+    P.rc = cand[c];
+    P.a.threads = cand[c].nt;
+    return true;
+  }
+  return false;
 }
 
-int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass out[4]) {
+int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass* out) {
   static const bool split = getenv("SMASH_COMPRESS_NOSPLIT") == nullptr;
   // (read per call: tests switch between the two kernels within a process)
   const bool rc = !(getenv("SMASH_COMPRESS_RC") && atoi(getenv("SMASH_COMPRESS_RC")) == 0) &&
@@ -574,19 +514,27 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
     if (plan_compress_rc(out[0], cnt, smem_limit, nsm)) return 1;
   }
   if (rc && split && cnt > nsm && A0.nmax > 64) {
-    const int rb[4] = {64, 128, 256, 0x7fffffff};
+    // size classes (.., 64], (64, 128], (128, 256], (256, 320] on the register-column kernel as
+    // far as its variants fit, one k_compress launch for the rest
+    const int rb[4] = {64, 128, 256, 320};
     int np = 0, lo = -1;
     for (int b : rb) {
       if (lo >= A0.nmax) break;
-      CompressPass& P = out[np++];
-      P = CompressPass();
+      CompressPass P;
       P.a = A0;
       P.a.n_lo = lo;
       P.a.n_hi = b;
       P.a.nmax = std::min(A0.nmax, b);
-      if (!plan_compress_rc(P, cnt, smem_limit, nsm))
-        P.smem = plan_compress_launch(P.a, cnt, smem_limit, nsm, &P.grid);
+      if (!plan_compress_rc(P, cnt, smem_limit, nsm)) break;
+      out[np++] = P;
       lo = b;
+    }
+    if (lo < A0.nmax) {
+      CompressPass& P = out[np++];
+      P = CompressPass();
+      P.a = A0;
+      P.a.n_lo = lo;
+      P.smem = plan_compress_launch(P.a, cnt, smem_limit, nsm, &P.grid);
     }
     return np;
   }
@@ -671,11 +619,7 @@ void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream
 #endif
 }
 
-size_t compress_rc_gws_doubles(int nt, int mmax, int grid) {
-  return rc_r11_global(nt) ? (size_t)grid * rc_r11_doubles(nt, mmax) : 0;
-}
-
-void launch_compress_rc(const CompressArgs& a_in, int nt, int grid, size_t smem, cudaStream_t s) {
+void launch_compress_rc(const CompressArgs& a_in, const RcVariant& v, int grid, size_t smem, cudaStream_t s) {
   CompressArgs a = a_in;
   a.chains4 = true;
   void* nx = nullptr;
@@ -688,28 +632,17 @@ void launch_compress_rc(const CompressArgs& a_in, int nt, int grid, size_t smem,
   SMASH_CUDA(cudaMemsetAsync(pp, 0, sizeof(g_compress_prof), s));
   a.prof = reinterpret_cast<unsigned long long*>(pp);
 #endif
-  auto go = [&](auto kern) {
-    SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, nt, smem, s>>>(a);
-  };
-  auto by_nt = [&](auto d) {
-    constexpr int D = decltype(d)::value;
-    if (nt == 64) go(k_compress_rc<D, 64>);
-    else if (nt == 128) go(k_compress_rc<D, 128>);
-    else go(k_compress_rc<D, 256>);
-  };
-  if (a.dim == 1) by_nt(std::integral_constant<int, 1>{});
-  else if (a.dim == 2) by_nt(std::integral_constant<int, 2>{});
-  else by_nt(std::integral_constant<int, 3>{});
-  SMASH_CUDA(cudaGetLastError());
+  if (a.dim == 1) launch_compress_rc_dim<1>(a, v, grid, smem, s);
+  else if (a.dim == 2) launch_compress_rc_dim<2>(a, v, grid, smem, s);
+  else launch_compress_rc_dim<3>(a, v, grid, smem, s);
 #ifdef SMASH_COMPRESS_PROF
   unsigned long long h[8];
   SMASH_CUDA(cudaMemcpyAsync(h, pp, sizeof(h), cudaMemcpyDeviceToHost, s));
   SMASH_CUDA(cudaStreamSynchronize(s));
   const double st = h[7] ? (double)h[7] : 1.0;
-  fprintf(stderr, "compress_rc nodes %d nt %d grid %d: Mcycles (thread 0 of every CTA) build %.2f qr %.2f solve %.2f reqr %.2f"
-          " | per step: argmax %.0f, publish %.0f, reflector %.0f, update+downdate %.0f cycles (%llu steps)\n",
-          a.le - a.lb, nt, grid, h[0] * 1e-6, (h[1] + h[2] + h[3] + h[4]) * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
+  fprintf(stderr, "compress_rc nodes %d nt %d rr %d grid %d: Mcycles (thread 0 of every CTA) build %.2f qr %.2f solve %.2f reqr %.2f"
+          " | per step: argmax %.0f, reflector (owner warp) %.0f, wait %.0f, update+downdate %.0f cycles (%llu steps)\n",
+          a.le - a.lb, v.nt, v.rr, grid, h[0] * 1e-6, (h[1] + h[2] + h[3] + h[4]) * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
           h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[7]);
 #endif
 }

@@ -76,16 +76,43 @@ size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
 // per CTA and the grid (persistent CTAs over the level's cnt nodes).
 size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, int* grid);
 void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s);
+// Register-column kernel (compress_rc.cuh): CTA size = maximum columns, rows kept in
+// registers, R11 of the back substitution in shared memory or in a global/L2 slice.
+struct RcVariant {
+  int nt = 0;  // 0: k_compress
+  int rr = 0;
+  bool r11g = false;
+};
+__host__ __device__ inline int rc_round4(int x) { return (x + 3) & ~3; }
+__host__ __device__ inline int rc_vhn(int mmax, int rr) { return rc_round4(mmax) + rr + 4; }
+__host__ __device__ inline int rc_kcap(int mmax, int nt) { return rc_round4(mmax < nt ? mmax : nt); }
+// row length of R11: >= rbase + rr of every node
+__host__ __device__ inline int rc_kld(int mmax, int rr) { return rc_round4(mmax) > rr ? rc_round4(mmax) : rr; }
+__host__ __device__ inline int rc_srows(int mmax, int rr) { return mmax > rr ? rc_round4(mmax - rr) : 0; }
+inline size_t rc_r11_doubles(const RcVariant& v, int mmax) { return (size_t)rc_kcap(mmax, v.nt) * rc_kld(mmax, v.rr); }
+inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax) {
+  const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 16 + 8 +
+                   (v.r11g ? 0 : rc_r11_doubles(v, mmax)) + (size_t)rc_srows(mmax, v.rr) * v.nt;
+  const size_t i = 16 + 8 + (size_t)v.nt;
+  return 8 * d + 4 * i + 16;
+}
+// global workspace (doubles) of a register-column launch: the R11 slices
+inline size_t compress_rc_gws_doubles(const RcVariant& v, int mmax, int grid) {
+  return v.r11g ? (size_t)grid * rc_r11_doubles(v, mmax) : 0;
+}
+void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
+template <int D>
+void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
+
+constexpr int MAX_COMPRESS_PASSES = 6;
 struct CompressPass {
   CompressArgs a;
   int grid = 0;
   size_t smem = 0;
-  int rc_nt = 0;  // > 0: register-column kernel with this CTA size (launch_compress_rc)
+  RcVariant rc;  // rc.nt > 0: register-column kernel (launch_compress_rc)
 };
-size_t compress_rc_gws_doubles(int nt, int mmax, int grid);  // global workspace of a register-column launch
-void launch_compress_rc(const CompressArgs& a, int nt, int grid, size_t smem, cudaStream_t s);
-// Up to four size-class launches of a level (see compress.cu); returns their count.
-int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass out[4]);
+// The size-class launches of a level (see compress.cu); returns their count (<= MAX_COMPRESS_PASSES).
+int plan_compress_passes(const CompressArgs& A, int cnt, int smem_limit, int nsm, CompressPass* out);
 void launch_basis_single(int dim, const double* plo, const double* phi, const BasisTables& tab,
                          int r, const double* pts_soa, int64_t n, double* out, int* err,
                          cudaStream_t s);

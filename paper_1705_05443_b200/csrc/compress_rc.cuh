@@ -1,8 +1,8 @@
-// K3 + K4, register-column variant (included by compress.cu, inside its namespaces).
+// K3 + K4, register-column variant (instantiated per point dimension by compress_rc_d{1,2,3}.cu).
 //
 // Same algorithm and the same floating-point operation order as k_compress (pivots,
 // ranks, swap decisions and G are bit-identical to it), with a different home for the
-// panel: thread j owns ibar column j for the whole node.  The last RC_RR rows of the
+// panel: thread j owns ibar column j for the whole node.  The last RR rows of the
 // column live in registers, the rows above them in shared memory (row-major, one column
 // per thread, conflict free).  Consequences:
 //  * a 64 x 256 panel needs 64 KB of shared memory instead of 128 KB: two CTAs per SM
@@ -11,7 +11,7 @@
 //  * columns are never swapped physically: dlaqp2's column order is a position kept per
 //    thread (pos) and the position -> column table jpvt; the first-maximum pivot rule is
 //    evaluated on positions;
-//  * register rows are indexed statically, so every step runs over all RC_RR register
+//  * register rows are indexed statically, so every step runs over all RR register
 //    rows with the reflector zero-padded above the pivot row (adds exact zeros); the
 //    four accumulation chains are assigned by row mod 4 and combined in the rotation
 //    that reproduces k_compress's (row - i - 1) mod 4 chains bit for bit;
@@ -20,52 +20,57 @@
 // Used for size classes of at most 256 columns (one column per thread, CTAs of 64 / 128 /
 // 256 threads); wider panels and the single-call compr stay on k_compress.
 
-constexpr int RC_RR = 32;
+#pragma once
+
+#include "compress_common.cuh"
+
+namespace smash {
+namespace {
+
+using namespace qr;
+using namespace cmn;
 
 struct RcShared {
-  double* vh0;     // reflector, zero at rows <= i        [vhn]
-  double* vh1;     // reflector, one at row i, zero above [vhn]
-  double* colbuf;  // published pivot column              [vhn]
+  double* vh0;     // reflector of the current step, zero at rows <= i   [vhn]
+  double* vh1;     // the same with a one at row i (dlarf's v)           [vhn]
+  double* colbuf;  // published register rows of the pivot column       [vhn]
   double* rdiag;   // [mmax]
   double* nodes;   // [3][MAX_M_AXIS_1D]
-  double* redv;    // [8]
+  double* redv;    // [16]
   double* misc;    // [8]
-  double* r11;     // R11, [kcap][kld], zero outside the strict upper triangle (global slice for NT = 64)
+  double* r11;     // R11, [kcap][kld], zero outside the strict upper triangle (shared or global)
   double* panel;   // [srows][NT]
-  int* redi;       // [8]
+  int* redi;       // [16]
   int* imisc;      // [8]
   int* jpvt;       // [NT]
 };
 
-__host__ __device__ inline int rc_round4(int x) { return (x + 3) & ~3; }
-inline int rc_vhn(int mmax) { return rc_round4(mmax) + RC_RR + 4; }
-inline int rc_kcap(int mmax, int nt) { return rc_round4(std::min(mmax, nt)); }
-inline int rc_kld(int mmax) { return std::max(rc_round4(mmax), RC_RR); }  // >= rbase + RC_RR of every node
-// CTAs of 64 threads (size class |ibar| <= 64, where k < |ibar| is the exception) keep R11 in a
-// global/L2 slice instead of shared memory: eight CTAs per SM instead of five
-inline bool rc_r11_global(int nt) { return nt == 64; }
-inline size_t rc_r11_doubles(int nt, int mmax) { return (size_t)rc_kcap(mmax, nt) * rc_kld(mmax); }
-inline int rc_srows(int mmax) { return std::max(0, rc_round4(mmax - RC_RR)); }
-
-size_t compress_rc_smem_bytes(int nt, int mmax) {
-  size_t d = 3 * (size_t)rc_vhn(mmax) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 8 + 8 +
-             (rc_r11_global(nt) ? 0 : rc_r11_doubles(nt, mmax)) + (size_t)rc_srows(mmax) * nt;
-  size_t i = 8 + 8 + (size_t)nt;
-  return 8 * d + 4 * i + 16;
+// x[s] for a CTA-uniform s: a tree of selects per block of 16 registers instead of a
+// dynamically indexed array (a dense switch measured slower: cfg5 build 30.9 -> 37.6 ms).
+__device__ __forceinline__ double rc_sel16(const double* x, int s) {
+  double a[8], b[4], c[2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) a[t] = (s & 1) ? x[2 * t + 1] : x[2 * t];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) b[t] = (s & 2) ? a[2 * t + 1] : a[2 * t];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) c[t] = (s & 4) ? b[2 * t + 1] : b[2 * t];
+  return (s & 8) ? c[1] : c[0];
 }
-
-// x[s], s uniform over the CTA (31 selects instead of a dynamically indexed array)
-__device__ __forceinline__ double rc_sel(const double (&x)[RC_RR], int s) {
-  double a[16], b[8], c[4], d[2];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) a[t] = (s & 1) ? x[2 * t + 1] : x[2 * t];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) b[t] = (s & 2) ? a[2 * t + 1] : a[2 * t];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) c[t] = (s & 4) ? b[2 * t + 1] : b[2 * t];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) d[t] = (s & 8) ? c[2 * t + 1] : c[2 * t];
-  return (s & 16) ? d[1] : d[0];
+template <int RR>
+__device__ __forceinline__ double rc_sel(const double (&x)[RR], int s) {
+  static_assert(RR % 4 == 0 && RR >= 16 && RR <= 48, "register rows");
+  // blocks [0,16), [16,32), [RR-16,RR) (the last one may overlap the second)
+  double r = rc_sel16(&x[0], s & 15);
+  if (RR > 16) {
+    const double r1 = rc_sel16(&x[RR >= 32 ? 16 : RR - 16], RR >= 32 ? (s & 15) : s - (RR - 16));
+    r = s >= 16 ? r1 : r;
+  }
+  if (RR > 32) {
+    const double r2 = rc_sel16(&x[RR - 16], s - (RR - 16));
+    r = s >= 32 ? r2 : r;
+  }
+  return r;
 }
 
 // (max value, smallest index) over the CTA with one barrier; two calls must be separated
@@ -140,11 +145,11 @@ __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, in
   }
 }
 
-template <int D, int NT>
+template <int D, int NT, int RR>
 __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int v, int n, int m,
                                         const NodeSrc& src, int vhn, int kld) {
   const int tid = threadIdx.x;
-  const int rbase = max(0, rc_round4(m - RC_RR));
+  const int rbase = max(0, rc_round4(m - RR));
   double* __restrict__ Ps = S.panel;
 #ifdef SMASH_COMPRESS_PROF
   long long pt0 = clock64();
@@ -153,7 +158,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
 #define RC_MARK(k)
 #endif
   const bool have = tid < n;
-  double xr[RC_RR];
+  double xr[RR];
 
   // ---- own column of the panel (smash/lowrank.py:103-144; HSS rows hss.py:287)
   auto build_col = [&]() {
@@ -179,7 +184,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       };
       for (int q = 0; q < rbase; ++q) Ps[q * NT + tid] = val(q);
 #pragma unroll
-      for (int t = 0; t < RC_RR; ++t) xr[t] = val(rbase + t);
+      for (int t = 0; t < RR; ++t) xr[t] = val(rbase + t);
     } else {
       double L[D][MAX_M_AXIS_ND];
 #pragma unroll
@@ -193,7 +198,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       };
       for (int q = 0; q < rbase; ++q) Ps[q * NT + tid] = val(q);
 #pragma unroll
-      for (int t = 0; t < RC_RR; ++t) xr[t] = val(rbase + t);
+      for (int t = 0; t < RR; ++t) xr[t] = val(rbase + t);
     }
   };
   // sum of squares of the own column over rows > i0, chains by (row - i0 - 1) mod 4
@@ -208,7 +213,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       s2 = __fma_rn(x2, x2, s2); s3 = __fma_rn(x3, x3, s3);
     }
 #pragma unroll
-    for (int t = 0; t < RC_RR; t += 4) {
+    for (int t = 0; t < RR; t += 4) {
       const double x0 = rbase + t + 0 > i0 ? xr[t + 0] : 0.0;
       const double x1 = rbase + t + 1 > i0 ? xr[t + 1] : 0.0;
       const double x2 = rbase + t + 2 > i0 ? xr[t + 2] : 0.0;
@@ -220,10 +225,10 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
                           : __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
   };
   // own entry of row i (uniform i)
-  auto own_row = [&](int i) -> double { return i < rbase ? Ps[i * NT + tid] : rc_sel(xr, i - rbase); };
+  auto own_row = [&](int i) -> double { return i < rbase ? Ps[i * NT + tid] : rc_sel<RR>(xr, i - rbase); };
   auto publish_col = [&]() {
 #pragma unroll
-    for (int t = 0; t < RC_RR; t += 2)
+    for (int t = 0; t < RR; t += 2)
       *reinterpret_cast<double2*>(S.colbuf + rbase + t) = make_double2(xr[t], xr[t + 1]);
   };
 
@@ -233,7 +238,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
     S.jpvt[tid] = tid;
   } else {
 #pragma unroll
-    for (int t = 0; t < RC_RR; ++t) xr[t] = 0.0;
+    for (int t = 0; t < RR; ++t) xr[t] = 0.0;
   }
   int pos = have ? tid : 0x7fffffff;
   double vn1 = 0.0, vn2 = 0.0;
@@ -282,6 +287,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
           const int a = (i + 1) & 3;
           s0 = a == 0 ? xi : 0.0; s1 = a == 1 ? xi : 0.0; s2 = a == 2 ? xi : 0.0; s3 = a == 3 ? xi : 0.0;
         }
+#pragma unroll 2
         for (int g = (i + 1) & ~3; g < rbase; g += 4) {
           const double2 va = *reinterpret_cast<const double2*>(S.vh0 + g);
           const double2 vb = *reinterpret_cast<const double2*>(S.vh0 + g + 2);
@@ -291,7 +297,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
           s2 = __fma_rn(vb.x, x2, s2); s3 = __fma_rn(vb.y, x3, s3);
         }
 #pragma unroll
-        for (int t = 0; t < RC_RR; t += 4) {
+        for (int t = 0; t < RR; t += 4) {
           const double2 va = *reinterpret_cast<const double2*>(S.vh0 + rbase + t);
           const double2 vb = *reinterpret_cast<const double2*>(S.vh0 + rbase + t + 2);
           s0 = __fma_rn(va.x, xr[t + 0], s0); s1 = __fma_rn(va.y, xr[t + 1], s1);
@@ -301,6 +307,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
                                        : __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
         const double tt = -__dmul_rn(tau, w);
         pij = __dadd_rn(xi, tt);
+#pragma unroll 2
         for (int g = i & ~3; g < rbase; g += 4) {
           const double2 va = *reinterpret_cast<const double2*>(S.vh1 + g);
           const double2 vb = *reinterpret_cast<const double2*>(S.vh1 + g + 2);
@@ -312,7 +319,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
           Ps[(g + 3) * NT + tid] = __fma_rn(tt, vb.y, x3);
         }
 #pragma unroll
-        for (int t = 0; t < RC_RR; t += 4) {
+        for (int t = 0; t < RR; t += 4) {
           const double2 va = *reinterpret_cast<const double2*>(S.vh1 + rbase + t);
           const double2 vb = *reinterpret_cast<const double2*>(S.vh1 + rbase + t + 2);
           xr[t + 0] = __fma_rn(tt, va.x, xr[t + 0]); xr[t + 1] = __fma_rn(tt, va.y, xr[t + 1]);
@@ -369,7 +376,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       const int top = min(pos, rbase);
       for (int a = 0; a < top; ++a) S.r11[a * kld + pos] = Ps[a * NT + tid];
 #pragma unroll
-      for (int t = 0; t < RC_RR; ++t)
+      for (int t = 0; t < RR; ++t)
         if (rbase + t < pos) S.r11[(rbase + t) * kld + pos] = xr[t];
     }
     __syncthreads();
@@ -381,13 +388,13 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       const bool odd = (k - 1) & 1;
       if (rbase < k) {
 #pragma unroll
-        for (int t = RC_RR - 1; t >= 0; --t) {
+        for (int t = RR - 1; t >= 0; --t) {
           const int a = rbase + t;
           if (a < k) {
             double s[4] = {0.0, 0.0, 0.0, 0.0};
             const double* __restrict__ Rr = S.r11 + a * kld + rbase;
 #pragma unroll
-            for (int p2 = RC_RR / 2 - 1; 2 * p2 + 1 > t; --p2) {
+            for (int p2 = RR / 2 - 1; 2 * p2 + 1 > t; --p2) {
               const double2 rr = *reinterpret_cast<const double2*>(Rr + 2 * p2);
               s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
               if (2 * p2 > t) s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
@@ -405,7 +412,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
         const double* __restrict__ Ra = S.r11 + a * kld;
         if (rbase < k) {
 #pragma unroll
-          for (int p2 = RC_RR / 2 - 1; p2 >= 0; --p2) {
+          for (int p2 = RR / 2 - 1; p2 >= 0; --p2) {
             const double2 rr = *reinterpret_cast<const double2*>(Ra + rbase + 2 * p2);
             s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
             s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
@@ -462,12 +469,12 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
         double w = xi;
         for (int row = i + 1; row < rbase; ++row) w = __fma_rn(S.vh0[row], Ps[row * NT + tid], w);
 #pragma unroll
-        for (int t = 0; t < RC_RR; ++t) w = __fma_rn(S.vh0[rbase + t], xr[t], w);
+        for (int t = 0; t < RR; ++t) w = __fma_rn(S.vh0[rbase + t], xr[t], w);
         const double tt = -__dmul_rn(tau, w);
         for (int row = i; row < rbase; ++row)
           Ps[row * NT + tid] = __fma_rn(tt, S.vh1[row], Ps[row * NT + tid]);
 #pragma unroll
-        for (int t = 0; t < RC_RR; ++t) xr[t] = __fma_rn(tt, S.vh1[rbase + t], xr[t]);
+        for (int t = 0; t < RR; ++t) xr[t] = __fma_rn(tt, S.vh1[rbase + t], xr[t]);
       }
       __syncthreads();  // the next reflector overwrites vh0 / vh1
     }
@@ -485,7 +492,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
     double* __restrict__ G = A.G + A.g_off[v] + (size_t)(pos - k) * k;
     for (int a = 0; a < ktop; ++a) G[a] = Ps[a * NT + tid];
 #pragma unroll
-    for (int t = 0; t < RC_RR; ++t)
+    for (int t = 0; t < RR; ++t)
       if (rbase + t < k) G[rbase + t] = xr[t];
   }
   if (A.tmp_lab) {
@@ -500,14 +507,13 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   __syncthreads();
 }
 
-template <int D, int NT>
-__global__ void __launch_bounds__(NT, NT >= 256 ? 2 : NT == 128 ? 4 : 8) k_compress_rc(CompressArgs A) {
+template <int D, int NT, int RR, bool R11G>
+__global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compress_rc(CompressArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int vhn = rc_round4(A.mmax) + RC_RR + 4;
-  const int kcap = rc_round4(min(A.mmax, NT));
-  const int kld = max(rc_round4(A.mmax), RC_RR);
-  const int srows = max(0, rc_round4(A.mmax - RC_RR));
-  constexpr bool R11G = NT == 64;
+  const int vhn = rc_vhn(A.mmax, RR);
+  const int kcap = rc_kcap(A.mmax, NT);
+  const int kld = rc_kld(A.mmax, RR);
+  const int srows = rc_srows(A.mmax, RR);
   RcShared S;
   {
     double* d = reinterpret_cast<double*>(smem_raw);
@@ -519,10 +525,10 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 2 : NT == 128 ? 4 : 8) k_compr
     S.panel = d; d += (size_t)srows * NT;
     S.rdiag = d; d += rc_round4(A.mmax);
     S.nodes = d; d += 3 * MAX_M_AXIS_1D;
-    S.redv = d; d += 8;
+    S.redv = d; d += 16;
     S.misc = d; d += 8;
     int* ip = reinterpret_cast<int*>(d);
-    S.redi = ip; ip += 8;
+    S.redi = ip; ip += 16;
     S.imisc = ip; ip += 8;
     S.jpvt = ip;
   }
@@ -578,7 +584,30 @@ __global__ void __launch_bounds__(NT, NT >= 256 ? 2 : NT == 128 ? 4 : 8) k_compr
       }
     }
     __syncthreads();
-    rc_node<D, NT>(A, S, v, n, m, src, vhn, kld);
+    rc_node<D, NT, RR>(A, S, v, n, m, src, vhn, kld);
     v = next_node();
   }
 }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launch (one translation unit per point dimension: compress_rc_d{1,2,3}.cu)
+// ---------------------------------------------------------------------------
+template <int D>
+void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s) {
+  auto go = [&](auto kern) {
+    SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, v.nt, smem, s>>>(a);
+  };
+  if (v.nt == 64 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 64, 32, true>);
+  else if (v.nt == 128 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 128, 32, false>);
+  else if (v.nt == 128 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 128, 32, true>);
+  else if (v.nt == 256 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 256, 32, false>);
+  else if (v.nt == 256 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 256, 48, true>);
+  else if (v.nt == 320 && v.rr == 44 && v.r11g) go(k_compress_rc<D, 320, 44, true>);
+  else SMASH_CHECK(false, SMASH_ERR_INVALID, "no register-column kernel for this launch shape");
+  SMASH_CUDA(cudaGetLastError());
+}
+
+}  // namespace smash

@@ -1,0 +1,7 @@
+// Register-column compression kernels for 2-D points (explicit instantiation;
+// one translation unit per dimension for parallel compilation).
+#include "compress_rc.cuh"
+
+namespace smash {
+template void launch_compress_rc_dim<2>(const CompressArgs&, const RcVariant&, int, size_t, cudaStream_t);
+}  // namespace smash
