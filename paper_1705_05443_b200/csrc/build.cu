@@ -415,12 +415,7 @@ struct SideBuild {
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
-      if (ps[k].rc.nt) {  // register-column launch: global R11 slices
-        const size_t need = compress_rc_gws_doubles(ps[k].rc, a.mmax, ps[k].grid);
-        if (need) {
-          if (gws.n < need) gws.alloc(need, s);
-          a.gws = gws.p;
-        }
+      if (ps[k].rc.nt) {  // register-column launch: everything on chip
       } else if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
         size_t need = (size_t)ps[k].grid * a.mmax * a.nmax;
         if (gws.n < need) gws.alloc(need, s);

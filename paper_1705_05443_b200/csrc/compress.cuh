@@ -81,7 +81,7 @@ void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t 
 struct RcVariant {
   int nt = 0;  // 0: k_compress
   int rr = 0;
-  bool r11g = false;
+  bool r11g = false;  // R11 of the back substitution streamed four rows at a time (else resident)
 };
 __host__ __device__ inline int rc_round4(int x) { return (x + 3) & ~3; }
 __host__ __device__ inline int rc_vhn(int mmax, int rr) { return rc_round4(mmax) + rr + 4; }
@@ -89,16 +89,14 @@ __host__ __device__ inline int rc_kcap(int mmax, int nt) { return rc_round4(mmax
 // row length of R11: >= rbase + rr of every node
 __host__ __device__ inline int rc_kld(int mmax, int rr) { return rc_round4(mmax) > rr ? rc_round4(mmax) : rr; }
 __host__ __device__ inline int rc_srows(int mmax, int rr) { return mmax > rr ? rc_round4(mmax - rr) : 0; }
-inline size_t rc_r11_doubles(const RcVariant& v, int mmax) { return (size_t)rc_kcap(mmax, v.nt) * rc_kld(mmax, v.rr); }
+inline size_t rc_r11_doubles(const RcVariant& v, int mmax) {  // resident, or four streamed rows
+  return (size_t)(v.r11g ? 4 : rc_kcap(mmax, v.nt)) * rc_kld(mmax, v.rr);
+}
 inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax) {
   const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 16 + 8 +
-                   (v.r11g ? 0 : rc_r11_doubles(v, mmax)) + (size_t)rc_srows(mmax, v.rr) * v.nt;
+                   rc_r11_doubles(v, mmax) + (size_t)rc_srows(mmax, v.rr) * v.nt;
   const size_t i = 16 + 8 + (size_t)v.nt;
   return 8 * d + 4 * i + 16;
-}
-// global workspace (doubles) of a register-column launch: the R11 slices
-inline size_t compress_rc_gws_doubles(const RcVariant& v, int mmax, int grid) {
-  return v.r11g ? (size_t)grid * rc_r11_doubles(v, mmax) : 0;
 }
 void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
 template <int D>

@@ -38,7 +38,7 @@ struct RcShared {
   double* nodes;   // [3][MAX_M_AXIS_1D]
   double* redv;    // [16]
   double* misc;    // [8]
-  double* r11;     // R11, [kcap][kld], zero outside the strict upper triangle (shared or global)
+  double* r11;     // R11 [kcap][kld], or a block of four of its rows (streaming variants)
   double* panel;   // [srows][NT]
   int* redi;       // [16]
   int* imisc;      // [8]
@@ -145,7 +145,7 @@ __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, in
   }
 }
 
-template <int D, int NT, int RR>
+template <int D, int NT, int RR, bool R11G>
 __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int v, int n, int m,
                                         const NodeSrc& src, int vhn, int kld) {
   const int tid = threadIdx.x;
@@ -365,51 +365,76 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   int swaps = 0;
   while (k > 0 && k < n) {
     const int nk = n - k;
-    // R11 -> compact [a][c] array, zero outside the strict upper triangle (so the solve's
-    // aligned groups need no bounds: out-of-range terms multiply by zero)
+    // R11 as a [a][c] array, zero outside the strict upper triangle (so the solve's aligned
+    // groups need no bounds: out-of-range terms multiply by zero).  Resident variants hold
+    // all of it in shared memory; streaming variants (R11G) a block of four rows at a time,
+    // written by the thread at position c for every c (zero where R11 has no entry).
     {
-      const int tot = k * kld;
+      const int tot = R11G ? 4 * kld : k * kld;
       for (int e = tid; e < tot; e += NT) S.r11[e] = 0.0;
     }
-    __syncthreads();
-    if (have && pos < k) {
-      const int top = min(pos, rbase);
-      for (int a = 0; a < top; ++a) S.r11[a * kld + pos] = Ps[a * NT + tid];
+    if (!R11G) {
+      __syncthreads();
+      if (have && pos < k) {
+        const int top = min(pos, rbase);
+        for (int a = 0; a < top; ++a) S.r11[a * kld + pos] = Ps[a * NT + tid];
 #pragma unroll
-      for (int t = 0; t < RR; ++t)
-        if (rbase + t < pos) S.r11[(rbase + t) * kld + pos] = xr[t];
+        for (int t = 0; t < RR; ++t)
+          if (rbase + t < pos) S.r11[(rbase + t) * kld + pos] = xr[t];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     double bv = -1.0;
     int bi = 0x7fffffff;
-    if (have && pos >= k) {
-      // W = R11^-1 R12 by back substitution on the own column, the same FMA sequence as
-      // k_compress (terms k-1 .. a+1 of row a on four chains by (k-1-c) mod 4)
-      const bool odd = (k - 1) & 1;
-      if (rbase < k) {
+    const bool solver = have && pos >= k;
+    const bool writer = have && pos < kld;
+    // W = R11^-1 R12 by back substitution on the own column, the same FMA sequence as
+    // k_compress (terms k-1 .. a+1 of row a on four chains by (k-1-c) mod 4)
+    const bool odd = (k - 1) & 1;
+    if (rbase < k) {
 #pragma unroll
-        for (int t = RR - 1; t >= 0; --t) {
-          const int a = rbase + t;
-          if (a < k) {
-            double s[4] = {0.0, 0.0, 0.0, 0.0};
-            const double* __restrict__ Rr = S.r11 + a * kld + rbase;
+      for (int t = RR - 1; t >= 0; --t) {
+        const int a = rbase + t;
+        if (R11G && (t & 3) == 3 && a - 3 < k) {  // next block of four register rows
+          __syncthreads();
+          if (writer) {
 #pragma unroll
-            for (int p2 = RR / 2 - 1; 2 * p2 + 1 > t; --p2) {
-              const double2 rr = *reinterpret_cast<const double2*>(Rr + 2 * p2);
-              s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
-              if (2 * p2 > t) s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
-            }
-            const double comb = odd ? __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]))
-                                    : __dadd_rn(__dadd_rn(s[1], s[2]), __dadd_rn(s[3], s[0]));
-            const double x = __ddiv_rn(__dadd_rn(xr[t], comb), S.rdiag[a]);
-            xr[t] = x;
-            argmax_combine(bv, bi, fabs(x), a * nk + (pos - k));
+            for (int r = 0; r < 4; ++r)
+              S.r11[r * kld + pos] = (pos > a - 3 + r && pos < k) ? xr[t - 3 + r] : 0.0;
           }
+          __syncthreads();
+        }
+        if (a < k && solver) {
+          double s[4] = {0.0, 0.0, 0.0, 0.0};
+          const double* __restrict__ Rr = S.r11 + (R11G ? (t & 3) : a) * kld + rbase;
+#pragma unroll
+          for (int p2 = RR / 2 - 1; 2 * p2 + 1 > t; --p2) {
+            const double2 rr = *reinterpret_cast<const double2*>(Rr + 2 * p2);
+            s[(2 * p2 + 1) & 3] = __fma_rn(-xr[2 * p2 + 1], rr.y, s[(2 * p2 + 1) & 3]);
+            if (2 * p2 > t) s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
+          }
+          const double comb = odd ? __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]))
+                                  : __dadd_rn(__dadd_rn(s[1], s[2]), __dadd_rn(s[3], s[0]));
+          const double x = __ddiv_rn(__dadd_rn(xr[t], comb), S.rdiag[a]);
+          xr[t] = x;
+          argmax_combine(bv, bi, fabs(x), a * nk + (pos - k));
         }
       }
-      for (int a = ktop - 1; a >= 0; --a) {
+    }
+    for (int a = ktop - 1; a >= 0; --a) {
+      if (R11G && ((a & 3) == 3 || a == ktop - 1)) {  // next block of four shared rows
+        const int a0 = a & ~3;
+        __syncthreads();
+        if (writer) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            S.r11[r * kld + pos] = (a0 + r < ktop && pos > a0 + r && pos < k) ? Ps[(a0 + r) * NT + tid] : 0.0;
+        }
+        __syncthreads();
+      }
+      if (solver) {
         double s[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* __restrict__ Ra = S.r11 + a * kld;
+        const double* __restrict__ Ra = S.r11 + (R11G ? (a & 3) : a) * kld;
         if (rbase < k) {
 #pragma unroll
           for (int p2 = RR / 2 - 1; p2 >= 0; --p2) {
@@ -418,6 +443,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
             s[(2 * p2) & 3] = __fma_rn(-xr[2 * p2], rr.x, s[(2 * p2) & 3]);
           }
         }
+#pragma unroll 2
         for (int g = (ktop - 1) & ~3; g + 3 > a; g -= 4) {
           const double2 r01 = *reinterpret_cast<const double2*>(Ra + g);
           const double2 r23 = *reinterpret_cast<const double2*>(Ra + g + 2);
@@ -520,8 +546,7 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
     S.vh0 = d; d += vhn;
     S.vh1 = d; d += vhn;
     S.colbuf = d; d += vhn;
-    if (R11G) S.r11 = A.gws + (size_t)blockIdx.x * kcap * kld;
-    else { S.r11 = d; d += (size_t)kcap * kld; }
+    S.r11 = d; d += R11G ? (size_t)4 * kld : (size_t)kcap * kld;
     S.panel = d; d += (size_t)srows * NT;
     S.rdiag = d; d += rc_round4(A.mmax);
     S.nodes = d; d += 3 * MAX_M_AXIS_1D;
@@ -584,7 +609,7 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
       }
     }
     __syncthreads();
-    rc_node<D, NT, RR>(A, S, v, n, m, src, vhn, kld);
+    rc_node<D, NT, RR, R11G>(A, S, v, n, m, src, vhn, kld);
     v = next_node();
   }
 }
