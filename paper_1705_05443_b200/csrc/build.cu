@@ -415,7 +415,12 @@ struct SideBuild {
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
-      if (ps[k].rc.nt) {  // register-column launch: everything on chip
+      if (ps[k].rc.nt) {  // register-column launch: everything on chip but the clusters' position tables
+        const size_t need = compress_rc_gws_doubles(ps[k].rc, ps[k].grid);
+        if (need) {
+          if (gws.n < need) gws.alloc(need, s);
+          a.gws = gws.p;
+        }
       } else if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
         size_t need = (size_t)ps[k].grid * a.mmax * a.nmax;
         if (gws.n < need) gws.alloc(need, s);
@@ -443,7 +448,7 @@ struct SideBuild {
                   nn ? (double)cols / nn : 0.0, nn ? ms * 1e3 * ps[k].grid / nn : 0.0);
         }
         fprintf(stderr, "compress launch: %s nodes %d class (%d, %d] nmax %d mmax %d threads %d grid %d smem %zu cap %lld: %.3f ms\n",
-                ps[k].rc.nt ? (ps[k].rc.rr > 32 ? "rc48" : "rc") : "sm", cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
+                ps[k].rc.nt ? (ps[k].rc.cs > 1 ? "rcc" : ps[k].rc.rr > 32 ? "rc48" : "rc") : "sm", cnt, a.n_lo, a.n_hi, a.nmax, a.mmax, a.threads, ps[k].grid, ps[k].smem, (long long)a.panel_cap, ms);
         cudaEventDestroy(e0); cudaEventDestroy(e1);
       }
     }

@@ -485,16 +485,19 @@ static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) 
   const int nmax = P.a.nmax, mmax = P.a.mmax;
   RcVariant cand[2];
   int nc = 0;
-  if (nmax <= 64) cand[nc++] = {64, 32, true};
+  if (nmax <= 64) { cand[nc++] = {64, mmax > 96 ? 48 : 32, true}; }
   else if (nmax <= 128) { cand[nc++] = {128, 32, false}; cand[nc++] = {128, 32, true}; }
   else if (nmax <= 256) { cand[nc++] = {256, 32, false}; cand[nc++] = {256, 48, true}; }
   else if (nmax <= 320) cand[nc++] = {320, 44, true};
+  else if (nmax <= 1024) cand[nc++] = {256, 48, true, 4};  // cluster of four CTAs
   for (int c = 0; c < nc; ++c) {
     const size_t smem = compress_rc_smem_bytes(cand[c], mmax);
     if ((int64_t)smem > (int64_t)smem_limit) continue;
-    const int by_regs = cand[c].rr > 32 ? 1 : 65536 / (cand[c].nt * 128);  // __launch_bounds__ of k_compress_rc
+    // __launch_bounds__ of k_compress_rc: 128 registers per thread, up to 255 with > 32 register rows
+    const int by_regs = cand[c].rr > 32 ? std::max(1, 65536 / (cand[c].nt * 256)) : 65536 / (cand[c].nt * 128);
     const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
     P.grid = std::min(cnt, nsm * std::min(by_regs, by_smem));
+    if (cand[c].cs > 1) P.grid = std::max(1, std::min(cnt, nsm / cand[c].cs)) * cand[c].cs;
     P.smem = smem;
     P.rc = cand[c];
     P.a.threads = cand[c].nt;
@@ -514,9 +517,9 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
     if (plan_compress_rc(out[0], cnt, smem_limit, nsm)) return 1;
   }
   if (rc && split && cnt > nsm && A0.nmax > 64) {
-    // size classes (.., 64], (64, 128], (128, 256], (256, 320] on the register-column kernel as
-    // far as its variants fit, one k_compress launch for the rest
-    const int rb[4] = {64, 128, 256, 320};
+    // size classes (.., 64], (64, 128], (128, 256], (256, 320], (320, 1024] on the
+    // register-column kernel as far as its variants fit, one k_compress launch for the rest
+    const int rb[5] = {64, 128, 256, 320, 1024};
     int np = 0, lo = -1;
     for (int b : rb) {
       if (lo >= A0.nmax) break;

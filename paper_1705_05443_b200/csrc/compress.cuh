@@ -82,6 +82,7 @@ struct RcVariant {
   int nt = 0;  // 0: k_compress
   int rr = 0;
   bool r11g = false;  // R11 of the back substitution streamed four rows at a time (else resident)
+  int cs = 1;         // thread-block cluster size: a node's columns spread over cs CTAs
 };
 __host__ __device__ inline int rc_round4(int x) { return (x + 3) & ~3; }
 __host__ __device__ inline int rc_vhn(int mmax, int rr) { return rc_round4(mmax) + rr + 4; }
@@ -93,10 +94,14 @@ inline size_t rc_r11_doubles(const RcVariant& v, int mmax) {  // resident, or fo
   return (size_t)(v.r11g ? 4 : rc_kcap(mmax, v.nt)) * rc_kld(mmax, v.rr);
 }
 inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax) {
-  const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 16 + 8 +
+  const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 32 + 8 +
                    rc_r11_doubles(v, mmax) + (size_t)rc_srows(mmax, v.rr) * v.nt;
-  const size_t i = 16 + 8 + (size_t)v.nt;
+  const size_t i = 32 + 8 + (size_t)v.nt;
   return 8 * d + 4 * i + 16;
+}
+// global workspace (doubles) of a register-column launch: the clusters' position tables
+inline size_t compress_rc_gws_doubles(const RcVariant& v, int grid) {
+  return v.cs > 1 ? (size_t)grid * v.nt / 2 + 1 : 0;
 }
 void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
 template <int D>

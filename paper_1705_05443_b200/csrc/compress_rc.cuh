@@ -22,6 +22,8 @@
 
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "compress_common.cuh"
 
 namespace smash {
@@ -29,6 +31,7 @@ namespace {
 
 using namespace qr;
 using namespace cmn;
+namespace cg = cooperative_groups;
 
 struct RcShared {
   double* vh0;     // reflector of the current step, zero at rows <= i   [vhn]
@@ -36,13 +39,34 @@ struct RcShared {
   double* colbuf;  // published register rows of the pivot column       [vhn]
   double* rdiag;   // [mmax]
   double* nodes;   // [3][MAX_M_AXIS_1D]
-  double* redv;    // [16]
+  double* redv;    // [32]
   double* misc;    // [8]
   double* r11;     // R11 [kcap][kld], or a block of four of its rows (streaming variants)
   double* panel;   // [srows][NT]
-  int* redi;       // [16]
+  int* redi;       // [32]
   int* imisc;      // [8]
-  int* jpvt;       // [NT]
+  int* jpvt;       // position -> column, [NT] (clusters: a global slice of CS * NT)
+};
+
+// The same shared arrays in every CTA of the cluster (CS = 1: the CTA itself).  Wide nodes
+// (|ibar| <= CS * NT) are spread over a thread-block cluster, NT columns per CTA: the pivot
+// candidates, the reflector and the streamed R11 rows are written into every CTA's shared
+// memory (DSMEM), and the barriers that order them become cluster barriers.
+template <int CS>
+struct RcPeers {
+  double* vh0[CS];
+  double* vh1[CS];
+  double* misc[CS];
+  double* rdiag[CS];
+  double* redv[CS];
+  double* r11[CS];
+  int* redi[CS];
+  int* imisc[CS];
+  int crank = 0;
+  __device__ __forceinline__ void sync() const {
+    if constexpr (CS > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  }
 };
 
 // x[s] for a CTA-uniform s: a tree of selects per block of 16 registers instead of a
@@ -78,9 +102,10 @@ __device__ __forceinline__ double rc_sel(const double (&x)[RR], int s) {
 // "none": their bit patterns order like unsigned integers, so each warp reduces with three
 // redux.sync operations (high word, low word among the leaders, smallest index among the
 // equals) instead of five shuffle rounds.  Returns the index, the value through v.
-template <int NT>
-__device__ __forceinline__ int rc_argmax(double& v, int i, RcShared& S) {
+template <int NT, int CS>
+__device__ __forceinline__ int rc_argmax(double& v, int i, RcShared& S, const RcPeers<CS>& P) {
   constexpr int NW = NT / 32;
+  static_assert(CS * NW <= 32, "one lane per warp partial of the cluster");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool valid = v >= 0.0;
   const unsigned long long key = valid ? (unsigned long long)__double_as_longlong(v) : 0ULL;
@@ -88,29 +113,51 @@ __device__ __forceinline__ int rc_argmax(double& v, int i, RcShared& S) {
   const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
   const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
   const unsigned mi = __reduce_min_sync(0xffffffffu, (valid && hi == mh && lo == ml) ? (unsigned)i : 0x7fffffffu);
-  if (lane == 0) {
-    reinterpret_cast<unsigned long long*>(S.redv)[wid] = ((unsigned long long)mh << 32) | ml;
-    S.redi[wid] = (int)mi;
-  }
-  __syncthreads();
-  unsigned long long bk = reinterpret_cast<const unsigned long long*>(S.redv)[0];
-  int bi = S.redi[0];
+  if constexpr (CS == 1) {
+    if (lane == 0) {
+      reinterpret_cast<unsigned long long*>(S.redv)[wid] = ((unsigned long long)mh << 32) | ml;
+      S.redi[wid] = (int)mi;
+    }
+    __syncthreads();
+    unsigned long long bk = reinterpret_cast<const unsigned long long*>(S.redv)[0];
+    int bi = S.redi[0];
 #pragma unroll
-  for (int w = 1; w < NW; ++w) {
-    const unsigned long long ok = reinterpret_cast<const unsigned long long*>(S.redv)[w];
-    const int oi = S.redi[w];
-    if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+    for (int w = 1; w < NW; ++w) {
+      const unsigned long long ok = reinterpret_cast<const unsigned long long*>(S.redv)[w];
+      const int oi = S.redi[w];
+      if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+    }
+    v = bi == 0x7fffffff ? -1.0 : __longlong_as_double((long long)bk);
+    return bi;
+  } else {
+    // every warp's partial goes to every CTA; after the cluster barrier one lane per
+    // partial and three more redux operations
+    const int slot = P.crank * NW + wid;
+#pragma unroll
+    for (int q = 0; q < CS; ++q)  // (static peer index: the pointer arrays stay in registers)
+      if (lane == q) {
+        reinterpret_cast<unsigned long long*>(P.redv[q])[slot] = ((unsigned long long)mh << 32) | ml;
+        P.redi[q][slot] = (int)mi;
+      }
+    P.sync();
+    const bool on = lane < CS * NW;
+    const unsigned long long k2 = on ? reinterpret_cast<const unsigned long long*>(S.redv)[lane] : 0ULL;
+    const int i2 = on ? S.redi[lane] : 0x7fffffff;
+    const unsigned h2 = (unsigned)(k2 >> 32), l2 = (unsigned)k2;
+    const unsigned gh = __reduce_max_sync(0xffffffffu, h2);
+    const unsigned gl = __reduce_max_sync(0xffffffffu, h2 == gh ? l2 : 0u);
+    const unsigned gi = __reduce_min_sync(0xffffffffu, (h2 == gh && l2 == gl) ? (unsigned)i2 : 0x7fffffffu);
+    v = gi == 0x7fffffffu ? -1.0 : __longlong_as_double((long long)(((unsigned long long)gh << 32) | gl));
+    return (int)gi;
   }
-  v = bi == 0x7fffffff ? -1.0 : __longlong_as_double((long long)bk);
-  return bi;
 }
 
 // dlarfg on the published pivot column c at step i, by one warp (the owner's), as
 // qr::householder: the lane-strided sum of squares, beta / tau / scal, the scaled
 // reflector to vh0 / vh1.
-template <int NT>
+template <int NT, int CS>
 __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, int rbase, int m, int i,
-                                               int c, RcShared& S) {
+                                               int c, RcShared& S, const RcPeers<CS>& P) {
   const int lane = threadIdx.x & 31;
   const double* __restrict__ pc = Ps + c;
   const double* __restrict__ cb = S.colbuf;
@@ -131,24 +178,28 @@ __device__ __forceinline__ void rc_householder(const double* __restrict__ Ps, in
 #pragma unroll 1
     for (int row = i + 1 + lane; row < m; row += 32) {
       const double x = __dmul_rn(scal, row < rbase ? pc[row * NT] : cb[row]);
-      S.vh0[row] = x;
-      S.vh1[row] = x;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) { P.vh0[q][row] = x; P.vh1[q][row] = x; }
     }
     diag = beta;
   }
-  if (lane == 0) {
-    S.vh0[i] = 0.0;
-    S.vh1[i] = 1.0;
-    if (i > 0) S.vh1[i - 1] = 0.0;
-    S.misc[0] = tau;
-    S.rdiag[i] = diag;
-  }
+#pragma unroll
+  for (int q = 0; q < CS; ++q)
+    if (lane == q) {
+      P.vh0[q][i] = 0.0;
+      P.vh1[q][i] = 1.0;
+      if (i > 0) P.vh1[q][i - 1] = 0.0;
+      P.misc[q][0] = tau;
+      P.rdiag[q][i] = diag;
+    }
 }
 
-template <int D, int NT, int RR, bool R11G>
-__device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int v, int n, int m,
-                                        const NodeSrc& src, int vhn, int kld) {
+template <int D, int NT, int RR, bool R11G, int CS>
+__device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, const RcPeers<CS>& P, int v,
+                                        int n, int m, const NodeSrc& src, int vhn, int kld) {
+  static_assert(CS == 1 || R11G, "clusters stream R11");
   const int tid = threadIdx.x;
+  const int gcol = P.crank * NT + tid;  // the own column of ibar
   const int rbase = max(0, rc_round4(m - RR));
   double* __restrict__ Ps = S.panel;
 #ifdef SMASH_COMPRESS_PROF
@@ -157,7 +208,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
 #else
 #define RC_MARK(k)
 #endif
-  const bool have = tid < n;
+  const bool have = gcol < n;
   double xr[RR];
 
   // ---- own column of the panel (smash/lowrank.py:103-144; HSS rows hss.py:287)
@@ -166,9 +217,9 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
     const int mt = A.tab.m;
     double x[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) x[a] = src.base[(size_t)a * src.stride + tid];
+    for (int a = 0; a < D; ++a) x[a] = src.base[(size_t)a * src.stride + gcol];
     const int kp = m - r;
-    const double* sv = kp > 0 ? A.sv + A.sv_off[v] + (size_t)tid * kp : nullptr;
+    const double* sv = kp > 0 ? A.sv + A.sv_off[v] + (size_t)gcol * kp : nullptr;
     if (D == 1) {
       const double* nd = S.nodes;
       bool exact = false;
@@ -235,12 +286,12 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   for (int e = tid; e < vhn; e += NT) { S.vh0[e] = 0.0; S.vh1[e] = 0.0; S.colbuf[e] = 0.0; }
   if (have) {
     build_col();
-    S.jpvt[tid] = tid;
+    S.jpvt[gcol] = gcol;
   } else {
 #pragma unroll
     for (int t = 0; t < RR; ++t) xr[t] = 0.0;
   }
-  int pos = have ? tid : 0x7fffffff;
+  int pos = have ? gcol : 0x7fffffff;
   double vn1 = 0.0, vn2 = 0.0;
   double cv = -1.0;
   int cp = 0x7fffffff;
@@ -254,22 +305,22 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   RC_MARK(0)
   // ---- dgeqp3 / dlaqp2 (two barriers per pivot step: pivot choice, reflector)
   for (int i = 0; i < kmax; ++i) {
-    int pp = rc_argmax<NT>(cv, cp, S);
+    int pp = rc_argmax<NT, CS>(cv, cp, S, P);
     if (pp >= n) pp = i;  // (all candidates NaN)
     RC_MARK(1)
     // the column at position pp becomes pivot i, the column at position i takes its place
     // (each of the two threads records itself in the position -> column table)
     const bool owner = have && pos == pp;
-    if (have && pos == i) { pos = pp; S.jpvt[pp] = tid; }
-    if (owner) { pos = i; S.jpvt[i] = tid; }
+    if (have && pos == i) { pos = pp; S.jpvt[pp] = gcol; }
+    if (owner) { pos = i; S.jpvt[i] = gcol; }
     const unsigned own_mask = __ballot_sync(0xffffffffu, owner);
     if (own_mask) {  // the owner's warp: publish the register rows, then dlarfg
       if (owner) publish_col();
       __syncwarp();
-      rc_householder<NT>(Ps, rbase, m, i, (tid & ~31) + (__ffs(own_mask) - 1), S);
+      rc_householder<NT, CS>(Ps, rbase, m, i, (tid & ~31) + (__ffs(own_mask) - 1), S, P);
     }
     RC_MARK(2)
-    __syncthreads();
+    P.sync();
     RC_MARK(3)
     cv = -1.0;
     cp = 0x7fffffff;
@@ -396,13 +447,16 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
       for (int t = RR - 1; t >= 0; --t) {
         const int a = rbase + t;
         if (R11G && (t & 3) == 3 && a - 3 < k) {  // next block of four register rows
-          __syncthreads();
+          P.sync();
           if (writer) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-              S.r11[r * kld + pos] = (pos > a - 3 + r && pos < k) ? xr[t - 3 + r] : 0.0;
+            for (int r = 0; r < 4; ++r) {
+              const double val = (pos > a - 3 + r && pos < k) ? xr[t - 3 + r] : 0.0;
+#pragma unroll
+              for (int q = 0; q < CS; ++q) P.r11[q][r * kld + pos] = val;
+            }
           }
-          __syncthreads();
+          P.sync();
         }
         if (a < k && solver) {
           double s[4] = {0.0, 0.0, 0.0, 0.0};
@@ -424,13 +478,16 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
     for (int a = ktop - 1; a >= 0; --a) {
       if (R11G && ((a & 3) == 3 || a == ktop - 1)) {  // next block of four shared rows
         const int a0 = a & ~3;
-        __syncthreads();
+        P.sync();
         if (writer) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-            S.r11[r * kld + pos] = (a0 + r < ktop && pos > a0 + r && pos < k) ? Ps[(a0 + r) * NT + tid] : 0.0;
+          for (int r = 0; r < 4; ++r) {
+            const double val = (a0 + r < ktop && pos > a0 + r && pos < k) ? Ps[(a0 + r) * NT + tid] : 0.0;
+#pragma unroll
+            for (int q = 0; q < CS; ++q) P.r11[q][r * kld + pos] = val;
+          }
         }
-        __syncthreads();
+        P.sync();
       }
       if (solver) {
         double s[4] = {0.0, 0.0, 0.0, 0.0};
@@ -459,36 +516,35 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
         argmax_combine(bv, bi, fabs(x), a * nk + (pos - k));
       }
     }
-    bi = rc_argmax<NT>(bv, bi, S);
+    bi = rc_argmax<NT, CS>(bv, bi, S, P);
     RC_MARK(5)
     if (!(bv > A.s_bound)) break;
     if (swaps >= MAX_SWAPS) {
       if (tid == 0) atomicOr(A.err, DEV_SWAP_CAP);
       break;
     }
-    if (tid == 0) {
-      const int a = bi / nk, jj = bi % nk;
-      const int ca = S.jpvt[a], cb = S.jpvt[k + jj];
-      S.jpvt[a] = cb;
-      S.jpvt[k + jj] = ca;
-      S.imisc[1] = ca; S.imisc[2] = cb; S.imisc[3] = a; S.imisc[5] = k + jj;
+    {
+      const int sa = bi / nk, sj = bi % nk;
+      const int ca = S.jpvt[sa], cb = S.jpvt[k + sj];
+      P.sync();  // every thread has read the two table entries
+      if (gcol == 0) { S.jpvt[sa] = cb; S.jpvt[k + sj] = ca; }
+      for (int e = tid; e < vhn; e += NT) { S.vh0[e] = 0.0; S.vh1[e] = 0.0; }
+      P.sync();
+      if (gcol == ca) pos = k + sj;
+      if (gcol == cb) pos = sa;
     }
-    for (int e = tid; e < vhn; e += NT) { S.vh0[e] = 0.0; S.vh1[e] = 0.0; }
-    __syncthreads();
-    if (tid == S.imisc[1]) pos = S.imisc[5];
-    if (tid == S.imisc[2]) pos = S.imisc[3];
     ++swaps;
     if (have) build_col();
     // unpivoted QR (dgeqr2) of the permuted panel; rows < k of R suffice.  Sequential
     // dot-product order, as k_compress's refactorisation.
     for (int i = 0; i < k; ++i) {
       const int c = S.jpvt[i];
-      if ((tid >> 5) == (c >> 5)) {
-        if (tid == c) publish_col();
+      if ((gcol >> 5) == (c >> 5)) {  // the owner's warp (of the owner's CTA)
+        if (gcol == c) publish_col();
         __syncwarp();
-        rc_householder<NT>(Ps, rbase, m, i, c, S);
+        rc_householder<NT, CS>(Ps, rbase, m, i, c - P.crank * NT, S, P);
       }
-      __syncthreads();
+      P.sync();
       const double tau = S.misc[0];
       if (have && pos > i && tau != 0.0) {
         const double xi = own_row(i);
@@ -502,18 +558,18 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
 #pragma unroll
         for (int t = 0; t < RR; ++t) xr[t] = __fma_rn(tt, S.vh1[rbase + t], xr[t]);
       }
-      __syncthreads();  // the next reflector overwrites vh0 / vh1
+      P.sync();  // the next reflector overwrites vh0 / vh1
     }
     RC_MARK(6)
   }
   __syncthreads();
   // ---- outputs
-  if (tid == 0) {
+  if (gcol == 0) {
     A.rank[v] = k;
     if (swaps) atomicAdd(A.swaps, (unsigned long long)swaps);
   }
   const int64_t io = A.ib_off[v];
-  if (have) A.perm[io + tid] = S.jpvt[tid];
+  if (have) A.perm[io + gcol] = S.jpvt[gcol];
   if (k > 0 && k < n && have && pos >= k) {
     double* __restrict__ G = A.G + A.g_off[v] + (size_t)(pos - k) * k;
     for (int a = 0; a < ktop; ++a) G[a] = Ps[a * NT + tid];
@@ -523,17 +579,17 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, int 
   }
   if (A.tmp_lab) {
     const int64_t lo = io - A.ib_level_base;
-    if (tid < k) {
-      const int pc = S.jpvt[tid];
-      A.tmp_lab[lo + tid] = src.lab ? src.lab[pc] : src.lab0 + pc;
+    if (gcol < k) {
+      const int pc = S.jpvt[gcol];
+      A.tmp_lab[lo + gcol] = src.lab ? src.lab[pc] : src.lab0 + pc;
       for (int d = 0; d < D; ++d)
-        A.tmp_pts[(size_t)d * A.tmp_stride + lo + tid] = src.base[(size_t)d * src.stride + pc];
+        A.tmp_pts[(size_t)d * A.tmp_stride + lo + gcol] = src.base[(size_t)d * src.stride + pc];
     }
   }
   __syncthreads();
 }
 
-template <int D, int NT, int RR, bool R11G>
+template <int D, int NT, int RR, bool R11G, int CS>
 __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compress_rc(CompressArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int vhn = rc_vhn(A.mmax, RR);
@@ -550,33 +606,59 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
     S.panel = d; d += (size_t)srows * NT;
     S.rdiag = d; d += rc_round4(A.mmax);
     S.nodes = d; d += 3 * MAX_M_AXIS_1D;
-    S.redv = d; d += 16;
+    S.redv = d; d += 32;
     S.misc = d; d += 8;
     int* ip = reinterpret_cast<int*>(d);
-    S.redi = ip; ip += 16;
+    S.redi = ip; ip += 32;
     S.imisc = ip; ip += 8;
     S.jpvt = ip;
   }
+  RcPeers<CS> P;
+  if constexpr (CS > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    P.crank = (int)cl.block_rank();
+#pragma unroll
+    for (int q = 0; q < CS; ++q) {
+      P.vh0[q] = cl.map_shared_rank(S.vh0, q);
+      P.vh1[q] = cl.map_shared_rank(S.vh1, q);
+      P.misc[q] = cl.map_shared_rank(S.misc, q);
+      P.rdiag[q] = cl.map_shared_rank(S.rdiag, q);
+      P.redv[q] = cl.map_shared_rank(S.redv, q);
+      P.r11[q] = cl.map_shared_rank(S.r11, q);
+      P.redi[q] = cl.map_shared_rank(S.redi, q);
+      P.imisc[q] = cl.map_shared_rank(S.imisc, q);
+    }
+    // position -> column table of the cluster's node: a global slice
+    S.jpvt = reinterpret_cast<int*>(A.gws) + (size_t)(blockIdx.x / CS) * (CS * NT);
+  } else {
+    P.vh0[0] = S.vh0; P.vh1[0] = S.vh1; P.misc[0] = S.misc; P.rdiag[0] = S.rdiag;
+    P.redv[0] = S.redv; P.r11[0] = S.r11; P.redi[0] = S.redi; P.imisc[0] = S.imisc;
+  }
   const int tid = threadIdx.x;
+  const int nteams = (int)gridDim.x / CS;  // CTAs (clusters) claiming nodes
   auto next_node = [&]() {
-    __syncthreads();
-    if (tid == 0) S.imisc[4] = A.lb + (int)gridDim.x + atomicAdd(A.next, 1);
-    __syncthreads();
+    P.sync();
+    if (P.crank == 0 && tid == 0) {
+      const int nv = A.lb + nteams + atomicAdd(A.next, 1);
+#pragma unroll
+      for (int q = 0; q < CS; ++q) P.imisc[q][4] = nv;
+    }
+    P.sync();
     return S.imisc[4];
   };
-  for (int v = A.lb + blockIdx.x; v < A.le;) {
+  for (int v = A.lb + (int)blockIdx.x / CS; v < A.le;) {
     const int n = A.nib[v];
     if (n <= A.n_lo || n > A.n_hi) {  // another launch of this level takes this size class
       v = next_node();
       continue;
     }
     if (n == 0) {
-      if (tid == 0) A.rank[v] = 0;
+      if (P.crank == 0 && tid == 0) A.rank[v] = 0;
       v = next_node();
       continue;
     }
     const int m = A.r + (A.keep ? A.keep[v] : 0);
-    SMASH_DASSERT(n <= NT && m <= A.mmax);
+    SMASH_DASSERT(n <= CS * NT && m <= A.mmax);
     const NodeSrc src = node_src(A, v);
     // ---- padded box + Chebyshev nodes (hss.py:39-45, lowrank.py:103-105,127-134)
     if (tid == 0) {
@@ -609,9 +691,10 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
       }
     }
     __syncthreads();
-    rc_node<D, NT, RR, R11G>(A, S, v, n, m, src, vhn, kld);
+    rc_node<D, NT, RR, R11G, CS>(A, S, P, v, n, m, src, vhn, kld);
     v = next_node();
   }
+  P.sync();  // (clusters: no CTA leaves while a peer may still write into its shared memory)
 }
 
 }  // namespace
@@ -623,14 +706,33 @@ template <int D>
 void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s) {
   auto go = [&](auto kern) {
     SMASH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, v.nt, smem, s>>>(a);
+    if (v.cs > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3((unsigned)v.nt);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)v.cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      SMASH_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+      kern<<<grid, v.nt, smem, s>>>(a);
+    }
   };
-  if (v.nt == 64 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 64, 32, true>);
-  else if (v.nt == 128 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 128, 32, false>);
-  else if (v.nt == 128 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 128, 32, true>);
-  else if (v.nt == 256 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 256, 32, false>);
-  else if (v.nt == 256 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 256, 48, true>);
-  else if (v.nt == 320 && v.rr == 44 && v.r11g) go(k_compress_rc<D, 320, 44, true>);
+  if (v.cs == 4 && v.nt == 256 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 256, 48, true, 4>);
+  else if (v.cs != 1) SMASH_CHECK(false, SMASH_ERR_INVALID, "no register-column cluster kernel for this launch shape");
+  else if (v.nt == 64 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 64, 32, true, 1>);
+  else if (v.nt == 64 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 64, 48, true, 1>);
+  else if (v.nt == 128 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 128, 32, false, 1>);
+  else if (v.nt == 128 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 128, 32, true, 1>);
+  else if (v.nt == 256 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 256, 32, false, 1>);
+  else if (v.nt == 256 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 256, 48, true, 1>);
+  else if (v.nt == 320 && v.rr == 44 && v.r11g) go(k_compress_rc<D, 320, 44, true, 1>);
   else SMASH_CHECK(false, SMASH_ERR_INVALID, "no register-column kernel for this launch shape");
   SMASH_CUDA(cudaGetLastError());
 }
