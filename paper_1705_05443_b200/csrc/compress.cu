@@ -490,20 +490,25 @@ static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) 
   else if (nmax <= 256) { cand[nc++] = {256, 32, false}; cand[nc++] = {256, 48, true}; }
   else if (nmax <= 320) cand[nc++] = {320, 44, true};
   else if (nmax <= 1024) cand[nc++] = {256, 48, true, 4};  // cluster of four CTAs
+  // the fitting variant with the most CTAs per SM (ties: the first, resident R11 before streamed)
+  int best = -1, best_per_sm = 0;
+  size_t best_smem = 0;
   for (int c = 0; c < nc; ++c) {
     const size_t smem = compress_rc_smem_bytes(cand[c], mmax);
     if ((int64_t)smem > (int64_t)smem_limit) continue;
     // __launch_bounds__ of k_compress_rc: 128 registers per thread, up to 255 with > 32 register rows
     const int by_regs = cand[c].rr > 32 ? std::max(1, 65536 / (cand[c].nt * 256)) : 65536 / (cand[c].nt * 128);
     const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
-    P.grid = std::min(cnt, nsm * std::min(by_regs, by_smem));
-    if (cand[c].cs > 1) P.grid = std::max(1, std::min(cnt, nsm / cand[c].cs)) * cand[c].cs;
-    P.smem = smem;
-    P.rc = cand[c];
-    P.a.threads = cand[c].nt;
-    return true;
+    const int per_sm = std::min(by_regs, by_smem);
+    if (per_sm > best_per_sm) { best = c; best_per_sm = per_sm; best_smem = smem; }
   }
-  return false;
+  if (best < 0) return false;
+  P.grid = std::min(cnt, nsm * best_per_sm);
+  if (cand[best].cs > 1) P.grid = std::max(1, std::min(cnt, nsm / cand[best].cs)) * cand[best].cs;
+  P.smem = best_smem;
+  P.rc = cand[best];
+  P.a.threads = cand[best].nt;
+  return true;
 }
 
 int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int nsm, CompressPass* out) {

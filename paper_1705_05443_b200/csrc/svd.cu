@@ -394,13 +394,17 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
           double* ja = J + (size_t)a * kp;
           double* jb = J + (size_t)b * kp;
           double ga = 0;
+          long long jt0 = 0, jt1 = 0, jt2 = 0;
+          if (dbg) jt0 = clock64();
           for (int r = gl; r < kp; r += 8) ga = fma(ja[r], jb[r], ga);
           ga = grp_sum(ga, gm);
+          if (dbg) jt1 = clock64();
           const double al = nrm[a], be = nrm[b];
           if (ga * ga > 1e-30 * (al * be) && ga != 0.0) {
             const double zeta = (be - al) / (2.0 * ga);
             const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             const double c = rsqrt(1.0 + t * t), s = c * t;
+            if (dbg) jt2 = clock64();
             double* va = V + (size_t)a * kp;
             double* vb = V + (size_t)b * kp;
             for (int r = gl; r < kp; r += 8) {
@@ -417,9 +421,16 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
               nrm[b] = be + t * ga;
               S.imisc[2] = 1;
             }
+            if (dbg && tid == 0) {
+              const long long jt3 = clock64();
+              A.dbg[34] += jt1 - jt0; A.dbg[35] += jt2 - jt1; A.dbg[36] += jt3 - jt2; A.dbg[38] += 1;
+            }
           }
         }
+        long long jb0 = 0;
+        if (dbg && tid == 0) jb0 = clock64();
         __syncthreads();
+        if (dbg && tid == 0) { A.dbg[37] += clock64() - jb0; A.dbg[39] += 1; }
       }
       if (S.imisc[2] == 0) break;
       __syncthreads();
@@ -664,7 +675,9 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
     for (int q = 0; q < 4; ++q)
       fprintf(stderr, " [asm %lld qr %lld qr2 %lld jac %lld back %lld kp %lld keep %lld n.nn %lld]", h[q * 8], h[q * 8 + 1],
               h[q * 8 + 2], h[q * 8 + 3], h[q * 8 + 4], h[q * 8 + 5], h[q * 8 + 6], h[q * 8 + 7]);
-    fprintf(stderr, " max_sweeps %lld capped %lld\n", h[32], h[33]);
+    fprintf(stderr, " max_sweeps %lld capped %lld | jacobi (thread 0 of traced nodes): dot %.0f scalar %.0f rotate %.0f per rotation (%lld), barrier wait %.0f per round (%lld)\n", h[32], h[33],
+            h[38] ? (double)h[34] / h[38] : 0.0, h[38] ? (double)h[35] / h[38] : 0.0, h[38] ? (double)h[36] / h[38] : 0.0, h[38],
+            h[39] ? (double)h[37] / h[39] : 0.0, h[39]);
   }
   return hk;
 }
