@@ -8,8 +8,10 @@ sys.path.insert(0, ".")
 import paper_1705_05443_b200 as sg
 from paper_1705_05443_b200.workloads import CONFIGS, build_params, make_points
 
+VAR = os.environ.get("AB_VAR", "SMASH_COMPRESS_RC")  # the switch under test (value 0 / 1)
+
 def build(cfg, N, rc):
-    os.environ["SMASH_COMPRESS_RC"] = str(rc)
+    os.environ[VAR] = str(rc)
     c = CONFIGS[cfg]
     X, Y, _ = make_points(cfg, N=N)
     spec, params = build_params(cfg)
@@ -49,8 +51,8 @@ for arg in sys.argv[1:]:
                 diffs.append("%s: %d of %d entries differ in bits (%d in value, max abs %.3e)" % (k, ne, x.size, nz, np.max(np.abs(x - y))))
         elif not np.array_equal(x, y):
             diffs.append("%s: %d of %d entries differ" % (k, int(np.sum(x != y)), x.size))
-    print("cfg%d N=%s: swaps %s / %s, build %.2f ms (k_compress) vs %.2f ms (k_compress_rc): %s" % (
-        cfg, N, sa, sb, ta * 1e3, tb * 1e3, "IDENTICAL" if not diffs else "DIFFERENT"))
+    print("cfg%d N=%s: swaps %s / %s, build %.2f ms (%s=0) vs %.2f ms (%s=1): %s" % (
+        cfg, N, sa, sb, ta * 1e3, VAR, tb * 1e3, VAR, "IDENTICAL" if not diffs else "DIFFERENT"))
     for d in diffs:
         print("   ", d)
     bad += bool(diffs)
