@@ -485,7 +485,8 @@ static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) 
   const int nmax = P.a.nmax, mmax = P.a.mmax;
   RcVariant cand[2];
   int nc = 0;
-  if (nmax <= 64) { cand[nc++] = {64, mmax > 96 ? 48 : 32, true}; }
+  if (nmax <= 32) { cand[nc++] = {32, mmax > 96 ? 48 : 32, true}; }
+  else if (nmax <= 64) { cand[nc++] = {64, mmax > 96 ? 48 : 32, true}; }
   else if (nmax <= 128) { cand[nc++] = {128, 32, false}; cand[nc++] = {128, 32, true}; }
   else if (nmax <= 256) { cand[nc++] = {256, 32, false}; cand[nc++] = {256, 48, true}; }
   else if (nmax <= 320) cand[nc++] = {320, 44, true};
@@ -494,10 +495,10 @@ static bool plan_compress_rc(CompressPass& P, int cnt, int smem_limit, int nsm) 
   int best = -1, best_per_sm = 0;
   size_t best_smem = 0;
   for (int c = 0; c < nc; ++c) {
-    const size_t smem = compress_rc_smem_bytes(cand[c], mmax);
+    const size_t smem = compress_rc_smem_bytes(cand[c], mmax, P.a.dim);
     if ((int64_t)smem > (int64_t)smem_limit) continue;
     // __launch_bounds__ of k_compress_rc: 128 registers per thread, up to 255 with > 32 register rows
-    const int by_regs = cand[c].rr > 32 ? std::max(1, 65536 / (cand[c].nt * 256)) : 65536 / (cand[c].nt * 128);
+    const int by_regs = cand[c].rr > 32 ? std::max(1, 65536 / (cand[c].nt * 256)) : std::min(16, 65536 / (cand[c].nt * 128));
     const int by_smem = (int)std::max<size_t>(1, SM_BYTES / (smem + CTA_RESERVED));
     const int per_sm = std::min(by_regs, by_smem);
     if (per_sm > best_per_sm) { best = c; best_per_sm = per_sm; best_smem = smem; }
@@ -516,15 +517,15 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
   // (read per call: tests switch between the two kernels within a process)
   const bool rc = !(getenv("SMASH_COMPRESS_RC") && atoi(getenv("SMASH_COMPRESS_RC")) == 0) &&
                   !A0.Cexp && compress_chains4();
-  if (rc && (!split || cnt <= nsm || A0.nmax <= 64)) {
+  if (rc && (!split || cnt <= nsm || A0.nmax <= 32)) {
     out[0] = CompressPass();
     out[0].a = A0;
     if (plan_compress_rc(out[0], cnt, smem_limit, nsm)) return 1;
   }
-  if (rc && split && cnt > nsm && A0.nmax > 64) {
-    // size classes (.., 64], (64, 128], (128, 256], (256, 320], (320, 1024] on the
+  if (rc && split && cnt > nsm && A0.nmax > 32) {
+    // size classes (.., 32], (32, 64], (64, 128], (128, 256], (256, 320], (320, 1024] on the
     // register-column kernel as far as its variants fit, one k_compress launch for the rest
-    const int rb[5] = {64, 128, 256, 320, 1024};
+    const int rb[6] = {32, 64, 128, 256, 320, 1024};
     int np = 0, lo = -1;
     for (int b : rb) {
       if (lo >= A0.nmax) break;

@@ -93,8 +93,10 @@ __host__ __device__ inline int rc_srows(int mmax, int rr) { return mmax > rr ? r
 inline size_t rc_r11_doubles(const RcVariant& v, int mmax) {  // resident, or four streamed rows
   return (size_t)(v.r11g ? 4 : rc_kcap(mmax, v.nt)) * rc_kld(mmax, v.rr);
 }
-inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax) {
-  const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + 3 * MAX_M_AXIS_1D + 32 + 8 +
+// Chebyshev nodes per axis: up to 128 in 1-D, 16 per axis in 2-D / 3-D
+__host__ __device__ constexpr int rc_nodes_stride(int dim) { return dim == 1 ? MAX_M_AXIS_1D : MAX_M_AXIS_ND; }
+inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax, int dim) {
+  const size_t d = 3 * (size_t)rc_vhn(mmax, v.rr) + rc_round4(mmax) + dim * rc_nodes_stride(dim) + 32 + 8 +
                    rc_r11_doubles(v, mmax) + (size_t)rc_srows(mmax, v.rr) * v.nt;
   const size_t i = 32 + 8 + (size_t)v.nt;
   return 8 * d + 4 * i + 16;
@@ -107,7 +109,7 @@ void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, siz
 template <int D>
 void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
 
-constexpr int MAX_COMPRESS_PASSES = 6;
+constexpr int MAX_COMPRESS_PASSES = 7;
 struct CompressPass {
   CompressArgs a;
   int grid = 0;

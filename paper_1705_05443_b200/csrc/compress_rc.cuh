@@ -38,7 +38,7 @@ struct RcShared {
   double* vh1;     // the same with a one at row i (dlarf's v)           [vhn]
   double* colbuf;  // published register rows of the pivot column       [vhn]
   double* rdiag;   // [mmax]
-  double* nodes;   // [3][MAX_M_AXIS_1D]
+  double* nodes;   // Chebyshev nodes per axis, [D][rc_nodes_stride(D)]
   double* redv;    // [32]
   double* misc;    // [8]
   double* r11;     // R11 [kcap][kld], or a block of four of its rows (streaming variants)
@@ -239,7 +239,7 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, cons
     } else {
       double L[D][MAX_M_AXIS_ND];
 #pragma unroll
-      for (int a = 0; a < D; ++a) lagrange_axis(x[a], S.nodes + a * MAX_M_AXIS_1D, A.tab.wv, mt, L[a]);
+      for (int a = 0; a < D; ++a) lagrange_axis(x[a], S.nodes + a * rc_nodes_stride(D), A.tab.wv, mt, L[a]);
       auto val = [&](int q) -> double {
         if (q >= r) return q < m ? sv[q - r] : 0.0;
         const int* o = A.tab.order + 3 * q;
@@ -590,7 +590,8 @@ __device__ __forceinline__ void rc_node(const CompressArgs& A, RcShared& S, cons
 }
 
 template <int D, int NT, int RR, bool R11G, int CS>
-__global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compress_rc(CompressArgs A) {
+__global__ void __launch_bounds__(NT, RR > 32 ? 1 : (65536 / (NT * 128) > 16 ? 16 : 65536 / (NT * 128)))
+k_compress_rc(CompressArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int vhn = rc_vhn(A.mmax, RR);
   const int kcap = rc_kcap(A.mmax, NT);
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
     S.r11 = d; d += R11G ? (size_t)4 * kld : (size_t)kcap * kld;
     S.panel = d; d += (size_t)srows * NT;
     S.rdiag = d; d += rc_round4(A.mmax);
-    S.nodes = d; d += 3 * MAX_M_AXIS_1D;
+    S.nodes = d; d += D * rc_nodes_stride(D);
     S.redv = d; d += 32;
     S.misc = d; d += 8;
     int* ip = reinterpret_cast<int*>(d);
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(NT, RR > 32 ? 1 : 65536 / (NT * 128)) k_compre
         double lo = S.misc[2 + a], hi = S.misc[5 + a];
         double t1 = __dmul_rn(0.5, __dadd_rn(lo, hi));
         double t2 = __dmul_rn(0.5, __dsub_rn(hi, lo));
-        S.nodes[a * MAX_M_AXIS_1D + k] = __dadd_rn(t1, __dmul_rn(t2, A.tab.cosv[k]));
+        S.nodes[a * rc_nodes_stride(D) + k] = __dadd_rn(t1, __dmul_rn(t2, A.tab.cosv[k]));
       }
     }
     __syncthreads();
@@ -726,6 +727,8 @@ void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid,
   };
   if (v.cs == 4 && v.nt == 256 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 256, 48, true, 4>);
   else if (v.cs != 1) SMASH_CHECK(false, SMASH_ERR_INVALID, "no register-column cluster kernel for this launch shape");
+  else if (v.nt == 32 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 32, 32, true, 1>);
+  else if (v.nt == 32 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 32, 48, true, 1>);
   else if (v.nt == 64 && v.rr == 32 && v.r11g) go(k_compress_rc<D, 64, 32, true, 1>);
   else if (v.nt == 64 && v.rr == 48 && v.r11g) go(k_compress_rc<D, 64, 48, true, 1>);
   else if (v.nt == 128 && v.rr == 32 && !v.r11g) go(k_compress_rc<D, 128, 32, false, 1>);
