@@ -226,6 +226,39 @@ int num_sms() {
 }  // namespace
 
 // Level-synchronous compression state of one side (row or column factors).
+// Streams and events for the concurrent size-class launches of a level, pooled per device
+// and handed to one SideBuild at a time.
+struct PassResources {
+  int dev = 0;
+  cudaStream_t st[MAX_COMPRESS_PASSES] = {};
+  cudaEvent_t ev[MAX_COMPRESS_PASSES + 1] = {};  // completion events, [MAX_COMPRESS_PASSES]: the fork
+  static std::mutex& mu() { static std::mutex m; return m; }
+  static std::vector<PassResources*>& pool() { static std::vector<PassResources*> p; return p; }
+  static PassResources* acquire() {
+    int dev = 0;
+    SMASH_CUDA(cudaGetDevice(&dev));
+    {
+      std::lock_guard<std::mutex> g(mu());
+      auto& p = pool();
+      for (size_t i = 0; i < p.size(); ++i)
+        if (p[i]->dev == dev) {
+          PassResources* r = p[i];
+          p.erase(p.begin() + i);
+          return r;
+        }
+    }
+    PassResources* r = new PassResources();
+    r->dev = dev;
+    for (cudaStream_t& x : r->st) SMASH_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : r->ev) SMASH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return r;
+  }
+  static void release(PassResources* r) {  // (its work was joined into the build's stream)
+    std::lock_guard<std::mutex> g(mu());
+    pool().push_back(r);
+  }
+};
+
 struct SideBuild {
   MatrixImpl* M;
   int side;
@@ -256,6 +289,10 @@ struct SideBuild {
   std::vector<int64_t> lvl_ib_b, lvl_g_b, lvl_ib_base;
   std::vector<int> lvl_nmax_b;
   DBuf<int> d_used;
+  PassResources* pres = nullptr;  // streams / events of a level's size-class launches
+  ~SideBuild() {
+    if (pres) PassResources::release(pres);
+  }
 
   void init() {
     TreeImpl* t = M->tree;
@@ -410,23 +447,53 @@ struct SideBuild {
     compact_level(l, tmp_lab.p, tmp_pts.p, lvl_ib);
   }
 
+  // The size-class launches of a level are independent: each runs on its own stream
+  // (forked from s, joined back into s), so their tails overlap.  The streams and events
+  // come from a per-device pool (creating them costs more than a small level's sweep).
+  cudaStream_t pass_stream(int k) {
+    if (!pres) pres = PassResources::acquire();
+    return pres->st[k];
+  }
+  cudaEvent_t pass_event(int k) {
+    if (!pres) pres = PassResources::acquire();
+    return pres->ev[k];
+  }
+
   void launch_level(CompressArgs& A, int cnt) {
     CompressPass ps[MAX_COMPRESS_PASSES];
     const int np = plan_compress_passes(A, cnt, smem_limit, nsm, ps);
+    static const bool dbg = getenv("SMASH_COMPRESS_DBG") != nullptr;
+#ifdef SMASH_COMPRESS_PROF
+    const bool conc = false;
+#else
+    // (small levels: the fork / join costs more than the overlapping tails save)
+    static const bool serial = getenv("SMASH_COMPRESS_SERIAL") != nullptr;
+    static const int conc_min = getenv("SMASH_COMPRESS_CONC_MIN") ? atoi(getenv("SMASH_COMPRESS_CONC_MIN")) : 0;
+    const bool conc = np > 1 && !dbg && !serial && cnt >= conc_min;
+#endif
+    // global workspace: one slice per launch (clusters' position tables, global/L2 panels)
+    size_t need[MAX_COMPRESS_PASSES], tot = 0;
+    for (int k = 0; k < np; ++k) {
+      const CompressArgs& a = ps[k].a;
+      need[k] = ps[k].rc.nt ? compress_rc_gws_doubles(ps[k].rc, ps[k].grid)
+                            : a.panel_cap < (int64_t)a.nmax * a.mmax ? (size_t)ps[k].grid * a.mmax * a.nmax : 0;
+      tot += need[k];
+    }
+    if (tot && gws.n < tot) gws.alloc(tot, s);
+    if (conc) SMASH_CUDA(cudaEventRecord(pass_event(MAX_COMPRESS_PASSES), s));
+    size_t goff = 0;
     for (int k = 0; k < np; ++k) {
       CompressArgs& a = ps[k].a;
-      if (ps[k].rc.nt) {  // register-column launch: everything on chip but the clusters' position tables
-        const size_t need = compress_rc_gws_doubles(ps[k].rc, ps[k].grid);
-        if (need) {
-          if (gws.n < need) gws.alloc(need, s);
-          a.gws = gws.p;
-        }
-      } else if (a.panel_cap < (int64_t)a.nmax * a.mmax) {  // some nodes may need the global workspace
-        size_t need = (size_t)ps[k].grid * a.mmax * a.nmax;
-        if (gws.n < need) gws.alloc(need, s);
-        a.gws = gws.p;
+      if (need[k]) { a.gws = gws.p + goff; goff += need[k]; }
+      if (conc) {
+        cudaStream_t sk = pass_stream(k);
+        SMASH_CUDA(cudaStreamWaitEvent(sk, pass_event(MAX_COMPRESS_PASSES), 0));
+        if (ps[k].rc.nt) launch_compress_rc(a, ps[k].rc, ps[k].grid, ps[k].smem, sk, k);
+        else launch_compress(a, ps[k].grid, ps[k].smem, sk, k);
+        SMASH_CUDA(cudaEventRecord(pass_event(k), sk));
+        SMASH_CUDA(cudaStreamWaitEvent(s, pass_event(k), 0));
+        continue;
       }
-      static const bool dbg = getenv("SMASH_COMPRESS_DBG") != nullptr;
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (dbg) {
         cudaEventCreate(&e0); cudaEventCreate(&e1);

@@ -584,16 +584,16 @@ int plan_compress_passes(const CompressArgs& A0, int cnt, int smem_limit, int ns
 #ifdef SMASH_COMPRESS_PROF
 __device__ unsigned long long g_compress_prof[8];
 #endif
-__device__ int g_compress_next;  // dynamic node counter (reset before every launch)
+__device__ int g_compress_next[MAX_COMPRESS_PASSES + 1];  // dynamic node counters (one per concurrent launch, reset before it)
 
-void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s) {
+void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream_t s, int slot) {
   CompressArgs a = a_in;
   a.chains4 = compress_chains4();
   {
     void* nx = nullptr;
     SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));
-    SMASH_CUDA(cudaMemsetAsync(nx, 0, sizeof(int), s));
-    a.next = reinterpret_cast<int*>(nx);
+    a.next = reinterpret_cast<int*>(nx) + slot;
+    SMASH_CUDA(cudaMemsetAsync(a.next, 0, sizeof(int), s));
   }
 #ifdef SMASH_COMPRESS_PROF
   void* pp = nullptr;
@@ -628,13 +628,13 @@ void launch_compress(const CompressArgs& a_in, int grid, size_t smem, cudaStream
 #endif
 }
 
-void launch_compress_rc(const CompressArgs& a_in, const RcVariant& v, int grid, size_t smem, cudaStream_t s) {
+void launch_compress_rc(const CompressArgs& a_in, const RcVariant& v, int grid, size_t smem, cudaStream_t s, int slot) {
   CompressArgs a = a_in;
   a.chains4 = true;
   void* nx = nullptr;
   SMASH_CUDA(cudaGetSymbolAddress(&nx, g_compress_next));
-  SMASH_CUDA(cudaMemsetAsync(nx, 0, sizeof(int), s));
-  a.next = reinterpret_cast<int*>(nx);
+  a.next = reinterpret_cast<int*>(nx) + slot;
+  SMASH_CUDA(cudaMemsetAsync(a.next, 0, sizeof(int), s));
 #ifdef SMASH_COMPRESS_PROF
   void* pp = nullptr;
   SMASH_CUDA(cudaGetSymbolAddress(&pp, g_compress_prof));

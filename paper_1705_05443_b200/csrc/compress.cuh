@@ -75,7 +75,8 @@ size_t compress_smem_bytes(int nmax, int mmax, bool panel_in_smem);
 // Launch plan of a level: sets A.panel_cap, returns the dynamic shared memory
 // per CTA and the grid (persistent CTAs over the level's cnt nodes).
 size_t plan_compress_launch(CompressArgs& A, int cnt, int smem_limit, int nsm, int* grid);
-void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s);
+// slot: the node counter of this launch (launches of one level may run concurrently)
+void launch_compress(const CompressArgs& a, int grid, size_t smem, cudaStream_t s, int slot = 0);
 // Register-column kernel (compress_rc.cuh): CTA size = maximum columns, rows kept in
 // registers, R11 of the back substitution in shared memory or in a global/L2 slice.
 struct RcVariant {
@@ -105,7 +106,7 @@ inline size_t compress_rc_smem_bytes(const RcVariant& v, int mmax, int dim) {
 inline size_t compress_rc_gws_doubles(const RcVariant& v, int grid) {
   return v.cs > 1 ? (size_t)grid * v.nt / 2 + 1 : 0;
 }
-void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
+void launch_compress_rc(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s, int slot = 0);
 template <int D>
 void launch_compress_rc_dim(const CompressArgs& a, const RcVariant& v, int grid, size_t smem, cudaStream_t s);
 
