@@ -64,3 +64,42 @@ def test_register_column_kernel_equals_k_compress(sg, cfg, N):
             assert np.array_equal(x.view(np.int64), y.view(np.int64)), k
         else:
             assert np.array_equal(x, y), k
+
+
+def _build_points(sg, X, cfg, rc):
+    from paper_1705_05443_b200.workloads import CONFIGS, build_params
+    old = os.environ.get("SMASH_COMPRESS_RC")
+    os.environ["SMASH_COMPRESS_RC"] = "1" if rc else "0"
+    try:
+        c = CONFIGS[cfg]
+        spec, params = build_params(cfg)
+        tree = sg.build_tree(sg.PointSet(X), nu0=c["nu0"], mode=c["mode"], tau=c["tau"])
+        M = sg.build_h2(tree, spec, None, None, params)
+        out = {"%d_%s" % (s, k): np.asarray(v) for s in (0, 1) for k, v in M.export_side(s).items()}
+        return out, M.swaps
+    finally:
+        if old is None:
+            os.environ.pop("SMASH_COMPRESS_RC", None)
+        else:
+            os.environ["SMASH_COMPRESS_RC"] = old
+
+
+@pytest.mark.parametrize("cfg,dim", [(3, 3), (5, 2)])
+def test_register_column_kernel_ragged_levels(sg, cfg, dim):
+    """Adaptive trees: narrow and wide nodes on the same level (a level launched whole on the
+    cluster kernel holds nodes that fill one of its four CTAs only), duplicated points
+    (rank-deficient panels: the back substitution and swap loop of the small classes)."""
+    rng = np.random.default_rng(100 + cfg)
+    n = 20000
+    blob = 0.5 + 0.01 * rng.standard_normal((n // 2, dim))
+    X = np.vstack([rng.random((n // 2 - 200, dim)), blob, np.repeat(rng.random((20, dim)), 10, axis=0)])
+    a, sa = _build_points(sg, X, cfg, rc=False)
+    b, sb = _build_points(sg, X, cfg, rc=True)
+    assert sa == sb
+    for k in a:
+        x, y = a[k], b[k]
+        assert x.shape == y.shape, k
+        if x.dtype.kind == "f":
+            assert np.array_equal(x.view(np.int64), y.view(np.int64)), k
+        else:
+            assert np.array_equal(x, y), k
