@@ -23,6 +23,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "qr_device.cuh"
@@ -36,9 +37,10 @@ using namespace qr;
 
 constexpr int SVD_THREADS = 256;
 constexpr int MAX_NEAR = 64;
-// shared-memory area (doubles) for B = R_k^T, then J / V, then the back-transform Y
-// (96 KB: two CTAs per SM; J + V fit up to rank 78)
-constexpr int SVD_BIG = 12288;
+// The shared-memory work area (SvdArgs::big doubles) holds the panel A while it is
+// factored, then B = R_k^T, then J, then the back-transform Y: about 96 KB where two CTAs
+// share an SM, up to the whole SM on levels of few nodes and in the HYB kernel.
+constexpr size_t SVD_SMEM_MAX = 227 * 1024;
 
 struct IbarSide {
   const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
@@ -71,6 +73,14 @@ struct SvdArgs {
   double* gws;
   int64_t gws_stride;  // doubles per CTA
   int nmax, nnmax;
+  int big;  // doubles in the shared-memory work area
+  int gq0;  // all-shared group-column QR allowed (SMASH_SVD_GQ0)
+  // split launch (wide HYB levels): mode 1 = assembly + pivoted QR only (HYB kernel, one CTA
+  // per SM), mode 2 = the later phases only (two CTAs per SM); the panel, kp and the taus of
+  // each node pass through a per-node workspace.  mode 0 = everything in one launch.
+  int mode, ws_lb;
+  int* kp_g;
+  double* taus_g;
   int* err;
   long long* dbg;  // SMASH_SVD_DBG: phase cycle counts of block 0's first nodes
 };
@@ -160,12 +170,457 @@ __device__ __forceinline__ double grp_reflect(double* c, int m, int i, double ta
   return ci + t;
 }
 
-template <int KER, int D>
-__global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
+// ---- Group-column pivoted QR (panels of at most 128 x 256).  The 8-lane group g owns the
+// physical columns g + 32 k (k < 8) for the whole factorisation, lane gl rows gl + 8 q
+// (q < NQ): columns k < KR live in registers, the others in shared memory (column stride
+// = 8 mod 16 doubles: the four groups of a warp fall on the two halves of the banks).
+// KR = 2 holds config 4's 128 x 256 leaf blocks (256 KB) on chip with one CTA per SM;
+// KR = 0 is the all-shared layout of the smaller panels (two CTAs per SM).
+// No column ever moves: the pivot order is a position per column (posof).  Every update
+// also leaves the EXACT squared norm of each column's remaining rows in vn1 and its next
+// row entry in arow, so a pivot step needs no reduction for the reflector: with the pivot
+// known, every thread forms beta = -sign(alpha) sqrt(norm^2), tau and the scaling itself,
+// reads the raw pivot column straight from its shared-memory home (a register column is
+// staged by its owner first) and updates its group's columns two at a time (independent
+// dot products and reductions interleaved).  Two barriers per step: after the update and
+// inside the argmax; dlaqp2's norm downdating (divisions, square roots, re-summing under
+// cancellation) is not needed.  The owner writes the scaled reflector and beta into the
+// pivot column after the update barrier, when nobody reads the raw column any more.  At the
+// end the columns are written to W in position order, the layout the later phases expect.
+constexpr int HQ_KC = 8;
+constexpr int HQ_ROWS = 128;
+constexpr int HQ_LDC = 136;
+constexpr int HQ_BIG = (HQ_KC - 2) * 32 * HQ_LDC;  // doubles of shared column storage, KR = 2
+
+template <int NQ>
+__device__ __forceinline__ double grp_sel(const double (&x)[NQ], int sq) {
+  // x[sq] for a CTA-uniform sq: a tree of selects on the bits of sq (a chain of compares
+  // is turned into a dynamically indexed local array by the compiler)
+  static_assert(NQ <= 16, "select tree over 16 register rows");
+  double a[8], b[4], c[2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const double lo = 2 * t < NQ ? x[2 * t < NQ ? 2 * t : 0] : 0.0;
+    const double hi = 2 * t + 1 < NQ ? x[2 * t + 1 < NQ ? 2 * t + 1 : 0] : 0.0;
+    a[t] = (sq & 1) ? hi : lo;
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) b[t] = (sq & 2) ? a[2 * t + 1] : a[2 * t];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) c[t] = (sq & 4) ? b[2 * t + 1] : b[2 * t];
+  return (sq & 8) ? c[1] : c[0];
+}
+
+template <int K, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (K > 0) {
+    static_for<K - 1>(f);
+    f(std::integral_constant<int, K - 1>{});
+  }
+}
+
+template <int KER, int D, int KR, int NQ>
+__device__ __forceinline__ int group_qr(const SvdArgs& A, Shared& S, double* sh, int ldc, double* arow,
+                                        double* W, double* taus, int n, int nn, int nnear,
+                                        const int* near_start, const double* const* near_base,
+                                        const int64_t* near_stride, const double* tb, int64_t ts,
+                                        double floor_v) {
+  static_assert(KR == 0 || KR == 2, "register columns are the two named arrays below");
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int g8 = tid >> 3, gl = tid & 7;
+  const unsigned gm = 0xffu << (lane & ~7);
+  int* posof = S.jpvt;
+  double cr0[NQ], cr1[NQ];
+  // column k of the group: registers (k < KR) or shared memory
+  auto col_load = [&](auto kc, double (&x)[NQ]) __attribute__((always_inline)) {
+    constexpr int k = decltype(kc)::value;
+    if constexpr (k < KR && k == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = cr0[q];
+    } else if constexpr (k < KR && k == 1) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = cr1[q];
+    } else {
+      const double* c = sh + (size_t)((k - KR) * 32 + g8) * ldc;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = c[gl + 8 * q];
+    }
+  };
+  auto col_store = [&](auto kc, const double (&x)[NQ]) __attribute__((always_inline)) {
+    constexpr int k = decltype(kc)::value;
+    if constexpr (k < KR && k == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) cr0[q] = x[q];
+    } else if constexpr (k < KR && k == 1) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) cr1[q] = x[q];
+    } else {
+      double* c = sh + (size_t)((k - KR) * 32 + g8) * ldc;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) c[gl + 8 * q] = x[q];
+    }
+  };
+  // the same for a CTA-uniform runtime k (the pivot's owner): a pointer for the shared
+  // columns, selects between the register columns
+  auto col_load_dyn = [&](int k, double (&x)[NQ]) __attribute__((always_inline)) {
+    if (k >= KR) {
+      const double* c = sh + (size_t)((k - KR) * 32 + g8) * ldc;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = c[gl + 8 * q];
+    } else if constexpr (KR > 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = k == 0 ? cr0[q] : cr1[q];
+    }
+  };
+  auto col_store_dyn = [&](int k, const double (&x)[NQ]) __attribute__((always_inline)) {
+    if (k >= KR) {
+      double* c = sh + (size_t)((k - KR) * 32 + g8) * ldc;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) c[gl + 8 * q] = x[q];
+    } else if constexpr (KR > 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        cr0[q] = k == 0 ? x[q] : cr0[q];
+        cr1[q] = k == 0 ? cr1[q] : x[q];
+      }
+    }
+  };
+  // (max norm, smallest column) over the CTA: warp shuffles, one partial per warp, the
+  // caller's barrier, then every thread folds the partials
+  auto argmax_put = [&](double bv, int bi) __attribute__((always_inline)) {
+    for (int off = 16; off; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      argmax_combine(bv, bi, ov, oi);
+    }
+    if (lane == 0) { S.redv[wid] = bv; S.redi[wid] = bi; }
+  };
+  auto argmax_get = [&]() __attribute__((always_inline)) {
+    double bv = S.redv[0];
+    int bi = S.redi[0];
+    for (int w = 1; w < nw; ++w) argmax_combine(bv, bi, S.redv[w], S.redi[w]);
+    return bi;
+  };
+  // ---- assemble the group's columns, initial norms
+  static_for<HQ_KC>([&](auto kc) __attribute__((always_inline)) {
+    constexpr int k = decltype(kc)::value;
+    const int j = g8 + 32 * k;
+    if (32 * k >= nn && k >= KR) return;
+    double x[NQ];
+    double s0 = 0.0;
+    if (j < nn) {
+      int g = 0;
+      while (g + 1 < nnear && near_start[g + 1] <= j) ++g;
+      const int bl = j - near_start[g];
+      double y[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = gl + 8 * q;
+        double xr[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) xr[d] = tb[(int64_t)d * ts + min(r, n - 1)];
+        const double val = A.transpose ? kval<KER, D>(y, xr, A.dx) : kval<KER, D>(xr, y, A.dx);
+        x[q] = r < n ? val : 0.0;
+        s0 = fma(x[q], x[q], s0);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) x[q] = 0.0;
+    }
+    col_store(kc, x);
+    const double nr2 = grp_sum(s0, gm);
+    if (gl == 0 && j < nn) {
+      S.vn1[j] = nr2;  // squared norm of the remaining rows
+      arow[j] = x[0];
+    }
+  });
+  if (tid < nn) posof[tid] = -1;
+  __syncthreads();
+  argmax_put(tid < nn ? S.vn1[tid] : -1.0, tid < nn ? tid : 0x7fffffff);
+  __syncthreads();
+  int pvt = argmax_get();
+  // a register pivot column is staged raw in S.vh by its owner
+  auto stage_pivot = [&]() __attribute__((always_inline)) {
+    if constexpr (KR > 0) {
+      if (pvt < 32 * KR) {  // CTA-uniform
+        if (g8 == (pvt & 31)) {
+          double x[NQ];
+          col_load_dyn(pvt >> 5, x);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            if (gl + 8 * q < n) S.vh[gl + 8 * q] = x[q];
+        }
+        __syncthreads();
+      }
+    }
+  };
+  stage_pivot();
+  const int kmax = min(n, nn);
+  int kp = 0, nsteps = 0;
+  double r0 = 0.0;
+  const bool gdbg = A.dbg && blockIdx.x == 0 && tid == 0;
+  long long gt0 = 0, gt1 = 0, gt2 = 0;
+  for (int i = 0; i < kmax; ++i) {
+    if (gdbg) gt0 = clock64();
+    // ---- dlarfg scalars of the pivot column, by every thread
+    const int og = pvt & 31, ok = pvt >> 5;
+    const double alpha = arow[pvt], n2 = S.vn1[pvt];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (n - i > 1 && n2 > alpha * alpha) {
+      beta = -copysign(__dsqrt_rn(n2), alpha);
+      tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+      scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
+    }
+    asm volatile("" : "+d"(tau), "+d"(beta), "+d"(scal));  // (no rematerialisation in the loops below)
+    if (i == 0) r0 = fabs(beta);
+    if (g8 == og && gl == 0) {
+      posof[pvt] = i;
+      taus[i] = tau;
+    }
+    __syncwarp(gm);
+    nsteps = i + 1;
+    if (r0 == 0.0 || !(fabs(beta) > floor_v * r0)) {
+      // the column stays unscaled: the later phases read the first kp = i rows only
+      break;
+    }
+    kp = i + 1;
+    double vv[NQ];
+    {
+      const double* pc = (KR > 0 && pvt < 32 * KR) ? S.vh : sh + (size_t)(pvt - 32 * KR) * ldc;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = gl + 8 * q;
+        const double pq = pc[min(r, n - 1)];  // (unconditional load: no branch per row)
+        vv[q] = (tau != 0.0 && r > i && r < n) ? pq * scal : (r == i ? 1.0 : 0.0);
+      }
+    }
+    // ---- H_i applied to the group's columns, two at a time; exact remaining norms
+    static_for<HQ_KC / 2>([&](auto bc) __attribute__((always_inline)) {
+      constexpr int k0 = 2 * decltype(bc)::value;
+      if (32 * k0 >= nn) return;  // CTA-uniform: no column of this pair exists
+      const std::integral_constant<int, k0> ka;
+      const std::integral_constant<int, k0 + 1> kb;
+      const int ja = g8 + 32 * k0, jb = ja + 32;
+      const bool acta = ja < nn && posof[ja] < 0, actb = jb < nn && posof[jb] < 0;
+      if (!acta && !actb) return;
+      double xa[NQ], xb[NQ];
+      col_load(ka, xa);
+      if (32 * (k0 + 1) < nn) {  // CTA-uniform: the pair's second column slot exists
+        col_load(kb, xb);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) xb[q] = 0.0;
+      }
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int q = 0; q + 1 < NQ; q += 2) {
+        a0 = fma(vv[q], xa[q], a0);
+        b0 = fma(vv[q], xb[q], b0);
+        a1 = fma(vv[q + 1], xa[q + 1], a1);
+        b1 = fma(vv[q + 1], xb[q + 1], b1);
+      }
+      if constexpr (NQ & 1) {
+        a0 = fma(vv[NQ - 1], xa[NQ - 1], a0);
+        b0 = fma(vv[NQ - 1], xb[NQ - 1], b0);
+      }
+      double wa = a0 + a1, wb = b0 + b1;
+      wa += __shfl_xor_sync(gm, wa, 4);
+      wb += __shfl_xor_sync(gm, wb, 4);
+      wa += __shfl_xor_sync(gm, wa, 2);
+      wb += __shfl_xor_sync(gm, wb, 2);
+      wa += __shfl_xor_sync(gm, wa, 1);
+      wb += __shfl_xor_sync(gm, wb, 1);
+      const double ta = acta ? -tau * wa : 0.0, tb2 = actb ? -tau * wb : 0.0;
+      a0 = a1 = b0 = b1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        xa[q] = fma(ta, vv[q], xa[q]);
+        xb[q] = fma(tb2, vv[q], xb[q]);
+        const bool below = gl + 8 * q > i;
+        const double ya = below ? xa[q] : 0.0, yb = below ? xb[q] : 0.0;
+        if (q & 1) {
+          a1 = fma(ya, ya, a1);
+          b1 = fma(yb, yb, b1);
+        } else {
+          a0 = fma(ya, ya, a0);
+          b0 = fma(yb, yb, b0);
+        }
+      }
+      if (acta) col_store(ka, xa);
+      if (actb) col_store(kb, xb);
+      double na = a0 + a1, nb = b0 + b1;
+      na += __shfl_xor_sync(gm, na, 4);
+      nb += __shfl_xor_sync(gm, nb, 4);
+      na += __shfl_xor_sync(gm, na, 2);
+      nb += __shfl_xor_sync(gm, nb, 2);
+      na += __shfl_xor_sync(gm, na, 1);
+      nb += __shfl_xor_sync(gm, nb, 1);
+      if (gl == ((i + 1) & 7)) {
+        if (acta) {
+          arow[ja] = grp_sel<NQ>(xa, (i + 1) >> 3);
+          S.vn1[ja] = na;
+        }
+        if (actb) {
+          arow[jb] = grp_sel<NQ>(xb, (i + 1) >> 3);
+          S.vn1[jb] = nb;
+        }
+      }
+    });
+    __syncthreads();
+    if (gdbg) gt1 = clock64();
+    // ---- the owner stores the scaled reflector and beta in the pivot column
+    if (g8 == og && tau != 0.0) {
+      double x[NQ];
+      col_load_dyn(ok, x);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = gl + 8 * q;
+        x[q] = r > i ? vv[q] : (r == i ? beta : x[q]);
+      }
+      col_store_dyn(ok, x);
+    }
+    if (i + 1 == kmax) break;
+    // ---- next pivot: largest remaining norm
+    const bool live = tid < nn && posof[tid] < 0;
+    argmax_put(live ? S.vn1[tid] : -1.0, live ? tid : 0x7fffffff);
+    __syncthreads();
+    pvt = argmax_get();
+    stage_pivot();
+    if (gdbg) {
+      gt2 = clock64();
+      A.dbg[40] += gt1 - gt0; A.dbg[42] += gt2 - gt1; A.dbg[43] += 1;
+    }
+  }
+  __syncthreads();
+  // ---- positions of the columns never chosen (after the pivoted ones, in column order)
+  {
+    const bool rest = tid < nn && posof[tid] < 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, rest);
+    if (lane == 0) S.redi[wid] = __popc(bal);
+    __syncthreads();
+    int base = nsteps;
+    for (int w = 0; w < wid; ++w) base += S.redi[w];
+    if (rest) posof[tid] = base + __popc(bal & ((1u << lane) - 1u));
+    __syncthreads();
+  }
+  static_for<HQ_KC>([&](auto kc) __attribute__((always_inline)) {
+    constexpr int k = decltype(kc)::value;
+    const int j = g8 + 32 * k;
+    if (j >= nn) return;
+    double x[NQ];
+    col_load(kc, x);
+    double* dst = W + (size_t)posof[j] * n;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int r = gl + 8 * q;
+      if (r < n) dst[r] = x[q];
+    }
+  });
+  __syncthreads();
+  return kp;
+}
+
+// One-sided Jacobi sweeps on the kp x kp column-major J (see k_svd); NJ register rows per
+// lane (8 covers kp <= 64).  Returns the number of sweeps.
+template <int NJ>
+__device__ __forceinline__ int jacobi_sweeps(double* J, int kp, double* nrm, Shared& S, long long* gdbg,
+                                             bool dbg) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g8 = tid >> 3, gl = tid & 7, ngr = blockDim.x >> 3;
+  const unsigned gm = 0xffu << (lane & ~7);
+    const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
+  int sweeps_done = 0;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      sweeps_done = sweep + 1;
+      for (int c = g8; c < kp; c += ngr) {  // exact squared norms
+        double s2 = 0.0;
+        for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
+        s2 = grp_sum(s2, gm);
+        if (gl == 0) nrm[c] = s2;
+      }
+      if (tid == 0) S.imisc[2] = 0;
+      __syncthreads();
+      for (int rnd = 0; rnd < np - 1; ++rnd) {
+        for (int pr = g8; pr < np / 2; pr += ngr) {
+          // circle method: position 0 fixed, others rotate
+          int a = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (np - 1);
+          int b = 1 + (np - 2 - pr + rnd) % (np - 1);
+          if (a >= kp || b >= kp) continue;
+          double* ja = J + (size_t)a * kp;
+          double* jb = J + (size_t)b * kp;
+          long long jt0 = 0, jt1 = 0, jt2 = 0;
+          if (dbg) jt0 = clock64();
+          double xa[NJ], xb[NJ];
+#pragma unroll
+          for (int q = 0; q < NJ; ++q) {
+            const int r = gl + 8 * q;
+            const double va = ja[min(r, kp - 1)], vb = jb[min(r, kp - 1)];  // (no branch per row)
+            xa[q] = r < kp ? va : 0.0;
+            xb[q] = r < kp ? vb : 0.0;
+          }
+          double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < NJ; q += 2) {
+            g0 = fma(xa[q], xb[q], g0);
+            g1 = fma(xa[q + 1], xb[q + 1], g1);
+          }
+          for (int r = gl + 8 * NJ; r < kp; r += 8) g0 = fma(ja[r], jb[r], g0);
+          const double ga = grp_sum(g0 + g1, gm);
+          if (dbg) jt1 = clock64();
+          const double al = nrm[a], be = nrm[b];
+          if (ga * ga > 1e-30 * (al * be) && ga != 0.0) {
+            // t = tan of the rotation angle, the smaller root: sign(d) 2g / (|d| + sqrt(d^2 + 4 g^2))
+            const double d = be - al, g2 = ga + ga;
+            const double t = copysign(g2, d * ga) / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+            double c = rsqrt_nr(fma(t, t, 1.0)), s = c * t;
+            // (pin c and s: under the 128-register cap ptxas rematerialised the whole
+            // reciprocal square root at every one of the 2 NJ stores of the rotation)
+            asm volatile("" : "+d"(c), "+d"(s));
+            if (dbg) jt2 = clock64();
+#pragma unroll
+            for (int q = 0; q < NJ; ++q) {
+              const int r = gl + 8 * q;
+              if (r < kp) {
+                ja[r] = c * xa[q] - s * xb[q];
+                jb[r] = s * xa[q] + c * xb[q];
+              }
+            }
+            for (int r = gl + 8 * NJ; r < kp; r += 8) {
+              const double x = ja[r], y = jb[r];
+              ja[r] = c * x - s * y;
+              jb[r] = s * x + c * y;
+            }
+            if (gl == 0) {
+              nrm[a] = fmax(al - t * ga, 0.0);
+              nrm[b] = be + t * ga;
+              S.imisc[2] = 1;
+            }
+            if (dbg && tid == 0) {
+              const long long jt3 = clock64();
+              gdbg[34] += jt1 - jt0; gdbg[35] += jt2 - jt1; gdbg[36] += jt3 - jt2; gdbg[38] += 1;
+            }
+          }
+        }
+        long long jb0 = 0;
+        if (dbg && tid == 0) jb0 = clock64();
+        __syncthreads();
+        if (dbg && tid == 0) { gdbg[37] += clock64() - jb0; gdbg[39] += 1; }
+      }
+      if (S.imisc[2] == 0) break;
+      __syncthreads();
+    }
+  return sweeps_done;
+}
+
+template <int KER, int D, bool HYB>
+__global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Shared S;
   double* taus;
   double* sig;
+  double* rrow;
   int* near_start;
   const double** near_base;
   int64_t* near_stride;
@@ -179,6 +634,7 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
     S.rdiag = d; d += max(A.nmax, A.nnmax);
     taus = d; d += A.nmax;
     sig = d; d += A.nmax;
+    rrow = d; d += A.nnmax;
     S.nodes = nullptr;
     S.redv = d; d += 32;
     S.misc = d; d += 8;
@@ -190,16 +646,19 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
     near_start = ip; ip += MAX_NEAR + 1;
     order = ip; ip += A.nmax;
     S.jpvt = ip; ip += A.nnmax;
-    big = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ip) + 15) & ~uintptr_t(15));
+    // (offset arithmetic on smem_raw itself: a uintptr_t round trip makes the pointer generic,
+    // and every access of the work area a branch-guarded LD instead of a predicated LDS)
+    const unsigned off = ((unsigned)(reinterpret_cast<unsigned char*>(ip) - smem_raw) + 15u) & ~15u;
+    big = reinterpret_cast<double*>(smem_raw + off);
   }
   const int tid = threadIdx.x, NT = blockDim.x;
   const int lane = tid & 31;
   // 8-lane groups: one column (or Jacobi pair) per group
   const int g8 = tid >> 3, gl = tid & 7, ngr = NT >> 3;
   const unsigned gm = 0xffu << (lane & ~7);
-  double* W = A.gws + (size_t)blockIdx.x * A.gws_stride;
   int dbg_n = 0;
   for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
+    double* W = A.gws + (size_t)(A.mode ? v - A.ws_lb : blockIdx.x) * A.gws_stride;
     const int n = A.self.nib[v];
     const int e0 = A.near_ptr[v], e1 = A.near_ptr[v + 1];
     if (tid == 0) {
@@ -232,93 +691,137 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
     int64_t ts;
     const double* tb = ibar_base(A.self, A.nchild, A.child_first, v, &ts);
     const int ldp = n;
-    {
-      int g = 0;
-      for (int b = tid / n, a = tid % n; b < nn;) {
-        while (g + 1 < nnear && near_start[g + 1] <= b) ++g;
-        const int bl = b - near_start[g];
-        double x[D], y[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          x[d] = tb[(int64_t)d * ts + a];
-          y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
-        }
-        W[(size_t)b * ldp + a] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
-        a += NT;
-        while (a >= n) { a -= n; ++b; }
-      }
-    }
-    __syncthreads();
-    if (dbg) tsv[1] = clock64();
-    // ---- column-pivoted QR of A, truncated at the noise floor
-    double* P = W;
-    const int kmax = min(n, nn);
-    for (int j = g8; j < nn; j += ngr) {
-      const double nr = __dsqrt_rn(grp_sumsq(P + (size_t)j * ldp, 0, n, gl, gm));
-      if (gl == 0) {
-        S.vn1[j] = nr;
-        S.vn2[j] = nr;
-      }
-    }
-    __syncthreads();
+    // the panel is factored in shared memory when it fits (copied out to W afterwards:
+    // the reflectors and R_k are read again by the later phases)
+    // group-column QR (on-chip columns, no swaps) when the node fits one of its shapes:
+    // HYB kernel: up to 128 x 256 with two register columns per group; otherwise up to
+    // 80 rows with every column in the shared work area
+    const int slots = (nn + 31) & ~31;
+    // all-shared layout: NQ = 9 (n <= 72) or 10 register rows per lane; the column stride
+    // covers all 8 NQ rows a group touches (72; 88, or 80 where 88 does not fit)
+    const int ldc0 = n <= 72 ? 72 : (slots * 88 <= A.big ? 88 : 80);
+    const bool gq2 = HYB && n <= HQ_ROWS && nn <= 32 * HQ_KC;
+    const bool gq0 = !HYB && A.gq0 && n <= 80 && nn <= 32 * HQ_KC && slots * ldc0 <= A.big;
+    const bool psm = !gq2 && !gq0 && n * nn <= A.big;
+    double* P = psm ? big : W;
     const double floor_v = A.nchild[v] ? A.floor_rel : A.floor_leaf;
+    const int kmax = min(n, nn);
     int kp = 0;
-    for (int i = 0; i < kmax; ++i) {
-      double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int j = i + tid; j < nn; j += NT)
-        if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
-      const int pvt = block_argmax_1bar(bv, bi, S);
-      if (pvt != i) {
-        double* ci = P + (size_t)i * ldp;
-        double* cp = P + (size_t)pvt * ldp;
-        for (int row = tid; row < n; row += NT) {
-          const double t = cp[row];
-          cp[row] = ci[row];
-          ci[row] = t;
-        }
-        if (tid == 0) {
-          S.vn1[pvt] = S.vn1[i];
-          S.vn2[pvt] = S.vn2[i];
+    if (A.mode == 2) {  // factored by the mode-1 launch
+      kp = A.kp_g[v - A.ws_lb];
+      for (int i = tid; i < kp; i += NT) taus[i] = A.taus_g[(size_t)(v - A.ws_lb) * A.nmax + i];
+      P = W;
+      __syncthreads();
+      if (dbg) tsv[1] = tsv[0];
+    } else if (gq2 || gq0) {
+      if constexpr (HYB)
+        kp = group_qr<KER, D, 2, 16>(A, S, big, HQ_LDC, rrow, W, taus, n, nn, nnear, near_start, near_base,
+                                     near_stride, tb, ts, floor_v);
+      else if (n <= 72)
+        kp = group_qr<KER, D, 0, 9>(A, S, big, ldc0, rrow, W, taus, n, nn, nnear, near_start, near_base,
+                                    near_stride, tb, ts, floor_v);
+      else
+        kp = group_qr<KER, D, 0, 10>(A, S, big, ldc0, rrow, W, taus, n, nn, nnear, near_start, near_base,
+                                     near_stride, tb, ts, floor_v);
+      P = W;
+      if (dbg) tsv[1] = tsv[0];
+    } else {
+      {
+        int g = 0;
+        for (int b = tid / n, a = tid % n; b < nn;) {
+          while (g + 1 < nnear && near_start[g + 1] <= b) ++g;
+          const int bl = b - near_start[g];
+          double x[D], y[D];
+  #pragma unroll
+          for (int d = 0; d < D; ++d) {
+            x[d] = tb[(int64_t)d * ts + a];
+            y[d] = near_base[g][(int64_t)d * near_stride[g] + bl];
+          }
+          P[(size_t)b * ldp + a] = A.transpose ? kval<KER, D>(y, x, A.dx) : kval<KER, D>(x, y, A.dx);
+          a += NT;
+          while (a >= n) { a -= n; ++b; }
         }
       }
       __syncthreads();
-      householder(P + (size_t)i * ldp - i, 1, n, i, S);  // column i (stride 1)
+      if (dbg) tsv[1] = clock64();
+      // ---- column-pivoted QR of A, truncated at the noise floor
+      for (int j = g8; j < nn; j += ngr) {
+        const double nr = __dsqrt_rn(grp_sumsq(P + (size_t)j * ldp, 0, n, gl, gm));
+        if (gl == 0) {
+          S.vn1[j] = nr;
+          S.vn2[j] = nr;
+        }
+      }
       __syncthreads();
-      const double tau = S.misc[0];
-      if (tid == 0) taus[i] = tau;
-      const double r0 = fabs(S.rdiag[0]);
-      if (r0 == 0.0 || !(fabs(S.rdiag[i]) > floor_v * r0)) break;
-      kp = i + 1;
-      for (int j = i + 1 + g8; j < nn; j += ngr) {
-        double* c = P + (size_t)j * ldp;
-        double x[GR];
-        const double rij = grp_reflect(c, n, i, tau, S.vh, gl, gm, x, true);
-        if (gl == 0 && tau != 0.0) c[i] = rij;
-        // norm downdate (dlaqp2), exact recomputation when cancellation is severe
-        const double v1 = S.vn1[j];
-        if (v1 != 0.0) {
-          const double q = fabs(rij) / v1;
-          const double temp = fmax(1.0 - q * q, 0.0);
-          const double q2 = v1 / S.vn2[j];
-          if (temp * (q2 * q2) <= TOL3Z) {
-            double s0 = 0.0;
-#pragma unroll
-            for (int qq = 0; qq < GR; ++qq) s0 = fma(x[qq], x[qq], s0);
-            for (int r = i + 1 + gl + 8 * GR; r < n; r += 8) s0 = fma(c[r], c[r], s0);
-            const double nv = i + 1 < n ? sqrt(grp_sum(s0, gm)) : 0.0;
-            if (gl == 0) {
-              S.vn1[j] = nv;
-              S.vn2[j] = nv;
-            }
-          } else if (gl == 0) {
-            S.vn1[j] = v1 * sqrt(temp);
+      kp = 0;
+      for (int i = 0; i < kmax; ++i) {
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int j = i + tid; j < nn; j += NT)
+          if (S.vn1[j] > bv) { bv = S.vn1[j]; bi = j; }
+        const int pvt = block_argmax_1bar(bv, bi, S);
+        if (pvt != i) {
+          double* ci = P + (size_t)i * ldp;
+          double* cp = P + (size_t)pvt * ldp;
+          for (int row = tid; row < n; row += NT) {
+            const double t = cp[row];
+            cp[row] = ci[row];
+            ci[row] = t;
+          }
+          if (tid == 0) {
+            S.vn1[pvt] = S.vn1[i];
+            S.vn2[pvt] = S.vn2[i];
           }
         }
+        __syncthreads();
+        householder(P + (size_t)i * ldp - i, 1, n, i, S);  // column i (stride 1)
+        __syncthreads();
+        const double tau = S.misc[0];
+        if (tid == 0) taus[i] = tau;
+        const double r0 = fabs(S.rdiag[0]);
+        if (r0 == 0.0 || !(fabs(S.rdiag[i]) > floor_v * r0)) break;
+        kp = i + 1;
+        for (int j = i + 1 + g8; j < nn; j += ngr) {
+          double* c = P + (size_t)j * ldp;
+          double x[GR];
+          const double rij = grp_reflect(c, n, i, tau, S.vh, gl, gm, x, true);
+          if (gl == 0 && tau != 0.0) c[i] = rij;
+          // norm downdate (dlaqp2), exact recomputation when cancellation is severe
+          const double v1 = S.vn1[j];
+          if (v1 != 0.0) {
+            const double q = fabs(rij) / v1;
+            const double temp = fmax(1.0 - q * q, 0.0);
+            const double q2 = v1 / S.vn2[j];
+            if (temp * (q2 * q2) <= TOL3Z) {
+              double s0 = 0.0;
+  #pragma unroll
+              for (int qq = 0; qq < GR; ++qq) s0 = fma(x[qq], x[qq], s0);
+              for (int r = i + 1 + gl + 8 * GR; r < n; r += 8) s0 = fma(c[r], c[r], s0);
+              const double nv = i + 1 < n ? sqrt(grp_sum(s0, gm)) : 0.0;
+              if (gl == 0) {
+                S.vn1[j] = nv;
+                S.vn2[j] = nv;
+              }
+            } else if (gl == 0) {
+              S.vn1[j] = v1 * sqrt(temp);
+            }
+          }
+        }
+        __syncthreads();
       }
       __syncthreads();
     }
-    __syncthreads();
+    if (psm && kp > 0 && A.mode != 2) {
+      for (int e = tid; e < n * nn; e += NT) W[e] = P[e];
+      __syncthreads();
+      P = W;
+    }
+    if (A.mode == 1) {
+      if (tid == 0) A.kp_g[v - A.ws_lb] = kp;
+      for (int i = tid; i < kp; i += NT) A.taus_g[(size_t)(v - A.ws_lb) * A.nmax + i] = taus[i];
+      __syncthreads();
+      continue;
+    }
     if (kp == 0) {
       if (tid == 0) A.keep[v] = 0;
       __syncthreads();
@@ -327,7 +830,7 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
     if (dbg) tsv[2] = clock64();
     // ---- B = R_k^T (nn x kp, column-major), unpivoted QR -> R2 (kp x kp); B in
     // shared memory when it fits
-    const bool bsm = (int64_t)nn * kp <= SVD_BIG;
+    const bool bsm = nn * kp <= A.big;
     double* B = bsm ? big : W + (size_t)n * nn;
     double* T = W + (size_t)n * nn;  // global staging (free once B is in shared memory / consumed)
     const int ldb = nn;
@@ -336,105 +839,121 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
       B[(size_t)j * ldb + b] = b >= j ? P[(size_t)b * ldp + j] : 0.0;
     }
     __syncthreads();
-    for (int i = 0; i < kp; ++i) {
-      householder(B + (size_t)i * ldb - i, 1, nn, i, S);
-      __syncthreads();
-      const double tau = S.misc[0];
-      if (tau != 0.0)
-        for (int j = i + 1 + g8; j < kp; j += ngr) {
-          double* c = B + (size_t)j * ldb;
-          double x[GR];
-          const double rij = grp_reflect(c, nn, i, tau, S.vh, gl, gm, x, true);
-          if (gl == 0) c[i] = rij;
+    // One barrier per step: the group that updates column i + 1 also leaves its next
+    // diagonal entry and the exact squared norm of its remaining rows in S.misc, so every
+    // thread forms dlarfg's beta / tau / scaling for step i + 1 itself and applies the
+    // reflector from the RAW column (v = scal * column); only beta is stored back (Q2 and
+    // the scaled reflectors are never used: R2 is the upper triangle).
+    // (instantiated for the shared-memory and the global B: LDS / LDG instead of generic loads)
+    auto qr2 = [&](double* Bq) __attribute__((always_inline)) {
+      if (g8 == 0) {
+        const double s2 = grp_sumsq(Bq, 0, nn, gl, gm);
+        if (gl == 0) {
+          S.misc[2] = Bq[0];
+          S.misc[3] = s2;
         }
+      }
       __syncthreads();
-    }
-    // ---- one-sided Jacobi on R2's columns (column-major J: J[c*kp + r]), V accumulated;
-    // J and V in shared memory when they fit (R2 staged through global scratch when
-    // B occupies that area).  Column norms are kept up to date through the rotation
-    // (one dot product per pair) and refreshed exactly at every sweep.
-    const bool jsm = 2 * kp * kp <= SVD_BIG;
+      for (int i = 0; i < kp; ++i) {
+        double* ci = Bq + (size_t)i * ldb;
+        const double alpha = S.misc[2 + 2 * (i & 1)], n2 = S.misc[3 + 2 * (i & 1)];
+        double tau = 0.0, beta = alpha, scal = 0.0;
+        if (nn - i > 1 && n2 > alpha * alpha) {
+          beta = -copysign(__dsqrt_rn(n2), alpha);
+          tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+          scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
+        }
+        asm volatile("" : "+d"(tau), "+d"(beta), "+d"(scal));  // (no rematerialisation in the loops below)
+        const int jn = i + 1;  // the next pivot column
+        for (int j = i + 1 + g8; j < kp; j += ngr) {
+          double* c = Bq + (size_t)j * ldb;
+          // rows i+1.. of the group: row i + 1 + gl + 8 q in x[q]
+          const int rb = i + 1 + gl;
+          double x[GR];
+  #pragma unroll
+          for (int q = 0; q < GR; ++q) {
+            const double cq = c[min(rb + 8 * q, nn - 1)];  // (unconditional loads: no branch per row)
+            x[q] = rb + 8 * q < nn ? cq : 0.0;
+          }
+          if (tau != 0.0) {
+            double vq[GR];
+  #pragma unroll
+            for (int q = 0; q < GR; ++q) vq[q] = ci[min(rb + 8 * q, nn - 1)];
+            double w0 = 0.0, w1 = 0.0;
+  #pragma unroll
+            for (int q = 0; q < GR; q += 2) {
+              w0 = fma(vq[q], x[q], w0);  // x is zero past the last row
+              w1 = fma(vq[q + 1], x[q + 1], w1);
+            }
+            for (int r = rb + 8 * GR; r < nn; r += 8) w0 = fma(ci[r], c[r], w0);
+            const double cii = c[i];
+            const double w = fma(scal, grp_sum(w0 + w1, gm), cii);
+            const double t = -tau * w, ts2 = t * scal;
+  #pragma unroll
+            for (int q = 0; q < GR; ++q) {
+              const int r = rb + 8 * q;
+              if (r < nn) {
+                x[q] = fma(ts2, vq[q], x[q]);
+                c[r] = x[q];
+              }
+            }
+            for (int r = rb + 8 * GR; r < nn; r += 8) c[r] = fma(ts2, ci[r], c[r]);
+            if (gl == 0) c[i] = cii + t;
+          }
+          if (j == jn) {  // next step's alpha and remaining norm
+            double s0 = 0.0, s1 = 0.0;
+  #pragma unroll
+            for (int q = 0; q < GR; q += 2) {
+              s0 = (gl == 0 && q == 0) ? s0 : fma(x[q], x[q], s0);
+              s1 = fma(x[q + 1], x[q + 1], s1);
+            }
+            __syncwarp(gm);
+            for (int r = rb + 8 * GR; r < nn; r += 8) s0 = fma(c[r], c[r], s0);
+            const double a2 = __shfl_sync(gm, x[0], lane & ~7);
+            const double s2 = grp_sum(s0 + s1, gm);
+            if (gl == 0) {
+              S.misc[2 + 2 * (jn & 1)] = a2;
+              S.misc[3 + 2 * (jn & 1)] = fma(a2, a2, s2);
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0) ci[i] = beta;
+      }
+      __syncthreads();
+    };
+    if (bsm) qr2(big);
+    else qr2(W + (size_t)n * nn);
+    // ---- one-sided (Hestenes) Jacobi on the columns of L = R2^T (kp x kp lower triangle,
+    // column-major J[c*kp + r]).  R_k = L Q2^T, so the left singular vectors of A are
+    // Q1 times those of L: L V = W gives them as the normalised columns of W and V is
+    // never formed.  L^T L = R2 R2^T is one more LR step towards diagonal than the
+    // R2^T R2 of the columns of R2 (Drmac / Veselic preconditioning), so fewer sweeps.
+    // A pair's two columns are loaded once into registers (rows gl + 8q of the 8-lane
+    // group), the dot product, the rotation and the stores all work from them.  Column
+    // norms are carried through the rotations and refreshed exactly at every sweep.
+    const bool jsm = kp * kp <= A.big;
     double* J = jsm ? big : W + (size_t)n * nn + (size_t)nn * kp;
-    double* V = J + (size_t)kp * kp;
     double* nrm = sig;  // squared column norms (reuses the sigma scratch)
     if (bsm && jsm) {
       for (int e = tid; e < kp * kp; e += NT) {
         const int c = e / kp, r = e - c * kp;
-        T[e] = r <= c ? B[(size_t)c * ldb + r] : 0.0;
+        T[e] = c <= r ? B[(size_t)r * ldb + c] : 0.0;
       }
       __syncthreads();
       for (int e = tid; e < kp * kp; e += NT) J[e] = T[e];
     } else {
       for (int e = tid; e < kp * kp; e += NT) {
         const int c = e / kp, r = e - c * kp;
-        J[e] = r <= c ? B[(size_t)c * ldb + r] : 0.0;
+        J[e] = c <= r ? B[(size_t)r * ldb + c] : 0.0;
       }
     }
-    for (int e = tid; e < kp * kp; e += NT) V[e] = (e % (kp + 1)) == 0 ? 1.0 : 0.0;
     __syncthreads();
-    const int np = kp + (kp & 1);  // round-robin over an even count (dummy = kp)
     if (dbg) tsv[3] = clock64();
-    int sweeps_done = 0;
-    for (int sweep = 0; sweep < 40; ++sweep) {
-      sweeps_done = sweep + 1;
-      for (int c = g8; c < kp; c += ngr) {  // exact squared norms
-        double s2 = 0.0;
-        for (int r = gl; r < kp; r += 8) s2 = fma(J[(size_t)c * kp + r], J[(size_t)c * kp + r], s2);
-        s2 = grp_sum(s2, gm);
-        if (gl == 0) nrm[c] = s2;
-      }
-      if (tid == 0) S.imisc[2] = 0;
-      __syncthreads();
-      for (int rnd = 0; rnd < np - 1; ++rnd) {
-        for (int pr = g8; pr < np / 2; pr += ngr) {
-          // circle method: position 0 fixed, others rotate
-          int a = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (np - 1);
-          int b = 1 + (np - 2 - pr + rnd) % (np - 1);
-          if (a >= kp || b >= kp) continue;
-          double* ja = J + (size_t)a * kp;
-          double* jb = J + (size_t)b * kp;
-          double ga = 0;
-          long long jt0 = 0, jt1 = 0, jt2 = 0;
-          if (dbg) jt0 = clock64();
-          for (int r = gl; r < kp; r += 8) ga = fma(ja[r], jb[r], ga);
-          ga = grp_sum(ga, gm);
-          if (dbg) jt1 = clock64();
-          const double al = nrm[a], be = nrm[b];
-          if (ga * ga > 1e-30 * (al * be) && ga != 0.0) {
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = rsqrt(1.0 + t * t), s = c * t;
-            if (dbg) jt2 = clock64();
-            double* va = V + (size_t)a * kp;
-            double* vb = V + (size_t)b * kp;
-            for (int r = gl; r < kp; r += 8) {
-              const double x = ja[r], y = jb[r];
-              ja[r] = c * x - s * y;
-              jb[r] = s * x + c * y;
-              const double p = va[r], q = vb[r];
-              va[r] = c * p - s * q;
-              vb[r] = s * p + c * q;
-            }
-            __syncwarp(gm);
-            if (gl == 0) {
-              nrm[a] = fmax(al - t * ga, 0.0);
-              nrm[b] = be + t * ga;
-              S.imisc[2] = 1;
-            }
-            if (dbg && tid == 0) {
-              const long long jt3 = clock64();
-              A.dbg[34] += jt1 - jt0; A.dbg[35] += jt2 - jt1; A.dbg[36] += jt3 - jt2; A.dbg[38] += 1;
-            }
-          }
-        }
-        long long jb0 = 0;
-        if (dbg && tid == 0) jb0 = clock64();
-        __syncthreads();
-        if (dbg && tid == 0) { A.dbg[37] += clock64() - jb0; A.dbg[39] += 1; }
-      }
-      if (S.imisc[2] == 0) break;
-      __syncthreads();
-    }
+    // (the shared-memory case is instantiated on the work area itself: LDS, not generic loads)
+    const int sweeps_done = jsm ? (kp <= 64 ? jacobi_sweeps<8>(big, kp, nrm, S, A.dbg, dbg)
+                                            : jacobi_sweeps<16>(big, kp, nrm, S, A.dbg, dbg))
+                                : jacobi_sweeps<16>(J, kp, nrm, S, A.dbg, dbg);
     if (dbg) tsv[4] = clock64();
     if (A.dbg && tid == 0) {  // every node: max sweeps, nodes at the sweep cap
       atomicMax(reinterpret_cast<unsigned long long*>(A.dbg + 32), (unsigned long long)sweeps_done);
@@ -470,45 +989,89 @@ __global__ void __launch_bounds__(SVD_THREADS, 2) k_svd(SvdArgs A) {
     __syncthreads();
     const int keep = S.imisc[3];
     if (keep == 0) continue;
-    // ---- U = Q1[:, :kp] V[:, kept]  (n x keep): Y staged in shared memory (over
-    // the J/V area, through registers) when it fits, reflectors applied by
-    // 8-lane groups per column
+    // ---- U = Q1[:, :kp] (W[:, kept] / sigma)  (n x keep).  Up to 128 rows: the kp
+    // reflectors are staged once in the shared work area and every 8-lane group carries
+    // one column of U in registers through all of them (no barrier between reflectors).
+    // Otherwise: U staged in shared memory when it fits, one barrier pair per reflector.
     double* Yg = A.sv + A.sv_off[v];
-    const bool ysm = n * (keep | 1) <= SVD_BIG;
-    double* Y = ysm ? big : Yg;
-    const int ldy = ysm ? (keep | 1) : keep;
-    {
-      // kept columns of V (descending sigma) -> T (global staging: Y may overlap V)
-      for (int e = tid; e < kp * keep; e += NT) {
-        const int a = e / keep, c = e - a * keep;
-        T[e] = V[(size_t)order[c] * kp + a];
+    // kept columns of W (descending sigma), normalised -> T (global staging: the work area is reused)
+    for (int e = tid; e < kp * keep; e += NT) {
+      const int a = e / keep, c = e - a * keep;
+      T[e] = J[(size_t)order[c] * kp + a] / sig[order[c]];
+    }
+    __syncthreads();
+    if (n <= 8 * GR && kp * n <= A.big) {
+      double* Vs = big;  // reflector i at Vs[i * n + row], rows > i
+      for (int e = tid; e < kp * n; e += NT) {
+        const int i = e / n, row = e - i * n;
+        Vs[e] = row > i ? P[(size_t)i * ldp + row] : 0.0;
       }
       __syncthreads();
+      for (int c = g8; c < keep; c += ngr) {
+        double y[GR];
+#pragma unroll
+        for (int q = 0; q < GR; ++q) {
+          const int r = gl + 8 * q;
+          const double tq = T[min(r, kp - 1) * keep + c];
+          y[q] = r < kp ? tq : 0.0;
+        }
+        for (int i = kp - 1; i >= 0; --i) {
+          const double tau = taus[i];
+          if (tau == 0.0) continue;
+          const double* vi = Vs + (size_t)i * n;
+          double vr[GR];
+          double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < GR; ++q) {
+            const int r = gl + 8 * q;
+            const double vq = vi[min(r, n - 1)];  // (unconditional load: no branch per row)
+            vr[q] = r < n ? (r == i ? 1.0 : vq) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < GR; q += 2) {
+            w0 = fma(vr[q], y[q], w0);
+            w1 = fma(vr[q + 1], y[q + 1], w1);
+          }
+          const double t = -tau * grp_sum(w0 + w1, gm);
+#pragma unroll
+          for (int q = 0; q < GR; ++q) y[q] = fma(t, vr[q], y[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < GR; ++q) {
+          const int r = gl + 8 * q;
+          if (r < n) Yg[(size_t)r * keep + c] = y[q];
+        }
+      }
+      __syncthreads();
+    } else {
+      const bool ysm = n * (keep | 1) <= A.big;
+      double* Y = ysm ? big : Yg;
+      const int ldy = ysm ? (keep | 1) : keep;
       for (int e = tid; e < n * ldy; e += NT) {
         const int a = e / ldy, c = e - a * ldy;
         Y[e] = (a < kp && c < keep) ? T[a * keep + c] : 0.0;
       }
-    }
-    __syncthreads();
-    for (int i = kp - 1; i >= 0; --i) {
-      const double tau = taus[i];
-      if (tau == 0.0) continue;
-      for (int row = i + 1 + tid; row < n; row += NT) S.vh[row] = P[(size_t)i * ldp + row];
       __syncthreads();
-      for (int c = g8; c < keep; c += ngr) {
-        double w = 0.0;
-        for (int row = i + gl; row < n; row += 8)
-          w = fma(row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c], w);
-        w = grp_sum(w, gm);
-        const double t = -tau * w;
-        for (int row = i + gl; row < n; row += 8)
-          Y[(size_t)row * ldy + c] = fma(t, row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c]);
+      for (int i = kp - 1; i >= 0; --i) {
+        const double tau = taus[i];
+        if (tau == 0.0) continue;
+        for (int row = i + 1 + tid; row < n; row += NT) S.vh[row] = P[(size_t)i * ldp + row];
+        __syncthreads();
+        for (int c = g8; c < keep; c += ngr) {
+          double w = 0.0;
+          for (int row = i + gl; row < n; row += 8)
+            w = fma(row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c], w);
+          w = grp_sum(w, gm);
+          const double t = -tau * w;
+          for (int row = i + gl; row < n; row += 8)
+            Y[(size_t)row * ldy + c] = fma(t, row == i ? 1.0 : S.vh[row], Y[(size_t)row * ldy + c]);
+        }
+        __syncthreads();
       }
-      __syncthreads();
-    }
-    if (ysm) {
-      for (int e = tid; e < n * keep; e += NT) Yg[e] = Y[(e / keep) * ldy + e % keep];
-      __syncthreads();
+      if (ysm) {
+        for (int e = tid; e < n * keep; e += NT) Yg[e] = Y[(e / keep) * ldy + e % keep];
+        __syncthreads();
+      }
     }
     if (dbg) {
       tsv[5] = clock64();
@@ -628,11 +1191,52 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   int dev = 0, nsm = 0;
   SMASH_CUDA(cudaGetDevice(&dev));
   SMASH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  static const int svd_per_sm = getenv("SMASH_SVD_PER_SM") ? atoi(getenv("SMASH_SVD_PER_SM")) : 2;
+  static const int svd_per_sm_env = getenv("SMASH_SVD_PER_SM") ? atoi(getenv("SMASH_SVD_PER_SM")) : 0;
+  static const bool hyb_on = !(getenv("SMASH_SVD_HYB") && atoi(getenv("SMASH_SVD_HYB")) == 0);
+  static const bool gq0_on = !(getenv("SMASH_SVD_GQ0") && atoi(getenv("SMASH_SVD_GQ0")) == 0);
+  static const int big_waves = getenv("SMASH_SVD_BIGW") ? atoi(getenv("SMASH_SVD_BIGW")) : 4;
+  const int64_t panel = (int64_t)A.nmax * A.nnmax;
+  const int mx = std::max(A.nmax, A.nnmax);
+  const size_t smem_small = 8 * ((size_t)3 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
+                            4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64 + 16;
+  // work area: the largest that leaves two CTAs per SM (about 96 KB)
+  SMASH_CHECK(smem_small + 8 * 4096 <= SVD_SMEM_MAX / 2 - 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
+  const int big2 = (int)(((SVD_SMEM_MAX / 2 - 1024) - smem_small) / 8) & ~1;
+  A.big = big2;
+  A.gq0 = gq0_on;
+  // level shapes: (a) at most 80 rows with every column of the panel in the two-per-SM work
+  // area: all-shared group-column QR; (b) up to 128 x 256 (config 4's leaf blocks and its
+  // middle levels): the HYB kernel, one CTA per SM, two register columns per group;
+  // (c) anything else on the swap-based QR -- panel in the work area if it fits, widened to
+  // one CTA per SM on levels of few nodes, else in the L2-resident workspace
+  const int slots = (A.nnmax + 31) & ~31;
+  const bool shape_a = gq0_on && A.nmax <= 80 && A.nnmax <= 32 * HQ_KC && (int64_t)slots * (A.nmax <= 72 ? 72 : 80) <= big2;
+  const bool hyb = hyb_on && !shape_a && panel > big2 && A.nmax <= HQ_ROWS && A.nnmax <= 32 * HQ_KC &&
+                   smem_small + 8 * (size_t)HQ_BIG <= SVD_SMEM_MAX;
+  if (hyb) {
+    A.big = HQ_BIG;
+  } else if (panel > big2 && run_le - run_lb <= big_waves * nsm) {
+    A.big = (int)std::min<int64_t>(panel, (int64_t)((SVD_SMEM_MAX - smem_small) / 8));
+  }
+  const int svd_per_sm = svd_per_sm_env ? svd_per_sm_env : (A.big > big2 ? 1 : 2);
+  static const bool split_on = !(getenv("SMASH_SVD_SPLIT") && atoi(getenv("SMASH_SVD_SPLIT")) == 0);
+  static const int split_chunk = getenv("SMASH_SVD_CHUNK") ? atoi(getenv("SMASH_SVD_CHUNK")) : 8;
+  const int run_cnt = run_le - run_lb;
+  // a wide HYB level is split: QR launches of one CTA per SM, the later phases at two
+  const bool split = hyb && split_on && run_cnt > 2 * nsm;
   const int grid = std::min(cnt, nsm * svd_per_sm);
+  const int chunk = split ? std::min(run_cnt, split_chunk * nsm) : 0;
   DBuf<double> gws;
-  gws.alloc((size_t)grid * A.gws_stride, s);
+  gws.alloc((size_t)(split ? chunk : grid) * A.gws_stride, s);
   A.gws = gws.p;
+  DBuf<int> kp_g;
+  DBuf<double> taus_g;
+  if (split) {
+    kp_g.alloc(chunk, s);
+    taus_g.alloc((size_t)chunk * A.nmax, s);
+    A.kp_g = kp_g.p;
+    A.taus_g = taus_g.p;
+  }
   DBuf<int> err;
   err.alloc(1, s);
   err.zero(s);
@@ -641,22 +1245,42 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   DBuf<long long> dbgbuf;
   A.dbg = nullptr;
   if (svd_dbg) {
-    dbgbuf.alloc(40, s);
+    dbgbuf.alloc(48, s);
     dbgbuf.zero(s);
     A.dbg = dbgbuf.p;
   }
-  const int mx = std::max(A.nmax, A.nnmax);
-  size_t smem = 8 * ((size_t)2 * A.nnmax + 2 * mx + 2 * A.nmax + 32 + 8 + 2 * MAX_NEAR) +
-                4 * ((size_t)32 + 8 + MAX_NEAR + 1 + A.nmax + A.nnmax) + 64 + 16 +
-                8 * (size_t)SVD_BIG;
-  SMASH_CHECK(smem <= 200 * 1024, SMASH_ERR_INVALID, "HSS nearfield block too large");
+  const size_t smem = smem_small + 8 * (size_t)A.big;
+  const size_t smem2 = smem_small + 8 * (size_t)big2;
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
-    SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
     SvdArgs Ar = A;
     Ar.lb = run_lb;
     Ar.le = run_le;
-    if (run_le > run_lb) k_svd<KER, D><<<std::min(grid, run_le - run_lb), SVD_THREADS, smem, s>>>(Ar);
+    if (run_le <= run_lb) return;
+    if (split) {
+      SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+      SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem2));
+      for (int c0 = run_lb; c0 < run_le; c0 += chunk) {
+        Ar.lb = c0;
+        Ar.le = std::min(run_le, c0 + chunk);
+        Ar.ws_lb = c0;
+        Ar.mode = 1;
+        Ar.big = A.big;
+        k_svd<KER, D, true><<<std::min(nsm, Ar.le - Ar.lb), SVD_THREADS, smem, s>>>(Ar);
+        Ar.mode = 2;
+        Ar.big = big2;
+        k_svd<KER, D, false><<<std::min(2 * nsm, Ar.le - Ar.lb), SVD_THREADS, smem2, s>>>(Ar);
+      }
+    } else if (hyb) {
+      SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+      k_svd<KER, D, true><<<std::min(grid, run_le - run_lb), SVD_THREADS, smem, s>>>(Ar);
+    } else {
+      SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+      k_svd<KER, D, false><<<std::min(grid, run_le - run_lb), SVD_THREADS, smem, s>>>(Ar);
+    }
   });
   SMASH_CUDA(cudaGetLastError());
   if (run_le > run_lb)
@@ -668,16 +1292,17 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   sync(s);
   SMASH_CHECK(he == 0, SMASH_ERR_INVALID, "nearfield set larger than the supported cap");
   if (svd_dbg) {
-    long long h[40];
-    d2h(h, dbgbuf.p, 40, s);
+    long long h[48];
+    d2h(h, dbgbuf.p, 48, s);
     sync(s);
     fprintf(stderr, "svd level %d side %d cnt %d:", level, side, cnt);
     for (int q = 0; q < 4; ++q)
       fprintf(stderr, " [asm %lld qr %lld qr2 %lld jac %lld back %lld kp %lld keep %lld n.nn %lld]", h[q * 8], h[q * 8 + 1],
               h[q * 8 + 2], h[q * 8 + 3], h[q * 8 + 4], h[q * 8 + 5], h[q * 8 + 6], h[q * 8 + 7]);
-    fprintf(stderr, " max_sweeps %lld capped %lld | jacobi (thread 0 of traced nodes): dot %.0f scalar %.0f rotate %.0f per rotation (%lld), barrier wait %.0f per round (%lld)\n", h[32], h[33],
+    fprintf(stderr, " max_sweeps %lld capped %lld | jacobi (thread 0 of traced nodes): dot %.0f scalar %.0f rotate %.0f per rotation (%lld), barrier wait %.0f per round (%lld) | group QR per step: scalars + update %.0f, write-back + argmax %.0f (%lld)\n", h[32], h[33],
             h[38] ? (double)h[34] / h[38] : 0.0, h[38] ? (double)h[35] / h[38] : 0.0, h[38] ? (double)h[36] / h[38] : 0.0, h[38],
-            h[39] ? (double)h[37] / h[39] : 0.0, h[39]);
+            h[39] ? (double)h[37] / h[39] : 0.0, h[39], h[43] ? (double)h[40] / h[43] : 0.0,
+            h[43] ? (double)h[42] / h[43] : 0.0, h[43]);
   }
   return hk;
 }
