@@ -2,23 +2,29 @@
 // per-node `block(ibar, near columns)` + `truncated_svd` of build_hss
 // (smash/hss.py:279-299, smash/lowrank.py:265-276).
 //
-// One CTA per node.  A (|ibar| x n_near) is generated from the kernel into an
-// L2-resident workspace, then its left singular subspace is computed as
-//   A P = Q1 R      column-pivoted Householder QR, stopped once |R_ii| falls
-//                   2^3 below the fp64 noise floor (2^-56 |R_00|, SMASH_SVD_FLOOR):
-//                   the discarded block perturbs the singular values by about
-//                   sqrt(n) 2^-56 sigma_1, the order of LAPACK's own rounding.
-//                   Stopping AT the noise floor (2^-53) made the kept vectors near
-//                   the eps_svd cut ~10x less accurate (cfg 4 full size: 21 rank
-//                   flips vs 1 for a LAPACK restatement; 2^-56 .. 2^-63 all give
-//                   the LAPACK restatement's counts, profiles/hss_skeleton_census_r02.txt);
-//   R_k^T = Q2 R2   unpivoted QR of the k' x n_near leading rows (transposed);
-//   R2 V = W        one-sided (Hestenes) Jacobi on the k' x k' triangle,
-//                   round-robin pair order, one warp per pair;
-// so sigma_j = ||W_j|| and U(A) = Q1[:, :k'] V.  keep = #{sigma >= eps sigma_1}
-// (lowrank.py:275) and S = U[:, kept] (descending sigma) is handed to the
+// One CTA per node.  The left singular subspace of A (|ibar| x n_near, generated from the
+// kernel on the fly) is computed as
+//   A P = Q1 R      column-pivoted Householder QR, stopped once |R_ii| falls a few bits
+//                   below the fp64 noise floor (2^-57 |R_00| internal nodes, 2^-56 leaves;
+//                   SMASH_SVD_FLOOR / _LEAF): the discarded block perturbs the singular
+//                   values by about sqrt(n) 2^-56 sigma_1, the order of LAPACK's own
+//                   rounding.  Stopping AT the noise floor (2^-53) made the kept vectors
+//                   near the eps_svd cut ~10x less accurate (cfg 4 full size: 21 rank
+//                   flips vs 1 for a LAPACK restatement; 2^-57 .. 2^-63 all give the LAPACK
+//                   restatement's counts on every fixture, profiles/hss_skeleton_census_r02.txt).
+//                   Panels up to 128 x 256 are factored on chip by the group-column QR
+//                   (group_qr below); larger ones by the swap-based QR on a shared or
+//                   L2-resident panel;
+//   R_k^T = Q2 R2   unpivoted QR of the k' leading rows (transposed), one barrier per step;
+//   L V = W         one-sided (Hestenes) Jacobi on the columns of L = R2^T (k' x k'),
+//                   round-robin pair order, one 8-lane group per pair;
+// so sigma_j = ||W_j|| and U(A) = Q1[:, :k'] W diag(1/sigma).  keep = #{sigma >= eps
+// sigma_1} (lowrank.py:275) and S = U[:, kept] (descending sigma) is handed to the
 // compression kernel as extra panel rows.  Column order and signs of S do not
 // change the pivoted QR of [U_basis, S]^T in exact arithmetic.
+// Wide levels of large panels (config 4's leaves) run as two launches per chunk of nodes:
+// the QR at one CTA per SM (255 registers, the whole SM's shared memory), the later phases
+// at two CTAs per SM; panel, k' and taus pass through a per-node workspace.
 #include <cub/cub.cuh>
 
 #include <cstdio>
@@ -41,6 +47,9 @@ constexpr int MAX_NEAR = 64;
 // factored, then B = R_k^T, then J, then the back-transform Y: about 96 KB where two CTAs
 // share an SM, up to the whole SM on levels of few nodes and in the HYB kernel.
 constexpr size_t SVD_SMEM_MAX = 227 * 1024;
+// doubles the unconditional register-row loads may run past the end of a matrix in the work
+// area (32 rows x 8 lanes + a pivot offset)
+constexpr int SVD_SLACK = 272;
 
 struct IbarSide {
   const int* nib;       // |ibar| per BFS node (valid for the current + deeper levels)
@@ -122,6 +131,16 @@ __device__ __forceinline__ double grp_sum(double x, unsigned gm) {
   x += __shfl_xor_sync(gm, x, 4);
   x += __shfl_xor_sync(gm, x, 2);
   x += __shfl_xor_sync(gm, x, 1);
+  return x;
+}
+
+// The same butterfly with the full-warp mask, for call sites every lane of the warp reaches
+// together: a shuffle under a computed 8-lane mask compiles to a WARPSYNC / collective
+// sequence per shuffle, under the constant full mask to a single SHFL.BFLY.
+__device__ __forceinline__ double grp_sum_w(double x) {
+  x += __shfl_xor_sync(0xffffffffu, x, 4);
+  x += __shfl_xor_sync(0xffffffffu, x, 2);
+  x += __shfl_xor_sync(0xffffffffu, x, 1);
   return x;
 }
 
@@ -392,7 +411,7 @@ __device__ __forceinline__ int group_qr(const SvdArgs& A, Shared& S, double* sh,
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int r = gl + 8 * q;
-        const double pq = pc[min(r, n - 1)];  // (unconditional load: no branch per row)
+        const double pq = pc[r];  // (unconditional load: a column slot holds all 8 NQ rows)
         vv[q] = (tau != 0.0 && r > i && r < n) ? pq * scal : (r == i ? 1.0 : 0.0);
       }
     }
@@ -404,7 +423,7 @@ __device__ __forceinline__ int group_qr(const SvdArgs& A, Shared& S, double* sh,
       const std::integral_constant<int, k0 + 1> kb;
       const int ja = g8 + 32 * k0, jb = ja + 32;
       const bool acta = ja < nn && posof[ja] < 0, actb = jb < nn && posof[jb] < 0;
-      if (!acta && !actb) return;
+      // (no group-level exit: the warp stays converged, the shuffles take the full mask)
       double xa[NQ], xb[NQ];
       col_load(ka, xa);
       if (32 * (k0 + 1) < nn) {  // CTA-uniform: the pair's second column slot exists
@@ -426,12 +445,12 @@ __device__ __forceinline__ int group_qr(const SvdArgs& A, Shared& S, double* sh,
         b0 = fma(vv[NQ - 1], xb[NQ - 1], b0);
       }
       double wa = a0 + a1, wb = b0 + b1;
-      wa += __shfl_xor_sync(gm, wa, 4);
-      wb += __shfl_xor_sync(gm, wb, 4);
-      wa += __shfl_xor_sync(gm, wa, 2);
-      wb += __shfl_xor_sync(gm, wb, 2);
-      wa += __shfl_xor_sync(gm, wa, 1);
-      wb += __shfl_xor_sync(gm, wb, 1);
+      wa += __shfl_xor_sync(0xffffffffu, wa, 4);
+      wb += __shfl_xor_sync(0xffffffffu, wb, 4);
+      wa += __shfl_xor_sync(0xffffffffu, wa, 2);
+      wb += __shfl_xor_sync(0xffffffffu, wb, 2);
+      wa += __shfl_xor_sync(0xffffffffu, wa, 1);
+      wb += __shfl_xor_sync(0xffffffffu, wb, 1);
       const double ta = acta ? -tau * wa : 0.0, tb2 = actb ? -tau * wb : 0.0;
       a0 = a1 = b0 = b1 = 0.0;
 #pragma unroll
@@ -451,12 +470,12 @@ __device__ __forceinline__ int group_qr(const SvdArgs& A, Shared& S, double* sh,
       if (acta) col_store(ka, xa);
       if (actb) col_store(kb, xb);
       double na = a0 + a1, nb = b0 + b1;
-      na += __shfl_xor_sync(gm, na, 4);
-      nb += __shfl_xor_sync(gm, nb, 4);
-      na += __shfl_xor_sync(gm, na, 2);
-      nb += __shfl_xor_sync(gm, nb, 2);
-      na += __shfl_xor_sync(gm, na, 1);
-      nb += __shfl_xor_sync(gm, nb, 1);
+      na += __shfl_xor_sync(0xffffffffu, na, 4);
+      nb += __shfl_xor_sync(0xffffffffu, nb, 4);
+      na += __shfl_xor_sync(0xffffffffu, na, 2);
+      nb += __shfl_xor_sync(0xffffffffu, nb, 2);
+      na += __shfl_xor_sync(0xffffffffu, na, 1);
+      nb += __shfl_xor_sync(0xffffffffu, nb, 1);
       if (gl == ((i + 1) & 7)) {
         if (acta) {
           arow[ja] = grp_sel<NQ>(xa, (i + 1) >> 3);
@@ -543,11 +562,16 @@ __device__ __forceinline__ int jacobi_sweeps(double* J, int kp, double* nrm, Sha
       if (tid == 0) S.imisc[2] = 0;
       __syncthreads();
       for (int rnd = 0; rnd < np - 1; ++rnd) {
-        for (int pr = g8; pr < np / 2; pr += ngr) {
-          // circle method: position 0 fixed, others rotate
+        for (int pr0 = 0; pr0 < np / 2; pr0 += ngr) {
+          // circle method: position 0 fixed, others rotate.  The loop is warp-uniform (a
+          // group without a pair works on a clamped one and stores nothing), so the
+          // reductions shuffle under the full mask.
+          const int pr = min(pr0 + g8, np / 2 - 1);
           int a = pr == 0 ? 0 : 1 + (pr - 1 + rnd) % (np - 1);
           int b = 1 + (np - 2 - pr + rnd) % (np - 1);
-          if (a >= kp || b >= kp) continue;
+          const bool pair_ok = pr0 + g8 < np / 2 && a < kp && b < kp;
+          a = min(a, kp - 1);
+          b = min(b, kp - 1);
           double* ja = J + (size_t)a * kp;
           double* jb = J + (size_t)b * kp;
           long long jt0 = 0, jt1 = 0, jt2 = 0;
@@ -556,7 +580,7 @@ __device__ __forceinline__ int jacobi_sweeps(double* J, int kp, double* nrm, Sha
 #pragma unroll
           for (int q = 0; q < NJ; ++q) {
             const int r = gl + 8 * q;
-            const double va = ja[min(r, kp - 1)], vb = jb[min(r, kp - 1)];  // (no branch per row)
+            const double va = ja[r], vb = jb[r];  // (unconditional: the work area has slack past J)
             xa[q] = r < kp ? va : 0.0;
             xb[q] = r < kp ? vb : 0.0;
           }
@@ -567,10 +591,10 @@ __device__ __forceinline__ int jacobi_sweeps(double* J, int kp, double* nrm, Sha
             g1 = fma(xa[q + 1], xb[q + 1], g1);
           }
           for (int r = gl + 8 * NJ; r < kp; r += 8) g0 = fma(ja[r], jb[r], g0);
-          const double ga = grp_sum(g0 + g1, gm);
+          const double ga = grp_sum_w(g0 + g1);
           if (dbg) jt1 = clock64();
           const double al = nrm[a], be = nrm[b];
-          if (ga * ga > 1e-30 * (al * be) && ga != 0.0) {
+          if (pair_ok && ga * ga > 1e-30 * (al * be) && ga != 0.0) {
             // t = tan of the rotation angle, the smaller root: sign(d) 2g / (|d| + sqrt(d^2 + 4 g^2))
             const double d = be - al, g2 = ga + ga;
             const double t = copysign(g2, d * ga) / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
@@ -830,7 +854,7 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
     if (dbg) tsv[2] = clock64();
     // ---- B = R_k^T (nn x kp, column-major), unpivoted QR -> R2 (kp x kp); B in
     // shared memory when it fits
-    const bool bsm = nn * kp <= A.big;
+    const bool bsm = nn * kp + SVD_SLACK <= A.big;  // (+ slack: unconditional row loads run past a column)
     double* B = bsm ? big : W + (size_t)n * nn;
     double* T = W + (size_t)n * nn;  // global staging (free once B is in shared memory / consumed)
     const int ldb = nn;
@@ -855,6 +879,8 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       }
       __syncthreads();
       for (int i = 0; i < kp; ++i) {
+        long long q0 = 0, q1 = 0, q2 = 0;
+        if (dbg) q0 = clock64();
         double* ci = Bq + (size_t)i * ldb;
         const double alpha = S.misc[2 + 2 * (i & 1)], n2 = S.misc[3 + 2 * (i & 1)];
         double tau = 0.0, beta = alpha, scal = 0.0;
@@ -864,6 +890,7 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
           scal = __ddiv_rn(1.0, __dsub_rn(alpha, beta));
         }
         asm volatile("" : "+d"(tau), "+d"(beta), "+d"(scal));  // (no rematerialisation in the loops below)
+        if (dbg) q1 = clock64();
         const int jn = i + 1;  // the next pivot column
         for (int j = i + 1 + g8; j < kp; j += ngr) {
           double* c = Bq + (size_t)j * ldb;
@@ -872,13 +899,13 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
           double x[GR];
   #pragma unroll
           for (int q = 0; q < GR; ++q) {
-            const double cq = c[min(rb + 8 * q, nn - 1)];  // (unconditional loads: no branch per row)
+            const double cq = c[rb + 8 * q];  // (unconditional: the work area has slack past B)
             x[q] = rb + 8 * q < nn ? cq : 0.0;
           }
           if (tau != 0.0) {
             double vq[GR];
   #pragma unroll
-            for (int q = 0; q < GR; ++q) vq[q] = ci[min(rb + 8 * q, nn - 1)];
+            for (int q = 0; q < GR; ++q) vq[q] = ci[rb + 8 * q];
             double w0 = 0.0, w1 = 0.0;
   #pragma unroll
             for (int q = 0; q < GR; q += 2) {
@@ -917,7 +944,11 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
             }
           }
         }
+        if (dbg) q2 = clock64();
         __syncthreads();
+        if (dbg && blockIdx.x == 0) {
+          A.dbg[44] += q1 - q0; A.dbg[45] += q2 - q1; A.dbg[46] += clock64() - q2; A.dbg[47] += 1;
+        }
         if (tid == 0) ci[i] = beta;
       }
       __syncthreads();
@@ -932,7 +963,7 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
     // A pair's two columns are loaded once into registers (rows gl + 8q of the 8-lane
     // group), the dot product, the rotation and the stores all work from them.  Column
     // norms are carried through the rotations and refreshed exactly at every sweep.
-    const bool jsm = kp * kp <= A.big;
+    const bool jsm = kp * kp + SVD_SLACK <= A.big;
     double* J = jsm ? big : W + (size_t)n * nn + (size_t)nn * kp;
     double* nrm = sig;  // squared column norms (reuses the sigma scratch)
     if (bsm && jsm) {
@@ -1000,14 +1031,16 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       T[e] = J[(size_t)order[c] * kp + a] / sig[order[c]];
     }
     __syncthreads();
-    if (n <= 8 * GR && kp * n <= A.big) {
+    if (n <= 8 * GR && kp * n + SVD_SLACK <= A.big) {
       double* Vs = big;  // reflector i at Vs[i * n + row], rows > i
       for (int e = tid; e < kp * n; e += NT) {
         const int i = e / n, row = e - i * n;
         Vs[e] = row > i ? P[(size_t)i * ldp + row] : 0.0;
       }
       __syncthreads();
-      for (int c = g8; c < keep; c += ngr) {
+      for (int c0 = 0; c0 < keep; c0 += ngr) {  // (warp-uniform passes: full-mask shuffles)
+        const bool cok = c0 + g8 < keep;
+        const int c = min(c0 + g8, keep - 1);
         double y[GR];
 #pragma unroll
         for (int q = 0; q < GR; ++q) {
@@ -1024,7 +1057,7 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
 #pragma unroll
           for (int q = 0; q < GR; ++q) {
             const int r = gl + 8 * q;
-            const double vq = vi[min(r, n - 1)];  // (unconditional load: no branch per row)
+            const double vq = vi[r];  // (unconditional load: slack past the last reflector)
             vr[q] = r < n ? (r == i ? 1.0 : vq) : 0.0;
           }
 #pragma unroll
@@ -1032,14 +1065,14 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
             w0 = fma(vr[q], y[q], w0);
             w1 = fma(vr[q + 1], y[q + 1], w1);
           }
-          const double t = -tau * grp_sum(w0 + w1, gm);
+          const double t = -tau * grp_sum_w(w0 + w1);
 #pragma unroll
           for (int q = 0; q < GR; ++q) y[q] = fma(t, vr[q], y[q]);
         }
 #pragma unroll
         for (int q = 0; q < GR; ++q) {
           const int r = gl + 8 * q;
-          if (r < n) Yg[(size_t)r * keep + c] = y[q];
+          if (cok && r < n) Yg[(size_t)r * keep + c] = y[q];
         }
       }
       __syncthreads();
@@ -1147,7 +1180,7 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.lb = lb; A.le = le; A.dim = t->dim; A.kernel = M->p.kernel;
   A.dx = M->p.kernel == SMASH_KERNEL_EXP ? 1.0 : M->p.dx;
   A.eps_svd = M->p.eps_svd;
-  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 60;
+  static const int floor_exp = getenv("SMASH_SVD_FLOOR") ? atoi(getenv("SMASH_SVD_FLOOR")) : 57;
   static const int floor_leaf = getenv("SMASH_SVD_FLOOR_LEAF") ? atoi(getenv("SMASH_SVD_FLOOR_LEAF")) : 56;
   A.floor_rel = ldexp(1.0, -floor_exp);
   A.floor_leaf = ldexp(1.0, -floor_leaf);
@@ -1187,7 +1220,7 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   A.nmax = std::max(nmax, 1);
   A.nnmax = nnmax;
   const int kpmax = std::min(A.nmax, A.nnmax);
-  A.gws_stride = (int64_t)A.nmax * A.nnmax + (int64_t)A.nnmax * kpmax + 2 * (int64_t)kpmax * kpmax;
+  A.gws_stride = (int64_t)A.nmax * A.nnmax + (int64_t)A.nnmax * kpmax + 2 * (int64_t)kpmax * kpmax + 2 * SVD_SLACK;
   int dev = 0, nsm = 0;
   SMASH_CUDA(cudaGetDevice(&dev));
   SMASH_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1299,10 +1332,11 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
     for (int q = 0; q < 4; ++q)
       fprintf(stderr, " [asm %lld qr %lld qr2 %lld jac %lld back %lld kp %lld keep %lld n.nn %lld]", h[q * 8], h[q * 8 + 1],
               h[q * 8 + 2], h[q * 8 + 3], h[q * 8 + 4], h[q * 8 + 5], h[q * 8 + 6], h[q * 8 + 7]);
-    fprintf(stderr, " max_sweeps %lld capped %lld | jacobi (thread 0 of traced nodes): dot %.0f scalar %.0f rotate %.0f per rotation (%lld), barrier wait %.0f per round (%lld) | group QR per step: scalars + update %.0f, write-back + argmax %.0f (%lld)\n", h[32], h[33],
+    fprintf(stderr, " max_sweeps %lld capped %lld | jacobi (thread 0 of traced nodes): dot %.0f scalar %.0f rotate %.0f per rotation (%lld), barrier wait %.0f per round (%lld) | group QR per step: scalars + update %.0f, write-back + argmax %.0f (%lld) | second QR per step: scalars %.0f columns %.0f barrier %.0f (%lld)\n", h[32], h[33],
             h[38] ? (double)h[34] / h[38] : 0.0, h[38] ? (double)h[35] / h[38] : 0.0, h[38] ? (double)h[36] / h[38] : 0.0, h[38],
             h[39] ? (double)h[37] / h[39] : 0.0, h[39], h[43] ? (double)h[40] / h[43] : 0.0,
-            h[43] ? (double)h[42] / h[43] : 0.0, h[43]);
+            h[43] ? (double)h[42] / h[43] : 0.0, h[43], h[47] ? (double)h[44] / h[47] : 0.0,
+            h[47] ? (double)h[45] / h[47] : 0.0, h[47] ? (double)h[46] / h[47] : 0.0, h[47]);
   }
   return hk;
 }
