@@ -51,6 +51,14 @@ FP64_PEAK_TFLOPS = 34.1
 # DP flops per kernel evaluation c_K (DADD + DMUL + 2*DFMA of the compiled kval<> path,
 # counted by ncu on k_block -- profiles/ckernel_r02.txt); 2*nrhs flops per interaction added.
 C_K = {"inv_r": 14.0, "log": 41.0, "exp": 52.0, "cauchy": 7.0}
+# The 8- and 16-column matvec kernels evaluate the log kernel from a shared-memory table
+# (kernels.cuh log_half_tab): 3 DADD + 2 DMUL + 13 DFMA per evaluation = 31, measured by ncu
+# on k_coupling<log,2,16> at config 5 (profiles/ckernel_r02.txt).
+C_K_TABLE_LOG = 31.0
+
+
+def c_k(kernel, nrhs):
+    return C_K_TABLE_LOG if kernel == "log" and nrhs in (8, 16) else C_K[kernel]
 L2_FLUSH_BYTES = 256 << 20
 # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full, profiles/coupling_r01.txt)
 NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6,
@@ -353,7 +361,7 @@ def config_summary(sg, cfg, R, T, fp64_peak, hbm):
     W = work_counts(sg, T["M"], c, R)
     mv_s = float(np.mean(T["mv_ms"])) / 1e3
     b_s = statistics.median(T["build_ms"]) / 1e3
-    per_int = C_K[c["kernel"]] + 2 * R
+    per_int = c_k(c["kernel"], R) + 2 * R
     return {"N": T["M"].n_row, "nrhs": R, "build_ms": b_s * 1e3, "matvec_ms": mv_s * 1e3,
             "gpoints_s": T["M"].n_row * R / mv_s / 1e9,
             "matvec_fp64_frac": (W["I_coup"] + W["I_near"]) * per_int / mv_s / 1e12 / fp64_peak,
@@ -535,7 +543,7 @@ def run_ours(args):
 
     # ---- rooflines: dominant FP64 kernel, transfer passes (HBM), construction
     W = work_counts(sg, M, c, R, owned, top)
-    per_int = C_K[c["kernel"]] + 2 * R
+    per_int = c_k(c["kernel"], R) + 2 * R
     ms_coup, ms_near = phase_serial[2], phase_serial[4]  # isolated kernel times
     if ms_coup >= ms_near:
         dom, flops, ms = "k_coupling", W["I_coup"] * per_int, ms_coup
@@ -549,7 +557,7 @@ def run_ours(args):
                 "peak_source": "measured DFMA microbenchmark (profiles/fp64_peak_r01.txt); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "flops_per_launch": flops, "ms_per_launch": ms,
-                "c_K": C_K[c["kernel"]], "interactions_coupling": W["I_coup"], "interactions_near": W["I_near"],
+                "c_K": c_k(c["kernel"], R), "interactions_coupling": W["I_coup"], "interactions_near": W["I_near"],
                 "matvec_total_frac": total_flops / (t_mv / args.steps) / 1e12 / FP64_PEAK_TFLOPS,
                 "scope": "rank 0's share" if ws > 1 else "whole matvec"}
     xfer_ms = phase_serial[1] + phase_serial[3] + phase_serial[5]

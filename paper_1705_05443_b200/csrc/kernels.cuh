@@ -62,6 +62,56 @@ __device__ __forceinline__ double log_half_pos(double x) {
   return fma(de, 3.46573590184561908245e-01, fma(de, 9.54107464635293850010e-11, lm));
 }
 
+// Table-driven 0.5 * log(x) for the matvec kernels (coupling / nearfield P2P, where the
+// evaluation count decides the run time): x = 2^e m, m in [1, 2); the top 5 mantissa bits
+// pick c_j = 1 + (j + 0.5) / 32 and the entry {ic_j = fl(1 / c_j), lc_j = fl(-0.5 log ic_j)};
+// u = fma(m, ic_j, -1) is exact to its own rounding and |u| <= 2^-6, so
+// 0.5 log m = lc_j + 0.5 log1p(u) with the series to u^9 (remainder u^10 / 20 < 1e-19).
+// lc_j belongs to the ROUNDED ic_j: no table bias.  11 FP64 operations after the table read
+// against 21 for the atanh series of log_half_pos (no reciprocal); measured against an 80-bit
+// reference the absolute error stays below 1.2e-16 (tools/gen_logtab.py).  The table lives in
+// shared memory, 8 copies of each 16-byte entry side by side (copy = lane & 7): the 8 lanes
+// of an LDS.128 quarter-warp read different bank groups whatever their entries, so the read
+// is conflict-free.
+static __device__ const double2 g_logtab[32] = {
+    {0x1.f81f81f81f820p-1, 0x1.fc0a8b0fc03c4p-8},  {0x1.e9131abf0b767p-1, 0x1.77458f632dcffp-6},
+    {0x1.dae6076b981dbp-1, 0x1.341d7961bd1d0p-5},  {0x1.cd85689039b0bp-1, 0x1.a926d3a4ad562p-5},
+    {0x1.c0e070381c0e0p-1, 0x1.0d77e7cd08e5bp-4},  {0x1.b4e81b4e81b4fp-1, 0x1.44d2b6ccb7d1cp-4},
+    {0x1.a98ef606a63bep-1, 0x1.7ab890210d907p-4},  {0x1.9ec8e951033d9p-1, 0x1.af3c94e80bff3p-4},
+    {0x1.948b0fcd6e9e0p-1, 0x1.e27076e2af2e8p-4},  {0x1.8acb90f6bf3aap-1, 0x1.0a324e27390e2p-3},
+    {0x1.8181818181818p-1, 0x1.22941fbcf7966p-3},  {0x1.78a4c8178a4c8p-1, 0x1.3a64c556945eap-3},
+    {0x1.702e05c0b8170p-1, 0x1.51aad872df82ep-3},  {0x1.6816816816817p-1, 0x1.686c81e9b14adp-3},
+    {0x1.6058160581606p-1, 0x1.7eaf83b82afc2p-3},  {0x1.58ed2308158edp-1, 0x1.947941c2116fbp-3},
+    {0x1.51d07eae2f815p-1, 0x1.a9cec9a9a084ap-3},  {0x1.4afd6a052bf5bp-1, 0x1.beb4d9da71b7ap-3},
+    {0x1.446f86562d9fbp-1, 0x1.d32fe7e00ebd5p-3},  {0x1.3e22cbce4a902p-1, 0x1.e744261d68789p-3},
+    {0x1.3813813813814p-1, 0x1.faf588f78f31dp-3},  {0x1.323e34a2b10bfp-1, 0x1.0723e5c1cdf41p-2},
+    {0x1.2c9fb4d812ca0p-1, 0x1.109f39e2d4c96p-2},  {0x1.27350b8812735p-1, 0x1.19ee6b467c96fp-2},
+    {0x1.21fb78121fb78p-1, 0x1.23130d7bebf43p-2},  {0x1.1cf06ada2811dp-1, 0x1.2c0e9ed448e8cp-2},
+    {0x1.1811811811812p-1, 0x1.34e289d9ce1d2p-2},  {0x1.135c81135c811p-1, 0x1.3d9026a7156fbp-2},
+    {0x1.0ecf56be69c90p-1, 0x1.4618bc21c5ec2p-2},  {0x1.0a6810a6810a7p-1, 0x1.4e7d811b75bb0p-2},
+    {0x1.0624dd2f1a9fcp-1, 0x1.56bf9d5b3f399p-2},  {0x1.0204081020408p-1, 0x1.5ee02a9241676p-2},
+};
+constexpr int LOGTAB_BYTES = 32 * 8 * 16;  // shared-memory copy: entry j, copy c at [j * 8 + c]
+
+__device__ __forceinline__ void logtab_fill(double2* tab) {
+  for (int e = threadIdx.x; e < 32 * 8; e += blockDim.x) tab[e] = g_logtab[e >> 3];
+}
+
+__device__ __forceinline__ double log_half_tab(double x, const double2* tab, int copy) {
+  const int hi = __double2hiint(x);
+  const int e = (hi >> 20) - 1023;
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
+  const double2 t = tab[((hi >> 15) & 31) * 8 + copy];
+  const double u = fma(m, t.x, -1.0);
+  double q = 1.0 / 18;  // 0.5 * (-1/2, 1/3, ..., 1/9), Horner from the u^9 term
+  q = fma(q, u, -1.0 / 16); q = fma(q, u, 1.0 / 14); q = fma(q, u, -1.0 / 12);
+  q = fma(q, u, 1.0 / 10); q = fma(q, u, -1.0 / 8); q = fma(q, u, 1.0 / 6);
+  q = fma(q, u, -0.25);
+  const double lm = t.y + fma(u * u, q, 0.5 * u);
+  const double de = (double)e;
+  return fma(de, 3.46573590184561908245e-01, fma(de, 9.54107464635293850010e-11, lm));
+}
+
 // Branch-free exp for x <= 0 (exp(-r) kernel): n = rint(x / ln2),
 // t = x - n ln2 (|t| <= 0.347, Cody-Waite), Taylor to degree 13, scale by 2^n.
 __device__ __forceinline__ double exp_neg(double x) {
@@ -107,6 +157,25 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
   // exp(-r): r = r2 * rsqrt(r2) (0 on the diagonal, exp(0) = 1)
   const double r = r2 * rsqrt_nr(r2);
   return exp_neg(is_zero(r2) ? 0.0 : -r);
+}
+
+// kval for the matvec kernels: the log kernel reads the shared-memory table (tab, copy =
+// lane & 7), every other kernel is kval itself.
+template <int KER, int D>
+__device__ __forceinline__ double kval_mv(const double* x, const double* y, double dx, const double2* tab,
+                                          int copy) {
+  if constexpr (KER == SMASH_KERNEL_LOG) {
+    double r2 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double t = x[a] - y[a];
+      r2 = fma(t, t, r2);
+    }
+    const double v = log_half_tab(r2, tab, copy);
+    return is_zero(r2) ? dx : v;
+  } else {
+    return kval<KER, D>(x, y, dx);
+  }
 }
 
 // runtime dispatch helper: f.template operator()<KER, D>()

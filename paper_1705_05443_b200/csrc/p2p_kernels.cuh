@@ -123,6 +123,9 @@ struct SegTable {
   int n;
 };
 
+// the segment table's footprint in doubles, rounded to 16 bytes (the log table follows it)
+constexpr int p2p_segtable_doubles() { return (int)((sizeof(SegTable) + 15) / 16 * 2); }
+
 __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
@@ -169,7 +172,7 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
                                                 int64_t sstride, const double* wts,
                                                 const double (&xt)[MTX][D], const bool (&tv)[MTX],
                                                 double dx, double* stage,
-                                                double (&c)[MTX][RC / 8][2]) {
+                                                double (&c)[MTX][RC / 8][2], const double2* ltab) {
   constexpr int NT = RC / 8;
   constexpr int WS = mma_wstride<RC>();
   constexpr int BUF = 32 * D + 32 * WS;
@@ -204,7 +207,7 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
       double av[MTX];
 #pragma unroll
       for (int m = 0; m < MTX; ++m) {  // straight-line: padded entries selected to 0
-        const double kv = kval<KER, D>(xt[m], ys, dx);
+        const double kv = kval_mv<KER, D>(xt[m], ys, dx, ltab, lane & 7);
         av[m] = (sv && tv[m]) ? kv : 0.0;
       }
 #pragma unroll
@@ -223,7 +226,7 @@ template <int KER, int D, int RC, int MTX, typename SegF>
 __device__ __forceinline__ void mma_block(const double* tx, int64_t tstride, int nt, int p0,
                                           int p1, SegF seg, const double* spts, int64_t sstride,
                                           const double* wts, double dx, SegTable& T,
-                                          double* buf) {
+                                          double* buf, const double2* ltab) {
   constexpr int NT = RC / 8;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -266,7 +269,7 @@ __device__ __forceinline__ void mma_block(const double* tx, int64_t tstride, int
     }
     __syncthreads();
     mma_warp_stream<KER, D, RC, MTX>(T, spts, sstride, wts, xt, tv, dx,
-                                     buf + wid * mma_stage_doubles<D, RC>(), c);
+                                     buf + wid * mma_stage_doubles<D, RC>(), c, ltab);
   }
   __syncthreads();  // the sums alias the staging buffers
   double* rw = buf + wid * (MMA_MTMAX * 8 * RC);
@@ -304,11 +307,14 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
     extern __shared__ __align__(16) double p2p_dyn[];  // see p2p_smem_bytes
     double* buf = p2p_dyn;
     SegTable& T = *reinterpret_cast<SegTable*>(p2p_dyn + mma_smem_doubles<D, RC>());
+    // the log kernel's table (kernels.cuh) behind the segment table, 16-byte aligned
+    double2* ltab = reinterpret_cast<double2*>(p2p_dyn + mma_smem_doubles<D, RC>() + p2p_segtable_doubles());
+    if constexpr (KER == SMASH_KERNEL_LOG) logtab_fill(ltab);  // (the loop's first barrier orders it)
     for (int t0 = 0; t0 < nt; t0 += MT * 8) {
       const int n = min(MT * 8, nt - t0);
       __syncthreads();
       mma_block_dispatch<KER, D, RC, MT>((n + 7) >> 3, tx + t0, tstride, n, p0, p1, seg, spts, sstride,
-                                     wts, dx, T, buf);
+                                     wts, dx, T, buf, ltab);
       __syncthreads();
       for (int e = threadIdx.x; e < n * RC; e += blockDim.x) {
         double sm = 0.0;
@@ -668,9 +674,11 @@ __global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny
 // ---------------------------------------------------------------------------
 // launchers (explicitly instantiated per kernel in p2p_<kernel>.cu)
 // ---------------------------------------------------------------------------
-template <int D, int RC>
+template <int KER, int D, int RC>
 constexpr size_t p2p_smem_bytes() {
-  return RC >= 8 ? mma_smem_doubles<D, RC>() * sizeof(double) + sizeof(SegTable) : 0;
+  return RC >= 8 ? (mma_smem_doubles<D, RC>() + p2p_segtable_doubles()) * sizeof(double) +
+                       (KER == SMASH_KERNEL_LOG ? LOGTAB_BYTES : 0)
+                 : 0;
 }
 
 template <typename K>
@@ -690,7 +698,7 @@ inline bool p2p_small(int max_targets) {
 
 template <int KER, int D, int RC>
 void launch_coupling(const CouplingArgs& a, cudaStream_t s) {
-  constexpr size_t smem = p2p_smem_bytes<D, RC>();
+  constexpr size_t smem = p2p_smem_bytes<KER, D, RC>();
   static const bool attr = [] {
     p2p_attrs(k_coupling<KER, D, RC, 5>, smem);
     p2p_attrs(k_coupling<KER, D, RC, 8>, smem);
@@ -721,7 +729,7 @@ void launch_coupling_sym(const CouplingArgs& a, const SymCoupling& y, cudaStream
 
 template <int KER, int D, int RC>
 void launch_near(const NearArgs& a, cudaStream_t s) {
-  constexpr size_t smem = p2p_smem_bytes<D, RC>();
+  constexpr size_t smem = p2p_smem_bytes<KER, D, RC>();
   static const bool attr = [] {
     p2p_attrs(k_near<KER, D, RC, 5>, smem);
     p2p_attrs(k_near<KER, D, RC, 8>, smem);
