@@ -51,14 +51,15 @@ FP64_PEAK_TFLOPS = 34.1
 # DP flops per kernel evaluation c_K (DADD + DMUL + 2*DFMA of the compiled kval<> path,
 # counted by ncu on k_block -- profiles/ckernel_r02.txt); 2*nrhs flops per interaction added.
 C_K = {"inv_r": 14.0, "log": 41.0, "exp": 52.0, "cauchy": 7.0}
-# The 8- and 16-column matvec kernels evaluate the log kernel from a shared-memory table
-# (kernels.cuh log_half_tab): 3 DADD + 2 DMUL + 13 DFMA per evaluation = 31, measured by ncu
-# on k_coupling<log,2,16> at config 5 (profiles/ckernel_r02.txt).
-C_K_TABLE_LOG = 31.0
+# The matvec kernels (k_coupling / k_near, all column counts) evaluate the log and exp kernels
+# from shared-memory tables (kernels.cuh log_half_tab / exp_neg_tab); DP ops per evaluation
+# measured by ncu on k_coupling itself (profiles/ckernel_r02.txt): log 2 DADD + 13 DFMA = 28,
+# exp 4 DADD + 5 DMUL + 15 DFMA = 39.  Construction (k_svd, k_block) keeps the series above.
+C_K_MATVEC = {"inv_r": 14.0, "log": 28.0, "exp": 39.0, "cauchy": 7.0}
 
 
 def c_k(kernel, nrhs):
-    return C_K_TABLE_LOG if kernel == "log" and nrhs in (8, 16) else C_K[kernel]
+    return C_K_MATVEC[kernel]
 L2_FLUSH_BYTES = 256 << 20
 # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full, profiles/coupling_r01.txt)
 NCU_TRAFFIC = {(2, 16, "k_coupling"): 26.45e6,

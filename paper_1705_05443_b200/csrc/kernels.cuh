@@ -69,7 +69,7 @@ __device__ __forceinline__ double log_half_pos(double x) {
 // 0.5 log m = lc_j + 0.5 log1p(u) with the series to u^9 (remainder u^10 / 20 < 1e-19).
 // lc_j belongs to the ROUNDED ic_j: no table bias.  11 FP64 operations after the table read
 // against 21 for the atanh series of log_half_pos (no reciprocal); measured against an 80-bit
-// reference the absolute error stays below 1.2e-16 (tools/gen_logtab.py).  The table lives in
+// reference the absolute error stays below 2.3e-16 (tools/gen_logtab.py).  The table lives in
 // shared memory, 8 copies of each 16-byte entry side by side (copy = lane & 7): the 8 lanes
 // of an LDS.128 quarter-warp read different bank groups whatever their entries, so the read
 // is conflict-free.
@@ -92,6 +92,7 @@ static __device__ const double2 g_logtab[32] = {
     {0x1.0624dd2f1a9fcp-1, 0x1.56bf9d5b3f399p-2},  {0x1.0204081020408p-1, 0x1.5ee02a9241676p-2},
 };
 constexpr int LOGTAB_BYTES = 32 * 8 * 16;  // shared-memory copy: entry j, copy c at [j * 8 + c]
+constexpr int KERTAB_BYTES = LOGTAB_BYTES;  // the exp table below has the same footprint
 
 __device__ __forceinline__ void logtab_fill(double2* tab) {
   for (int e = threadIdx.x; e < 32 * 8; e += blockDim.x) tab[e] = g_logtab[e >> 3];
@@ -107,9 +108,10 @@ __device__ __forceinline__ double log_half_tab(double x, const double2* tab, int
   q = fma(q, u, -1.0 / 16); q = fma(q, u, 1.0 / 14); q = fma(q, u, -1.0 / 12);
   q = fma(q, u, 1.0 / 10); q = fma(q, u, -1.0 / 8); q = fma(q, u, 1.0 / 6);
   q = fma(q, u, -0.25);
-  const double lm = t.y + fma(u * u, q, 0.5 * u);
-  const double de = (double)e;
-  return fma(de, 3.46573590184561908245e-01, fma(de, 9.54107464635293850010e-11, lm));
+  // 0.5 log1p(u) = u (0.5 + u q); e ln2 / 2 with the constant in one piece: its representation
+  // error |e| 2^-55 stays below 2.3e-16 absolute for |e| <= 80 (measured, tools/gen_logtab.py)
+  const double lm = fma(u, fma(u, q, 0.5), t.y);
+  return fma((double)e, 3.4657359027997264e-01, lm);
 }
 
 // Branch-free exp for x <= 0 (exp(-r) kernel): n = rint(x / ln2),
@@ -159,20 +161,73 @@ __device__ __forceinline__ double kval(const double* x, const double* y, double 
   return exp_neg(is_zero(r2) ? 0.0 : -r);
 }
 
-// kval for the matvec kernels: the log kernel reads the shared-memory table (tab, copy =
-// lane & 7), every other kernel is kval itself.
+// Table-driven exp(x), x <= 0, for the matvec kernels: k = rint(32 x / ln2), x = k ln2 / 32 + t,
+// |t| <= ln2 / 64, exp(x) = 2^(k >> 5) * 2^((k & 31) / 32) * exp(t) with exp(t) to t^6 (remainder
+// t^7 / 5040 < 4e-18): 12 FP64 operations against 19 for the degree-13 Taylor sum of exp_neg;
+// relative error <= 3.2e-16 against an 80-bit reference (tools/gen_logtab.py).  The 32 doubles
+// 2^(j/32) sit in shared memory as 16 copies side by side (copy = lane & 15): the 16 lanes of an
+// LDS.64 half-warp read different banks whatever their entries.
+static __device__ const double g_exptab[32] = {
+    0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0,
+    0x1.306fe0a31b715p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123422p+0, 0x1.44e086061892dp+0,
+    0x1.4bfdad5362a27p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd485429p+0, 0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0,
+    0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0,
+};
+
+__device__ __forceinline__ void exptab_fill(double* tab) {
+  for (int e = threadIdx.x; e < 32 * 16; e += blockDim.x) tab[e] = g_exptab[e >> 4];
+}
+
+__device__ __forceinline__ double exp_neg_tab(double x, const double* tab, int copy) {
+  const bool under = x < -708.0;
+  x = under ? -708.0 : x;
+  const double sh = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double kd = fma(x, 46.16624130844683, sh);  // 32 / ln2
+  const int k = __double2loint(kd);
+  const double nd = kd - sh;
+  double t = fma(-nd, 0x1.62e42fef80000p-6, x);  // ln2 / 32, high part (35 bits: k * hi exact)
+  t = fma(-nd, 0x1.1cf79ac000000p-41, t);
+  const double tj = tab[(k & 31) * 16 + copy];
+  double p = 1.0 / 720.0;
+  p = fma(p, t, 1.0 / 120.0); p = fma(p, t, 1.0 / 24.0); p = fma(p, t, 1.0 / 6.0);
+  p = fma(p, t, 0.5); p = fma(p, t, 1.0); p = fma(p, t, 1.0);
+  const double sc = __hiloint2double(((k >> 5) + 1023) << 20, 0);
+  return under ? 0.0 : (tj * p) * sc;
+}
+
+// kval for the matvec kernels: the log and exp kernels read their shared-memory table (tab:
+// KERTAB_BYTES, filled by kertab_fill), every other kernel is kval itself.
+template <int KER>
+constexpr bool kertab_used() { return KER == SMASH_KERNEL_LOG || KER == SMASH_KERNEL_EXP; }
+
+template <int KER>
+__device__ __forceinline__ void kertab_fill(double2* tab) {
+  if constexpr (KER == SMASH_KERNEL_LOG) logtab_fill(tab);
+  if constexpr (KER == SMASH_KERNEL_EXP) exptab_fill(reinterpret_cast<double*>(tab));
+}
+
 template <int KER, int D>
 __device__ __forceinline__ double kval_mv(const double* x, const double* y, double dx, const double2* tab,
-                                          int copy) {
-  if constexpr (KER == SMASH_KERNEL_LOG) {
+                                          int lane) {
+  if constexpr (KER == SMASH_KERNEL_LOG || KER == SMASH_KERNEL_EXP) {
     double r2 = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       double t = x[a] - y[a];
       r2 = fma(t, t, r2);
     }
-    const double v = log_half_tab(r2, tab, copy);
-    return is_zero(r2) ? dx : v;
+    if constexpr (KER == SMASH_KERNEL_LOG) {
+      const double v = log_half_tab(r2, tab, lane & 7);
+      return is_zero(r2) ? dx : v;
+    } else {
+      // exp(-r): r = r2 * rsqrt(r2) (0 on the diagonal, exp(0) = 1)
+      const double r = r2 * rsqrt_nr(r2);
+      return exp_neg_tab(is_zero(r2) ? 0.0 : -r, reinterpret_cast<const double*>(tab), lane & 15);
+    }
   } else {
     return kval<KER, D>(x, y, dx);
   }

@@ -29,7 +29,7 @@ namespace mv {
 template <int KER, int D, int RC>
 __device__ __forceinline__ void p2p_sources(const double* xt, const double* ys, int64_t ystride,
                                             const double* w, int ns, double dx, double* acc,
-                                            double* stage, int lane) {
+                                            double* stage, int lane, const double2* ktab) {
   for (int s0 = 0; s0 < ns; s0 += 32) {
     const int cnt = min(32, ns - s0);
     double vc[D], vw[RC];
@@ -43,11 +43,12 @@ __device__ __forceinline__ void p2p_sources(const double* xt, const double* ys, 
 #pragma unroll
     for (int r = 0; r < RC; ++r) stage[(D + r) * 32 + lane] = vw[r];
     __syncwarp();
+#pragma unroll 4  // independent evaluations in flight (the lane's chain is ~25 dependent FP64 ops)
     for (int s = 0; s < cnt; ++s) {
       double y[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) y[a] = stage[a * 32 + s];
-      const double kv = kval<KER, D>(xt, y, dx);
+      const double kv = kval_mv<KER, D>(xt, y, dx, ktab, lane);
 #pragma unroll
       for (int r = 0; r < RC; ++r) acc[r] = fma(kv, stage[(D + r) * 32 + s], acc[r]);
     }
@@ -62,7 +63,12 @@ __device__ __forceinline__ void dfma_block(const double* tx, int64_t tstride, in
                                            const double* wts, double dx, OutF out) {
   __shared__ double stage[P2P_WARPS][32 * (D + RC)];
   __shared__ double red[P2P_WARPS][32 * RC];
+  __shared__ double2 ktab[kertab_used<KER>() ? KERTAB_BYTES / 16 : 1];  // log / exp table (kernels.cuh)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if constexpr (kertab_used<KER>()) {
+    kertab_fill<KER>(ktab);
+    __syncthreads();
+  }
   for (int t0 = 0; t0 < nt; t0 += 32) {
     const int t = t0 + lane;
     double xt[D];
@@ -74,7 +80,7 @@ __device__ __forceinline__ void dfma_block(const double* tx, int64_t tstride, in
     for (int e = p0 + wid; e < p1; e += P2P_WARPS) {
       const int2 oc = seg(e);
       p2p_sources<KER, D, RC>(xt, spts + oc.x, sstride, wts + (int64_t)oc.x * RC, oc.y, dx, acc,
-                              stage[wid], lane);
+                              stage[wid], lane, ktab);
     }
 #pragma unroll
     for (int r = 0; r < RC; ++r) red[wid][r * 32 + lane] = acc[r];
@@ -207,7 +213,7 @@ __device__ __forceinline__ void mma_warp_stream(const SegTable& T, const double*
       double av[MTX];
 #pragma unroll
       for (int m = 0; m < MTX; ++m) {  // straight-line: padded entries selected to 0
-        const double kv = kval_mv<KER, D>(xt[m], ys, dx, ltab, lane & 7);
+        const double kv = kval_mv<KER, D>(xt[m], ys, dx, ltab, lane);
         av[m] = (sv && tv[m]) ? kv : 0.0;
       }
 #pragma unroll
@@ -307,9 +313,9 @@ __device__ __forceinline__ void p2p_block(const double* tx, int64_t tstride, int
     extern __shared__ __align__(16) double p2p_dyn[];  // see p2p_smem_bytes
     double* buf = p2p_dyn;
     SegTable& T = *reinterpret_cast<SegTable*>(p2p_dyn + mma_smem_doubles<D, RC>());
-    // the log kernel's table (kernels.cuh) behind the segment table, 16-byte aligned
+    // the log / exp kernel's table (kernels.cuh) behind the segment table, 16-byte aligned
     double2* ltab = reinterpret_cast<double2*>(p2p_dyn + mma_smem_doubles<D, RC>() + p2p_segtable_doubles());
-    if constexpr (KER == SMASH_KERNEL_LOG) logtab_fill(ltab);  // (the loop's first barrier orders it)
+    if constexpr (kertab_used<KER>()) kertab_fill<KER>(ltab);  // (the loop's first barrier orders it)
     for (int t0 = 0; t0 < nt; t0 += MT * 8) {
       const int n = min(MT * 8, nt - t0);
       __syncthreads();
@@ -677,7 +683,7 @@ __global__ void k_block(const double* X, int64_t nx, const double* Y, int64_t ny
 template <int KER, int D, int RC>
 constexpr size_t p2p_smem_bytes() {
   return RC >= 8 ? (mma_smem_doubles<D, RC>() + p2p_segtable_doubles()) * sizeof(double) +
-                       (KER == SMASH_KERNEL_LOG ? LOGTAB_BYTES : 0)
+                       (kertab_used<KER>() ? KERTAB_BYTES : 0)
                  : 0;
 }
 

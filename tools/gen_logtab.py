@@ -12,3 +12,15 @@ for j in range(64):
     lc = np.float64(-ld(0.5) * np.log(ld(ic)))
     print("    {%s, %s}," % (float(ic).hex(), float(lc).hex()))
 print("};")
+
+# exp table of exp_neg_tab: 2^(j/32) rounded to double, and the Cody-Waite split of ln2 / 32
+import struct
+ln2 = np.log(ld(2))
+L = ln2 / ld(32)
+b = struct.unpack("<Q", struct.pack("<d", float(np.float64(L))))[0] & ~((1 << 18) - 1)
+hi = struct.unpack("<d", struct.pack("<Q", b))[0]
+print("// ln2/32 = %s + %s, 32/ln2 = %r" % (float(hi).hex(), float(np.float64(L - ld(hi))).hex(),
+                                              float(np.float64(ld(32) / ln2))))
+print("static __device__ const double g_exptab[32] = {")
+print("    " + ", ".join(float(np.float64(np.exp(ld(j) * ln2 / ld(32)))).hex() for j in range(32)))
+print("};")
