@@ -359,3 +359,39 @@ def test_h2_requires_2d_tree_and_supported_basis(sg):
     tree = sg.build_tree(X, nu0=8, mode="2d")
     with pytest.raises(NotImplementedError):
         sg.build_h2(tree, sg.KernelSpec("cauchy", dx=0.0), X, X, sg.BuildParams(basis=None))
+
+
+# ---------------------------------------------------------------- table-driven log / exp of the matvec kernels
+
+@pytest.mark.parametrize("kind,dim", [("log", 1), ("log", 2), ("log", 3), ("exp", 1), ("exp", 2), ("exp", 3),
+                                      ("inv_r", 2)])
+@pytest.mark.parametrize("nrhs", [1, 4, 16])
+def test_nearfield_only_matvec_equals_dense_product(sg, kind, dim, nrhs):
+    """A tree of nearfield blocks only: z = K q comes from the matvec kernels' own kernel
+    evaluation (shared-memory tables for log / exp, kernels.cuh) and must equal the dense
+    product in extended precision to a few ulp of the column norm -- for every column-count
+    path (DFMA: 1, 4; DMMA: 16) and for distances from 1e-9 to ~30 (every table entry, the
+    exponent range of r^2, exp arguments down to the 1e-13 tail)."""
+    rng = np.random.default_rng(17 + dim)
+    n = 96
+    # four tight clusters inside one small box + a wide spread: r from 1e-9 to ~30
+    pts = np.vstack([rng.random((n // 2, dim)) * 30.0,
+                     15.0 + rng.random((n // 4, dim)) * 1e-3,
+                     15.0 + rng.random((n // 4, dim)) * 1e-8])
+    X = sg.PointSet(pts)
+    tree = sg.build_tree(X, nu0=n, mode="binary" if dim == 1 else "2d", tau=0.7)
+    spec = sg.KernelSpec(kind, dx=0.0)
+    M = sg.build_h2(tree, spec, X, X, sg.BuildParams(r=4, tau=0.7, basis="interp"))
+    assert M.pairs_L == []
+    q = rng.standard_normal((n, nrhs))
+    z = sg.matvec_nodewise(M, q if nrhs > 1 else q[:, 0]).reshape(n, nrhs)
+    ld = np.longdouble
+    d = np.sqrt(((pts[:, None, :].astype(ld) - pts[None, :, :].astype(ld)) ** 2).sum(-1))
+    with np.errstate(divide="ignore"):
+        K = {"log": lambda r: np.log(r), "exp": lambda r: np.exp(-r), "inv_r": lambda r: 1.0 / r}[kind](d)
+    if kind != "exp":
+        K[np.arange(n), np.arange(n)] = 0.0  # dx on the diagonal; exp keeps exp(0) = 1
+    ref = (K @ q.astype(ld))
+    scale = (np.abs(K) @ np.abs(q).astype(ld)).max(axis=0)
+    err = np.abs(z.astype(ld) - ref).max(axis=0) / scale
+    assert float(err.max()) <= 2e-15, (kind, dim, nrhs, err)
