@@ -87,9 +87,14 @@ struct SvdArgs {
   // split launch (wide HYB levels): mode 1 = assembly + pivoted QR only (HYB kernel, one CTA
   // per SM), mode 2 = the later phases only (two CTAs per SM); the panel, kp and the taus of
   // each node pass through a per-node workspace.  mode 0 = everything in one launch.
-  int mode, ws_lb;
+  // Jacobi split (wide levels): mode 3 = everything up to L = R2^T in the per-node workspace
+  // (the QR too unless prefac: done by a mode-1 launch), then k_jacobi rotates L in place at
+  // four CTAs per SM (it needs 36 KB of shared memory, not the 96 KB work area), then
+  // mode 4 = singular values, selection and back-transform.
+  int mode, ws_lb, prefac;
   int* kp_g;
   double* taus_g;
+  int64_t* joff_g;  // mode 3: offset of L in the node's workspace
   int* err;
   long long* dbg;  // SMASH_SVD_DBG: phase cycle counts of block 0's first nodes
 };
@@ -731,7 +736,8 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
     const double floor_v = A.nchild[v] ? A.floor_rel : A.floor_leaf;
     const int kmax = min(n, nn);
     int kp = 0;
-    if (A.mode == 2) {  // factored by the mode-1 launch
+    const bool loaded = A.mode == 2 || A.mode == 4 || (A.mode == 3 && A.prefac);
+    if (loaded) {  // factored by an earlier launch
       kp = A.kp_g[v - A.ws_lb];
       for (int i = tid; i < kp; i += NT) taus[i] = A.taus_g[(size_t)(v - A.ws_lb) * A.nmax + i];
       P = W;
@@ -835,7 +841,7 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       }
       __syncthreads();
     }
-    if (psm && kp > 0 && A.mode != 2) {
+    if (psm && kp > 0 && !loaded) {
       for (int e = tid; e < n * nn; e += NT) W[e] = P[e];
       __syncthreads();
       P = W;
@@ -847,17 +853,27 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       continue;
     }
     if (kp == 0) {
-      if (tid == 0) A.keep[v] = 0;
+      if (tid == 0) {
+        A.keep[v] = 0;
+        if (A.mode == 3) A.kp_g[v - A.ws_lb] = 0;
+      }
       __syncthreads();
       continue;
     }
     if (dbg) tsv[2] = clock64();
     // ---- B = R_k^T (nn x kp, column-major), unpivoted QR -> R2 (kp x kp); B in
     // shared memory when it fits
+    const bool pre = A.mode == 3, post = A.mode == 4;
     const bool bsm = nn * kp + SVD_SLACK <= A.big;  // (+ slack: unconditional row loads run past a column)
     double* B = bsm ? big : W + (size_t)n * nn;
     double* T = W + (size_t)n * nn;  // global staging (free once B is in shared memory / consumed)
     const int ldb = nn;
+    // L stays in the workspace when k_jacobi rotates it (modes 3 / 4)
+    const bool jsm = !pre && !post && kp * kp + SVD_SLACK <= A.big;
+    double* J = jsm ? big : W + (size_t)n * nn + (size_t)nn * kp;
+    double* nrm = sig;  // squared column norms (reuses the sigma scratch)
+    int sweeps_done = 0;
+    if (!post) {
     for (int e = tid; e < nn * kp; e += NT) {
       const int j = e / nn, b = e - j * nn;
       B[(size_t)j * ldb + b] = b >= j ? P[(size_t)b * ldp + j] : 0.0;
@@ -963,9 +979,6 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
     // A pair's two columns are loaded once into registers (rows gl + 8q of the 8-lane
     // group), the dot product, the rotation and the stores all work from them.  Column
     // norms are carried through the rotations and refreshed exactly at every sweep.
-    const bool jsm = kp * kp + SVD_SLACK <= A.big;
-    double* J = jsm ? big : W + (size_t)n * nn + (size_t)nn * kp;
-    double* nrm = sig;  // squared column norms (reuses the sigma scratch)
     if (bsm && jsm) {
       for (int e = tid; e < kp * kp; e += NT) {
         const int c = e / kp, r = e - c * kp;
@@ -980,11 +993,22 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       }
     }
     __syncthreads();
+    if (pre) {  // k_jacobi takes over
+      if (tid == 0) {
+        A.kp_g[v - A.ws_lb] = kp;
+        A.joff_g[v - A.ws_lb] = (int64_t)n * nn + (int64_t)nn * kp;
+      }
+      for (int i = tid; i < kp; i += NT) A.taus_g[(size_t)(v - A.ws_lb) * A.nmax + i] = taus[i];
+      __syncthreads();
+      continue;
+    }
     if (dbg) tsv[3] = clock64();
     // (the shared-memory case is instantiated on the work area itself: LDS, not generic loads)
-    const int sweeps_done = jsm ? (kp <= 64 ? jacobi_sweeps<8>(big, kp, nrm, S, A.dbg, dbg)
-                                            : jacobi_sweeps<16>(big, kp, nrm, S, A.dbg, dbg))
-                                : jacobi_sweeps<16>(J, kp, nrm, S, A.dbg, dbg);
+    sweeps_done = jsm ? (kp <= 64 ? jacobi_sweeps<8>(big, kp, nrm, S, A.dbg, dbg)
+                                  : jacobi_sweeps<16>(big, kp, nrm, S, A.dbg, dbg))
+                      : jacobi_sweeps<16>(J, kp, nrm, S, A.dbg, dbg);
+    }  // !post
+    if (dbg && post) tsv[2] = tsv[3] = clock64();
     if (dbg) tsv[4] = clock64();
     if (A.dbg && tid == 0) {  // every node: max sweeps, nodes at the sweep cap
       atomicMax(reinterpret_cast<unsigned long long*>(A.dbg + 32), (unsigned long long)sweeps_done);
@@ -1113,6 +1137,46 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
       o[5] = kp; o[6] = keep + 1000 * sweeps_done; o[7] = n * 1000 + nn;
     }
     ++dbg_n;
+  }
+}
+
+// Jacobi sweeps of a chunk of nodes on the L factors a mode-3 launch left in the per-node
+// workspace: one CTA per node at a time, L (up to 64 x 64) in 36 KB of shared memory, four
+// CTAs per SM -- twice the nodes in flight of the fused kernel, whose 96 KB work area the
+// sweeps do not need.  Larger L are rotated in place in the workspace.
+constexpr int JAC_KP = 64;
+constexpr int JAC_SMEM_DOUBLES = JAC_KP * JAC_KP + SVD_SLACK + 256 + 8;
+
+struct JacArgs {
+  int lb, le, ws_lb;
+  double* gws;
+  int64_t gws_stride;
+  const int* kp_g;
+  const int64_t* joff_g;
+};
+
+__global__ void __launch_bounds__(SVD_THREADS, 4) k_jacobi(JacArgs A) {
+  extern __shared__ __align__(16) double jac_smem[];
+  double* Js = jac_smem;
+  double* nrm = jac_smem + JAC_KP * JAC_KP + SVD_SLACK;
+  Shared S{};
+  S.imisc = reinterpret_cast<int*>(nrm + 256);
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int v = A.lb + blockIdx.x; v < A.le; v += gridDim.x) {
+    const int kp = A.kp_g[v - A.ws_lb];
+    if (kp == 0) continue;
+    double* Jg = A.gws + (size_t)(v - A.ws_lb) * A.gws_stride + A.joff_g[v - A.ws_lb];
+    if (kp <= JAC_KP) {
+      for (int e = tid; e < kp * kp; e += NT) Js[e] = Jg[e];
+      __syncthreads();
+      jacobi_sweeps<8>(Js, kp, nrm, S, nullptr, false);
+      __syncthreads();
+      for (int e = tid; e < kp * kp; e += NT) Jg[e] = Js[e];
+    } else {
+      __syncthreads();
+      jacobi_sweeps<16>(Jg, kp, nrm, S, nullptr, false);
+    }
+    __syncthreads();
   }
 }
 
@@ -1257,18 +1321,28 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   const int run_cnt = run_le - run_lb;
   // a wide HYB level is split: QR launches of one CTA per SM, the later phases at two
   const bool split = hyb && split_on && run_cnt > 2 * nsm;
+  // wide levels also hand the Jacobi sweeps to k_jacobi (four CTAs per SM)
+  static const bool jsplit_on = !(getenv("SMASH_SVD_JSPLIT") && atoi(getenv("SMASH_SVD_JSPLIT")) == 0);
+  const bool jsplit = jsplit_on && run_cnt > 2 * nsm && (split || (!hyb && A.big == big2));
   const int grid = std::min(cnt, nsm * svd_per_sm);
-  const int chunk = split ? std::min(run_cnt, split_chunk * nsm) : 0;
+  // per-node workspaces: chunks of 8 x SMs nodes (HYB split), or at most ~1 GB of workspace
+  int chunk = 0;
+  if (split) chunk = std::min(run_cnt, split_chunk * nsm);
+  else if (jsplit)
+    chunk = std::min<int64_t>(run_cnt, std::max<int64_t>(2 * nsm, ((int64_t)1 << 27) / A.gws_stride / (2 * nsm) * (2 * nsm)));
   DBuf<double> gws;
-  gws.alloc((size_t)(split ? chunk : grid) * A.gws_stride, s);
+  gws.alloc((size_t)(chunk ? chunk : grid) * A.gws_stride, s);
   A.gws = gws.p;
   DBuf<int> kp_g;
   DBuf<double> taus_g;
-  if (split) {
+  DBuf<int64_t> joff_g;
+  if (chunk) {
     kp_g.alloc(chunk, s);
     taus_g.alloc((size_t)chunk * A.nmax, s);
+    joff_g.alloc(chunk, s);
     A.kp_g = kp_g.p;
     A.taus_g = taus_g.p;
+    A.joff_g = joff_g.p;
   }
   DBuf<int> err;
   err.alloc(1, s);
@@ -1284,26 +1358,46 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   }
   const size_t smem = smem_small + 8 * (size_t)A.big;
   const size_t smem2 = smem_small + 8 * (size_t)big2;
+  constexpr size_t jac_smem = JAC_SMEM_DOUBLES * sizeof(double);
+  static const bool jac_attr = [] {
+    SMASH_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jac_smem));
+    return true;
+  }();
+  (void)jac_attr;
   dispatch_kernel_dim(A.kernel, A.dim, [&]<int KER, int D>() {
     SvdArgs Ar = A;
     Ar.lb = run_lb;
     Ar.le = run_le;
     if (run_le <= run_lb) return;
-    if (split) {
-      SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+    if (chunk) {
+      if (split)
+        SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
       SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem2));
       for (int c0 = run_lb; c0 < run_le; c0 += chunk) {
         Ar.lb = c0;
         Ar.le = std::min(run_le, c0 + chunk);
         Ar.ws_lb = c0;
-        Ar.mode = 1;
-        Ar.big = A.big;
-        k_svd<KER, D, true><<<std::min(nsm, Ar.le - Ar.lb), SVD_THREADS, smem, s>>>(Ar);
-        Ar.mode = 2;
+        const int cn = Ar.le - Ar.lb;
+        if (split) {
+          Ar.mode = 1;
+          Ar.big = A.big;
+          k_svd<KER, D, true><<<std::min(nsm, cn), SVD_THREADS, smem, s>>>(Ar);
+        }
         Ar.big = big2;
-        k_svd<KER, D, false><<<std::min(2 * nsm, Ar.le - Ar.lb), SVD_THREADS, smem2, s>>>(Ar);
+        Ar.prefac = split ? 1 : 0;
+        if (jsplit) {
+          Ar.mode = 3;
+          k_svd<KER, D, false><<<std::min(2 * nsm, cn), SVD_THREADS, smem2, s>>>(Ar);
+          JacArgs Ja{Ar.lb, Ar.le, Ar.ws_lb, A.gws, A.gws_stride, kp_g.p, joff_g.p};
+          k_jacobi<<<std::min(4 * nsm, cn), SVD_THREADS, jac_smem, s>>>(Ja);
+          Ar.mode = 4;
+          k_svd<KER, D, false><<<std::min(2 * nsm, cn), SVD_THREADS, smem2, s>>>(Ar);
+        } else {
+          Ar.mode = 2;
+          k_svd<KER, D, false><<<std::min(2 * nsm, cn), SVD_THREADS, smem2, s>>>(Ar);
+        }
       }
     } else if (hyb) {
       SMASH_CUDA(cudaFuncSetAttribute(k_svd<KER, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
