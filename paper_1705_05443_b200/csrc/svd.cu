@@ -1004,8 +1004,9 @@ __global__ void __launch_bounds__(SVD_THREADS, HYB ? 1 : 2) k_svd(SvdArgs A) {
     }
     if (dbg) tsv[3] = clock64();
     // (the shared-memory case is instantiated on the work area itself: LDS, not generic loads)
-    sweeps_done = jsm ? (kp <= 64 ? jacobi_sweeps<8>(big, kp, nrm, S, A.dbg, dbg)
-                                  : jacobi_sweeps<16>(big, kp, nrm, S, A.dbg, dbg))
+    sweeps_done = jsm ? (kp <= 64   ? jacobi_sweeps<8>(big, kp, nrm, S, A.dbg, dbg)
+                         : kp <= 80 ? jacobi_sweeps<10>(big, kp, nrm, S, A.dbg, dbg)
+                                    : jacobi_sweeps<16>(big, kp, nrm, S, A.dbg, dbg))
                       : jacobi_sweeps<16>(J, kp, nrm, S, A.dbg, dbg);
     }  // !post
     if (dbg && post) tsv[2] = tsv[3] = clock64();
@@ -1325,14 +1326,25 @@ int hss_level_svd(MatrixImpl* M, int side, int level, NearSets* near, int nmax, 
   static const bool jsplit_on = !(getenv("SMASH_SVD_JSPLIT") && atoi(getenv("SMASH_SVD_JSPLIT")) == 0);
   const bool jsplit = jsplit_on && run_cnt > 2 * nsm && (split || (!hyb && A.big == big2));
   const int grid = std::min(cnt, nsm * svd_per_sm);
-  // per-node workspaces: chunks of 8 x SMs nodes (HYB split), or at most ~1 GB of workspace
+  // per-node workspaces: every chunked level works inside the same 1 GB block (allocated once
+  // per build, always the same size: the stream-ordered pool hands the block back instead of
+  // mapping fresh memory for each level's different size, which cost sporadic 0.2 - 0.7 s)
+  constexpr int64_t WS_DOUBLES = (int64_t)1 << 27;
   int chunk = 0;
-  if (split) chunk = std::min(run_cnt, split_chunk * nsm);
-  else if (jsplit)
-    chunk = std::min<int64_t>(run_cnt, std::max<int64_t>(2 * nsm, ((int64_t)1 << 27) / A.gws_stride / (2 * nsm) * (2 * nsm)));
-  DBuf<double> gws;
-  gws.alloc((size_t)(chunk ? chunk : grid) * A.gws_stride, s);
-  A.gws = gws.p;
+  if (split || jsplit) {
+    const int64_t fit = std::max<int64_t>(1, WS_DOUBLES / A.gws_stride);
+    const int64_t unit = 2 * nsm;
+    chunk = (int)std::min<int64_t>(run_cnt, fit >= unit ? fit / unit * unit : fit);
+    if (split) chunk = std::min(chunk, split_chunk * nsm);
+  }
+  DBuf<double> gws_local;
+  if (chunk) {
+    if (ws.gws.n < (size_t)WS_DOUBLES) ws.gws.alloc(WS_DOUBLES, s);
+    A.gws = ws.gws.p;
+  } else {
+    gws_local.alloc((size_t)grid * A.gws_stride, s);
+    A.gws = gws_local.p;
+  }
   DBuf<int> kp_g;
   DBuf<double> taus_g;
   DBuf<int64_t> joff_g;

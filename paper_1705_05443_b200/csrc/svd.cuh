@@ -9,6 +9,7 @@ struct SvdWorkspace {
   DBuf<int> keep;       // per BFS node: number of kept singular vectors
   DBuf<int64_t> sv_off; // per BFS node: offset of S (nib x keep, row-major)
   DBuf<double> sv;      // kept left singular vectors
+  DBuf<double> gws;     // per-node workspaces of the chunked (split) launches: one fixed-size block
 };
 
 // For every node of level l on `side`, assemble the nearfield block row
